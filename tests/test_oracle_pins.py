@@ -1,0 +1,511 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Each test names the passage or closed form it checks.  None of them retypes the
+oracle's own formula: they use hand-derived closed forms (tests/golden/),
+textbook identities (SH orthonormality by quadrature), brute force written in a
+different form (Eq. 11 as explicit products), invariants, and float64 central
+finite differences of every gradient (north_star).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import scenegen
+from scenegen import Camera, identity_camera, scene_from_gaussians
+
+GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "closed_forms.json")))
+
+
+def one_gaussian(mean, sigma, logit=0.0, quat=(1, 0, 0, 0), rgb=(0.2, 0.5, 0.9), deg=0, scales=None):
+    s = scales if scales is not None else (sigma, sigma, sigma)
+    sh = np.zeros(((deg + 1) ** 2, 3))
+    sh[0] = (np.asarray(rgb) - 0.5) / GOLDEN["sh_dc"]["Y00"]
+    return scene_from_gaussians([mean], [np.log(s)], [quat], [logit], [sh], deg)
+
+
+def tiny_cam(bg=(0, 0, 0)):
+    c = GOLDEN["ewa_on_axis_isotropic"]["camera"]
+    cam = identity_camera(c["width"], c["height"], c["fx"], c["cx"], c["cy"])
+    cam.bg = bg
+    return cam
+
+
+# --------------------------------------------------------------------------- O3-O4
+def test_pinhole_projection_example(oracle):
+    g = GOLDEN["pinhole_projection"]
+    c = g["camera"]
+    cam = identity_camera(c["width"], c["height"], c["fx"], c["cx"], c["cy"])
+    pr = oracle.project(cam, one_gaussian(g["point"], 0.01), oracle.F64)
+    assert pr["mu_x"][0] == pytest.approx(g["mu"][0], abs=1e-12)
+    assert pr["mu_y"][0] == pytest.approx(g["mu"][1], abs=1e-12)
+    assert pr["z"][0] == pytest.approx(1.0)
+
+
+def test_pose_world_to_camera():
+    """Camera pose conventions (R2): a point on the camera's forward axis maps to (cx, cy)."""
+    from oracle import gsref
+    pos = np.array([1.0, -2.0, 1.5])
+    fwd = np.array([0.3, 0.8, -0.1])
+    cam = scenegen.camera_from_forward(640, 480, 500.0, 319.5, 239.5, pos, fwd)
+    p = pos + 2.5 * fwd / np.linalg.norm(fwd)
+    pr = gsref.project(cam, one_gaussian(p, 0.01), gsref.F64)
+    assert pr["mu_x"][0] == pytest.approx(319.5, abs=1e-4)
+    assert pr["mu_y"][0] == pytest.approx(239.5, abs=1e-4)
+    assert pr["z"][0] == pytest.approx(2.5, rel=1e-6)
+
+
+def test_near_plane_and_behind_culled(oracle):
+    cam = tiny_cam()
+    for z in (-1.0, 0.0, 0.19):
+        pr = oracle.project(cam, one_gaussian([0, 0, z], 0.05))
+        assert pr["radius"][0] == 0 and pr["tiles"][0] == 0 and pr["flags"][0] & oracle.FLAG_CULLED
+
+
+# --------------------------------------------------------------------------- O1-O2, O5-O7
+def _sigma_hat_from_conic(pr):
+    A, B, C = pr["conic_A"][0], pr["conic_B"][0], pr["conic_C"][0]
+    return np.linalg.inv(np.array([[A, B], [B, C]]))
+
+
+def test_covariance_identity_rotation(oracle):
+    """Eq. 2 with R = I: Sigma = diag(s^2); on axis Sigma_hat = (f/z)^2 Sigma_xy + 0.3 I."""
+    s = GOLDEN["covariance_identity_rotation"]["s"]
+    cam, z = tiny_cam(), 3.0
+    pr = oracle.project(cam, one_gaussian([0, 0, z], None, scales=s), oracle.F64)
+    Sh = _sigma_hat_from_conic(pr)
+    f = cam.fx
+    # parameters are stored in fp32 (log-scale), hence 1e-6 rather than fp64 round-off
+    np.testing.assert_allclose(Sh, np.diag([f * f * s[0] ** 2 / z ** 2 + 0.3, f * f * s[1] ** 2 / z ** 2 + 0.3]),
+                               rtol=1e-6, atol=1e-12)
+
+
+def test_covariance_rot90z(oracle):
+    g = GOLDEN["covariance_rot90z"]
+    cam, z, k = tiny_cam(), 3.0, 0.02
+    pr = oracle.project(cam, one_gaussian([0, 0, z], None, quat=g["quat_wxyz"], scales=[k * v for v in g["s"]]),
+                        oracle.F64)
+    Sh = _sigma_hat_from_conic(pr)
+    f = cam.fx
+    want = np.diag([f * f * k * k * g["Sigma_diag"][0] / z ** 2 + 0.3, f * f * k * k * g["Sigma_diag"][1] / z ** 2 + 0.3])
+    np.testing.assert_allclose(Sh, want, rtol=1e-6, atol=1e-9)
+
+
+def test_isotropic_rotation_invariance(oracle):
+    cam = tiny_cam()
+    rng = np.random.default_rng(5)
+    ref = None
+    for _ in range(5):
+        q = rng.normal(size=4)
+        pr = oracle.project(cam, one_gaussian([0, 0, 3.0], 0.05, quat=q), oracle.F64)
+        Sh = _sigma_hat_from_conic(pr)
+        ref = Sh if ref is None else ref
+        np.testing.assert_allclose(Sh, ref, rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(Sh, 1.3 * np.eye(2), rtol=1e-6, atol=1e-12)
+
+
+def test_ewa_worked_example_radius_rect(oracle):
+    """Tiny camera, sigma .05, z 3: Sigma_hat = 1.3 I, r = ceil(3 sqrt 1.3) = 4, 2 tiles (fp32)."""
+    g = GOLDEN["ewa_on_axis_isotropic"]
+    cam = tiny_cam()
+    pr = oracle.project(cam, one_gaussian([0, 0, g["z"]], g["sigma"]))
+    assert pr["radius"][0] == g["radius"]
+    assert list(pr["rect"][:, 0]) == g["rect_x0x1y0y1"]
+    assert pr["tiles"][0] == g["tiles"]
+    assert pr["conic_A"][0] == pytest.approx(1 / g["Sigma_hat_diag"], rel=1e-5)
+    assert pr["conic_B"][0] == pytest.approx(0.0, abs=1e-7)
+
+
+def test_ewa_off_axis_closed_form(oracle):
+    """(x, 0, z), isotropic sigma: a = s^2 f^2 (z^2+x^2)/z^4 + .3, b = 0, c = s^2 f^2/z^2 + .3."""
+    cam = identity_camera(320, 240, 300.0, 159.5, 119.5)
+    sig, z = 0.03, 2.0
+    for x in (0.2, -0.5, 0.9):
+        pr = oracle.project(cam, one_gaussian([x, 0, z], sig), oracle.F64)
+        Sh = _sigma_hat_from_conic(pr)
+        f = cam.fx
+        a = sig ** 2 * f * f * (z * z + x * x) / z ** 4 + 0.3
+        c = sig ** 2 * f * f / z ** 2 + 0.3
+        np.testing.assert_allclose(Sh, np.diag([a, c]), rtol=1e-6, atol=1e-9)
+
+
+def test_ewa_clamped_closed_form(oracle):
+    """R7: beyond 1.3x the half-tangent, J uses tx = kappa z: a = s^2 f^2 (1 + kappa^2)/z^2 + .3."""
+    cam = identity_camera(320, 240, 300.0, 159.5, 119.5)
+    sig, z, x = 0.4, 2.0, 2.0
+    kappa = 1.3 * 320 / (2 * 300.0)
+    pr = oracle.project(cam, one_gaussian([x, 0, z], sig), oracle.F64)
+    assert pr["flags"][0] & 8  # J x-clamp flag
+    Sh = _sigma_hat_from_conic(pr)
+    f = cam.fx
+    np.testing.assert_allclose(Sh[0, 0], sig ** 2 * f * f * (1 + kappa ** 2) / z ** 2 + 0.3, rtol=1e-6)
+
+
+def test_splat_size_scales_inverse_depth(oracle):
+    """doubling z halves the on-axis splat std (before the 0.3 low-pass)."""
+    cam = tiny_cam()
+    v = []
+    for z in (2.0, 4.0):
+        Sh = _sigma_hat_from_conic(oracle.project(cam, one_gaussian([0, 0, z], 0.1), oracle.F64))
+        v.append(Sh[0, 0] - 0.3)
+    assert v[0] / v[1] == pytest.approx(4.0, rel=1e-9)  # same fp32 sigma on both sides
+
+
+# --------------------------------------------------------------------------- O8 (SH)
+def test_sh_orthonormal_quadrature(oracle):
+    """Real SH up to degree 3 are orthonormal on the sphere (pins every basis constant)."""
+    nt, nphi = 24, 48
+    x, w = np.polynomial.legendre.leggauss(nt)
+    phi = (np.arange(nphi) + 0.5) * 2 * np.pi / nphi
+    ct, ph = np.meshgrid(x, phi, indexing="ij")
+    st = np.sqrt(1 - ct ** 2)
+    dirs = np.stack([st * np.cos(ph), st * np.sin(ph), ct], -1).reshape(-1, 3)
+    weights = (w[:, None] * np.full(nphi, 2 * np.pi / nphi)[None, :]).reshape(-1)
+    Y, _ = oracle.sh_basis(3, dirs)
+    G = (Y * weights[:, None]).T @ Y
+    np.testing.assert_allclose(G, np.eye(16), atol=1e-12)
+
+
+def test_sh_dc_value_and_condon_shortley_band1(oracle):
+    Y, _ = oracle.sh_basis(1, np.array([[1.0, 0, 0], [0, 1.0, 0], [0, 0, 1.0]]))
+    c1 = math.sqrt(3 / (4 * math.pi))
+    assert Y[0, 0] == pytest.approx(GOLDEN["sh_dc"]["Y00"], abs=1e-15)
+    assert Y[0, 0] == pytest.approx(0.5 / math.sqrt(math.pi), abs=1e-15)
+    # Condon-Shortley phase: Y_1^{-1} = -c1 y, Y_1^0 = c1 z, Y_1^1 = -c1 x  (k = l^2 + l + m)
+    assert Y[0, 3] == pytest.approx(-c1) and Y[1, 1] == pytest.approx(-c1) and Y[2, 2] == pytest.approx(c1)
+
+
+def test_sh_gradient_tangential_fd(oracle):
+    rng = np.random.default_rng(1)
+    d = rng.normal(size=(20, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    Y, dY = oracle.sh_basis(3, d)
+    h = 1e-6
+    for c in range(3):
+        e = np.zeros(3)
+        e[c] = h
+        Yp, _ = oracle.sh_basis(3, d + e)
+        Ym, _ = oracle.sh_basis(3, d - e)
+        np.testing.assert_allclose((Yp - Ym) / (2 * h), dY[:, :, c], atol=1e-7)
+
+
+def test_degree0_colour_equals_rgb(oracle):
+    """R14: DC = (rgb - .5)/Y00 makes the degree-0 colour equal rgb."""
+    cam = tiny_cam()
+    rgb = (0.13, 0.5, 0.97)
+    pr = oracle.project(cam, one_gaussian([0.1, -0.2, 3.0], 0.05, rgb=rgb), oracle.F64)
+    np.testing.assert_allclose([pr["r"][0], pr["g"][0], pr["b"][0]], rgb, atol=1e-7)
+
+
+# --------------------------------------------------------------------------- O9 (binning)
+def test_bin_matches_per_pixel_brute_force(oracle):
+    """Per-tile lists equal a per-pixel brute-force stable sort over all Gaussians whose
+    rect holds the pixel's tile; K = sum tiles_touched = sum range lengths (O9)."""
+    for seed, P, deg in ((0, 64, 0), (1, 40, 1), (2, 16, 3)):
+        scene, cam = scenegen.random_small_scene(seed, P, deg, width=48, height=40, f=40.0)
+        # ties in depth: duplicate a few z values to exercise the index tie-break (R12)
+        scene.params[2, 5:9] = scene.params[2, 5]
+        pr = oracle.project(cam, scene)
+        b = oracle.bin_tiles(cam, scene)
+        assert b["K"] == int(pr["tiles"].sum())
+        assert int((b["tile_ranges"][:, 1] - b["tile_ranges"][:, 0]).sum()) == b["K"]
+        zf = pr["z"].astype(np.float32)
+        for py in range(cam.height):
+            for px in range(cam.width):
+                tx, ty = px // 16, py // 16
+                cand = [i for i in range(P) if pr["radius"][i] > 0
+                        and pr["rect"][0, i] <= tx < pr["rect"][1, i] and pr["rect"][2, i] <= ty < pr["rect"][3, i]]
+                want = sorted(cand, key=lambda i: (zf[i], i))
+                t = ty * cam.tiles_x + tx
+                s, e = b["tile_ranges"][t]
+                assert list(b["sorted_ids"][s:e]) == want
+
+
+# --------------------------------------------------------------------------- O10 (composite)
+def test_peak_closed_form(oracle):
+    """Isotropic on-axis Gaussian, a0 < .99: C(cx,cy) = c a0 + (1-a0) bg, D = z a0, T = 1 - a0."""
+    bg = (0.1, 0.2, 0.3)
+    cam = tiny_cam(bg)
+    rgb = (0.9, 0.4, 0.05)
+    for logit in (-1.0, 0.0, 2.0):
+        a0 = 1 / (1 + math.exp(-logit))
+        f = oracle.render_fwd(cam, one_gaussian([0, 0, 3.0], 0.05, logit=logit, rgb=rgb), oracle.F64)
+        px, py = 32, 24
+        for ch in range(3):
+            assert f["rgb"][ch, py, px] == pytest.approx(rgb[ch] * a0 + (1 - a0) * bg[ch], abs=1e-7)  # fp32-stored SH DC and bg
+        assert f["depth"][py, px] == pytest.approx(3.0 * a0, abs=1e-12)
+        assert f["T_final"][py, px] == pytest.approx(1 - a0, abs=1e-12)
+
+
+@pytest.mark.parametrize("case", ["footprint_alpha_half", "footprint_logit3"])
+def test_footprint_closed_form(oracle, case):
+    """Contributing pixels are exactly the lattice points with (i-cx)^2 + (j-cy)^2 <=
+    2 s^2 ln(255 a0), s^2 = f^2 sigma^2/z^2 + .3 (skip below 1/255, north_star)."""
+    g = GOLDEN[case]
+    cam = tiny_cam()
+    logit = g["logit"]
+    a0 = 1 / (1 + math.exp(-logit))
+    f = oracle.render_fwd(cam, one_gaussian([0, 0, 3.0], 0.05, logit=logit), oracle.F64)
+    s2 = 60.0 ** 2 * 0.05 ** 2 / 9.0 + 0.3
+    rr = 2 * s2 * math.log(255 * a0)
+    want = sum(1 for j in range(cam.height) for i in range(cam.width)
+               if (i - 32) ** 2 + (j - 24) ** 2 <= rr and 16 <= i < 48 and 16 <= j < 32)
+    assert want == g["pixels"]
+    assert f["blended"] == g["pixels"]
+    assert int((f["n_contrib"] > 0).sum()) == g["pixels"]
+
+
+def test_two_coincident_and_capped(oracle):
+    bg = (0.3, 0.6, 0.1)
+    cam = tiny_cam(bg)
+    c1, c2 = np.array([0.9, 0.1, 0.4]), np.array([0.2, 0.8, 0.7])
+    sh = np.zeros((2, 1, 3))
+    sh[0, 0] = (c1 - 0.5) / GOLDEN["sh_dc"]["Y00"]
+    sh[1, 0] = (c2 - 0.5) / GOLDEN["sh_dc"]["Y00"]
+    sc = scene_from_gaussians([[0, 0, 2.0], [0, 0, 3.0]], np.log([[0.05] * 3, [0.07] * 3]),
+                              [[1, 0, 0, 0]] * 2, [0.0, 0.0], sh, 0)
+    f = oracle.render_fwd(cam, sc, oracle.F64)
+    w = GOLDEN["composite_two_coincident"]["weights"]
+    np.testing.assert_allclose(f["rgb"][:, 24, 32], w[0] * c1 + w[1] * c2 + w[2] * np.array(bg), atol=1e-7)
+    # N = 1 with opacity above the cap: 0.99 c + 0.01 bg
+    f = oracle.render_fwd(cam, one_gaussian([0, 0, 3.0], 0.05, logit=8.0, rgb=c1), oracle.F64)
+    w = GOLDEN["composite_single_capped"]["weights"]
+    np.testing.assert_allclose(f["rgb"][:, 24, 32], w[0] * c1 + w[1] * np.array(bg), atol=1e-7)
+
+
+def test_depth_order_nearer_wins(oracle):
+    cam = tiny_cam()
+    red, blue = np.array([1.0, 0, 0]), np.array([0, 0, 1.0])
+    sh = np.zeros((2, 1, 3))
+    sh[0, 0] = (blue - 0.5) / GOLDEN["sh_dc"]["Y00"]  # index 0 is the FAR one
+    sh[1, 0] = (red - 0.5) / GOLDEN["sh_dc"]["Y00"]
+    sc = scene_from_gaussians([[0, 0, 3.5], [0, 0, 2.0]], np.log([[0.3] * 3, [0.3] * 3]),
+                              [[1, 0, 0, 0]] * 2, [8.0, 8.0], sh, 0)
+    f = oracle.render_fwd(cam, sc, oracle.F64)
+    # SPEC.md:359 with the 0.99 cap: the near one gives .99, the far one .01 * .99
+    assert f["rgb"][0, 24, 32] == pytest.approx(0.99, abs=1e-7)
+    assert f["rgb"][2, 24, 32] == pytest.approx(0.01 * 0.99, abs=1e-7)
+
+
+def _product_form_render(pr, cam, P, bg):
+    """Eq. 11 written with explicit products prod_{j<k}(1 - a_j) and a brute-force
+    per-pixel depth sort (independent of the oracle's running-T loop)."""
+    H, W = cam.height, cam.width
+    out = np.zeros((3, H, W))
+    dep = np.zeros((H, W))
+    ncon = np.zeros((H, W), np.int64)
+    for py in range(H):
+        for px in range(W):
+            tx, ty = px // 16, py // 16
+            cand = [i for i in range(P) if pr["radius"][i] > 0
+                    and pr["rect"][0, i] <= tx < pr["rect"][1, i] and pr["rect"][2, i] <= ty < pr["rect"][3, i]]
+            cand.sort(key=lambda i: (pr["z"][i], i))
+            alphas, ids, pos = [], [], []
+            for p_, i in enumerate(cand):
+                dx, dy = pr["mu_x"][i] - px, pr["mu_y"][i] - py
+                q = pr["conic_A"][i] * dx * dx + 2 * pr["conic_B"][i] * dx * dy + pr["conic_C"][i] * dy * dy
+                if -0.5 * q > 0:
+                    continue
+                a = min(0.99, pr["opacity"][i] * math.exp(-0.5 * q))
+                if a < 1 / 255:
+                    continue
+                if np.prod([1 - x for x in alphas + [a]]) < 1e-4:
+                    break
+                alphas.append(a)
+                ids.append(i)
+                pos.append(p_)
+            for k, i in enumerate(ids):
+                wk = alphas[k] * np.prod([1 - x for x in alphas[:k]])
+                for ch, key in enumerate("rgb"):
+                    out[ch, py, px] += pr[key][i] * wk
+                dep[py, px] += pr["z"][i] * wk
+            Tf = np.prod([1 - x for x in alphas])
+            out[:, py, px] += Tf * np.asarray(bg)
+            ncon[py, px] = pos[-1] + 1 if pos else 0
+    return out, dep, ncon
+
+
+@pytest.mark.parametrize("seed,deg", [(3, 0), (4, 1), (5, 3)])
+def test_composite_matches_product_form(oracle, seed, deg):
+    scene, cam = scenegen.random_small_scene(seed, 12, deg, width=40, height=36, f=36.0)
+    cam.bg = (0.25, 0.5, 0.75)
+    pr = oracle.project(cam, scene, oracle.F64)
+    f = oracle.render_fwd(cam, scene, oracle.F64)
+    rgb, dep, ncon = _product_form_render(pr, cam, scene.P, cam.bg)
+    np.testing.assert_allclose(f["rgb"], rgb, atol=1e-12)
+    np.testing.assert_allclose(f["depth"], dep, atol=1e-12)
+    np.testing.assert_array_equal(f["n_contrib"], ncon)
+
+
+def test_composite_invariants(oracle):
+    """T_final in [1e-4, 1] (R16); sum a_k T_k = 1 - T_final (white scene, black bg);
+    energy bound; D/(1-T) within the contributors' depth range."""
+    w = scenegen.make("tiny")
+    cam = w.cameras[0]
+    sc = scenegen.Scene(w.scene.P, 0, w.scene.params.copy())
+    sc.params[11:14, :sc.P] = 0.5 / GOLDEN["sh_dc"]["Y00"]  # colour exactly 1
+    f = oracle.render_fwd(cam, sc, oracle.F64)
+    T = f["T_final"]
+    assert T.min() >= 1e-4 and T.max() <= 1.0
+    np.testing.assert_allclose(f["rgb"][0], 1 - T, atol=1e-12)
+    f32 = oracle.render_fwd(cam, w.scene, oracle.F32)
+    pr = oracle.project(cam, w.scene)
+    assert f32["rgb"].max() <= max(pr["r"].max(), pr["g"].max(), pr["b"].max()) + 1e-6
+    m = T < 0.999
+    ratio = f["depth"][m] / (1 - T[m])
+    zs = pr["z"][pr["radius"] > 0]
+    assert ratio.min() >= zs.min() - 1e-9 and ratio.max() <= zs.max() + 1e-9
+
+
+def test_permutation_invariance(oracle):
+    """rendering is invariant to insertion order (distinct depths)."""
+    scene, cam = scenegen.random_small_scene(11, 16, 1, width=40, height=32, f=32.0)
+    f0 = oracle.render_fwd(cam, scene)
+    perm = np.random.default_rng(0).permutation(scene.P)
+    p2 = scene.params.copy()
+    p2[:, :scene.P] = scene.params[:, perm]
+    f1 = oracle.render_fwd(cam, scenegen.Scene(scene.P, scene.sh_degree, p2))
+    np.testing.assert_array_equal(f0["rgb"], f1["rgb"])
+    np.testing.assert_array_equal(f0["depth"], f1["depth"])
+
+
+def test_float_mode_close_to_double(oracle):
+    w = scenegen.make("tiny")
+    a = oracle.render_fwd(w.cameras[0], w.scene, oracle.F32)
+    b = oracle.render_fwd(w.cameras[0], w.scene, oracle.F64)
+    np.testing.assert_allclose(a["rgb"], b["rgb"], atol=2e-5)
+
+
+# --------------------------------------------------------------------------- O11 (gradients)
+def _fd_scenes():
+    out = []
+    for seed in range(20):  # SPEC.md:700 acceptance: >= 20 random scenes, <= 10 Gaussians
+        deg = (0, 1, 3)[seed % 3]
+        sc, cam = scenegen.random_small_scene(100 + seed, 4 + seed % 7, deg)
+        cam.bg = (0.2, 0.1, 0.4)
+        out.append((f"rand{seed}", sc, cam))
+    # clamped-J case (R7): a wide Gaussian beyond 1.3x the half tangent still on screen
+    sh = np.zeros((4, 2, 3))
+    sh[0, 0] = [0.3, -0.2, 0.5]
+    sh[1, 0] = [-1.0, 0.6, 0.2]
+    sh[:, 1] = 0.1
+    sc = scene_from_gaussians([[1.8, 0.1, 2.0], [0.1, -0.1, 2.5]], np.log([[0.5, 0.3, 0.4], [0.2, 0.15, 0.25]]),
+                              [[0.9, 0.1, 0.3, -0.2], [0.5, 0.5, -0.1, 0.2]], [0.3, 0.8], sh, 1)
+    cam = identity_camera(32, 32, 30.0, 15.5, 15.5)
+    out.append(("jclamp", sc, cam))
+    # capped opacity (alpha = .99 at the centre) and a clamped colour channel
+    sh = np.zeros((3, 1, 3))
+    sh[0, 0] = [1.0, -3.0, 0.2]
+    sh[1, 0] = [0.1, 0.2, 0.3]
+    sh[2, 0] = [-0.5, 0.5, 0.9]
+    sc = scene_from_gaussians([[0, 0, 2.0], [0.2, 0.1, 2.4], [-0.15, 0.05, 3.0]],
+                              np.log([[0.12, 0.1, 0.11], [0.15, 0.2, 0.1], [0.3, 0.3, 0.3]]),
+                              [[1, 0.2, 0, 0], [0.3, 0.7, 0.1, 0.0], [1, 0, 0, 0.4]], [7.0, 1.0, 2.0], sh, 0)
+    out.append(("capped", sc, identity_camera(32, 32, 30.0, 15.5, 15.5)))
+    return out
+
+
+@pytest.mark.parametrize("name,scene,cam", _fd_scenes(), ids=[s[0] for s in _fd_scenes()])
+def test_gradients_central_fd_float64(oracle, name, scene, cam):
+    """Every gradient of L = <g_C, C> + <g_D, D> against float64 central differences:
+    rel < 1e-3 or abs < 1e-6 (north_star).  Perturbations that change any
+    decision (cull, rect, clamp, composited set, stop, cap) are skipped (guard)."""
+    g_rgb, g_d = scenegen.upstream_fields(7, cam.width, cam.height)
+    grad, _ = oracle.render_bwd(cam, scene, g_rgb, g_d, mode=oracle.F64)
+
+    def loss(params):
+        f = oracle.render_fwd(cam, scenegen.Scene(scene.P, scene.sh_degree, params), oracle.F64,
+                              want_signature=True)
+        return float((g_rgb * f["rgb"]).sum() + (g_d * f["depth"]).sum()), f["signature"]
+
+    _, sig0 = loss(scene.params)
+    checked = skipped = 0
+    bad = []
+    for r in range(scene.F):
+        for i in range(scene.P):
+            th = float(scene.params[r, i])
+            h = 1e-4 * max(1.0, abs(th))
+            pp, pm = scene.params.copy(), scene.params.copy()
+            pp[r, i] = np.float32(th + h)
+            pm[r, i] = np.float32(th - h)
+            lp, sp = loss(pp)
+            lm, sm = loss(pm)
+            if sp != sig0 or sm != sig0:
+                skipped += 1
+                continue
+            fd = (lp - lm) / (float(pp[r, i]) - float(pm[r, i]))
+            g = grad[r, i]
+            checked += 1
+            if not (abs(fd - g) < 1e-6 or abs(fd - g) < 1e-3 * abs(g)):
+                bad.append((r, i, g, fd))
+    assert not bad, f"{len(bad)} FD mismatches, e.g. {bad[:5]}"
+    assert checked >= 0.9 * (checked + skipped)
+
+
+def test_zero_upstream_gives_exact_zero(oracle):
+    scene, cam = scenegen.random_small_scene(3, 10, 3)
+    z = np.zeros((3, cam.height, cam.width), np.float32)
+    grad, screen = oracle.render_bwd(cam, scene, z, np.zeros((cam.height, cam.width), np.float32))
+    assert np.all(grad == 0) and np.all(screen == 0)
+
+
+def test_occluded_gaussian_zero_gradient(oracle):
+    """a Gaussian behind a stack that drives T below 1e-4 is never
+    composited, so its gradient is exactly zero."""
+    cam = identity_camera(32, 32, 30.0, 15.5, 15.5)
+    sh = np.zeros((4, 1, 3))
+    sh[:, 0] = [0.1, 0.2, 0.3]
+    sc = scene_from_gaussians([[0, 0, 1.0], [0, 0, 1.1], [0, 0, 1.2], [0, 0, 3.0]],
+                              np.log([[2.0] * 3] * 3 + [[0.2] * 3]), [[1, 0, 0, 0]] * 4, [9.0, 9.0, 9.0, 0.0], sh, 0)
+    g_rgb, g_d = scenegen.upstream_fields(2, 32, 32)
+    grad, _ = oracle.render_bwd(cam, sc, g_rgb, g_d, mode=oracle.F64)
+    assert np.all(grad[:, 3] == 0)
+    assert np.any(grad[:, 0] != 0)
+
+
+def test_mixed_mode_matches_f64_on_smooth_scene(oracle):
+    w = scenegen.make("tiny")
+    cam = w.cameras[0]
+    g_rgb, g_d = scenegen.upstream_fields(1, cam.width, cam.height)
+    a, _ = oracle.render_bwd(cam, w.scene, g_rgb, g_d, mode=oracle.MIXED)
+    b, _ = oracle.render_bwd(cam, w.scene, g_rgb, g_d, mode=oracle.F64)
+    # identical decisions on this scene (checked by signature) => same values up to fp64 rounding
+    s32 = oracle.render_fwd(cam, w.scene, oracle.F32, want_signature=True)["signature"]
+    s64 = oracle.render_fwd(cam, w.scene, oracle.F64, want_signature=True)["signature"]
+    if s32 == s64:
+        np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-9)
+
+
+# --------------------------------------------------------------------------- O12 (Adam)
+def test_adam_closed_forms(oracle):
+    """From zero state the first step is -lr g/(|g|+eps); a constant g for t steps moves
+    t lr g/(|g|+eps) (bias correction makes m_hat = g, v_hat = g^2); g = 0 is a no-op."""
+    rng = np.random.default_rng(0)
+    F, P = 3, 8
+    p0 = rng.normal(size=(F, P)).astype(np.float32)
+    g = rng.normal(size=(F, P)).astype(np.float32)
+    g[0, 0] = 0.0
+    lr = np.array([1e-3, 5e-2, 2.5e-3], np.float32)
+    eps = 1e-15
+    m = np.zeros((F, P), np.float32)
+    v = np.zeros((F, P), np.float32)
+    p = p0.copy()
+    for t in range(1, 6):
+        pn, mn, vn = oracle.adam_step(p, g, m, v, lr, t, eps=eps)
+        p, m, v = pn.astype(np.float32), mn.astype(np.float32), vn.astype(np.float32)
+        want = p0.astype(np.float64) - t * lr[:, None] * g / (np.abs(g) + eps)
+        np.testing.assert_allclose(pn, want, rtol=0, atol=1e-5 * t)
+    assert p[0, 0] == p0[0, 0]
+
+
+def test_l1_loss_closed_form(oracle):
+    rgb = np.array([[[0.5, 0.25]], [[0.125, 0.125]], [[0.0, 1.0]]])
+    tr = np.array([[[0.375, 0.25]], [[0.25, 0.0]], [[0.0, 0.5]]], np.float32)
+    d = np.array([[2.0, 1.0]])
+    td = np.array([[1.0, 1.5]], np.float32)
+    L, gr, gd = oracle.l1_loss_grad(rgb, d, tr, td, 1.0)
+    assert L == pytest.approx((0.125 + 0 + 0.125 + 0.125 + 0 + 0.5) / 6 + (1.0 + 0.5) / 2, rel=1e-12)
+    np.testing.assert_array_equal(np.sign(gr), [[[1, 0]], [[-1, 1]], [[0, 1]]])
+    np.testing.assert_array_equal(np.sign(gd), [[1, -1]])
