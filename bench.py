@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: fwd + bwd + Adam iterations of the GSFusion rasterizer hot path.
+
+python bench.py [--gpus N --steps K --warmup W --config scannetpp]
+N > 1: launched with torch.distributed.run, one rank per GPU (NCCL); the views of
+the batch are sharded contiguously over ranks and the gradient is all-reduced
+(SUM) over NVLink before a replicated Adam step.
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd+Adam iters/s and blended Gaussian-pixels/s, 1/2/4/8 B200"
+UNIT = "blended Gaussian-pixels/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="scannetpp", choices=["tiny", "small", "replica", "scannetpp", "large"])
+    ap.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[4 + k].lower() == "active"})
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle legs
+def cpu_window_camera(cam, size=584):
+    """Central size x size window of a view (tile-aligned origin), same intrinsics:
+    a bounded sample of the same workload for the CPU oracle."""
+    import copy
+    c = copy.copy(cam)
+    x0 = (cam.width - size) // 2 // 16 * 16
+    y0 = (cam.height - size) // 2 // 16 * 16
+    c.width, c.height = min(size, cam.width), min(size, cam.height)
+    c.cx, c.cy = cam.cx - x0, cam.cy - y0
+    return c
+
+
+def oracle_step_sample(w, view=0, size=584):
+    """One view's fwd (F32) + L1 + bwd (MIXED) + Adam on the oracle, on a window."""
+    import numpy as np
+    from oracle import gsref
+    from paper_2408_12677_b200.pipeline import lr_per_row
+    cam = cpu_window_camera(w.cameras[view], size)
+    t0 = time.perf_counter()
+    tgt = gsref.render_fwd(cam, w.target_scene, gsref.F32)
+    t1 = time.perf_counter()
+    f = gsref.render_fwd(cam, w.scene, gsref.F32)
+    L, g_rgb, g_d = gsref.l1_loss_grad(f["rgb"], f["depth"], tgt["rgb"].astype(np.float32),
+                                       tgt["depth"].astype(np.float32), 1.0)
+    grad, _ = gsref.render_bwd(cam, w.scene, g_rgb.astype(np.float32), g_d.astype(np.float32), mode=gsref.MIXED)
+    S = w.scene.params.shape[1]
+    gfull = np.zeros_like(w.scene.params)
+    gfull[:, :w.scene.P] = grad
+    z = np.zeros_like(w.scene.params)
+    gsref.adam_step(w.scene.params, gfull, z, z, np.array(lr_per_row(w.scene.sh_degree), np.float32), 1, P=S)
+    t2 = time.perf_counter()
+    return {"seconds": t2 - t1, "blended": f["blended"], "window": f"{cam.width}x{cam.height}",
+            "target_seconds": t1 - t0}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, timed on this box's host cores."""
+    if rank != 0:
+        return
+    import scenegen
+    from oracle import gsref
+    gsref.build()
+    kw = {"num_views": 1} if args.config in ("replica", "scannetpp", "large") else {}
+    w = scenegen.make(args.config, args.seed, **kw)
+    size = 584 if args.config in ("replica", "scannetpp", "large") else 10 ** 6
+    for _ in range(min(args.warmup, 1)):
+        oracle_step_sample(w, 0, size)
+    tot_s, tot_b = 0.0, 0
+    for _ in range(args.steps):
+        r = oracle_step_sample(w, 0, size)
+        tot_s += r["seconds"]
+        tot_b += r["blended"]
+    value = tot_b / tot_s
+    sample = f"1 view, {r['window']} central window of config '{args.config}', fwd(F32)+L1+bwd(MIXED)+Adam per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": args.config, "seed": args.seed},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import scenegen
+    from paper_2408_12677_b200 import gsr, pipeline
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = gsr.load()
+
+    w = scenegen.make(args.config, args.seed)
+    cams = w.cameras
+    B = len(cams)
+    my_views = scenegen.shard_views(B, rank, world)
+    model = pipeline.GaussianModel(w.scene, dev)
+    tgt_model = pipeline.GaussianModel(w.target_scene, dev)
+    my_cams = [cams[v] for v in my_views]
+    K0 = max(pipeline.measure_keys(lib, model, my_cams, dev), pipeline.measure_keys(lib, tgt_model, my_cams, dev))
+    cap = pipeline.default_capacity(K0)
+    tg = pipeline.render_targets(lib, tgt_model, my_cams, dev, cap)
+    targets = [None] * B
+    for v, t in zip(my_views, tg):
+        targets[v] = t
+    del tgt_model, tg
+    torch.cuda.empty_cache()
+
+    allreduce = None
+    if world > 1:
+        allreduce = lambda g: dist.all_reduce(g, op=dist.ReduceOp.SUM)  # noqa: E731
+    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce)
+    stream = torch.cuda.current_stream()
+
+    # --- warm-up
+    for _ in range(args.warmup):
+        tr.step(my_views)
+    torch.cuda.synchronize()
+
+    # --- timed region (device time, CUDA events, max over ranks)
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+    tr.blended.zero_()
+    tr.num_keys.zero_()
+    fwd_ev, bwd_ev = [], []
+    l0 = lib.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        for v in my_views:
+            b, cam, m = tr.buf, cams[v], model
+            gcam = gsr.camera(cam)
+            lib.project(gcam, m.desc, m.params, b.proj)
+            lib.bin_tiles(gcam, m.desc, b.proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
+                          num_keys_dev=tr.num_keys[v:v + 1])
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            lib.render_fwd(gcam, m.desc, b.proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=tr.blended)
+            a1.record(stream)
+            lib.l1_loss_grad(b.rgb, b.depth, targets[v][0], targets[v][1], tr.w_depth, b.g_rgb, b.g_depth, tr.loss)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            lib.render_bwd(gcam, m.desc, m.params, b.proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
+                           b.bwd_ws, m.grad)
+            c1.record(stream)
+            fwd_ev.append((a0, a1))
+            bwd_ev.append((c0, c1))
+        if allreduce is not None:
+            allreduce(model.grad)
+        model.step_count += 1
+        lib.adam_step(model.desc, model.params, model.grad, model.m, model.v, model.lr, model.step_count)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = lib.launch_count() - l0
+    clk = clocks.stop() if not args.profile else None
+    ms = e0.elapsed_time(e1)
+    fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / max(len(fwd_ev), 1)
+    bwd_ms = sum(a.elapsed_time(b) for a, b in bwd_ev) / max(len(bwd_ev), 1)
+    kmax = int(tr.num_keys.max().item())
+    if kmax > cap:
+        raise RuntimeError(f"key capacity overflow during the timed region: K={kmax} > {cap}")
+    blended = int(tr.blended.item())
+    stats = torch.tensor([ms, float(blended), fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, blended = float(mx[0]), int(sm[1])
+    ms_step = ms / args.steps
+    value = blended / (ms / 1000.0)
+    iters = args.steps / (ms / 1000.0)
+
+    # --- end to end: targets from pinned host memory every step, loss read back
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        host_t = {v: (targets[v][0].cpu().pin_memory(), targets[v][1].cpu().pin_memory()) for v in my_views}
+        dev_t = {v: (torch.empty_like(targets[v][0]), torch.empty_like(targets[v][1])) for v in my_views}
+        h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in host_t.values())
+        loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+        tr.blended.zero_()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            for v in my_views:
+                dev_t[v][0].copy_(host_t[v][0], non_blocking=True)
+                dev_t[v][1].copy_(host_t[v][1], non_blocking=True)
+            tr.loss.zero_()
+            tr.step(my_views, targets_override=dev_t)
+            loss_host.copy_(tr.loss, non_blocking=True)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ems = s0.elapsed_time(s1)
+        eb = int(tr.blended.item())
+        st = torch.tensor([ems, float(eb)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = st.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = st.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            ems, eb = float(mx[0]), int(sm[1])
+        e2e = {"value": eb / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
+               "iters_per_s": args.steps / (ems / 1000.0)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # --- roofline of the dominant kernel
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    n_views = len(my_views) * args.steps
+    roof = roofline(dev, peaks, clk, fwd_ms, bwd_ms, blended / max(world, 1) / n_views)
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        try:
+            from oracle import gsref
+            gsref.build()
+            size = 584 if args.config in ("replica", "scannetpp", "large") else 10 ** 6
+            r = oracle_step_sample(w, 0, size)
+            cpu = {"value": r["blended"] / r["seconds"], "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": f"1 view, {r['window']} central window of '{args.config}' view 0, "
+                             f"fwd(F32)+L1+bwd(MIXED)+Adam, {r['seconds']:.1f} s"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "iters_per_s": iters, "higher_is_better": True,
+        "scaling": "strong" if args.config in ("scannetpp", "large") else "replicas",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "views_per_step": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
+                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}",
+                   "key_capacity": cap, "max_keys_per_view": kmax,
+                   "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
+                       4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
+        "gpu_launches": int(launches),
+        "stage_ms": {"render_fwd": fwd_ms, "render_bwd": bwd_ms},
+        "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(dev, peaks, clk, fwd_ms, bwd_ms, blended_per_view):
+    """Issue-bound roofline of the dominant kernel (render_bwd); see DESIGN.md."""
+    import torch
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    mhz = (clk or {}).get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    peak = sms * 128 * mhz * 1e6 / 1e12  # FP32 lane-ops/s (T/s) at the measured clock
+    ops_per_blended = 40.0  # algorithmic FP32 ops per blended pair in the backward
+    achieved = blended_per_view * ops_per_blended / (bwd_ms / 1e3) / 1e12
+    return {"kernel": "gs_render_bwd", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": None,
+            "peak_source": f"{sms} SMs x 128 FP32 lanes x {mhz:.0f} MHz (clock measured during the run)"}
+
+
+if __name__ == "__main__":
+    main()

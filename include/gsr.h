@@ -1,0 +1,197 @@
+/* gsr.h -- C ABI of the B200-native GSFusion rasterizer hot path (libgsr.so).
+ *
+ * GSFusion (arXiv 2408.12677) optimises 3D Gaussians online with "a tile-based
+ * rasterizer which divides the screen into multiple tiles.  3D Gaussians lying in
+ * the current view frustum are sorted based on depth in each tile" (PAPER.md:139,
+ * §III-B3), renders Eq. 11, minimises Eq. 12 with "explicitly
+ * derived" gradients and updates every parameter by a
+ * first-order method.  The five calls below are that problem
+ * statement, one call per step (BASELINE.json north_star):
+ *
+ *   gs_project    Eqs. 2, 4, 5 + SH colour
+ *   gs_bin_tiles  per-tile depth sort
+ *   gs_render_fwd Eq. 11 + depth channel
+ *   gs_render_bwd dEq.11 -> dEq.5/4/2
+ *   gs_adam_step  first-order update          (Adam per north_star)
+ *
+ * plus the harness call gs_l1_loss_grad (Eq. 12) and diagnostics.
+ *
+ * CONVENTIONS (apply to every call)
+ *  - Pointers are DEVICE pointers unless marked HOST.  Every buffer is allocated and
+ *    owned by the caller; the library never allocates, frees or retains device
+ *    memory and keeps no state between calls except a process-wide launch counter.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t passed as void*; NULL =
+ *    the legacy default stream).  The only exception is gs_bin_tiles with a non-NULL
+ *    num_keys_host, which synchronises `stream` to report the key count.
+ *  - Float buffers used with 128-bit access must be 16-byte aligned and P_stride must
+ *    be a multiple of 4; violations return GS_ERR_ALIGN before anything is launched.
+ *  - Errors: every call returns a gs_status; no C++ exception crosses the ABI.
+ *    Argument errors are detected on the host before any launch.  A failed kernel
+ *    launch returns GS_ERR_CUDA; gs_last_error() then holds a thread-local message.
+ *    Culling is not an error: a culled Gaussian gets radius = tiles = 0 and exactly
+ *    zero gradient (readings R6, R23 in DESIGN.md).
+ *  - Precision: fp32 everywhere (R25).  All calls are re-entrant.
+ *  - The camera model, parameter layout and every reading (R1-R27) are documented
+ *    in DESIGN.md; the readings are frozen and shared with the CPU oracle's tests.
+ */
+#ifndef GSR_H_
+#define GSR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSR_VERSION 1
+#define GS_TILE 16         /* 16x16-pixel tiles (north_star) */
+#define GS_MAX_SH_DEGREE 3
+#define GS_MAX_TILES 65536 /* tile ids are sorted as 16-bit keys */
+#define GS_REC_FLOATS 12   /* floats per projected-Gaussian record */
+#define GS_SGRAD_FLOATS 12 /* floats per Gaussian in the render_bwd workspace */
+
+typedef enum {
+  GS_OK = 0,
+  GS_ERR_ARG = -1,      /* invalid argument (NULL, negative size, bad degree, ...) */
+  GS_ERR_ALIGN = -2,    /* pointer not 16-byte aligned or P_stride % 4 != 0 */
+  GS_ERR_CAPACITY = -3, /* gs_bin_tiles: K > key_capacity (required K reported) */
+  GS_ERR_STATE = -4,    /* inconsistent sizes between calls (SPEC StateMismatch) */
+  GS_ERR_EMPTY = -5,    /* gs_adam_step with P == 0 (SPEC NoGaussians) */
+  GS_ERR_CUDA = -6      /* a CUDA launch or runtime call failed; see gs_last_error() */
+} gs_status;
+
+/* Pinhole camera, OpenCV axes (x right, y down, z forward).  R_cw/t_cw map world to
+ * camera: the rotation W and translation of T_WC^{-1}, row-major.
+ * Pixel (i, j) is sampled at continuous (i, j) (R1).  Gaussians with camera-space
+ * z <= z_near are culled (R6).  bg is the background colour (R26). */
+typedef struct {
+  int32_t width, height;
+  float fx, fy, cx, cy;
+  float R_cw[9];
+  float t_cw[3];
+  float z_near;
+  float bg[3];
+} gs_camera;
+
+/* Parameters: float[F][P_stride], F = 11 + 3(deg+1)^2 rows (R3-R5):
+ *   rows 0-2 mean xyz (m) | 3-5 log-scale | 6-9 quaternion (w,x,y,z), need not be unit
+ *   10 opacity logit       | 11 + 3k + ch  SH coefficient k (k = 0 is DC), channel ch.
+ * The same layout is used for grad, Adam's m and v.  Columns >= P are never read. */
+typedef struct {
+  int64_t P;
+  int64_t P_stride;
+  int32_t sh_degree; /* 0..3 */
+} gs_scene;
+
+/* Per-view projection outputs (written by gs_project, read by every later call).
+ *  rec:    float[P][12] records, 48 B each (16-B aligned):
+ *            0 mu_x  1 mu_y  2 z  3 opacity  4 conic A  5 conic B  6 conic C
+ *            7 r  8 g  9 b  10-11 reserved
+ *          conic (A, B, C) is Sigma_hat^{-1} = [[A, B], [B, C]] (Eq. 3).  Records of
+ *          culled Gaussians are left untouched (undefined).
+ *  radius: int32[P]  ceil(3 sqrt(lambda_max)) in pixels, 0 = culled (R10)
+ *  tiles:  int32[P]  number of 16x16 tiles touched, 0 = culled (R11)
+ *  flags:  uint8[P]  bit0-2 colour channel clamped at 0 (R13), bit3/4 J x/y tangent
+ *                    clamp active (R7), bit7 culled */
+typedef struct {
+  float* rec;
+  int32_t* radius;
+  int32_t* tiles;
+  uint8_t* flags;
+} gs_proj;
+
+#define GS_FLAG_CLAMP_R 1
+#define GS_FLAG_CLAMP_G 2
+#define GS_FLAG_CLAMP_B 4
+#define GS_FLAG_JCLAMP_X 8
+#define GS_FLAG_JCLAMP_Y 16
+#define GS_FLAG_CULLED 128
+
+/* ---------------------------------------------------------------- diagnostics */
+int gs_version(void);
+const char* gs_last_error(void);  /* thread-local text of the last failure ("" if none) */
+int64_t gs_launch_count(void);    /* kernels launched by this library (process-wide) */
+int gs_exact_exp(void);           /* 1 in the GSR_EXACT_EXP debug build (libgsr_exact.so) */
+
+/* ---------------------------------------------------------------- gs_project
+ * Steps O1-O8: activations (R3-R5, R9), Sigma = R S S^T R^T (Eq. 2),
+ * p_c = W p + t and mu = pi(p_c) (Eq. 4), Sigma_hat = J W Sigma W^T J^T + 0.3 I
+ * (Eq. 5, R7, R8), conic, 3-sigma radius and tile rectangle (R10, R11), SH colour
+ * at the mean (R13).  In: params (see gs_scene).  Out: `out` (see gs_proj).
+ * Integer outputs and mu, z, conic, opacity are computed with a fixed fp32
+ * operation order (R9) and match the oracle bit for bit.
+ * P == 0 is valid (nothing launched). */
+gs_status gs_project(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
+                     gs_proj out, void* stream);
+
+/* ---------------------------------------------------------------- gs_bin_tiles
+ * Duplicates every visible Gaussian into one key per touched tile and orders the
+ * keys by (tile id = ty * tiles_x + tx, depth z, Gaussian index) (R12):
+ * an order-preserving compaction of the visible set, a 4-pass onesweep LSD radix
+ * sort of the depths, key emission in depth order, and a 1-2-pass onesweep radix
+ * sort of the 16-bit tile ids.
+ *  ws / ws_bytes:   scratch of at least gs_bin_tiles_workspace() bytes (16-B aligned)
+ *  sorted_ids:      int32[key_capacity] Gaussian index of each sorted key
+ *  tile_ranges:     int32[num_tiles][2] [start, end) of each tile's keys
+ *  num_keys_dev:    nullable DEVICE int64: receives K asynchronously
+ *  num_keys_host:   nullable HOST int64: if set, the call synchronises `stream`
+ *                   and writes K; returns GS_ERR_CAPACITY if K > key_capacity
+ * If K > key_capacity no key is written past key_capacity and every tile range is
+ * empty (renders give background); in async mode the caller detects this from
+ * num_keys_dev and retries with a larger buffer.  num_tiles must be <= 65536. */
+size_t gs_bin_tiles_workspace(const gs_camera* cam /*HOST*/, int64_t P, int64_t key_capacity);
+gs_status gs_bin_tiles(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj, void* ws,
+                       size_t ws_bytes, int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges,
+                       int64_t* num_keys_dev, int64_t* num_keys_host /*HOST*/, void* stream);
+
+/* ---------------------------------------------------------------- gs_render_fwd
+ * Eq. 11 per pixel over its tile's depth-sorted list, front to back: alpha =
+ * min(0.99, o exp(power)), skip alpha < 1/255 (and power > 0), stop before a
+ * Gaussian that would take T below 1e-4 (R15, R16, R27); C += c alpha T,
+ * D += z alpha T (R17); finally C += T bg.
+ *  rgb: float[3][H][W]   depth, T_final: float[H][W]   n_contrib: int32[H][W]
+ *       (1 + position in the tile list of the last composited Gaussian, 0 if none)
+ *  blended: nullable u64 counter, += number of composited (pixel, Gaussian) pairs. */
+gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
+                        const int32_t* sorted_ids, const int32_t* tile_ranges, float* rgb, float* depth,
+                        float* T_final, int32_t* n_contrib, unsigned long long* blended, void* stream);
+
+/* ---------------------------------------------------------------- gs_render_bwd
+ * Exact derivative of gs_project + gs_render_fwd (R18) for upstream
+ * dL/drgb float[3][H][W] and dL/ddepth float[H][W] (nullable = 0).  Consumes the
+ * forward's T_final and n_contrib (it does not re-render).  Reverses each pixel's
+ * composite per tile, reduces per-Gaussian screen-space gradients across each warp
+ * and scatters them with one atomic per (warp, Gaussian, component), then chains
+ * them to every parameter row.
+ *  ws: float[P][12] screen-space gradients (dmu_x, dmu_y, dA, dB, dC, dopacity,
+ *      dr, dg, db, dz, pad, pad); >= gs_render_bwd_workspace() bytes; cleared here.
+ *  grad: float[F][P_stride], ACCUMULATED (+=) so that views sum (R21).
+ * Float atomics make grad order-dependent in the last bits. */
+size_t gs_render_bwd_workspace(const gs_scene* scene /*HOST*/);
+gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
+                        gs_proj proj, const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                        const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, void* ws,
+                        size_t ws_bytes, float* grad, void* stream);
+
+/* ---------------------------------------------------------------- gs_adam_step
+ * Dense bias-corrected Adam over all F * P scalars (R20):
+ *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
+ *   p -= lr_row * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ *  lr_per_row: HOST float[F].  step: 1-based t.  zero_grad != 0 also writes grad = 0.
+ *  Returns GS_ERR_EMPTY if P == 0. */
+gs_status gs_adam_step(const gs_scene* scene /*HOST*/, float* params, float* grad, float* m, float* v,
+                       const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
+                       int zero_grad, void* stream);
+
+/* ---------------------------------------------------------------- harness: Eq. 12
+ * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
+ * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */
+gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
+                          const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
+                          void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSR_H_ */

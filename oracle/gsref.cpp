@@ -706,6 +706,42 @@ int gsref_render_fwd(const RefCamera* cam, int64_t P, int64_t P_stride, int deg,
   return 0;
 }
 
+// O10 at n selected pixels (px[j], py[j]) only; outputs per sample: rgb [3][n],
+// depth/T_final [n] (double), n_contrib [n], margin [n] (nullable).  Tile lists are
+// built exactly as in gsref_render_fwd; used for sampled parity at full size.
+int gsref_render_pixels(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, const float* params, int mode,
+                        int64_t n, const int32_t* px, const int32_t* py, double* rgb, double* depth, double* T_final,
+                        int32_t* n_contrib, double* margin) {
+  if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || mode < 0 || mode > 2 || n < 0) return -1;
+  const int TX = (cam->width + kTile - 1) / kTile;
+  auto run = [&](const auto& pd, const auto& ps) {
+    using DT = std::decay_t<decltype(pd.mux[0])>;
+    using ST = std::decay_t<decltype(ps.mux[0])>;
+    const auto lists = tile_lists(*cam, pd);
+    for (int64_t j = 0; j < n; ++j) {
+      if (px[j] < 0 || py[j] < 0 || px[j] >= cam->width || py[j] >= cam->height) return -1;
+      const auto& list = lists[(py[j] / kTile) * TX + px[j] / kTile];
+      const PixelResult<DT, ST> r = composite_pixel<DT, ST>(px[j], py[j], list, pd, ps, *cam, false);
+      for (int ch = 0; ch < 3; ++ch) rgb[ch * n + j] = (double)r.C[ch];
+      depth[j] = (double)r.Dep;
+      T_final[j] = (double)r.T;
+      n_contrib[j] = r.n;
+      if (margin) margin[j] = r.margin;
+    }
+    return 0;
+  };
+  if (mode == 0) {
+    const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
+    return run(pf, pf);
+  } else if (mode == 1) {
+    const Proj<double> pd = project_all<double>(*cam, P, P_stride, deg, params);
+    return run(pd, pd);
+  }
+  const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
+  const Proj<double> pd = project_all<double>(*cam, P, P_stride, deg, params);
+  return run(pf, pd);
+}
+
 // O10 + O11 for one view: parameter gradients of L = <g_rgb, C> + <g_depth, D>
 // (the vector-Jacobian product the harness feeds in; R19).  grad_out: double
 // [F][P] (overwritten, not accumulated); screen_out (nullable): double [10][P] =
@@ -721,9 +757,12 @@ int gsref_render_bwd(const RefCamera* cam, int64_t P, int64_t P_stride, int deg,
     std::vector<ScreenGrad<ST>> sg((size_t)P);
     for (int py = 0; py < H; ++py)
       for (int px = 0; px < W; ++px) {
+        const int64_t pix = (int64_t)py * W + px;
+        if (g_rgb[pix] == 0.f && g_rgb[(int64_t)W * H + pix] == 0.f && g_rgb[2 * (int64_t)W * H + pix] == 0.f &&
+            (!g_depth || g_depth[pix] == 0.f))
+          continue;  // zero upstream: this pixel contributes exactly zero (linearity)
         const auto& list = lists[(py / kTile) * TX + px / kTile];
         const PixelResult<DT, ST> r = composite_pixel<DT, ST>(px, py, list, pd, ps, *cam, true);
-        const int64_t pix = (int64_t)py * W + px;
         ST gC[3];
         for (int ch = 0; ch < 3; ++ch) gC[ch] = ST(g_rgb[ch * (int64_t)W * H + pix]);
         const ST gD = g_depth ? ST(g_depth[pix]) : ST(0);

@@ -66,6 +66,7 @@ def lib():
         _lib.gsref_project.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P]
         _lib.gsref_bin_tiles.argtypes = [P, i64, i64, C.c_int, P, i64, P, P, P, P]
         _lib.gsref_render_fwd.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P, P, P, P]
+        _lib.gsref_render_pixels.argtypes = [P, i64, i64, C.c_int, P, C.c_int, i64, P, P, P, P, P, P, P]
         _lib.gsref_render_bwd.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P]
         _lib.gsref_adam_step.argtypes = [i64, i64, i64, P, P, P, P, P, C.c_double, C.c_double, C.c_double,
                                          i64, P, P, P]
@@ -153,6 +154,23 @@ def render_fwd(cam, scene, mode=F32, want_margin=False, want_signature=False):
     if want_signature:
         out["signature"] = int(sig[0])
     return out
+
+
+def render_pixels(cam, scene, px, py, mode=F32):
+    """O10 at selected pixels (sampled parity at full size)."""
+    px = np.ascontiguousarray(px, dtype=np.int32)
+    py = np.ascontiguousarray(py, dtype=np.int32)
+    n = px.size
+    rgb = np.zeros((3, n))
+    depth = np.zeros(n)
+    T = np.zeros(n)
+    nc = np.zeros(n, np.int32)
+    margin = np.zeros(n)
+    rc = ref_camera(cam)
+    prm = _params(scene)
+    _check(lib().gsref_render_pixels(C.byref(rc), scene.P, scene.P_stride, scene.sh_degree, _p(prm), mode, n,
+                                     _p(px), _p(py), _p(rgb), _p(depth), _p(T), _p(nc), _p(margin)), "render_pixels")
+    return {"rgb": rgb, "depth": depth, "T_final": T, "n_contrib": nc, "margin": margin}
 
 
 def render_bwd(cam, scene, g_rgb, g_depth=None, mode=MIXED):

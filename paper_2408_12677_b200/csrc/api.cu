@@ -1,0 +1,276 @@
+// C-ABI entry points of libgsr.so (include/gsr.h): host-side argument validation,
+// camera marshalling and kernel dispatch.  No device memory is allocated here.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "gsr_internal.cuh"
+
+namespace gsr {
+
+namespace {
+thread_local char g_err[512] = "";
+std::atomic<long long> g_launches{0};
+int g_sms[64] = {0};
+}  // namespace
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+gs_status check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return GS_ERR_CUDA;
+  }
+  return GS_OK;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (g_sms[dev] == 0) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = n > 0 ? n : 148;
+  }
+  return g_sms[dev];
+}
+
+DevCam make_devcam(const gs_camera& c) {
+  DevCam d{};
+  d.W = c.width, d.H = c.height;
+  d.TX = (c.width + kTile - 1) / kTile;
+  d.TY = (c.height + kTile - 1) / kTile;
+  d.fx = c.fx, d.fy = c.fy, d.cx = c.cx, d.cy = c.cy;
+  for (int i = 0; i < 9; ++i) d.R[i] = c.R_cw[i];
+  for (int i = 0; i < 3; ++i) d.t[i] = c.t_cw[i], d.bg[i] = c.bg[i];
+  d.z_near = c.z_near;
+  for (int j = 0; j < 3; ++j) {  // camera centre -R^T t
+    double acc = 0.0;
+    for (int i = 0; i < 3; ++i) acc += (double)c.R_cw[3 * i + j] * (double)c.t_cw[i];
+    d.ocam[j] = (float)(-acc);
+  }
+  return d;
+}
+
+}  // namespace gsr
+
+using namespace gsr;
+
+namespace {
+
+gs_status check_camera(const gs_camera* cam, const char* fn) {
+  if (!cam) {
+    set_error("%s: camera is NULL", fn);
+    return GS_ERR_ARG;
+  }
+  if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0.f) || !(cam->fy > 0.f) || !std::isfinite(cam->cx) ||
+      !std::isfinite(cam->cy) || !(cam->z_near >= 0.f)) {
+    set_error("%s: invalid camera (width=%d height=%d fx=%g fy=%g z_near=%g)", fn, cam->width, cam->height,
+              (double)cam->fx, (double)cam->fy, (double)cam->z_near);
+    return GS_ERR_ARG;
+  }
+  const long long nt = (long long)((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);
+  if (nt > GS_MAX_TILES) {
+    set_error("%s: %lld tiles exceed GS_MAX_TILES (%d)", fn, nt, GS_MAX_TILES);
+    return GS_ERR_ARG;
+  }
+  return GS_OK;
+}
+
+gs_status check_scene(const gs_scene* sc, const char* fn) {
+  if (!sc) {
+    set_error("%s: scene is NULL", fn);
+    return GS_ERR_ARG;
+  }
+  if (sc->P < 0 || sc->P_stride < sc->P || sc->sh_degree < 0 || sc->sh_degree > GS_MAX_SH_DEGREE ||
+      sc->P >= (1ll << 31)) {
+    set_error("%s: invalid scene (P=%lld P_stride=%lld sh_degree=%d)", fn, (long long)sc->P, (long long)sc->P_stride,
+              sc->sh_degree);
+    return GS_ERR_ARG;
+  }
+  if (sc->P_stride % 4 != 0) {
+    set_error("%s: P_stride=%lld is not a multiple of 4", fn, (long long)sc->P_stride);
+    return GS_ERR_ALIGN;
+  }
+  return GS_OK;
+}
+
+gs_status check_ptrs(const char* fn, std::initializer_list<std::pair<const void*, const char*>> ptrs) {
+  for (const auto& p : ptrs) {
+    if (!p.first) {
+      set_error("%s: %s is NULL", fn, p.second);
+      return GS_ERR_ARG;
+    }
+    if (!aligned16(p.first)) {
+      set_error("%s: %s is not 16-byte aligned", fn, p.second);
+      return GS_ERR_ALIGN;
+    }
+  }
+  return GS_OK;
+}
+
+#define GS_TRY(x)                   \
+  do {                              \
+    const gs_status _s = (x);       \
+    if (_s != GS_OK) return _s;     \
+  } while (0)
+
+int rows_of(const gs_scene* sc) { return 11 + 3 * (sc->sh_degree + 1) * (sc->sh_degree + 1); }
+
+}  // namespace
+
+extern "C" {
+
+int gs_version(void) { return GSR_VERSION; }
+const char* gs_last_error(void) { return g_err; }
+int64_t gs_launch_count(void) { return (int64_t)g_launches.load(); }
+int gs_exact_exp(void) {
+#ifdef GSR_EXACT_EXP
+  return 1;
+#else
+  return 0;
+#endif
+}
+
+gs_status gs_project(const gs_camera* cam, const gs_scene* scene, const float* params, gs_proj out, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_project"));
+  GS_TRY(check_scene(scene, "gs_project"));
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_project", {{params, "params"}, {out.rec, "out.rec"}, {out.radius, "out.radius"},
+                                   {out.tiles, "out.tiles"}, {out.flags, "out.flags"}}));
+  launch_project(make_devcam(*cam), scene->P, scene->P_stride, scene->sh_degree, params, out,
+                 static_cast<cudaStream_t>(stream));
+  return check_launch("gs_project");
+}
+
+size_t gs_bin_tiles_workspace(const gs_camera* cam, int64_t P, int64_t key_capacity) {
+  if (!cam || P < 0 || key_capacity < 0) return 0;
+  const int nt = ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);
+  return bin_workspace_bytes(P, key_capacity, nt);
+}
+
+gs_status gs_bin_tiles(const gs_camera* cam, const gs_scene* scene, gs_proj proj, void* ws, size_t ws_bytes,
+                       int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges, int64_t* num_keys_dev,
+                       int64_t* num_keys_host, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_bin_tiles"));
+  GS_TRY(check_scene(scene, "gs_bin_tiles"));
+  if (key_capacity < 0 || key_capacity >= (1ll << 30)) {
+    set_error("gs_bin_tiles: key_capacity=%lld out of range [0, 2^30)", (long long)key_capacity);
+    return GS_ERR_ARG;
+  }
+  GS_TRY(check_ptrs("gs_bin_tiles", {{ws, "ws"}, {tile_ranges, "tile_ranges"}}));
+  if (scene->P > 0) {
+    GS_TRY(check_ptrs("gs_bin_tiles", {{proj.rec, "proj.rec"}, {proj.tiles, "proj.tiles"}}));
+    if (key_capacity > 0) GS_TRY(check_ptrs("gs_bin_tiles", {{sorted_ids, "sorted_ids"}}));
+  }
+  if (num_keys_dev && (reinterpret_cast<uintptr_t>(num_keys_dev) & 7u)) {
+    set_error("gs_bin_tiles: num_keys_dev is not 8-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  return launch_bin_tiles(make_devcam(*cam), scene->P, proj, ws, ws_bytes, key_capacity, sorted_ids, tile_ranges,
+                          num_keys_dev, num_keys_host, static_cast<cudaStream_t>(stream));
+}
+
+gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
+                        const int32_t* tile_ranges, float* rgb, float* depth, float* T_final, int32_t* n_contrib,
+                        unsigned long long* blended, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_render_fwd"));
+  GS_TRY(check_scene(scene, "gs_render_fwd"));
+  GS_TRY(check_ptrs("gs_render_fwd", {{tile_ranges, "tile_ranges"}, {rgb, "rgb"}, {depth, "depth"},
+                                      {T_final, "T_final"}, {n_contrib, "n_contrib"}}));
+  if (scene->P > 0) GS_TRY(check_ptrs("gs_render_fwd", {{proj.rec, "proj.rec"}}));
+  if (blended && (reinterpret_cast<uintptr_t>(blended) & 7u)) {
+    set_error("gs_render_fwd: blended is not 8-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  launch_render_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended,
+                    static_cast<cudaStream_t>(stream));
+  return check_launch("gs_render_fwd");
+}
+
+size_t gs_render_bwd_workspace(const gs_scene* scene) {
+  if (!scene || scene->P < 0) return 0;
+  return (size_t)scene->P * GS_SGRAD_FLOATS * sizeof(float);
+}
+
+gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float* params, gs_proj proj,
+                        const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                        const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, void* ws,
+                        size_t ws_bytes, float* grad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_render_bwd"));
+  GS_TRY(check_scene(scene, "gs_render_bwd"));
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_render_bwd", {{params, "params"}, {proj.rec, "proj.rec"}, {proj.radius, "proj.radius"},
+                                      {proj.flags, "proj.flags"}, {tile_ranges, "tile_ranges"}, {T_final, "T_final"},
+                                      {n_contrib, "n_contrib"}, {dL_drgb, "dL_drgb"}, {ws, "ws"}, {grad, "grad"}}));
+  if (dL_ddepth && !aligned16(dL_ddepth)) {
+    set_error("gs_render_bwd: dL_ddepth is not 16-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  const size_t need = gs_render_bwd_workspace(scene);
+  if (ws_bytes < need) {
+    set_error("gs_render_bwd: workspace %zu B < required %zu B", ws_bytes, need);
+    return GS_ERR_ARG;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemsetAsync(ws, 0, need, s) != cudaSuccess) return check_launch("gs_render_bwd memset");
+  const DevCam dc = make_devcam(*cam);
+  launch_render_bwd(dc, proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
+                    static_cast<float*>(ws), s);
+  launch_project_bwd(dc, scene->P, scene->P_stride, scene->sh_degree, params, proj, static_cast<const float*>(ws),
+                     grad, s);
+  return check_launch("gs_render_bwd");
+}
+
+gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float* m, float* v, const float* lr_per_row,
+                       float beta1, float beta2, float eps, int64_t step, int zero_grad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_adam_step"));
+  if (scene->P == 0) {
+    set_error("gs_adam_step: no Gaussians (P == 0)");
+    return GS_ERR_EMPTY;
+  }
+  if (!lr_per_row || step < 1 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f)) {
+    set_error("gs_adam_step: invalid hyper-parameters (step=%lld beta1=%g beta2=%g eps=%g)", (long long)step,
+              (double)beta1, (double)beta2, (double)eps);
+    return GS_ERR_ARG;
+  }
+  GS_TRY(check_ptrs("gs_adam_step", {{params, "params"}, {grad, "grad"}, {m, "m"}, {v, "v"}}));
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  launch_adam(rows_of(scene), scene->P_stride, params, grad, m, v, lr_per_row, beta1, beta2, eps, (float)bc1,
+              (float)bc2, zero_grad, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_adam_step");
+}
+
+gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
+                          const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
+                          void* stream) {
+  g_err[0] = 0;
+  if (npix <= 0) {
+    set_error("gs_l1_loss_grad: npix=%lld", (long long)npix);
+    return GS_ERR_ARG;
+  }
+  GS_TRY(check_ptrs("gs_l1_loss_grad", {{rgb, "rgb"}, {depth, "depth"}, {target_rgb, "target_rgb"},
+                                        {target_depth, "target_depth"}, {dL_drgb, "dL_drgb"},
+                                        {dL_ddepth, "dL_ddepth"}}));
+  launch_l1(npix, rgb, depth, target_rgb, target_depth, w_depth, dL_drgb, dL_ddepth, loss,
+            static_cast<cudaStream_t>(stream));
+  return check_launch("gs_l1_loss_grad");
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Internal helpers shared by the libgsr.so translation units (product path only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <utility>
+
+#include "gsr.h"
+
+namespace gsr {
+
+constexpr int kTile = GS_TILE;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Per-view camera constants passed to kernels by value.
+struct DevCam {
+  int W, H, TX, TY;
+  float fx, fy, cx, cy;
+  float R[9], t[3];
+  float z_near;
+  float bg[3];
+  float ocam[3];  // camera centre in world coordinates, -R^T t (SH view direction)
+};
+
+DevCam make_devcam(const gs_camera& c);
+
+// error plumbing (api.cu)
+void set_error(const char* fmt, ...);
+gs_status check_launch(const char* what);
+void count_launch(int n = 1);
+int sm_count();  // SMs of the current device (cached per device)
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// ------------------------------------------------------------------ launchers
+// project.cu
+void launch_project(const DevCam& cam, int64_t P, int64_t P_stride, int deg, const float* params, gs_proj out,
+                    cudaStream_t s);
+void launch_project_bwd(const DevCam& cam, int64_t P, int64_t P_stride, int deg, const float* params,
+                        gs_proj proj, const float* sgrad, float* grad, cudaStream_t s);
+// binning.cu
+size_t bin_workspace_bytes(int64_t P, int64_t key_capacity, int num_tiles);
+gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes,
+                           int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges, int64_t* num_keys_dev,
+                           int64_t* num_keys_host, cudaStream_t s);
+// render.cu
+void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+                       float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
+                       cudaStream_t s);
+void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+                       const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
+                       float* sgrad, cudaStream_t s);
+// optim.cu
+void launch_adam(int64_t F, int64_t P_stride, float* params, float* grad, float* m, float* v, const float* lr,
+                 float beta1, float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s);
+void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
+               float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s);
+
+}  // namespace gsr

@@ -1,0 +1,79 @@
+// K9 adam_step (first-order update; Adam per north_star, R20) and
+// K10 the Eq. 12 L1 harness (R19).  Both are HBM-streaming kernels:
+// 128-bit vector loads/stores, grid-stride loops over a grid of a few waves.
+#include "gsr_internal.cuh"
+
+namespace gsr {
+namespace {
+
+struct LrTable {
+  float step[64];  // lr_row / (1 - beta1^t)
+};
+
+__global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
+                                              float4* __restrict__ v, int64_t n4, int64_t S4, LrTable lr, float b1,
+                                              float b2, float eps, float rs_bc2, int zero_grad) {
+  const float c1 = 1.f - b1, c2 = 1.f - b2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float step = lr.step[i / S4];
+    const float4 gg = g[i];
+    float4 mm = m[i], vv = v[i], pp = p[i];
+#define ADAM_LANE(c)                                              \
+  mm.c = b1 * mm.c + c1 * gg.c;                                  \
+  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
+  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
+    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
+#undef ADAM_LANE
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+    if (zero_grad) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restrict__ rgb, const float* __restrict__ dep,
+                                            const float* __restrict__ trgb, const float* __restrict__ tdep, float sc,
+                                            float sd, float* __restrict__ grgb, float* __restrict__ gdep,
+                                            float* loss) {
+  float L = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npix; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      const int64_t j = ch * npix + i;
+      const float r = rgb[j] - trgb[j];
+      L += fabsf(r) * sc;
+      grgb[j] = r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
+    }
+    const float r = dep[i] - tdep[i];
+    L += fabsf(r) * sd;
+    gdep[i] = r > 0.f ? sd : (r < 0.f ? -sd : 0.f);
+  }
+  if (loss) {
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(kFull, L, o);
+    if ((threadIdx.x & 31) == 0 && L != 0.f) atomicAdd(loss, L);
+  }
+}
+
+}  // namespace
+
+void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
+                 float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s) {
+  LrTable t{};
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
+  const int64_t n4 = F * S / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
+  k_adam<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
+                                           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, S / 4, t,
+                                           beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
+  count_launch();
+}
+
+void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
+               float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s) {
+  const float sc = (float)(1.0 / (3.0 * (double)npix)), sd = (float)((double)w_depth / (double)npix);
+  const int grid = (int)std::min<int64_t>((npix + 255) / 256, (int64_t)sm_count() * 8);
+  k_l1<<<std::max(grid, 1), 256, 0, s>>>(npix, rgb, depth, t_rgb, t_depth, sc, sd, g_rgb, g_depth, loss);
+  count_launch();
+}
+
+}  // namespace gsr

@@ -1,0 +1,187 @@
+"""Thin ctypes binding of libgsr.so (include/gsr.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module only
+turns torch tensors into device pointers and the current torch stream into a
+cudaStream_t.  There is no CPU fallback: if the library is missing or the call
+fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+
+GS_OK, GS_ERR_ARG, GS_ERR_ALIGN, GS_ERR_CAPACITY, GS_ERR_STATE, GS_ERR_EMPTY, GS_ERR_CUDA = 0, -1, -2, -3, -4, -5, -6
+STATUS_NAMES = {0: "GS_OK", -1: "GS_ERR_ARG", -2: "GS_ERR_ALIGN", -3: "GS_ERR_CAPACITY", -4: "GS_ERR_STATE",
+                -5: "GS_ERR_EMPTY", -6: "GS_ERR_CUDA"}
+REC_FLOATS = 12
+SGRAD_FLOATS = 12
+TILE = 16
+FLAG_CULLED = 128
+
+
+class GsError(RuntimeError):
+    def __init__(self, fn, status, msg):
+        super().__init__(f"{fn} -> {STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class GsCamera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32),
+                ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float), ("cy", C.c_float),
+                ("R_cw", C.c_float * 9), ("t_cw", C.c_float * 3),
+                ("z_near", C.c_float), ("bg", C.c_float * 3)]
+
+
+class GsScene(C.Structure):
+    _fields_ = [("P", C.c_int64), ("P_stride", C.c_int64), ("sh_degree", C.c_int32)]
+
+
+class GsProj(C.Structure):
+    _fields_ = [("rec", C.c_void_p), ("radius", C.c_void_p), ("tiles", C.c_void_p), ("flags", C.c_void_p)]
+
+
+def camera(cam) -> GsCamera:
+    """Marshal a scenegen.Camera (or any object with the same fields)."""
+    g = GsCamera()
+    g.width, g.height = int(cam.width), int(cam.height)
+    g.fx, g.fy, g.cx, g.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    R = [float(x) for x in list(getattr(cam.R_cw, "reshape", lambda n: cam.R_cw)(9))]
+    t = [float(x) for x in list(cam.t_cw)]
+    for i in range(9):
+        g.R_cw[i] = R[i]
+    for i in range(3):
+        g.t_cw[i] = t[i]
+        g.bg[i] = float(cam.bg[i])
+    g.z_near = float(cam.z_near)
+    return g
+
+
+def scene_desc(P: int, P_stride: int, sh_degree: int) -> GsScene:
+    return GsScene(int(P), int(P_stride), int(sh_degree))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Library:
+    """One loaded copy of libgsr (fast build) or libgsr_exact (GSR_EXACT_EXP)."""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        self.path = path
+        lib = C.CDLL(path)
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+        lib.gs_version.restype = C.c_int
+        lib.gs_last_error.restype = C.c_char_p
+        lib.gs_launch_count.restype = i64
+        lib.gs_exact_exp.restype = C.c_int
+        lib.gs_project.argtypes = [vp, vp, vp, GsProj, vp]
+        lib.gs_bin_tiles_workspace.argtypes = [vp, i64, i64]
+        lib.gs_bin_tiles_workspace.restype = C.c_size_t
+        lib.gs_bin_tiles.argtypes = [vp, vp, GsProj, vp, C.c_size_t, i64, vp, vp, vp, vp, vp]
+        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_bwd_workspace.argtypes = [vp]
+        lib.gs_render_bwd_workspace.restype = C.c_size_t
+        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+        lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
+        lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
+        for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_adam_step", "gs_l1_loss_grad"):
+            getattr(lib, fn).restype = i32
+        self.lib = lib
+        self.exact = bool(lib.gs_exact_exp())
+
+    # -- diagnostics ------------------------------------------------------
+    def launch_count(self) -> int:
+        return int(self.lib.gs_launch_count())
+
+    def last_error(self) -> str:
+        return self.lib.gs_last_error().decode()
+
+    def _check(self, fn, st, allow=()):
+        if st != GS_OK and st not in allow:
+            raise GsError(fn, st, self.last_error())
+        return st
+
+    # -- the five calls ----------------------------------------------------
+    def project(self, cam: GsCamera, sc: GsScene, params, proj: GsProj, stream=None):
+        return self._check("gs_project", self.lib.gs_project(C.byref(cam), C.byref(sc), _ptr(params), proj,
+                                                             _stream(stream)))
+
+    def bin_tiles_workspace(self, cam: GsCamera, P: int, key_capacity: int) -> int:
+        return int(self.lib.gs_bin_tiles_workspace(C.byref(cam), int(P), int(key_capacity)))
+
+    def bin_tiles(self, cam, sc, proj, ws, key_capacity, sorted_ids, tile_ranges, num_keys_dev=None, sync=False,
+                  stream=None, allow_capacity=False):
+        k_host = C.c_int64(-1)
+        st = self.lib.gs_bin_tiles(C.byref(cam), C.byref(sc), proj, _ptr(ws), ws.numel() * ws.element_size(),
+                                   int(key_capacity), _ptr(sorted_ids), _ptr(tile_ranges), _ptr(num_keys_dev),
+                                   C.byref(k_host) if sync else None, _stream(stream))
+        self._check("gs_bin_tiles", st, allow=(GS_ERR_CAPACITY,) if allow_capacity else ())
+        return (int(k_host.value) if sync else None), st
+
+    def render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
+                   stream=None):
+        return self._check("gs_render_fwd", self.lib.gs_render_fwd(
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(rgb), _ptr(depth),
+            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _stream(stream)))
+
+    def render_bwd_workspace(self, sc: GsScene) -> int:
+        return int(self.lib.gs_render_bwd_workspace(C.byref(sc)))
+
+    def render_bwd(self, cam, sc, params, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, ws,
+                   grad, stream=None):
+        return self._check("gs_render_bwd", self.lib.gs_render_bwd(
+            C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final),
+            _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(ws), ws.numel() * ws.element_size(), _ptr(grad),
+            _stream(stream)))
+
+    def adam_step(self, sc, params, grad, m, v, lr_per_row, step, beta1=0.9, beta2=0.999, eps=1e-15, zero_grad=True,
+                  stream=None):
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        return self._check("gs_adam_step", self.lib.gs_adam_step(
+            C.byref(sc), _ptr(params), _ptr(grad), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
+            1 if zero_grad else 0, _stream(stream)))
+
+    def l1_loss_grad(self, rgb, depth, t_rgb, t_depth, w_depth, g_rgb, g_depth, loss=None, stream=None):
+        return self._check("gs_l1_loss_grad", self.lib.gs_l1_loss_grad(
+            int(depth.numel()), _ptr(rgb), _ptr(depth), _ptr(t_rgb), _ptr(t_depth), float(w_depth), _ptr(g_rgb),
+            _ptr(g_depth), _ptr(loss), _stream(stream)))
+
+
+_LIBS = {}
+
+
+def load(exact: bool = False) -> Library:
+    name = "libgsr_exact.so" if exact else "libgsr.so"
+    if name not in _LIBS:
+        _LIBS[name] = Library(os.path.join(PKG, name))
+    return _LIBS[name]
+
+
+def make_proj(P: int, device) -> tuple:
+    """Allocate projection buffers for P Gaussians; returns (GsProj, dict of tensors)."""
+    t = {
+        "rec": torch.empty((max(P, 1), REC_FLOATS), dtype=torch.float32, device=device),
+        "radius": torch.empty(max(P, 1), dtype=torch.int32, device=device),
+        "tiles": torch.empty(max(P, 1), dtype=torch.int32, device=device),
+        "flags": torch.empty(max(P, 1) + 16, dtype=torch.uint8, device=device),
+    }
+    proj = GsProj(t["rec"].data_ptr(), t["radius"].data_ptr(), t["tiles"].data_ptr(), t["flags"].data_ptr())
+    proj._tensors = t  # the struct holds raw pointers: keep the storage alive as long as the struct
+    return proj, t

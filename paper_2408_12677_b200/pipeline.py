@@ -1,0 +1,160 @@
+"""Host orchestration of one optimisation iteration through the C ABI.
+
+This is the user-facing API: it owns the device buffers (torch tensors) and
+issues the ABI calls in the order of SURVEY.md CS2/CS3 -- per view
+gs_project -> gs_bin_tiles -> gs_render_fwd -> gs_l1_loss_grad -> gs_render_bwd,
+then (optionally) a gradient all-reduce across ranks and gs_adam_step.  No
+arithmetic of the method happens here.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import gsr
+
+# Per-row learning rates (reading R20; SPEC.md:436 defaults)
+LR_MEAN, LR_LOGSCALE, LR_QUAT, LR_OPACITY, LR_SH = 2e-4, 5e-3, 1e-3, 5e-2, 2.5e-3
+
+
+def lr_per_row(sh_degree: int):
+    F = 11 + 3 * (sh_degree + 1) ** 2
+    return [LR_MEAN] * 3 + [LR_LOGSCALE] * 3 + [LR_QUAT] * 4 + [LR_OPACITY] + [LR_SH] * (F - 11)
+
+
+class GaussianModel:
+    """Parameters, gradient and Adam moments, each float32 [F][P_stride] on one device."""
+
+    def __init__(self, scene, device, params=None):
+        self.P, self.sh_degree = int(scene.P), int(scene.sh_degree)
+        self.F, self.P_stride = int(scene.params.shape[0]), int(scene.params.shape[1])
+        self.params = params if params is not None else torch.from_numpy(scene.params).to(device)
+        self.grad = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step_count = 0
+        self.lr = lr_per_row(self.sh_degree)
+        self.desc = gsr.scene_desc(self.P, self.P_stride, self.sh_degree)
+
+    @property
+    def nbytes(self):
+        return 4 * self.params.numel()
+
+
+class ViewBuffers:
+    """Device buffers for one view in flight (reused across views of equal size)."""
+
+    def __init__(self, lib: gsr.Library, cam, P: int, key_capacity: int, device):
+        self.lib = lib
+        self.W, self.H = int(cam.width), int(cam.height)
+        self.NT = ((self.W + 15) // 16) * ((self.H + 15) // 16)
+        self.key_capacity = int(key_capacity)
+        self.proj, self.proj_t = gsr.make_proj(P, device)
+        gcam = gsr.camera(cam)
+        self.bin_ws = torch.empty(lib.bin_tiles_workspace(gcam, P, key_capacity) // 4 + 4, dtype=torch.int32,
+                                  device=device)
+        self.sorted_ids = torch.empty(max(key_capacity, 1), dtype=torch.int32, device=device)
+        self.ranges = torch.empty((self.NT, 2), dtype=torch.int32, device=device)
+        npx = self.W * self.H
+        self.rgb = torch.empty((3, self.H, self.W), dtype=torch.float32, device=device)
+        self.depth = torch.empty((self.H, self.W), dtype=torch.float32, device=device)
+        self.T = torch.empty((self.H, self.W), dtype=torch.float32, device=device)
+        self.n = torch.empty((self.H, self.W), dtype=torch.int32, device=device)
+        self.g_rgb = torch.empty((3, self.H, self.W), dtype=torch.float32, device=device)
+        self.g_depth = torch.empty((self.H, self.W), dtype=torch.float32, device=device)
+        sgrad_bytes = lib.render_bwd_workspace(gsr.scene_desc(P, P, 0))
+        self.bwd_ws = torch.empty(max(sgrad_bytes // 4, 4), dtype=torch.float32, device=device)
+        assert npx > 0
+
+
+def render(lib, model: GaussianModel, cam, buf: ViewBuffers, num_keys_dev=None, blended=None, sync_keys=False):
+    """gs_project -> gs_bin_tiles -> gs_render_fwd for one view.  Returns K if sync_keys."""
+    gcam = gsr.camera(cam)
+    lib.project(gcam, model.desc, model.params, buf.proj)
+    K, _ = lib.bin_tiles(gcam, model.desc, buf.proj, buf.bin_ws, buf.key_capacity, buf.sorted_ids, buf.ranges,
+                         num_keys_dev=num_keys_dev, sync=sync_keys, allow_capacity=sync_keys)
+    lib.render_fwd(gcam, model.desc, buf.proj, buf.sorted_ids, buf.ranges, buf.rgb, buf.depth, buf.T, buf.n,
+                   blended=blended)
+    return K
+
+
+def measure_keys(lib, model: GaussianModel, cameras, device) -> int:
+    """Exact max K over the views (synchronous, setup only)."""
+    best = 0
+    P = model.P
+    cap = 1 << 20
+    buf = None
+    for cam in cameras:
+        while True:
+            if buf is None or buf.key_capacity < cap or (buf.W, buf.H) != (cam.width, cam.height):
+                buf = ViewBuffers(lib, cam, P, cap, device)
+            K = render(lib, model, cam, buf, sync_keys=True)
+            if K <= cap:
+                break
+            cap = int(K * 1.25) + 1024
+        best = max(best, K)
+    return best
+
+
+class Trainer:
+    """fwd + bwd + Adam over a batch of views.
+
+    ``allreduce`` (optional) is called on the gradient tensor between the last
+    view's backward and the Adam step -- the one exchange of the data-parallel
+    path (NCCL all-reduce over NVLink in bench.py)."""
+
+    def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
+                 w_depth: float = 1.0, allreduce=None):
+        self.lib, self.model, self.cameras, self.targets = lib, model, cameras, targets
+        self.device, self.w_depth, self.allreduce = device, w_depth, allreduce
+        self.buf = ViewBuffers(lib, cameras[0], model.P, key_capacity, device)
+        self.num_keys = torch.zeros(len(cameras), dtype=torch.int64, device=device)
+        self.blended = torch.zeros(1, dtype=torch.int64, device=device)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=device)
+
+    def view_fwd_bwd(self, v: int, t_rgb=None, t_depth=None):
+        lib, m, b, cam = self.lib, self.model, self.buf, self.cameras[v]
+        if t_rgb is None:
+            t_rgb, t_depth = self.targets[v]
+        render(lib, m, cam, b, num_keys_dev=self.num_keys[v:v + 1], blended=self.blended)
+        lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
+        lib.render_bwd(gsr.camera(cam), m.desc, m.params, b.proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb,
+                       b.g_depth, b.bwd_ws, m.grad)
+
+    def step(self, views, targets_override=None):
+        """One iteration over ``views``; targets_override: {v: (rgb, depth)} device tensors."""
+        for v in views:
+            if targets_override is not None:
+                self.view_fwd_bwd(v, *targets_override[v])
+            else:
+                self.view_fwd_bwd(v)
+        if self.allreduce is not None:
+            self.allreduce(self.model.grad)
+        m = self.model
+        m.step_count += 1
+        self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=True)
+
+    def check_capacity(self) -> int:
+        """Max K seen since construction (host sync); raises if any view overflowed."""
+        k = int(self.num_keys.max().item())
+        if k > self.buf.key_capacity:
+            raise gsr.GsError("gs_bin_tiles", gsr.GS_ERR_CAPACITY, f"K={k} > capacity {self.buf.key_capacity}")
+        return k
+
+
+def render_targets(lib, target_model: GaussianModel, cameras, device, key_capacity: int):
+    """Target images per view, rendered through the same kernels (setup, untimed)."""
+    buf = ViewBuffers(lib, cameras[0], target_model.P, key_capacity, device)
+    out = []
+    for cam in cameras:
+        K = render(lib, target_model, cam, buf, sync_keys=True)
+        if K > key_capacity:
+            buf = ViewBuffers(lib, cam, target_model.P, int(K * 1.25), device)
+            render(lib, target_model, cam, buf, sync_keys=True)
+        out.append((buf.rgb.clone(), buf.depth.clone()))
+    return out
+
+
+def default_capacity(K: int) -> int:
+    return int(math.ceil(K * 1.3)) + 4096

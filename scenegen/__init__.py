@@ -214,6 +214,8 @@ def camera_from_forward(width, height, f, cx, cy, position, forward, z_near=0.2)
     fwd = fwd / np.linalg.norm(fwd)
     up = np.array([0.0, 0.0, 1.0])
     right = np.cross(fwd, up)
+    if np.linalg.norm(right) < 1e-9:
+        raise ValueError("forward direction parallel to the world up axis")
     right /= np.linalg.norm(right)
     down = np.cross(fwd, right)
     R_wc = np.stack([right, down, fwd], axis=1)  # columns: camera axes in world
@@ -221,6 +223,17 @@ def camera_from_forward(width, height, f, cx, cy, position, forward, z_near=0.2)
     t_cw = -R_cw @ np.asarray(position, dtype=np.float64)
     return Camera(width, height, float(f), float(f), float(cx), float(cy),
                   R_cw.astype(np.float32), t_cw.astype(np.float32), z_near)
+
+
+def camera_rt(width, height, f, cx, cy, R_cw, t_cw, z_near=0.2):
+    return Camera(width, height, float(f), float(f), float(cx), float(cy),
+                  np.asarray(R_cw, dtype=np.float32).reshape(3, 3), np.asarray(t_cw, dtype=np.float32).reshape(3),
+                  z_near)
+
+
+def rot_y(theta):
+    c, s = math.cos(theta), math.sin(theta)
+    return np.array([[c, 0.0, s], [0.0, 1.0, 0.0], [-s, 0.0, c]])
 
 
 def identity_camera(width, height, f, cx, cy, z_near=0.2):

@@ -1,0 +1,416 @@
+"""GPU-vs-oracle parity through the C ABI (-m gpu).
+
+Stage-wise parity is binding (SURVEY.md §8(c) parity policy): each GPU call is
+fed the ORACLE's outputs of the previous stage on identical seeded inputs.
+  gs_project    bit-exact radius, tiles, rect, mu, z, conic, opacity; colour 1e-6
+  gs_bin_tiles  bit-exact sorted ids, tile ranges, K
+  gs_render_fwd 1e-5 absolute rgb/depth, exact n_contrib, except proven threshold
+                flips (oracle decision margin < 1e-5 relative); the GSR_EXACT_EXP
+                build is bit-identical
+  gs_render_bwd rel < 1e-3 or abs < 1e-6 per gradient element against the MIXED
+                oracle (fp32 decisions, fp64 values); pixels with a proven flip
+                have their upstream gradient zeroed on both sides
+  gs_adam_step  1e-6 relative
+Full-size configs are checked on sampled pixels / sampled upstream gradients.
+"""
+import numpy as np
+import pytest
+import torch
+
+import scenegen
+from oracle import gsref
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2408_12677_b200 import gsr, pipeline
+    from gpu_helpers import (DEV, gpu_bin, gpu_bwd, gpu_project, gpu_render, grad_mismatch, proj_from_oracle)
+
+FLIP_MARGIN = 1e-5
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return gsr.load()
+
+
+@pytest.fixture(scope="module")
+def lib_exact():
+    return gsr.load(exact=True)
+
+
+_WL = {}
+
+
+def workload(name):
+    if name not in _WL:
+        kw = {}
+        if name == "replica":
+            kw = {"num_views": 2}
+        if name == "large":
+            kw = {"num_views": 2}
+        _WL[name] = scenegen.make(name, **kw)
+    return _WL[name]
+
+
+def test_libraries_load(lib, lib_exact):
+    assert not lib.exact and lib_exact.exact
+    assert lib.lib.gs_version() == 1
+
+
+# ----------------------------------------------------------------------------- gs_project
+@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp"])
+def test_project_bitexact(lib, name):
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    ref = gsref.project(cam, scene, gsref.F32)
+    proj, t, _ = gpu_project(lib, cam, scene)
+    P = scene.P
+    radius = t["radius"][:P].cpu().numpy()
+    tiles = t["tiles"][:P].cpu().numpy()
+    flags = t["flags"][:P].cpu().numpy()
+    np.testing.assert_array_equal(radius, ref["radius"])
+    np.testing.assert_array_equal(tiles, ref["tiles"])
+    vis = ref["radius"] > 0
+    assert vis.sum() > 0
+    np.testing.assert_array_equal(flags & 0xF8, ref["flags"] & 0xF8)  # cull + J clamps exact
+    rec = t["rec"][:P].cpu().numpy()
+    for k, nm in enumerate(["mu_x", "mu_y", "z", "opacity", "conic_A", "conic_B", "conic_C"]):
+        np.testing.assert_array_equal(rec[vis, k], ref[nm][vis].astype(np.float32), err_msg=nm)
+    rx = rec[vis, 10].view(np.uint32)
+    ry = rec[vis, 11].view(np.uint32)
+    np.testing.assert_array_equal(rx & 0xFFFF, ref["rect"][0][vis])
+    np.testing.assert_array_equal(rx >> 16, ref["rect"][1][vis])
+    np.testing.assert_array_equal(ry & 0xFFFF, ref["rect"][2][vis])
+    np.testing.assert_array_equal(ry >> 16, ref["rect"][3][vis])
+    for k, nm in zip((7, 8, 9), "rgb"):
+        np.testing.assert_allclose(rec[vis, k], ref[nm][vis], atol=1e-6, rtol=0, err_msg=nm)
+    # colour clamp flags exact except where the unclamped value is within 1e-6 of 0
+    diff = (flags ^ ref["flags"]) & 0x7
+    assert np.all(diff[~vis] == 0)
+    for ch, nm in enumerate("rgb"):
+        d = ((diff >> ch) & 1).astype(bool) & vis
+        assert np.all(np.abs(ref[nm][d]) <= 1e-6)
+
+
+# ----------------------------------------------------------------------------- gs_bin_tiles
+@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp"])
+def test_bin_bitexact_stagewise(lib, name):
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    pr = gsref.project(cam, scene, gsref.F32)
+    ref = gsref.bin_tiles(cam, scene)
+    proj, _ = proj_from_oracle(pr)
+    out = gpu_bin(lib, cam, scene, proj)
+    K = out["K"]
+    assert K == ref["K"] == out["K_dev"]
+    np.testing.assert_array_equal(out["sorted_ids"][:K].cpu().numpy(), ref["sorted_ids"])
+    np.testing.assert_array_equal(out["ranges"].cpu().numpy(), ref["tile_ranges"])
+
+
+def test_bin_depth_ties_and_one_pass_tile_sort(lib):
+    """Equal depths fall back to the index (R12); <= 256 tiles use one radix pass."""
+    scene, cam = scenegen.random_small_scene(4, 300, 1, width=96, height=80, f=80.0)
+    scene.params[2, :150] = scene.params[2, 0]  # 150 exactly-equal depths
+    proj, _, _ = gpu_project(lib, cam, scene)
+    out = gpu_bin(lib, cam, scene, proj)
+    ref = gsref.bin_tiles(cam, scene)
+    assert out["K"] == ref["K"]
+    np.testing.assert_array_equal(out["sorted_ids"][:out["K"]].cpu().numpy(), ref["sorted_ids"])
+
+
+def test_bin_capacity_overflow(lib):
+    w = workload("small")
+    cam, scene = w.cameras[0], w.scene
+    proj, _, _ = gpu_project(lib, cam, scene)
+    K_true = int(gsref.project(cam, scene)["tiles"].sum())
+    out = gpu_bin(lib, cam, scene, proj, capacity=K_true - 1, sync=True)
+    assert out["status"] == gsr.GS_ERR_CAPACITY and out["K"] == K_true
+    r = out["ranges"].cpu().numpy()
+    assert np.all(r[:, 1] - r[:, 0] == 0)  # every tile empty -> background only
+    out = gpu_bin(lib, cam, scene, proj, capacity=K_true - 1, sync=False)  # async mode reports K on device
+    assert out["K_dev"] == K_true and out["status"] == gsr.GS_OK
+    out = gpu_bin(lib, cam, scene, proj, capacity=K_true, sync=True)
+    assert out["status"] == gsr.GS_OK and out["K"] == K_true
+
+
+# ----------------------------------------------------------------------------- gs_render_fwd
+def _fwd_stagewise(lib, cam, scene):
+    pr = gsref.project(cam, scene, gsref.F32)
+    b = gsref.bin_tiles(cam, scene)
+    proj, _ = proj_from_oracle(pr)
+    ids = torch.from_numpy(np.ascontiguousarray(b["sorted_ids"])).to(DEV) if b["K"] else torch.zeros(1, dtype=torch.int32, device=DEV)
+    ranges = torch.from_numpy(b["tile_ranges"]).to(DEV)
+    return proj, ids, ranges, gpu_render(lib, cam, scene, proj, ids, ranges)
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_render_fwd_exact_build_bitexact(lib_exact, name):
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    ref = gsref.render_fwd(cam, scene, gsref.F32)
+    _, _, _, out = _fwd_stagewise(lib_exact, cam, scene)
+    np.testing.assert_array_equal(out["rgb"].cpu().numpy(), ref["rgb"].astype(np.float32))
+    np.testing.assert_array_equal(out["depth"].cpu().numpy(), ref["depth"].astype(np.float32))
+    np.testing.assert_array_equal(out["T_final"].cpu().numpy(), ref["T_final"].astype(np.float32))
+    np.testing.assert_array_equal(out["n_contrib"].cpu().numpy(), ref["n_contrib"])
+    assert out["blended"] == ref["blended"]
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_render_fwd_parity_with_flip_accounting(lib, name):
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    _, _, _, out = _fwd_stagewise(lib, cam, scene)
+    rgb = out["rgb"].cpu().numpy()
+    dep = out["depth"].cpu().numpy()
+    n = out["n_contrib"].cpu().numpy()
+    bad = (np.abs(rgb - ref["rgb"]).max(0) > 1e-5) | (np.abs(dep - ref["depth"]) > 1e-5) | (n != ref["n_contrib"])
+    flips = bad & (ref["margin"] < FLIP_MARGIN)
+    unexplained = bad & ~flips
+    assert unexplained.sum() == 0, f"{int(unexplained.sum())} pixels off without a threshold flip"
+    assert flips.sum() <= max(2, 1e-4 * bad.size)
+    T = out["T_final"].cpu().numpy()
+    assert T.min() >= 1e-4 and T.max() <= 1.0  # R16 invariant on the GPU path
+
+
+@pytest.mark.parametrize("name", ["replica", "scannetpp"])
+def test_render_fwd_sampled_full_size(lib, name):
+    """Full-size config, GPU chain project -> bin -> fwd (the bench launch), checked
+    on 3000 sampled pixels (random + two complete tiles + the ragged last row/col)."""
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    proj, _, _ = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+    rng = np.random.default_rng(0)
+    px = list(rng.integers(0, cam.width, 2000))
+    py = list(rng.integers(0, cam.height, 2000))
+    for tx, ty in ((cam.tiles_x // 2, cam.tiles_y // 2), (cam.tiles_x - 1, cam.tiles_y - 1)):
+        for j in range(16):
+            for i in range(16):
+                x, y = tx * 16 + i, ty * 16 + j
+                if x < cam.width and y < cam.height:
+                    px.append(x)
+                    py.append(y)
+    px, py = np.array(px), np.array(py)
+    ref = gsref.render_pixels(cam, scene, px, py, gsref.F32)
+    rgb = out["rgb"].cpu().numpy()[:, py, px]
+    dep = out["depth"].cpu().numpy()[py, px]
+    n = out["n_contrib"].cpu().numpy()[py, px]
+    # depth is unnormalised (z * alpha * T sums up to ~10 m): 1e-5 absolute on rgb, 1e-5 relative on depth
+    bad = (np.abs(rgb - ref["rgb"]).max(0) > 1e-5) | (np.abs(dep - ref["depth"]) > 1e-5 * np.maximum(1.0, np.abs(ref["depth"]))) | (n != ref["n_contrib"])
+    unexplained = bad & ~(ref["margin"] < FLIP_MARGIN)
+    assert unexplained.sum() == 0, f"{int(unexplained.sum())} sampled pixels off without a flip"
+
+
+# ----------------------------------------------------------------------------- gs_render_bwd
+def _bwd_stagewise(lib, cam, scene, seed=1, sample_mask=None):
+    pr = gsref.project(cam, scene, gsref.F32)
+    b = gsref.bin_tiles(cam, scene)
+    f = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    g_rgb, g_d = scenegen.upstream_fields(seed, cam.width, cam.height)
+    flips = f["margin"] < FLIP_MARGIN
+    keep = ~flips if sample_mask is None else (~flips & sample_mask)
+    g_rgb = (g_rgb * keep[None]).astype(np.float32)
+    g_d = (g_d * keep).astype(np.float32)
+    proj, _ = proj_from_oracle(pr)
+    ids = torch.from_numpy(np.ascontiguousarray(b["sorted_ids"])).to(DEV)
+    ranges = torch.from_numpy(b["tile_ranges"]).to(DEV)
+    T = torch.from_numpy(f["T_final"].astype(np.float32)).to(DEV)
+    n = torch.from_numpy(f["n_contrib"]).to(DEV)
+    params = torch.from_numpy(scene.params).to(DEV)
+    g, ws = gpu_bwd(lib, cam, scene, params, proj, ids, ranges, T, n, g_rgb, g_d)
+    ref, screen = gsref.render_bwd(cam, scene, g_rgb, g_d, mode=gsref.MIXED)
+    return g, ref, ws, screen
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_render_bwd_parity_stagewise(lib, name):
+    w = workload(name)
+    g, ref, ws, screen = _bwd_stagewise(lib, w.cameras[0], w.scene)
+    bad = grad_mismatch(g, ref)
+    frac = bad.mean()
+    worst = np.argsort(-(np.abs(g - ref) / (np.abs(ref) + 1e-6)).ravel())[:5]
+    assert frac <= 1e-3, f"{int(bad.sum())}/{bad.size} gradient elements outside tolerance; worst {[(g.ravel()[k], ref.ravel()[k]) for k in worst]}"
+
+
+@pytest.mark.parametrize("name", ["replica", "scannetpp"])
+def test_render_bwd_sampled_full_size(lib, name):
+    """Full-size view with upstream gradient on a sampled set of 64 tiles."""
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    rng = np.random.default_rng(3)
+    mask = np.zeros((cam.height, cam.width), bool)
+    for t in rng.choice(cam.num_tiles, 64, replace=False):
+        ty, tx = divmod(int(t), cam.tiles_x)
+        mask[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
+    g, ref, _, _ = _bwd_stagewise(lib, cam, scene, sample_mask=mask)
+    bad = grad_mismatch(g, ref)
+    assert bad.mean() <= 1e-3, f"{int(bad.sum())}/{bad.size} gradient elements outside tolerance"
+
+
+# ----------------------------------------------------------------------------- end-to-end chain
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_chain_end_to_end(lib, name):
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    rgb = out["rgb"].cpu().numpy()
+    bad = np.abs(rgb - ref["rgb"]).max(0) > 1e-5
+    assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
+    assert abs(out["blended"] - ref["blended"]) <= 4 * (ref["margin"] < FLIP_MARGIN).sum()
+    g_rgb, g_d = scenegen.upstream_fields(2, cam.width, cam.height)
+    keep = ~(ref["margin"] < FLIP_MARGIN)
+    g_rgb = (g_rgb * keep[None]).astype(np.float32)
+    g_d = (g_d * keep).astype(np.float32)
+    g, _ = gpu_bwd(lib, cam, scene, params, proj, b["sorted_ids"], b["ranges"], out["T_final"], out["n_contrib"],
+                   g_rgb, g_d)
+    gref, _ = gsref.render_bwd(cam, scene, g_rgb, g_d, mode=gsref.MIXED)
+    assert grad_mismatch(g, gref).mean() <= 1e-3
+
+
+# ----------------------------------------------------------------------------- Adam / L1
+def test_adam_parity(lib):
+    rng = np.random.default_rng(0)
+    P, deg = 1000, 3
+    F = 11 + 3 * 16
+    S = scenegen.pad4(P)
+    sc = gsr.scene_desc(P, S, deg)
+    p = rng.normal(size=(F, S)).astype(np.float32)
+    m = (rng.normal(size=(F, S)) * 1e-2).astype(np.float32)
+    v = (rng.uniform(0, 1e-3, size=(F, S))).astype(np.float32)
+    g = rng.normal(size=(F, S)).astype(np.float32)
+    lr = pipeline.lr_per_row(deg)
+    tp, tm, tv, tg = (torch.from_numpy(a).to(DEV) for a in (p, m, v, g))
+    lib.adam_step(sc, tp, tg, tm, tv, lr, 7, zero_grad=True)
+    torch.cuda.synchronize()
+    rp, rm, rv = gsref.adam_step(p, g, m, v, np.array(lr, np.float32), 7, P=S)
+    # 1e-6 relative to the magnitude of the terms each fp32 update combines (m and v
+    # are differences of two products and can cancel; p moves by ~lr per step)
+    b1, b2 = 0.9, 0.999
+    sm = b1 * np.abs(m) + (1 - b1) * np.abs(g)
+    sv = b2 * np.abs(v) + (1 - b2) * g * g
+    lr_col = np.array(lr, np.float64)[:, None]
+    assert np.all(np.abs(tm.cpu().numpy() - rm) <= 1e-6 * sm + 1e-12)
+    assert np.all(np.abs(tv.cpu().numpy() - rv) <= 1e-6 * sv + 1e-15)
+    assert np.all(np.abs(tp.cpu().numpy() - rp) <= 1e-6 * (np.abs(p) + lr_col))
+    assert torch.count_nonzero(tg) == 0
+
+
+def test_l1_parity(lib):
+    rng = np.random.default_rng(1)
+    H, W = 37, 29
+    rgb, trgb = rng.uniform(size=(2, 3, H, W)).astype(np.float32)
+    d, td = rng.uniform(1, 5, size=(2, H, W)).astype(np.float32)
+    trgb[0, 0, 0] = rgb[0, 0, 0]
+    t = [torch.from_numpy(a).to(DEV) for a in (rgb, d, trgb, td)]
+    g1 = torch.empty_like(t[0])
+    g2 = torch.empty_like(t[1])
+    loss = torch.zeros(1, device=DEV)
+    lib.l1_loss_grad(t[0], t[1], t[2], t[3], 0.5, g1, g2, loss)
+    L, r1, r2 = gsref.l1_loss_grad(rgb.astype(np.float64), d.astype(np.float64), trgb, td, 0.5)
+    assert loss.item() == pytest.approx(L, rel=1e-5)
+    np.testing.assert_allclose(g1.cpu().numpy(), r1, rtol=1e-6)
+    np.testing.assert_allclose(g2.cpu().numpy(), r2, rtol=1e-6)
+
+
+# ----------------------------------------------------------------------------- edge cases
+def test_empty_scene(lib):
+    cam = scenegen.identity_camera(40, 24, 30.0, 19.5, 11.5)
+    cam.bg = (0.25, 0.5, 0.75)
+    scene = scenegen.Scene(0, 0, np.zeros((14, 0), np.float32))
+    proj, t = gsr.make_proj(0, DEV)
+    sc = gsr.scene_desc(0, 0, 0)
+    params = torch.zeros(4, device=DEV)
+    lib.project(gsr.camera(cam), sc, params, proj)
+    out = gpu_bin(lib, cam, scene, proj, capacity=16)
+    assert out["K"] == 0
+    r = gpu_render(lib, cam, scene, proj, out["sorted_ids"], out["ranges"])
+    assert torch.all(r["rgb"][0] == 0.25) and torch.all(r["rgb"][2] == 0.75) and torch.all(r["T_final"] == 1)
+    with pytest.raises(gsr.GsError) as e:
+        lib.adam_step(sc, params, params, params, params, [1e-3] * 14, 1)
+    assert e.value.status == gsr.GS_ERR_EMPTY
+
+
+def test_all_culled(lib):
+    w = scenegen.make("tiny")
+    scene = scenegen.Scene(w.scene.P, 0, w.scene.params.copy())
+    scene.params[2, :scene.P] = -3.0  # everything behind the camera
+    proj, t, params = gpu_project(lib, w.cameras[0], scene)
+    assert int(t["radius"][:scene.P].abs().sum()) == 0
+    out = gpu_bin(lib, w.cameras[0], scene, proj, capacity=64)
+    assert out["K"] == 0
+    g, _ = gpu_bwd(lib, w.cameras[0], scene, params, proj, out["sorted_ids"], out["ranges"],
+                   torch.ones((48, 64), device=DEV), torch.zeros((48, 64), dtype=torch.int32, device=DEV),
+                   np.ones((3, 48, 64), np.float32), np.ones((48, 64), np.float32))
+    assert np.all(g == 0)
+
+
+@pytest.mark.parametrize("wh", [(37, 29), (16, 16), (17, 1), (1000, 8)])
+def test_ragged_images(lib, wh):
+    W, H = wh
+    scene, cam = scenegen.random_small_scene(7, 60, 1, width=W, height=H, f=0.8 * max(W, H))
+    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    proj, _, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+    bad = np.abs(out["rgb"].cpu().numpy() - ref["rgb"]).max(0) > 1e-5
+    assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
+
+
+def test_single_gaussian_peak_closed_form(lib):
+    """Isotropic on-axis Gaussian: C(cx, cy) = c a0 + (1 - a0) bg, D = z a0, T = 1 - a0."""
+    cam = scenegen.identity_camera(64, 48, 60.0, 32.0, 24.0)
+    cam.bg = (0.1, 0.2, 0.3)
+    c = np.array([0.9, 0.4, 0.05])
+    sh = np.zeros((1, 1, 3))
+    sh[0, 0] = (c - 0.5) / 0.28209479177387814
+    sc = scenegen.scene_from_gaussians([[0, 0, 3.0]], np.log([[0.05] * 3]), [[1, 0, 0, 0]], [0.0], sh, 0)
+    proj, t, _ = gpu_project(lib, cam, sc)
+    assert int(t["radius"][0]) == 4 and int(t["tiles"][0]) == 2
+    b = gpu_bin(lib, cam, sc, proj)
+    out = gpu_render(lib, cam, sc, proj, b["sorted_ids"], b["ranges"])
+    np.testing.assert_allclose(out["rgb"][:, 24, 32].cpu().numpy(), c * 0.5 + 0.5 * np.array(cam.bg), atol=1e-6)
+    assert out["depth"][24, 32].item() == pytest.approx(1.5, abs=1e-6)
+    assert out["T_final"][24, 32].item() == pytest.approx(0.5, abs=1e-6)
+    assert out["blended"] == 37  # footprint closed form (tests/golden/closed_forms.json)
+
+
+def test_huge_footprint(lib):
+    """A near-camera Gaussian whose footprint covers every tile (> 256 tiles: 2-pass tile sort)."""
+    cam = scenegen.identity_camera(320, 240, 300.0, 160.0, 120.0)
+    sh = np.zeros((2, 1, 3))
+    sh[0, 0] = (np.array([0.9, 0.4, 0.05]) - 0.5) / 0.28209479177387814
+    sh[1, 0] = (np.array([0.2, 0.2, 0.2]) - 0.5) / 0.28209479177387814
+    sc = scenegen.scene_from_gaussians([[0, 0, 3.0], [0.0, 0.0, 0.5]], np.log([[0.02] * 3, [2.0] * 3]),
+                                       [[1, 0, 0, 0]] * 2, [0.0, -4.0], sh, 0)
+    proj, t, params = gpu_project(lib, cam, sc)
+    assert int(t["tiles"][1]) == cam.num_tiles
+    b = gpu_bin(lib, cam, sc, proj)
+    ref_b = gsref.bin_tiles(cam, sc)
+    np.testing.assert_array_equal(b["sorted_ids"][:b["K"]].cpu().numpy(), ref_b["sorted_ids"])
+    out = gpu_render(lib, cam, sc, proj, b["sorted_ids"], b["ranges"])
+    ref = gsref.render_fwd(cam, sc, gsref.F32)
+    np.testing.assert_allclose(out["rgb"].cpu().numpy(), ref["rgb"], atol=1e-5)
+
+
+def test_trainer_step_runs_and_decreases_loss(lib):
+    w = workload("small")
+    model = pipeline.GaussianModel(w.scene, DEV)
+    tgt_model = pipeline.GaussianModel(w.target_scene, DEV)
+    K = pipeline.measure_keys(lib, model, w.cameras, DEV)
+    cap = pipeline.default_capacity(K)
+    targets = pipeline.render_targets(lib, tgt_model, w.cameras, DEV, cap)
+    tr = pipeline.Trainer(lib, model, w.cameras, targets, DEV, cap)
+    losses = []
+    for _ in range(20):
+        tr.loss.zero_()
+        tr.step([0])
+        losses.append(tr.loss.item())
+    tr.check_capacity()
+    assert losses[-1] < losses[0]
