@@ -204,45 +204,40 @@ def main():
         clocks.start()
     tr.blended.zero_()
     tr.num_keys.zero_()
-    fwd_ev, bwd_ev = [], []
+    stage_ev = {"render_fwd": [], "render_bwd": [], "project_bwd": []}
+    open_ev = {}
+
+    def hooks(stage, what):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        if what == "begin":
+            open_ev[stage] = ev
+        else:
+            stage_ev[stage].append((open_ev.pop(stage), ev))
+
     l0 = lib.launch_count()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tr.hooks = hooks
     e0.record(stream)
+    if args.profile:
+        torch.cuda.nvtx.range_push("timed")
     for _ in range(args.steps):
-        for v in my_views:
-            b, cam, m = tr.buf, cams[v], model
-            gcam = gsr.camera(cam)
-            lib.project(gcam, m.desc, m.params, b.proj)
-            lib.bin_tiles(gcam, m.desc, b.proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
-                          num_keys_dev=tr.num_keys[v:v + 1])
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            lib.render_fwd(gcam, m.desc, b.proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=tr.blended)
-            a1.record(stream)
-            lib.l1_loss_grad(b.rgb, b.depth, targets[v][0], targets[v][1], tr.w_depth, b.g_rgb, b.g_depth, tr.loss)
-            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            c0.record(stream)
-            lib.render_bwd(gcam, m.desc, m.params, b.proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
-                           b.bwd_ws, m.grad)
-            c1.record(stream)
-            fwd_ev.append((a0, a1))
-            bwd_ev.append((c0, c1))
-        if allreduce is not None:
-            allreduce(model.grad)
-        model.step_count += 1
-        lib.adam_step(model.desc, model.params, model.grad, model.m, model.v, model.lr, model.step_count)
+        tr.step(my_views)
     e1.record(stream)
+    if args.profile:
+        torch.cuda.nvtx.range_pop()
+    tr.hooks = None
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = lib.launch_count() - l0
     clk = clocks.stop() if not args.profile else None
     ms = e0.elapsed_time(e1)
-    fwd_ms = sum(a.elapsed_time(b) for a, b in fwd_ev) / max(len(fwd_ev), 1)
-    bwd_ms = sum(a.elapsed_time(b) for a, b in bwd_ev) / max(len(bwd_ev), 1)
+    stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(v), 1) for k, v in stage_ev.items()}
+    fwd_ms, bwd_ms = stage_ms["render_fwd"], stage_ms["render_bwd"]
     kmax = int(tr.num_keys.max().item())
     if kmax > cap:
         raise RuntimeError(f"key capacity overflow during the timed region: K={kmax} > {cap}")
@@ -304,7 +299,17 @@ def main():
     except OSError:
         pass
     n_views = len(my_views) * args.steps
-    roof = roofline(dev, peaks, clk, fwd_ms, bwd_ms, blended / max(world, 1) / n_views)
+    # evaluated pairs of the backward = sum of n_contrib over the views (untimed re-render)
+    evaluated = 0
+    for v in my_views:
+        pipeline.render(lib, model, cams[v], tr.buf)
+        evaluated += int(tr.buf.n.sum().item())
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get("k_render_bwd")
+    except (OSError, ValueError):
+        pass
+    roof = roofline(dev, peaks, clk, stage_ms, blended / max(world, 1) / n_views, evaluated / len(my_views), traffic)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -330,7 +335,7 @@ def main():
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),
-        "stage_ms": {"render_fwd": fwd_ms, "render_bwd": bwd_ms},
+        "stage_ms": stage_ms,
         "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
@@ -338,18 +343,22 @@ def main():
         dist.destroy_process_group()
 
 
-def roofline(dev, peaks, clk, fwd_ms, bwd_ms, blended_per_view):
-    """Issue-bound roofline of the dominant kernel (render_bwd); see DESIGN.md."""
+def roofline(dev, peaks, clk, stage_ms, blended_per_view, evaluated_per_view, traffic):
+    """Issue-bound roofline of the dominant kernel, k_render_bwd:
+    algorithmic FP32 ops = 8 per evaluated pair + 21 per blended pair, against the
+    FP32 issue peak SMs x 128 lanes x SM clock measured during the run."""
     import torch
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     mhz = (clk or {}).get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
-    peak = sms * 128 * mhz * 1e6 / 1e12  # FP32 lane-ops/s (T/s) at the measured clock
-    ops_per_blended = 40.0  # algorithmic FP32 ops per blended pair in the backward (DESIGN.md)
-    achieved = blended_per_view * ops_per_blended / (bwd_ms / 1e3) / 1e12
-    return {"kernel": "gs_render_bwd", "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None,
-            "peak_source": f"{sms} SMs x 128 FP32 lanes x {mhz:.0f} MHz (clock measured during the run)"}
+    peak = sms * 128 * mhz * 1e6 / 1e12
+    ops = 8.0 * evaluated_per_view + 21.0 * blended_per_view
+    ms = stage_ms["render_bwd"]
+    achieved = ops / (ms / 1e3) / 1e12
+    return {"kernel": "k_render_bwd (gs_render_bwd_screen)", "bound": "alu", "achieved": achieved, "peak": peak,
+            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+            "algorithmic_ops_per_launch": ops, "launch_ms": ms,
+            "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x {mhz:.0f} MHz (SM clock sampled during the run)"}
 
 
 if __name__ == "__main__":

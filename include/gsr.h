@@ -174,6 +174,33 @@ gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
                         const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, void* ws,
                         size_t ws_bytes, float* grad, void* stream);
 
+/* ---------------------------------------------------------------- batched backward
+ * gs_render_bwd split in its two halves so that a batch of views (R21) chains the
+ * projection backward ONCE per up to 8 views instead of once per view:
+ *
+ *  gs_render_bwd_screen: the raster half of gs_render_bwd for one view.  Accumulates
+ *    (+=) the view's screen-space gradients into sgrad float[P][12] (layout of the
+ *    gs_render_bwd workspace).  sgrad must be zero at every visible Gaussian's entry
+ *    before the first call (cudaMemset once at allocation); gs_project_bwd_views
+ *    leaves it zero again.
+ *  gs_project_bwd_views: grad += sum over the n_views views of d(projection_v)^T sgrad_v
+ *    (exact derivative of gs_project, R18).  cams: HOST array of n_views cameras;
+ *    flags: HOST array of n_views DEVICE pointers to each view's gs_proj.flags (uint8[P],
+ *    as written by gs_project for that view); sgrads: HOST array of n_views DEVICE
+ *    pointers to float[P][12].  Each params row is read and each grad row updated once
+ *    per 8 views; every consumed sgrad entry is reset to zero.  accumulate != 0:
+ *    grad += the batch's gradient; accumulate == 0: grad := the batch's gradient
+ *    (every row of every Gaussian written, none read -- the first batch of an
+ *    iteration, so that the optimiser need not zero grad). */
+gs_status gs_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
+                               const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                               const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, float* sgrad,
+                               void* stream);
+gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views]*/, const gs_scene* scene /*HOST*/,
+                               const float* params, const uint8_t* const* flags /*HOST[n_views] of DEVICE*/,
+                               float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
+                               void* stream);
+
 /* ---------------------------------------------------------------- gs_adam_step
  * Dense bias-corrected Adam over all F * P scalars (R20):
  *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 
 #include "gsr_internal.cuh"
 
@@ -231,9 +232,65 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
   const DevCam dc = make_devcam(*cam);
   launch_render_bwd(dc, proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
                     static_cast<float*>(ws), s);
-  launch_project_bwd(dc, scene->P, scene->P_stride, scene->sh_degree, params, proj, static_cast<const float*>(ws),
-                     grad, s);
+  const uint8_t* fl = proj.flags;
+  float* sg = static_cast<float*>(ws);
+  launch_project_bwd_views(1, &dc, &fl, &sg, scene->P, scene->P_stride, scene->sh_degree, params, grad, 1, s);
   return check_launch("gs_render_bwd");
+}
+
+gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
+                               const int32_t* tile_ranges, const float* T_final, const int32_t* n_contrib,
+                               const float* dL_drgb, const float* dL_ddepth, float* sgrad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_render_bwd_screen"));
+  GS_TRY(check_scene(scene, "gs_render_bwd_screen"));
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_render_bwd_screen", {{proj.rec, "proj.rec"}, {tile_ranges, "tile_ranges"},
+                                             {T_final, "T_final"}, {n_contrib, "n_contrib"}, {dL_drgb, "dL_drgb"},
+                                             {sgrad, "sgrad"}}));
+  if (dL_ddepth && !aligned16(dL_ddepth)) {
+    set_error("gs_render_bwd_screen: dL_ddepth is not 16-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
+                    sgrad, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_render_bwd_screen");
+}
+
+gs_status gs_project_bwd_views(int n_views, const gs_camera* cams, const gs_scene* scene, const float* params,
+                               const uint8_t* const* flags, float* const* sgrads, float* grad, int accumulate,
+                               void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_project_bwd_views"));
+  if (n_views < 0 || (n_views > 0 && (!cams || !flags || !sgrads))) {
+    set_error("gs_project_bwd_views: invalid view arrays (n_views=%d)", n_views);
+    return GS_ERR_ARG;
+  }
+  if (scene->P == 0 || (n_views == 0 && accumulate)) return GS_OK;
+  if (n_views == 0) {  // overwrite with an empty batch: grad := 0
+    GS_TRY(check_ptrs("gs_project_bwd_views", {{grad, "grad"}}));
+    if (cudaMemsetAsync(grad, 0, (size_t)rows_of(scene) * scene->P_stride * sizeof(float),
+                        static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      return check_launch("gs_project_bwd_views memset");
+    return GS_OK;
+  }
+  GS_TRY(check_ptrs("gs_project_bwd_views", {{params, "params"}, {grad, "grad"}}));
+  std::vector<DevCam> dc((size_t)n_views);
+  for (int v = 0; v < n_views; ++v) {
+    GS_TRY(check_camera(cams + v, "gs_project_bwd_views"));
+    if (!flags[v] || !sgrads[v]) {
+      set_error("gs_project_bwd_views: view %d has a NULL flags or sgrad pointer", v);
+      return GS_ERR_ARG;
+    }
+    if (!aligned16(sgrads[v])) {
+      set_error("gs_project_bwd_views: sgrads[%d] is not 16-byte aligned", v);
+      return GS_ERR_ALIGN;
+    }
+    dc[v] = make_devcam(cams[v]);
+  }
+  launch_project_bwd_views(n_views, dc.data(), flags, sgrads, scene->P, scene->P_stride, scene->sh_degree, params,
+                           grad, accumulate ? 1 : 0, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_project_bwd_views");
 }
 
 gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float* m, float* v, const float* lr_per_row,

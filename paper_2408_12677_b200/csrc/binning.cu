@@ -25,7 +25,9 @@ namespace gsr {
 namespace {
 
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
-constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32, kRsItems = 16, kRsTile = kRsThreads * kRsItems;
+constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32;
+constexpr int kRsItemsKeys = 16, kRsItemsDepth = 4;  // items per thread: tile-key passes / depth passes
+constexpr int kRsTileKeys = kRsThreads * kRsItemsKeys, kRsTileDepth = kRsThreads * kRsItemsDepth;
 constexpr uint32_t kLbAgg = 1u << 30, kLbInc = 2u << 30, kLbMask = (1u << 30) - 1;
 constexpr unsigned long long kScAgg = 1ull << 62, kScInc = 2ull << 62, kScMask = (1ull << 62) - 1;
 
@@ -210,64 +212,126 @@ __global__ void __launch_bounds__(kScanThreads) k_offsets(const int32_t* __restr
 }
 
 // ---------------------------------------------------------------------------
-// K3: emit one 16-bit tile key per touched tile, in depth order; fused 2 x 256-bin
-// histograms of the tile-key bytes.  One warp broadcasts 32 Gaussians at a time
-// and strides its lanes over each footprint (coalesced writes for any size).
+// K3: emit one 16-bit tile key per touched tile, in depth order, with a
+// load-balanced (merge-path) expansion: CTA b owns output keys [2048 b, 2048 b +
+// 2048), finds the Gaussians spanning them by a 32-ary search over the key
+// offsets, stages their offsets / ids / rects in shared memory, and each thread
+// writes 8 consecutive keys with 16-B vector stores.  Work per thread is constant
+// whatever the footprint distribution (one Gaussian can touch > 6000 tiles).
+// Fused: the 2 x 256-bin histograms of the tile-key bytes for the tile sort.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ sorted_gid,
-                                              const uint32_t* __restrict__ offs, const float* __restrict__ rec,
-                                              int TX, const Counters* __restrict__ ctr, int64_t cap,
-                                              uint16_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
-                                              uint32_t* __restrict__ ghist /* [2][256] */) {
+constexpr int kEmThreads = 256, kEmItems = 8, kEmTile = kEmThreads * kEmItems;
+
+// largest s in [0, V) with offs[s] <= k (offs strictly increasing, offs[0] = 0)
+__device__ __forceinline__ int64_t warp_search(const uint32_t* __restrict__ offs, int64_t V, uint32_t k, int lane) {
+  int64_t lo = 0, hi = V;  // offs[lo] <= k < offs[hi] (offs[V] := +inf)
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + step * (lane + 1);
+    const bool le = p < hi && offs[p] <= k;
+    const int c = __popc(__ballot_sync(kFull, le));
+    lo = lo + step * c;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict__ sorted_gid,
+                                                     const uint32_t* __restrict__ offs, const float* __restrict__ rec,
+                                                     int TX, const Counters* __restrict__ ctr, int64_t cap,
+                                                     uint16_t* __restrict__ tkeys, uint32_t* __restrict__ tvals,
+                                                     uint32_t* __restrict__ ghist /* [2][256] */) {
+  __shared__ uint32_t s_off[kEmTile + 1];
+  __shared__ uint32_t s_gid[kEmTile];
+  __shared__ uint32_t s_rx[kEmTile], s_ry[kEmTile];
   __shared__ uint32_t s_hist[2][256];
-  for (int t = threadIdx.x; t < 512; t += 256) (&s_hist[0][0])[t] = 0;
-  __syncthreads();
-  const int64_t V = (int64_t)ctr->V;
-  const bool ok = (int64_t)ctr->K <= cap;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  if (ok) {
-    for (int64_t chunk = gw; chunk * 32 < V; chunk += nw) {
-      const int64_t s = chunk * 32 + lane;
-      uint32_t gid = 0, off = 0, rx = 0, ry = 0;
-      if (s < V) {
-        gid = sorted_gid[s];
-        off = offs[s];
-        const float2 r = *reinterpret_cast<const float2*>(rec + 12 * (int64_t)gid + 10);
-        rx = __float_as_uint(r.x);
-        ry = __float_as_uint(r.y);
+  __shared__ int64_t s_lo[2];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < 512; i += kEmThreads) (&s_hist[0][0])[i] = 0;
+  const int64_t V = (int64_t)ctr->V, K = (int64_t)ctr->K;
+  const int64_t nblk = K <= cap ? (K + kEmTile - 1) / kEmTile : 0;
+  for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int64_t k0 = blk * kEmTile, k1 = min(K, k0 + kEmTile);
+    if (warp < 2) {
+      const int64_t s = warp_search(offs, V, (uint32_t)(warp == 0 ? k0 : k1 - 1), lane);
+      if (lane == 0) s_lo[warp] = s;
+    }
+    __syncthreads();
+    const int64_t slo = s_lo[0];
+    const int ns = (int)(s_lo[1] - slo + 1);
+    for (int j = t; j < ns; j += kEmThreads) {
+      const uint32_t g = sorted_gid[slo + j];
+      s_off[j] = offs[slo + j];
+      s_gid[j] = g;
+      const uint2 r = *reinterpret_cast<const uint2*>(rec + 12 * (int64_t)g + 10);
+      s_rx[j] = r.x;
+      s_ry[j] = r.y;
+    }
+    if (t == 0) s_off[ns] = (slo + ns < V) ? offs[slo + ns] : (uint32_t)K;
+    __syncthreads();
+    const int64_t kb = k0 + (int64_t)t * kEmItems;
+    if (kb < k1) {
+      // locate the Gaussian of key kb in the staged offsets
+      int lo = 0, hi = ns;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_off[mid] <= (uint32_t)kb) lo = mid; else hi = mid;
       }
-      const int nvalid = (int)((V - chunk * 32) < 32 ? (V - chunk * 32) : 32);
-      for (int k = 0; k < nvalid; ++k) {
-        const uint32_t g = __shfl_sync(kFull, gid, k);
-        const uint32_t o = __shfl_sync(kFull, off, k);
-        const uint32_t xr = __shfl_sync(kFull, rx, k), yr = __shfl_sync(kFull, ry, k);
-        const int x0 = xr & 0xffff, x1 = xr >> 16, y0 = yr & 0xffff, y1 = yr >> 16;
-        const int w = x1 - x0, cnt = w * (y1 - y0);
-        for (int j0 = 0; j0 < cnt; j0 += 32) {
-          const int j = j0 + lane;
-          const bool act = j < cnt;
-          uint32_t tile = 0;
-          if (act) {
-            const int dyq = j / w;
-            tile = (uint32_t)((y0 + dyq) * TX + x0 + (j - dyq * w));
-            tkeys[o + j] = (uint16_t)tile;
-            tvals[o + j] = g;
-            atomicAdd(&s_hist[0][tile & 255], 1u);
+      int j = lo;
+      uint32_t next = s_off[j + 1];
+      int x0 = s_rx[j] & 0xffff, w = (int)(s_rx[j] >> 16) - x0, y0 = s_ry[j] & 0xffff;
+      int local = (int)(kb - s_off[j]);
+      int row = local / w, col = local - row * w;
+      uint32_t gid = s_gid[j];
+      uint16_t kk[kEmItems];
+      uint32_t vv[kEmItems];
+      uint32_t hb_run = 0xffffffffu, hb_cnt = 0;
+      const int nk = (int)((k1 - kb) < kEmItems ? (k1 - kb) : kEmItems);
+#pragma unroll
+      for (int q = 0; q < kEmItems; ++q) {
+        if (q < nk) {
+          if ((uint32_t)(kb + q) >= next) {
+            ++j;
+            next = s_off[j + 1];
+            x0 = s_rx[j] & 0xffff, w = (int)(s_rx[j] >> 16) - x0, y0 = s_ry[j] & 0xffff;
+            gid = s_gid[j];
+            row = 0, col = 0;
           }
-          // high byte: warp-aggregated (a footprint row shares it)
-          const uint32_t hb = act ? (tile >> 8) : 0xffffffffu;
-          const uint32_t peers = __match_any_sync(kFull, hb);
-          if (act && (peers & lanemask_lt()) == 0) atomicAdd(&s_hist[1][hb], (uint32_t)__popc(peers));
+          const uint32_t tile = (uint32_t)((y0 + row) * TX + x0 + col);
+          kk[q] = (uint16_t)tile;
+          vv[q] = gid;
+          atomicAdd(&s_hist[0][tile & 255], 1u);
+          const uint32_t hb = tile >> 8;
+          if (hb != hb_run) {
+            if (hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
+            hb_run = hb, hb_cnt = 0;
+          }
+          ++hb_cnt;
+          if (++col == w) col = 0, ++row;
         }
       }
+      if (hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
+      if (nk == kEmItems) {
+        uint4 k4;
+        k4.x = kk[0] | ((uint32_t)kk[1] << 16);
+        k4.y = kk[2] | ((uint32_t)kk[3] << 16);
+        k4.z = kk[4] | ((uint32_t)kk[5] << 16);
+        k4.w = kk[6] | ((uint32_t)kk[7] << 16);
+        *reinterpret_cast<uint4*>(tkeys + kb) = k4;
+        reinterpret_cast<uint4*>(tvals + kb)[0] = make_uint4(vv[0], vv[1], vv[2], vv[3]);
+        reinterpret_cast<uint4*>(tvals + kb)[1] = make_uint4(vv[4], vv[5], vv[6], vv[7]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kEmItems; ++q)
+          if (q < nk) tkeys[kb + q] = kk[q], tvals[kb + q] = vv[q];
+      }
     }
+    __syncthreads();
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < 512; t += 256) {
-    const uint32_t c = (&s_hist[0][0])[t];
-    if (c) atomicAdd(&ghist[t], c);
+  for (int i = t; i < 512; i += kEmThreads) {
+    const uint32_t c = (&s_hist[0][0])[i];
+    if (c) atomicAdd(&ghist[i], c);
   }
 }
 
@@ -275,21 +339,22 @@ __global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ sorte
 // K4: one onesweep LSD pass (8-bit digit at `shift`) over n = *n_ptr items
 // (n := 0 if n > cap).  Persistent CTAs pull 4096-item partitions in order.
 // ---------------------------------------------------------------------------
-template <typename KeyT>
-__global__ void __launch_bounds__(kRsThreads) k_onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                         KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                         const unsigned long long* n_ptr, int64_t cap,
-                                                         const uint32_t* __restrict__ ghist, uint32_t* lookback,
-                                                         uint32_t* part_ctr, int shift) {
-  __shared__ uint32_t s_keys[kRsTile];
-  __shared__ uint32_t s_vals[kRsTile];
+template <typename KeyT, int ITEMS>
+__global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                            KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                            const unsigned long long* n_ptr, int64_t cap,
+                                                            const uint32_t* __restrict__ ghist, uint32_t* lookback,
+                                                            uint32_t* part_ctr, int shift) {
+  constexpr int TILE = kRsThreads * ITEMS;
+  __shared__ uint32_t s_keys[TILE];
+  __shared__ uint32_t s_vals[TILE];
   __shared__ uint32_t s_whist[kRsWarps][256];
   __shared__ uint32_t s_gpref[256], s_gbase[256], s_bexcl[256];
   __shared__ uint32_t s_scan[8];
   __shared__ uint32_t s_part;
   int64_t n = (int64_t)*n_ptr;
   if (n > cap) n = 0;
-  const int64_t num_parts = (n + kRsTile - 1) / kRsTile;
+  const int64_t num_parts = (n + TILE - 1) / TILE;
   if (num_parts == 0) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   {
@@ -304,14 +369,16 @@ __global__ void __launch_bounds__(kRsThreads) k_onesweep(const KeyT* __restrict_
     __syncthreads();
     const uint32_t part = s_part;
     if ((int64_t)part >= num_parts) break;
-    const int64_t base = (int64_t)part * kRsTile + warp * (kRsItems * 32);
-    uint32_t key[kRsItems], val[kRsItems], rank[kRsItems];
+    const int64_t base = (int64_t)part * TILE + warp * (ITEMS * 32);
+    uint32_t key[ITEMS], rank[ITEMS];
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
       const int64_t idx = base + i * 32 + lane;
-      const bool valid = idx < n;
-      key[i] = valid ? (uint32_t)kin[idx] : 0u;
-      val[i] = valid ? vin[idx] : 0u;
+      key[i] = idx < n ? (uint32_t)kin[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+      const bool valid = base + i * 32 + lane < n;
       const uint32_t d = valid ? ((key[i] >> shift) & 255u) : (256u + lane);
       const uint32_t peers = __match_any_sync(kFull, d);
       const uint32_t r = __popc(peers & lt);
@@ -323,7 +390,7 @@ __global__ void __launch_bounds__(kRsThreads) k_onesweep(const KeyT* __restrict_
       rank[i] = valid ? (b + r) : 0xffffffffu;
     }
     __syncthreads();
-    // per digit: exclusive over warps, partition count
+    // per digit t: exclusive over warps and the partition count; publish it early
     uint32_t cnt = 0;
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
@@ -331,38 +398,46 @@ __global__ void __launch_bounds__(kRsThreads) k_onesweep(const KeyT* __restrict_
       s_whist[w][t] = cnt;
       cnt += c;
     }
+    uint32_t* lb = lookback + (int64_t)part * 256 + t;
+    st_vol(lb, (part == 0 ? kLbInc : kLbAgg) | cnt);
     uint32_t tot;
     s_bexcl[t] = block_excl_scan256<uint32_t>(cnt, s_scan, tot);
-    uint32_t* lb = lookback + (int64_t)part * 256 + t;
+    // decoupled look-back over a window of 4 predecessors per round trip
     uint32_t excl = 0;
-    if (part == 0) {
-      st_vol(lb, kLbInc | cnt);
-    } else {
-      st_vol(lb, kLbAgg | cnt);
-      for (int64_t p = (int64_t)part - 1; p >= 0;) {
-        const uint32_t v = ld_vol(lookback + p * 256 + t);
-        const uint32_t f = v >> 30;
-        if (f == 0) continue;
-        excl += v & kLbMask;
-        if (f == 2) break;
-        --p;
+    for (int64_t p = (int64_t)part - 1; p >= 0;) {
+      uint32_t v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = (p - k >= 0) ? ld_vol(lookback + (p - k) * 256 + t) : kLbInc;
+      int k = 0;
+      bool done = false;
+#pragma unroll
+      for (; k < 4; ++k) {
+        const uint32_t f = v[k] >> 30;
+        if (f == 0) break;
+        excl += v[k] & kLbMask;
+        if (f == 2) {
+          done = true;
+          break;
+        }
       }
-      st_vol(lb, kLbInc | (excl + cnt));
+      if (done) break;
+      p -= k;
     }
+    if (part != 0) st_vol(lb, kLbInc | (excl + cnt));
     s_gbase[t] = s_gpref[t] + excl;
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
       if (rank[i] != 0xffffffffu) {
         const uint32_t d = (key[i] >> shift) & 255u;
         const uint32_t pos = s_bexcl[d] + s_whist[warp][d] + rank[i];
         s_keys[pos] = key[i];
-        s_vals[pos] = val[i];
+        s_vals[pos] = vin[base + i * 32 + lane];
       }
     }
     __syncthreads();
-    const int64_t rem = n - (int64_t)part * kRsTile;
-    const int nv = (int)(rem < kRsTile ? rem : kRsTile);
+    const int64_t rem = n - (int64_t)part * TILE;
+    const int nv = (int)(rem < TILE ? rem : TILE);
     for (int j = t; j < nv; j += kRsThreads) {
       const uint32_t k = s_keys[j];
       const uint32_t d = (k >> shift) & 255u;
@@ -403,8 +478,8 @@ Layout make_layout(int64_t P, int64_t cap) {
     return at;
   };
   const int64_t scan_parts = (P + kScanTile - 1) / kScanTile + 1;
-  L.depth_parts = (P + kRsTile - 1) / kRsTile + 1;
-  L.tile_parts = (cap + kRsTile - 1) / kRsTile + 1;
+  L.depth_parts = (P + kRsTileDepth - 1) / kRsTileDepth + 1;
+  L.tile_parts = (cap + kRsTileKeys - 1) / kRsTileKeys + 1;
   L.ctr = take(sizeof(Counters));
   L.ghist = take(6 * 256 * sizeof(uint32_t));
   L.lb_scan0 = take(scan_parts * 8);
@@ -466,13 +541,13 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
                                                reinterpret_cast<unsigned long long*>(w + L.lb_scan0), dk0, dv0, ghist);
   count_launch();
   // depth sort: 4 passes, result back in (dk0, dv0)
-  const int rs_grid_d = (int)std::min<int64_t>((P + kRsTile - 1) / kRsTile, (int64_t)nsm * 4);
+  const int rs_grid_d = (int)std::min<int64_t>((P + kRsTileDepth - 1) / kRsTileDepth, (int64_t)nsm * 3);
   uint32_t* kin = dk0;
   uint32_t* vin = dv0;
   uint32_t* kout = dk1;
   uint32_t* vout = dv1;
   for (int pass = 0; pass < 4; ++pass) {
-    k_onesweep<uint32_t><<<rs_grid_d, kRsThreads, 0, s>>>(kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256,
+    k_onesweep<uint32_t, kRsItemsDepth><<<rs_grid_d, kRsThreads, 0, s>>>(kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256,
                                                            lbd + (int64_t)pass * L.depth_parts * 256,
                                                            &ctr->part[2 + pass], 8 * pass);
     count_launch();
@@ -484,21 +559,21 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
                                                reinterpret_cast<unsigned long long*>(w + L.lb_scan1), offs,
                                                reinterpret_cast<long long*>(num_keys_dev));
   count_launch();
-  const int emit_grid = (int)std::min<int64_t>((P + 255) / 256, (int64_t)nsm * 8);
-  k_emit<<<emit_grid, 256, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0, ghist + 4 * 256);
+  const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * 4);
+  k_emit<<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0, ghist + 4 * 256);
   count_launch();
-  const int rs_grid_t = (int)std::min<int64_t>((cap + kRsTile - 1) / kRsTile, (int64_t)nsm * 4);
+  const int rs_grid_t = (int)std::max<int64_t>(1, std::min<int64_t>((cap + kRsTileKeys - 1) / kRsTileKeys, (int64_t)nsm * 3));
   const uint16_t* final_keys;
   if (NT <= 256) {
-    k_onesweep<uint16_t><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, reinterpret_cast<uint32_t*>(sorted_ids),
+    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, reinterpret_cast<uint32_t*>(sorted_ids),
                                                            &ctr->K, cap, ghist + 4 * 256, lbt, &ctr->part[6], 0);
     count_launch();
     final_keys = tk1;
   } else {
-    k_onesweep<uint16_t><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, tv1, &ctr->K, cap, ghist + 4 * 256, lbt,
+    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, tv1, &ctr->K, cap, ghist + 4 * 256, lbt,
                                                            &ctr->part[6], 0);
     count_launch();
-    k_onesweep<uint16_t><<<rs_grid_t, kRsThreads, 0, s>>>(tk1, tv1, tk0, reinterpret_cast<uint32_t*>(sorted_ids),
+    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk1, tv1, tk0, reinterpret_cast<uint32_t*>(sorted_ids),
                                                            &ctr->K, cap, ghist + 5 * 256,
                                                            lbt + (int64_t)L.tile_parts * 256, &ctr->part[7], 8);
     count_launch();

@@ -39,8 +39,10 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 // project.cu
 void launch_project(const DevCam& cam, int64_t P, int64_t P_stride, int deg, const float* params, gs_proj out,
                     cudaStream_t s);
-void launch_project_bwd(const DevCam& cam, int64_t P, int64_t P_stride, int deg, const float* params,
-                        gs_proj proj, const float* sgrad, float* grad, cudaStream_t s);
+constexpr int kMaxViews = 8;  // views chained per pass of the projection backward
+void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* const* flags, float* const* sgrads,
+                              int64_t P, int64_t S, int deg, const float* params, float* grad, int accumulate,
+                              cudaStream_t s);
 // binning.cu
 size_t bin_workspace_bytes(int64_t P, int64_t key_capacity, int num_tiles);
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes,

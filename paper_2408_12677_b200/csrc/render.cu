@@ -77,12 +77,86 @@ __device__ __forceinline__ bool eval_gauss(const Eval& e, float my, float pyf, f
   }
 }
 
-__device__ __forceinline__ void load_rec(const float4* s, float& mx, float& my, float& z, float& o, float& A, float& B,
-                                         float& C, float& r, float& g, float& b) {
+// Support box of alpha >= 1/255: {d : 0.5 d^T Sigma_hat^{-1} d <= ln(255 o)} has
+// half-extents sqrt(2 L Sigma_hat_xx), sqrt(2 L Sigma_hat_yy).  Returns the 8-bit mask
+// of the tile's 8x4 pixel blocks (block b = (b & 1, b >> 1): x offset 8 (b & 1), y
+// offset 4 (b >> 1)) that intersect it, with a relative 1% + 1 px safety margin so
+// that a skipped pixel can never pass the alpha test (the result is identical to
+// evaluating every pixel; the oracle parity tests check it).
+__device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, float B, float C, float o, int ox,
+                                               int oy) {
+  const float L = __logf(255.f * o);
+  if (!(L >= -1e-3f)) return 0u;  // o < 1/255: alpha can never reach 1/255
+  const float detc = A * C - B * B;
+  if (!(detc > 0.f) || !(A > 0.f) || !(C > 0.f)) return 0xffu;
+  const float two_l = 2.f * fmaxf(L, 0.f) * 1.0201f;  // (1.01)^2
+  const float idet = __fdividef(1.f, detc);
+  const float tx = two_l * C * idet, ty = two_l * A * idet;
+  const float hx = tx * rsqrtf(fmaxf(tx, 1e-30f)) + 1.f, hy = ty * rsqrtf(fmaxf(ty, 1e-30f)) + 1.f;
+  if (!(hx < 1e6f) || !(hy < 1e6f)) return 0xffu;
+  // exact test: min over the block of q(d) = A dx^2 + 2 B dx dy + C dy^2 (power = -q/2)
+  // against 2 L (with the 1% margin), the block taken as the rectangle of its pixel
+  // centres grown by 0.5 px.  The minimum of a convex quadratic over a rectangle is 0
+  // if the mean is inside, else on an edge, where it is a 1-D convex quadratic.
+  const float qmax = two_l + 1e-3f;
+  const float iA = __fdividef(1.f, A), iC = __fdividef(1.f, C);
+  const float fx0 = (float)ox - 0.5f - mx, fy0 = (float)oy - 0.5f - my;
+  uint32_t m = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const float ax0 = fx0 + 8.f * (b & 1), ax1 = ax0 + 8.f;
+    const float ay0 = fy0 + 4.f * (b >> 1), ay1 = ay0 + 4.f;
+    bool hit = (ax1 >= -hx) && (ax0 <= hx) && (ay1 >= -hy) && (ay0 <= hy);  // bounding-box pre-test
+    if (hit && !(ax0 <= 0.f && ax1 >= 0.f && ay0 <= 0.f && ay1 >= 0.f)) {
+      float qmin = 3.4e38f;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float dx = e ? ax1 : ax0;  // vertical edge dx = const
+        const float dy = fminf(fmaxf(-B * dx * iC, ay0), ay1);
+        qmin = fminf(qmin, fmaf(A * dx, dx, fmaf(2.f * B * dx, dy, C * dy * dy)));
+        const float ey = e ? ay1 : ay0;  // horizontal edge dy = const
+        const float ex = fminf(fmaxf(-B * ey * iA, ax0), ax1);
+        qmin = fminf(qmin, fmaf(A * ex, ex, fmaf(2.f * B * ex, ey, C * ey * ey)));
+      }
+      hit = qmin <= qmax;
+    }
+    m |= hit ? (1u << b) : 0u;
+  }
+  return m;
+}
+
+struct StagedRec {
+  float mx, my, z, o, A, B, C, r, g, b;
+  uint32_t mask;
+};
+
+__device__ __forceinline__ StagedRec load_staged(const float4* s) {
   const float4 q0 = s[0], q1 = s[1], q2 = s[2];
-  mx = q0.x, my = q0.y, z = q0.z, o = q0.w;
-  A = q1.x, B = q1.y, C = q1.z, r = q1.w;
-  g = q2.x, b = q2.y;
+  StagedRec r;
+  r.mx = q0.x, r.my = q0.y, r.z = q0.z, r.o = q0.w;
+  r.A = q1.x, r.B = q1.y, r.C = q1.z, r.r = q1.w;
+  r.g = q2.x, r.b = q2.y, r.mask = __float_as_uint(q2.w);
+  return r;
+}
+
+// Stage record `g` into shared memory, replacing the (unused here) rect word with
+// the tile's block mask.
+__device__ __forceinline__ void stage_rec(const float4* __restrict__ rec, int64_t g, float4* dst, int ox, int oy) {
+  const float4* r = rec + 3 * g;
+  const float4 q0 = r[0], q1 = r[1];
+  float4 q2 = r[2];
+  q2.w = __uint_as_float(block_mask(q0.x, q0.y, q1.x, q1.y, q1.z, q0.w, ox, oy));
+  dst[0] = q0;
+  dst[1] = q1;
+  dst[2] = q2;
+}
+
+// Blocks (8x4) all of whose pixels in this warp have bit set in `bits`.
+__device__ __forceinline__ uint32_t blocks_all(uint32_t bits) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) m |= __all_sync(kFull, (bits >> b) & 1u) ? (1u << b) : 0u;
+  return m;
 }
 
 // ---------------------------------------------------------------------------
@@ -98,87 +172,105 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
   const int tile = blockIdx.x * kWarpsPerCta + warp;
   if (tile >= cam.TX * cam.TY) return;
   const int tx = tile % cam.TX, ty = tile / cam.TX;
-  const int px = tx * kTile + (lane & 15);
-  const int py0 = ty * kTile + (lane >> 4) * kPix;
-  const float pxf = (float)px;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int lx = lane & 7, ly = lane >> 3;
+  // pixel b of this lane: x = ox + lx + 8 (b & 1), y = oy + ly + 4 (b >> 1)
+  const float pxf0 = (float)(ox + lx), pxf1 = pxf0 + 8.f, pyf0 = (float)(oy + ly);
   const int2 rg = ranges[tile];
 
   float T[kPix], Cr[kPix], Cg[kPix], Cb[kPix], D[kPix];
   int n[kPix];
   uint32_t done = 0;
 #pragma unroll
-  for (int i = 0; i < kPix; ++i) {
-    T[i] = 1.f, Cr[i] = Cg[i] = Cb[i] = D[i] = 0.f, n[i] = 0;
-    if (px >= cam.W || py0 + i >= cam.H) done |= 1u << i;
+  for (int b = 0; b < kPix; ++b) {
+    T[b] = 1.f, Cr[b] = Cg[b] = Cb[b] = D[b] = 0.f, n[b] = 0;
+    if (ox + lx + 8 * (b & 1) >= cam.W || oy + ly + 4 * (b >> 1) >= cam.H) done |= 1u << b;
   }
   uint32_t nblend = 0;
-  bool all_done = __all_sync(kFull, done == 0xffu);
-  for (int b = rg.x; b < rg.y && !all_done; b += 32) {
-    const int idx = b + lane;
-    if (idx < rg.y) {
-      const float4* r = rec + 3 * (int64_t)ids[idx];
-      s_rec[warp][lane][0] = r[0];
-      s_rec[warp][lane][1] = r[1];
-      s_rec[warp][lane][2] = r[2];
-    }
+  uint32_t bdone = blocks_all(done);
+  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32) {
+    const int idx = b0 + lane;
+    if (idx < rg.y) stage_rec(rec, ids[idx], s_rec[warp][lane], ox, oy);
     __syncwarp();
-    const int cnt = min(32, rg.y - b);
+    const int cnt = min(32, rg.y - b0);
     for (int j = 0; j < cnt; ++j) {
-      float mx, my, z, o, A, B, C, cr, cg, cb;
-      load_rec(s_rec[warp][j], mx, my, z, o, A, B, C, cr, cg, cb);
-      const Eval e = make_eval(mx, A, B, C, pxf);
-      const int pos1 = b + j - rg.x + 1;
+      const StagedRec q = load_staged(s_rec[warp][j]);
+      const uint32_t m = q.mask & ~bdone;
+      if (m == 0) continue;
+      const int pos1 = b0 + j - rg.x + 1;
+      const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
+      const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
+      if (kExact) {
 #pragma unroll
-      for (int i = 0; i < kPix; ++i) {
-        float G, dy;
-        const bool pok = eval_gauss(e, my, (float)(py0 + i), G, dy);
-        const float alpha = fminf(kAlphaCap, kExact ? __fmul_rn(o, G) : o * G);
-        const bool act = !((done >> i) & 1u) && pok && !(alpha < kAlphaMin);
-        const float Tn = kExact ? __fmul_rn(T[i], __fsub_rn(1.f, alpha)) : T[i] * (1.f - alpha);
-        const bool stop = act && (Tn < kTStop);
-        if (stop) done |= 1u << i;
-        if (act && !stop) {
-          if (kExact) {
-            const float w = __fmul_rn(alpha, T[i]);
-            Cr[i] = __fadd_rn(Cr[i], __fmul_rn(cr, w));
-            Cg[i] = __fadd_rn(Cg[i], __fmul_rn(cg, w));
-            Cb[i] = __fadd_rn(Cb[i], __fmul_rn(cb, w));
-            D[i] = __fadd_rn(D[i], __fmul_rn(z, w));
-          } else {
-            const float w = alpha * T[i];
-            Cr[i] = fmaf(cr, w, Cr[i]);
-            Cg[i] = fmaf(cg, w, Cg[i]);
-            Cb[i] = fmaf(cb, w, Cb[i]);
-            D[i] = fmaf(z, w, D[i]);
+        for (int b = 0; b < kPix; ++b) {
+          if (!((m >> b) & 1u)) continue;
+          float G, dy;
+          const bool pok = eval_gauss((b & 1) ? e1 : e0, q.my, pyf0 + 4.f * (b >> 1), G, dy);
+          const float alpha = fminf(kAlphaCap, __fmul_rn(q.o, G));
+          const bool act = !((done >> b) & 1u) && pok && !(alpha < kAlphaMin);
+          const float Tn = __fmul_rn(T[b], __fsub_rn(1.f, alpha));
+          const bool stop = act && (Tn < kTStop);
+          if (stop) done |= 1u << b;
+          if (act && !stop) {
+            const float w = __fmul_rn(alpha, T[b]);
+            Cr[b] = __fadd_rn(Cr[b], __fmul_rn(q.r, w));
+            Cg[b] = __fadd_rn(Cg[b], __fmul_rn(q.g, w));
+            Cb[b] = __fadd_rn(Cb[b], __fmul_rn(q.b, w));
+            D[b] = __fadd_rn(D[b], __fmul_rn(q.z, w));
+            T[b] = Tn;
+            n[b] = pos1;
+            ++nblend;
           }
-          T[i] = Tn;
-          n[i] = pos1;
-          ++nblend;
+        }
+      } else {
+        // branch-free per pixel; a block is skipped (warp-uniform) when no lane passes
+        const float dy0 = q.my - pyf0;
+#pragma unroll
+        for (int b = 0; b < kPix; ++b) {
+          if (!((m >> b) & 1u)) continue;
+          const Eval& e = (b & 1) ? e1 : e0;
+          const float dy = dy0 - 4.f * (b >> 1);
+          const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
+          const float alpha = fminf(kAlphaCap, q.o * ex2_approx(p2));
+          const bool act = (p2 <= 0.f) && (alpha >= kAlphaMin) && !((done >> b) & 1u);
+          if (!__any_sync(kFull, act)) continue;
+          const float Tn = fmaf(-alpha, T[b], T[b]);
+          const bool stop = act && (Tn < kTStop);
+          const bool comp = act && !stop;
+          done |= stop ? (1u << b) : 0u;
+          const float w = comp ? alpha * T[b] : 0.f;
+          Cr[b] = fmaf(q.r, w, Cr[b]);
+          Cg[b] = fmaf(q.g, w, Cg[b]);
+          Cb[b] = fmaf(q.b, w, Cb[b]);
+          D[b] = fmaf(q.z, w, D[b]);
+          T[b] = comp ? Tn : T[b];
+          n[b] = comp ? pos1 : n[b];
+          nblend += comp ? 1u : 0u;
         }
       }
-      all_done = __all_sync(kFull, done == 0xffu);
-      if (all_done) break;
+      if ((j & 7) == 7) bdone = blocks_all(done);
     }
+    bdone = blocks_all(done);
     __syncwarp();
   }
   const int64_t npix = (int64_t)cam.W * cam.H;
 #pragma unroll
-  for (int i = 0; i < kPix; ++i) {
-    const int py = py0 + i;
+  for (int b = 0; b < kPix; ++b) {
+    const int px = ox + lx + 8 * (b & 1), py = oy + ly + 4 * (b >> 1);
     if (px < cam.W && py < cam.H) {
       const int64_t p = (int64_t)py * cam.W + px;
       if (kExact) {
-        out_rgb[p] = __fadd_rn(Cr[i], __fmul_rn(T[i], cam.bg[0]));
-        out_rgb[npix + p] = __fadd_rn(Cg[i], __fmul_rn(T[i], cam.bg[1]));
-        out_rgb[2 * npix + p] = __fadd_rn(Cb[i], __fmul_rn(T[i], cam.bg[2]));
+        out_rgb[p] = __fadd_rn(Cr[b], __fmul_rn(T[b], cam.bg[0]));
+        out_rgb[npix + p] = __fadd_rn(Cg[b], __fmul_rn(T[b], cam.bg[1]));
+        out_rgb[2 * npix + p] = __fadd_rn(Cb[b], __fmul_rn(T[b], cam.bg[2]));
       } else {
-        out_rgb[p] = fmaf(T[i], cam.bg[0], Cr[i]);
-        out_rgb[npix + p] = fmaf(T[i], cam.bg[1], Cg[i]);
-        out_rgb[2 * npix + p] = fmaf(T[i], cam.bg[2], Cb[i]);
+        out_rgb[p] = fmaf(T[b], cam.bg[0], Cr[b]);
+        out_rgb[npix + p] = fmaf(T[b], cam.bg[1], Cg[b]);
+        out_rgb[2 * npix + p] = fmaf(T[b], cam.bg[2], Cb[b]);
       }
-      out_d[p] = D[i];
-      out_T[p] = T[i];
-      out_n[p] = n[i];
+      out_d[p] = D[b];
+      out_T[p] = T[b];
+      out_n[p] = n[b];
     }
   }
   if (blended) {
@@ -240,88 +332,97 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   const int tile = blockIdx.x * kWarpsPerCta + warp;
   if (tile >= cam.TX * cam.TY) return;
   const int tx = tile % cam.TX, ty = tile / cam.TX;
-  const int px = tx * kTile + (lane & 15);
-  const int py0 = ty * kTile + (lane >> 4) * kPix;
-  const float pxf = (float)px;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int lx = lane & 7, ly = lane >> 3;
+  const float pxf0 = (float)(ox + lx), pxf1 = pxf0 + 8.f, pyf0 = (float)(oy + ly);
   const int2 rg = ranges[tile];
   const int64_t npix = (int64_t)cam.W * cam.H;
 
   float T[kPix], Q[kPix], gr[kPix], gg[kPix], gb[kPix], gd[kPix];
   int n[kPix];
+  int bmaxn[kPix];  // per 8x4 block: max n_contrib over its 32 pixels (warp-uniform)
   int maxn = 0;
 #pragma unroll
-  for (int i = 0; i < kPix; ++i) {
-    const int py = py0 + i;
+  for (int b = 0; b < kPix; ++b) {
+    const int px = ox + lx + 8 * (b & 1), py = oy + ly + 4 * (b >> 1);
     if (px < cam.W && py < cam.H) {
       const int64_t p = (int64_t)py * cam.W + px;
-      T[i] = T_final[p];
-      n[i] = n_contrib[p];
-      gr[i] = g_rgb[p];
-      gg[i] = g_rgb[npix + p];
-      gb[i] = g_rgb[2 * npix + p];
-      gd[i] = g_dep ? g_dep[p] : 0.f;
+      T[b] = T_final[p];
+      n[b] = n_contrib[p];
+      gr[b] = g_rgb[p];
+      gg[b] = g_rgb[npix + p];
+      gb[b] = g_rgb[2 * npix + p];
+      gd[b] = g_dep ? g_dep[p] : 0.f;
     } else {
-      T[i] = 1.f, n[i] = 0, gr[i] = gg[i] = gb[i] = gd[i] = 0.f;
+      T[b] = 1.f, n[b] = 0, gr[b] = gg[b] = gb[b] = gd[b] = 0.f;
     }
-    Q[i] = T[i] * (gr[i] * cam.bg[0] + gg[i] * cam.bg[1] + gb[i] * cam.bg[2]);
-    maxn = max(maxn, n[i]);
+    Q[b] = T[b] * (gr[b] * cam.bg[0] + gg[b] * cam.bg[1] + gb[b] * cam.bg[2]);
+    bmaxn[b] = __reduce_max_sync(kFull, n[b]);
+    maxn = max(maxn, bmaxn[b]);
   }
-  maxn = __reduce_max_sync(kFull, maxn);
   for (int hi = rg.x + maxn; hi > rg.x; hi -= 32) {
     const int lo = max(rg.x, hi - 32);
     const int idx = lo + lane;
     if (idx < hi) {
       const int g = ids[idx];
-      const float4* r = rec + 3 * (int64_t)g;
       s_gid[warp][lane] = g;
-      s_rec[warp][lane][0] = r[0];
-      s_rec[warp][lane][1] = r[1];
-      s_rec[warp][lane][2] = r[2];
+      stage_rec(rec, g, s_rec[warp][lane], ox, oy);
     }
     __syncwarp();
     for (int j = hi - 1 - lo; j >= 0; --j) {
-      float mx, my, z, o, A, B, C, cr, cg, cb;
-      load_rec(s_rec[warp][j], mx, my, z, o, A, B, C, cr, cg, cb);
-      const Eval e = make_eval(mx, A, B, C, pxf);
+      const StagedRec q = load_staged(s_rec[warp][j]);
       const int pos = lo + j - rg.x;
-      float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f, acc_o = 0.f, s0 = 0.f, s1 = 0.f, s2 = 0.f;
-      bool any = false;
+      uint32_t m = q.mask;
 #pragma unroll
-      for (int i = 0; i < kPix; ++i) {
+      for (int b = 0; b < kPix; ++b)
+        if (pos >= bmaxn[b]) m &= ~(1u << b);
+      if (m == 0) continue;
+      const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
+      const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
+      float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f, acc_o = 0.f;
+      float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, s2 = 0.f;
+      bool any = false;  // warp-uniform
+#pragma unroll
+      for (int b = 0; b < kPix; ++b) {
+        if (!((m >> b) & 1u)) continue;
         float G, dy;
-        const bool pok = eval_gauss(e, my, (float)(py0 + i), G, dy);
-        const float raw = kExact ? __fmul_rn(o, G) : o * G;
+        const bool pok = eval_gauss((b & 1) ? e1 : e0, q.my, pyf0 + 4.f * (b >> 1), G, dy);
+        const float raw = kExact ? __fmul_rn(q.o, G) : q.o * G;
         const float alpha = fminf(kAlphaCap, raw);
-        if (pos < n[i] && pok && !(alpha < kAlphaMin)) {
-          any = true;
-          const float inv = __fdividef(1.f, 1.f - alpha);
-          const float Tk = T[i] * inv;
-          const float w = alpha * Tk;
-          const float u = fmaf(gr[i], cr, fmaf(gg[i], cg, fmaf(gb[i], cb, gd[i] * z)));
-          const float dal = Tk * u - inv * Q[i];
-          Q[i] = fmaf(w, u, Q[i]);
-          T[i] = Tk;
-          acc_r = fmaf(gr[i], w, acc_r);
-          acc_g = fmaf(gg[i], w, acc_g);
-          acc_b = fmaf(gb[i], w, acc_b);
-          acc_z = fmaf(gd[i], w, acc_z);
-          if (!(raw > kAlphaCap)) {  // capped alpha has no derivative (R18)
-            acc_o = fmaf(G, dal, acc_o);
-            const float dp = raw * dal;
-            const float t = dp * dy;
-            s0 += dp;
-            s1 += t;
-            s2 = fmaf(t, dy, s2);
-          }
-        }
+        const bool valid = pos < n[b] && pok && !(alpha < kAlphaMin);
+        if (!__any_sync(kFull, valid)) continue;
+        any = true;
+        // predicated body: invalid lanes contribute exact zeros and keep their state
+        const float inv = __fdividef(1.f, 1.f - alpha);
+        const float Tk = T[b] * inv;
+        const float w = valid ? alpha * Tk : 0.f;
+        const float u = fmaf(gr[b], q.r, fmaf(gg[b], q.g, fmaf(gb[b], q.b, gd[b] * q.z)));
+        const bool unc = valid && !(raw > kAlphaCap);  // capped alpha has no derivative (R18)
+        const float dal = unc ? (Tk * u - inv * Q[b]) : 0.f;
+        Q[b] = fmaf(w, u, Q[b]);
+        T[b] = valid ? Tk : T[b];
+        acc_r = fmaf(gr[b], w, acc_r);
+        acc_g = fmaf(gg[b], w, acc_g);
+        acc_b = fmaf(gb[b], w, acc_b);
+        acc_z = fmaf(gd[b], w, acc_z);
+        acc_o = fmaf(G, dal, acc_o);
+        const float dp = raw * dal;
+        const float t = dp * dy;
+        s0[b & 1] += dp;
+        s1[b & 1] += t;
+        s2 = fmaf(t, dy, s2);
       }
-      if (__any_sync(kFull, any)) {
-        const float dx = e.dx;
+      if (any) {
+        const float dx0 = e0.dx, dx1 = e1.dx;
+        const float sx = dx0 * s0[0] + dx1 * s0[1];        // sum dp dx
+        const float sxx = dx0 * dx0 * s0[0] + dx1 * dx1 * s0[1];  // sum dp dx^2
+        const float sy = s1[0] + s1[1];                      // sum dp dy
+        const float sxy = dx0 * s1[0] + dx1 * s1[1];         // sum dp dx dy
         float v[10];
-        v[0] = -(A * dx * s0 + B * s1);
-        v[1] = -(B * dx * s0 + C * s1);
-        v[2] = -0.5f * dx * dx * s0;
-        v[3] = -dx * s1;
+        v[0] = -(q.A * sx + q.B * sy);
+        v[1] = -(q.B * sx + q.C * sy);
+        v[2] = -0.5f * sxx;
+        v[3] = -sxy;
         v[4] = -0.5f * s2;
         v[5] = acc_o;
         v[6] = acc_r;

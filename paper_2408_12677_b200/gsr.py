@@ -99,9 +99,12 @@ class Library:
         lib.gs_render_bwd_workspace.argtypes = [vp]
         lib.gs_render_bwd_workspace.restype = C.c_size_t
         lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
-        for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_adam_step", "gs_l1_loss_grad"):
+        for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
+                   "gs_project_bwd_views", "gs_adam_step", "gs_l1_loss_grad"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -150,6 +153,21 @@ class Library:
             C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final),
             _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(ws), ws.numel() * ws.element_size(), _ptr(grad),
             _stream(stream)))
+
+    def render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, sgrad,
+                          stream=None):
+        return self._check("gs_render_bwd_screen", self.lib.gs_render_bwd_screen(
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
+            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _stream(stream)))
+
+    def project_bwd_views(self, cams, sc, params, flags, sgrads, grad, accumulate=True, stream=None):
+        """cams: list of GsCamera; flags / sgrads: lists of device tensors (one per view)."""
+        n = len(cams)
+        cam_arr = (GsCamera * max(n, 1))(*cams)
+        fl = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in flags])
+        sg = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in sgrads])
+        return self._check("gs_project_bwd_views", self.lib.gs_project_bwd_views(
+            n, cam_arr, C.byref(sc), _ptr(params), fl, sg, _ptr(grad), 1 if accumulate else 0, _stream(stream)))
 
     def adam_step(self, sc, params, grad, m, v, lr_per_row, step, beta1=0.9, beta2=0.999, eps=1e-15, zero_grad=True,
                   stream=None):

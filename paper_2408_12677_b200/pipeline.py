@@ -100,40 +100,77 @@ def measure_keys(lib, model: GaussianModel, cameras, device) -> int:
 class Trainer:
     """fwd + bwd + Adam over a batch of views.
 
-    ``allreduce`` (optional) is called on the gradient tensor between the last
-    view's backward and the Adam step -- the one exchange of the data-parallel
-    path (NCCL all-reduce over NVLink in bench.py)."""
+    Per view: gs_project -> gs_bin_tiles -> gs_render_fwd -> gs_l1_loss_grad ->
+    gs_render_bwd_screen (screen-space gradients of that view); after every
+    ``chunk`` views (<= 8) one gs_project_bwd_views chains them all to the parameter
+    gradient in a single pass.  ``allreduce`` (optional) is called on the gradient
+    between the last view and the Adam step -- the one exchange of the data-parallel
+    path (NCCL all-reduce over NVLink in bench.py).  ``hooks`` (optional) is called
+    as hooks(stage, "begin"/"end") around the render_fwd and render_bwd stages (used
+    by bench.py to time them with CUDA events on the launching stream)."""
 
     def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
-                 w_depth: float = 1.0, allreduce=None):
+                 w_depth: float = 1.0, allreduce=None, chunk: int = 8):
         self.lib, self.model, self.cameras, self.targets = lib, model, cameras, targets
         self.device, self.w_depth, self.allreduce = device, w_depth, allreduce
+        self.chunk = max(1, min(8, int(chunk)))
         self.buf = ViewBuffers(lib, cameras[0], model.P, key_capacity, device)
+        P = max(model.P, 1)
+        # per in-flight view: projection flags and screen-space gradients (zeroed once;
+        # gs_project_bwd_views leaves them zero again)
+        self.flags = [torch.empty(P + 16, dtype=torch.uint8, device=device) for _ in range(self.chunk)]
+        self.sgrad = [torch.zeros((P, gsr.SGRAD_FLOATS), dtype=torch.float32, device=device)
+                      for _ in range(self.chunk)]
         self.num_keys = torch.zeros(len(cameras), dtype=torch.int64, device=device)
         self.blended = torch.zeros(1, dtype=torch.int64, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
+        self.hooks = None
 
-    def view_fwd_bwd(self, v: int, t_rgb=None, t_depth=None):
+    def _hook(self, stage, what):
+        if self.hooks is not None:
+            self.hooks(stage, what)
+
+    def _view(self, v: int, slot: int, t_rgb, t_depth):
         lib, m, b, cam = self.lib, self.model, self.buf, self.cameras[v]
-        if t_rgb is None:
-            t_rgb, t_depth = self.targets[v]
-        render(lib, m, cam, b, num_keys_dev=self.num_keys[v:v + 1], blended=self.blended)
+        gcam = gsr.camera(cam)
+        proj = gsr.GsProj(b.proj.rec, b.proj.radius, b.proj.tiles, self.flags[slot].data_ptr())
+        lib.project(gcam, m.desc, m.params, proj)
+        lib.bin_tiles(gcam, m.desc, proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
+                      num_keys_dev=self.num_keys[v:v + 1])
+        self._hook("render_fwd", "begin")
+        lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=self.blended)
+        self._hook("render_fwd", "end")
         lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
-        lib.render_bwd(gsr.camera(cam), m.desc, m.params, b.proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb,
-                       b.g_depth, b.bwd_ws, m.grad)
+        self._hook("render_bwd", "begin")
+        lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
+                              self.sgrad[slot])
+        self._hook("render_bwd", "end")
+        return gcam
 
     def step(self, views, targets_override=None):
         """One iteration over ``views``; targets_override: {v: (rgb, depth)} device tensors."""
-        for v in views:
-            if targets_override is not None:
-                self.view_fwd_bwd(v, *targets_override[v])
-            else:
-                self.view_fwd_bwd(v)
-        if self.allreduce is not None:
-            self.allreduce(self.model.grad)
         m = self.model
+        pending = []
+        first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
+        for v in views:
+            t_rgb, t_depth = (targets_override[v] if targets_override is not None else self.targets[v])
+            pending.append(self._view(v, len(pending), t_rgb, t_depth))
+            if len(pending) == self.chunk:
+                self._chain(pending, accumulate=not first)
+                pending, first = [], False
+        if pending or first:
+            self._chain(pending, accumulate=not first)
+        if self.allreduce is not None:
+            self.allreduce(m.grad)
         m.step_count += 1
-        self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=True)
+        self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False)
+
+    def _chain(self, gcams, accumulate):
+        n = len(gcams)
+        self._hook("project_bwd", "begin")
+        self.lib.project_bwd_views(gcams, self.model.desc, self.model.params, self.flags[:n], self.sgrad[:n],
+                                   self.model.grad, accumulate=accumulate)
+        self._hook("project_bwd", "end")
 
     def check_capacity(self) -> int:
         """Max K seen since construction (host sync); raises if any view overflowed."""

@@ -289,10 +289,12 @@ def test_adam_parity(lib):
     tp, tm, tv, tg = (torch.from_numpy(a).to(DEV) for a in (p, m, v, g))
     lib.adam_step(sc, tp, tg, tm, tv, lr, 7, zero_grad=True)
     torch.cuda.synchronize()
-    rp, rm, rv = gsref.adam_step(p, g, m, v, np.array(lr, np.float32), 7, P=S)
+    # the ABI takes fp32 hyper-parameters: give the oracle the same fp32-rounded betas
+    rp, rm, rv = gsref.adam_step(p, g, m, v, np.array(lr, np.float32), 7, P=S, beta1=float(np.float32(0.9)),
+                                 beta2=float(np.float32(0.999)), eps=float(np.float32(1e-15)))
     # 1e-6 relative to the magnitude of the terms each fp32 update combines (m and v
     # are differences of two products and can cancel; p moves by ~lr per step)
-    b1, b2 = 0.9, 0.999
+    b1, b2 = float(np.float32(0.9)), float(np.float32(0.999))
     sm = b1 * np.abs(m) + (1 - b1) * np.abs(g)
     sv = b2 * np.abs(v) + (1 - b2) * g * g
     lr_col = np.array(lr, np.float64)[:, None]
@@ -414,3 +416,41 @@ def test_trainer_step_runs_and_decreases_loss(lib):
         losses.append(tr.loss.item())
     tr.check_capacity()
     assert losses[-1] < losses[0]
+
+
+def test_batched_views_backward_matches_per_view(lib):
+    """gs_render_bwd_screen x n + gs_project_bwd_views == sum of per-view gs_render_bwd
+    (and the sgrad buffers are left zero)."""
+    w = workload("small")
+    scene = w.scene
+    cams = []
+    for k in range(3):
+        c = scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.05 * (k - 1)), [0.1 * k, -0.05 * k, 0.0])
+        cams.append(c)
+    params = torch.from_numpy(scene.params).to(DEV)
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    grad_sum = torch.zeros_like(params)
+    grad_b = torch.zeros_like(params)
+    flags, sgrads, gcams, keep = [], [], [], []
+    for k, cam in enumerate(cams):
+        proj, t, _ = gpu_project(lib, cam, scene)
+        b = gpu_bin(lib, cam, scene, proj)
+        out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+        g_rgb, g_d = (torch.from_numpy(a).to(DEV) for a in scenegen.upstream_fields(10 + k, 320, 240))
+        ws = torch.zeros(scene.P * 12, dtype=torch.float32, device=DEV)
+        lib.render_bwd(gsr.camera(cam), sc, params, proj, b["sorted_ids"], b["ranges"], out["T_final"],
+                       out["n_contrib"], g_rgb, g_d, ws, grad_sum)
+        sg = torch.zeros((scene.P, 12), dtype=torch.float32, device=DEV)
+        lib.render_bwd_screen(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], out["T_final"],
+                              out["n_contrib"], g_rgb, g_d, sg)
+        flags.append(t["flags"])
+        sgrads.append(sg)
+        gcams.append(gsr.camera(cam))
+        keep.append((proj, t, b, out))
+    lib.project_bwd_views(gcams, sc, params, flags, sgrads, grad_b)
+    torch.cuda.synchronize()
+    a, bb = grad_sum.cpu().numpy(), grad_b.cpu().numpy()
+    assert np.abs(a).max() > 0
+    np.testing.assert_allclose(bb, a, rtol=1e-4, atol=1e-6 * np.abs(a).max())
+    for sg in sgrads:
+        assert int(torch.count_nonzero(sg)) == 0
