@@ -1,12 +1,16 @@
 // K6 render_fwd and K7 render_bwd (Eq. 11; backward PAPER.md:147).
 //
-// Work decomposition (B200-first): one warp per 16x16 tile, each
-// lane owns a column of 8 pixels (lane & 15 = column, lane >> 4 = upper/lower half).
-// A warp stages 32 of its tile's Gaussian records (48 B each, gathered from L2 by
-// id) into shared memory, then every lane evaluates each record against its 8
-// pixels.  Because the 8 pixels share x, the per-record part of the Gaussian
-// exponent (A dx^2, B dx) is computed once per lane and each pixel costs one FADD +
-// two FFMA + one MUFU.EX2 for its exponent.  The backward reverses the composite
+// Work decomposition (B200-first): one warp per 16x16 tile, split into
+// eight 8x4 pixel blocks; lane (lx, ly) owns pixel (lx + 8 (b & 1), ly + 4 (b >> 1))
+// of every block b.  A warp gathers 32 of its tile's Gaussian records (48 B each, by
+// id, from L2) into shared memory with cp.async, one batch ahead of the one being
+// composited; on arrival each lane computes, for its record, the 8-bit mask of the
+// blocks the record's alpha >= 1/255 support can reach (exact ellipse-rectangle
+// test).  Blocks outside the mask, and blocks whose pixels have all terminated, are
+// skipped warp-uniformly; records reaching >= 3 blocks run a branch-free path over
+// all 8 blocks (8 independent chains), the others a per-block path.  Each lane's two
+// columns share x, so the x part of the exponent (A dx^2, B dx) is computed once per
+// record and a pixel costs one FADD + two FFMA + one MUFU.EX2.  The backward reverses the composite
 // with T_k = T_{k+1} / (1 - alpha_k), keeps the suffix term as one scalar per pixel
 // (Q = sum_ch g_ch S^C_ch + g_D S^D), accumulates the 10 screen-space gradient
 // components of the current Gaussian over the lane's 8 pixels in registers, and
@@ -24,6 +28,8 @@ namespace {
 
 constexpr int kWarpsPerCta = 4;
 constexpr int kPix = 8;  // pixels per lane
+constexpr int kDenseBlocks = 3;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
+constexpr int kDenseBlocksBwd = 6;  // bwd: same (its per-block body is ~4x longer)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kTStop = 1e-4f;
@@ -139,16 +145,27 @@ __device__ __forceinline__ StagedRec load_staged(const float4* s) {
   return r;
 }
 
-// Stage record `g` into shared memory, replacing the (unused here) rect word with
-// the tile's block mask.
-__device__ __forceinline__ void stage_rec(const float4* __restrict__ rec, int64_t g, float4* dst, int ox, int oy) {
-  const float4* r = rec + 3 * g;
-  const float4 q0 = r[0], q1 = r[1];
-  float4 q2 = r[2];
-  q2.w = __uint_as_float(block_mask(q0.x, q0.y, q1.x, q1.y, q1.z, q0.w, ox, oy));
-  dst[0] = q0;
-  dst[1] = q1;
-  dst[2] = q2;
+// Asynchronous gather of one 48-B record into shared memory (cp.async, L2 -> SMEM,
+// bypassing registers) so that batch k+1's gathers are in flight while batch k is
+// composited; finish_stage then replaces the rect word with the block mask.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void gather_rec_async(const float4* __restrict__ rec, int id, float4* dst) {
+  const float4* src = rec + 3 * (int64_t)id;
+  cp_async16(dst + 0, src + 0);
+  cp_async16(dst + 1, src + 1);
+  cp_async16(dst + 2, src + 2);
+}
+__device__ __forceinline__ void finish_stage(float4* dst, int ox, int oy) {
+  const float4 q0 = dst[0], q1 = dst[1];
+  reinterpret_cast<float*>(dst + 2)[3] = __uint_as_float(block_mask(q0.x, q0.y, q1.x, q1.y, q1.z, q0.w, ox, oy));
 }
 
 // Blocks (8x4) all of whose pixels in this warp have bit set in `bits`.
@@ -167,7 +184,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
                                                                    float* __restrict__ out_d, float* __restrict__ out_T,
                                                                    int32_t* __restrict__ out_n,
                                                                    unsigned long long* blended) {
-  __shared__ float4 s_rec[kWarpsPerCta][32][3];
+  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kWarpsPerCta + warp;
   if (tile >= cam.TX * cam.TY) return;
@@ -188,13 +205,22 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
   }
   uint32_t nblend = 0;
   uint32_t bdone = blocks_all(done);
-  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32) {
-    const int idx = b0 + lane;
-    if (idx < rg.y) stage_rec(rec, ids[idx], s_rec[warp][lane], ox, oy);
+  // double-buffered staging: ids two batches ahead, records one batch ahead
+  if (rg.x + lane < rg.y) gather_rec_async(rec, ids[rg.x + lane], s_rec[warp][0][lane]);
+  cp_async_commit();
+  int nxt_id = (rg.x + 32 + lane < rg.y) ? ids[rg.x + 32 + lane] : -1;
+  int buf = 0;
+  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32, buf ^= 1) {
+    if (nxt_id >= 0) gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
+    cp_async_commit();
+    nxt_id = (b0 + 64 + lane < rg.y) ? ids[b0 + 64 + lane] : -1;
+    cp_async_wait<1>();
+    __syncwarp();
+    if (b0 + lane < rg.y) finish_stage(s_rec[warp][buf][lane], ox, oy);
     __syncwarp();
     const int cnt = min(32, rg.y - b0);
     for (int j = 0; j < cnt; ++j) {
-      const StagedRec q = load_staged(s_rec[warp][j]);
+      const StagedRec q = load_staged(s_rec[warp][buf][j]);
       const uint32_t m = q.mask & ~bdone;
       if (m == 0) continue;
       const int pos1 = b0 + j - rg.x + 1;
@@ -223,8 +249,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
           }
         }
       } else {
-        // branch-free per pixel; a block is skipped (warp-uniform) when no lane passes
         const float dy0 = q.my - pyf0;
+        if (__popc(m) >= kDenseBlocks) {
+          // dense: all 8 blocks without branches (8 independent chains for the
+          // scheduler); masked-out blocks and failing pixels contribute exact zeros
+          float al[kPix];
+          bool ac[kPix];
+#pragma unroll
+          for (int b = 0; b < kPix; ++b) {
+            const Eval& e = (b & 1) ? e1 : e0;
+            const float dy = dy0 - 4.f * (b >> 1);
+            const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
+            al[b] = fminf(kAlphaCap, q.o * ex2_approx(p2));
+            ac[b] = ((m >> b) & 1u) && (p2 <= 0.f) && (al[b] >= kAlphaMin) && !((done >> b) & 1u);
+          }
+#pragma unroll
+          for (int b = 0; b < kPix; ++b) {
+            const float Tn = fmaf(-al[b], T[b], T[b]);
+            const bool stop = ac[b] && (Tn < kTStop);
+            const bool comp = ac[b] && !stop;
+            done |= stop ? (1u << b) : 0u;
+            const float w = comp ? al[b] * T[b] : 0.f;
+            Cr[b] = fmaf(q.r, w, Cr[b]);
+            Cg[b] = fmaf(q.g, w, Cg[b]);
+            Cb[b] = fmaf(q.b, w, Cb[b]);
+            D[b] = fmaf(q.z, w, D[b]);
+            T[b] = comp ? Tn : T[b];
+            n[b] = comp ? pos1 : n[b];
+            nblend += comp ? 1u : 0u;
+          }
+          if ((j & 7) == 7) bdone = blocks_all(done);
+          continue;
+        }
+        // sparse: per block, skipped (warp-uniform) when masked out or no lane passes
 #pragma unroll
         for (int b = 0; b < kPix; ++b) {
           if (!((m >> b) & 1u)) continue;
@@ -253,6 +310,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
     bdone = blocks_all(done);
     __syncwarp();
   }
+  cp_async_wait<0>();
   const int64_t npix = (int64_t)cam.W * cam.H;
 #pragma unroll
   for (int b = 0; b < kPix; ++b) {
@@ -326,8 +384,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
                                                                    float* __restrict__ sgrad) {
-  __shared__ float4 s_rec[kWarpsPerCta][32][3];
-  __shared__ int s_gid[kWarpsPerCta][32];
+  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
+  __shared__ int s_gid[kWarpsPerCta][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kWarpsPerCta + warp;
   if (tile >= cam.TX * cam.TY) return;
@@ -360,17 +418,41 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
     bmaxn[b] = __reduce_max_sync(kFull, n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
-  for (int hi = rg.x + maxn; hi > rg.x; hi -= 32) {
-    const int lo = max(rg.x, hi - 32);
-    const int idx = lo + lane;
-    if (idx < hi) {
-      const int g = ids[idx];
-      s_gid[warp][lane] = g;
-      stage_rec(rec, g, s_rec[warp][lane], ox, oy);
+  // double-buffered staging (back to front): ids two batches ahead, records one ahead
+  int hi = rg.x + maxn;
+  if (hi > rg.x) {
+    const int l0 = max(rg.x, hi - 32);
+    if (l0 + lane < hi) {
+      const int g = ids[l0 + lane];
+      s_gid[warp][0][lane] = g;
+      gather_rec_async(rec, g, s_rec[warp][0][lane]);
     }
+  }
+  cp_async_commit();
+  int nxt_id = -1;
+  if (hi - 32 > rg.x) {
+    const int l1 = max(rg.x, hi - 64);
+    if (l1 + lane < hi - 32) nxt_id = ids[l1 + lane];
+  }
+  int buf = 0;
+  for (; hi > rg.x; hi -= 32, buf ^= 1) {
+    const int lo = max(rg.x, hi - 32);
+    if (nxt_id >= 0) {
+      s_gid[warp][buf ^ 1][lane] = nxt_id;
+      gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
+    }
+    cp_async_commit();
+    nxt_id = -1;
+    if (hi - 64 > rg.x) {
+      const int l2 = max(rg.x, hi - 96);
+      if (l2 + lane < hi - 64) nxt_id = ids[l2 + lane];
+    }
+    cp_async_wait<1>();
+    __syncwarp();
+    if (lo + lane < hi) finish_stage(s_rec[warp][buf][lane], ox, oy);
     __syncwarp();
     for (int j = hi - 1 - lo; j >= 0; --j) {
-      const StagedRec q = load_staged(s_rec[warp][j]);
+      const StagedRec q = load_staged(s_rec[warp][buf][j]);
       const int pos = lo + j - rg.x;
       uint32_t m = q.mask;
 #pragma unroll
@@ -382,6 +464,49 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
       float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f, acc_o = 0.f;
       float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, s2 = 0.f;
       bool any = false;  // warp-uniform
+      if (!kExact && __popc(m) >= kDenseBlocksBwd) {
+        // dense: all 8 blocks without branches; invalid pixels contribute exact zeros
+        const float dy0 = q.my - pyf0;
+        float Gv[kPix], rawv[kPix];
+        bool vv[kPix];
+        bool lane_any = false;
+#pragma unroll
+        for (int b = 0; b < kPix; ++b) {
+          const Eval& e = (b & 1) ? e1 : e0;
+          const float dy = dy0 - 4.f * (b >> 1);
+          const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
+          Gv[b] = ex2_approx(p2);
+          rawv[b] = q.o * Gv[b];
+          vv[b] = ((m >> b) & 1u) && pos < n[b] && (p2 <= 0.f) && (fminf(kAlphaCap, rawv[b]) >= kAlphaMin);
+          lane_any |= vv[b];
+        }
+#pragma unroll
+        for (int b = 0; b < kPix; ++b) {
+          const bool valid = vv[b];
+          const float dy = dy0 - 4.f * (b >> 1);
+          const float alpha = fminf(kAlphaCap, rawv[b]);
+          const float inv = __fdividef(1.f, 1.f - alpha);
+          const float Tk = T[b] * inv;
+          const float w = valid ? alpha * Tk : 0.f;
+          const float u = fmaf(gr[b], q.r, fmaf(gg[b], q.g, fmaf(gb[b], q.b, gd[b] * q.z)));
+          const bool unc = valid && !(rawv[b] > kAlphaCap);
+          const float dal = unc ? (Tk * u - inv * Q[b]) : 0.f;
+          Q[b] = fmaf(w, u, Q[b]);
+          T[b] = valid ? Tk : T[b];
+          acc_r = fmaf(gr[b], w, acc_r);
+          acc_g = fmaf(gg[b], w, acc_g);
+          acc_b = fmaf(gb[b], w, acc_b);
+          acc_z = fmaf(gd[b], w, acc_z);
+          acc_o = fmaf(Gv[b], dal, acc_o);
+          const float dp = rawv[b] * dal;
+          const float t = dp * dy;
+          s0[b & 1] += dp;
+          s1[b & 1] += t;
+          s2 = fmaf(t, dy, s2);
+        }
+        any = __any_sync(kFull, lane_any);
+        m = 0;  // skip the sparse loop below
+      }
 #pragma unroll
       for (int b = 0; b < kPix; ++b) {
         if (!((m >> b) & 1u)) continue;
@@ -432,7 +557,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
         float out;
         int slot;
         warp_reduce10(v, lane, out, slot);
-        if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][j] + slot, out);
+        if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
       }
     }
     __syncwarp();
