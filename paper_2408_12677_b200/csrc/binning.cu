@@ -19,7 +19,11 @@
 // per-digit counts, resolves its global offsets by decoupled look-back over the
 // preceding partitions, stages keys in shared memory in block-sorted order and
 // writes them out as per-digit coalesced runs.
+#include <cstdlib>
+#include <cstring>
+
 #include "gsr_internal.cuh"
+#include "radix_rts.cuh"
 
 namespace gsr {
 namespace {
@@ -380,7 +384,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restri
     for (int i = 0; i < ITEMS; ++i) {
       const bool valid = base + i * 32 + lane < n;
       const uint32_t d = valid ? ((key[i] >> shift) & 255u) : (256u + lane);
-      const uint32_t peers = __match_any_sync(kFull, d);
+      const uint32_t peers = digit_peers(d & 255u, valid);
       const uint32_t r = __popc(peers & lt);
       uint32_t b = 0;
       if (valid) b = s_whist[warp][d];
@@ -502,6 +506,14 @@ Layout make_layout(int64_t P, int64_t cap) {
 
 }  // namespace
 
+// Radix pass implementation: decoupled look-back onesweep (default) or
+// reduce-then-scan (GSR_SORT=rts).  Both produce identical output; onesweep measured
+// faster end to end on B200 (profiles/r01/sort_ab.txt).
+bool use_rts() {
+  const char* e = std::getenv("GSR_SORT");
+  return e && std::strcmp(e, "rts") == 0;
+}
+
 size_t bin_workspace_bytes(int64_t P, int64_t cap, int /*num_tiles*/) { return make_layout(P, cap).total; }
 
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes, int64_t cap,
@@ -546,11 +558,18 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   uint32_t* vin = dv0;
   uint32_t* kout = dk1;
   uint32_t* vout = dv1;
+  const bool rts_mode = use_rts();
   for (int pass = 0; pass < 4; ++pass) {
-    k_onesweep<uint32_t, kRsItemsDepth><<<rs_grid_d, kRsThreads, 0, s>>>(kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256,
-                                                           lbd + (int64_t)pass * L.depth_parts * 256,
-                                                           &ctr->part[2 + pass], 8 * pass);
-    count_launch();
+    uint32_t* lb = lbd + (int64_t)pass * L.depth_parts * 256;
+    if (rts_mode) {
+      rts::radix_pass<uint32_t, kRsItemsDepth>(kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256, lb, L.depth_parts,
+                                               8 * pass, s);
+    } else {
+      k_onesweep<uint32_t, kRsItemsDepth><<<rs_grid_d, kRsThreads, 0, s>>>(kin, vin, kout, vout, &ctr->V, P,
+                                                                           ghist + pass * 256, lb,
+                                                                           &ctr->part[2 + pass], 8 * pass);
+      count_launch();
+    }
     std::swap(kin, kout);
     std::swap(vin, vout);
   }
@@ -564,19 +583,26 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   count_launch();
   const int rs_grid_t = (int)std::max<int64_t>(1, std::min<int64_t>((cap + kRsTileKeys - 1) / kRsTileKeys, (int64_t)nsm * 3));
   const uint16_t* final_keys;
+  uint32_t* lbt1 = lbt + (int64_t)L.tile_parts * 256;
+  uint32_t* ids_out = reinterpret_cast<uint32_t*>(sorted_ids);
+  auto tile_pass = [&](const uint16_t* ki, const uint32_t* vi, uint16_t* ko, uint32_t* vo, int pass) {
+    uint32_t* lb = pass == 0 ? lbt : lbt1;
+    if (rts_mode) {
+      rts::radix_pass<uint16_t, kRsItemsKeys>(ki, vi, ko, vo, &ctr->K, cap, ghist + (4 + pass) * 256, lb,
+                                              L.tile_parts, 8 * pass, s);
+    } else {
+      k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(ki, vi, ko, vo, &ctr->K, cap,
+                                                                          ghist + (4 + pass) * 256, lb,
+                                                                          &ctr->part[6 + pass], 8 * pass);
+      count_launch();
+    }
+  };
   if (NT <= 256) {
-    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, reinterpret_cast<uint32_t*>(sorted_ids),
-                                                           &ctr->K, cap, ghist + 4 * 256, lbt, &ctr->part[6], 0);
-    count_launch();
+    tile_pass(tk0, tv0, tk1, ids_out, 0);
     final_keys = tk1;
   } else {
-    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk0, tv0, tk1, tv1, &ctr->K, cap, ghist + 4 * 256, lbt,
-                                                           &ctr->part[6], 0);
-    count_launch();
-    k_onesweep<uint16_t, kRsItemsKeys><<<rs_grid_t, kRsThreads, 0, s>>>(tk1, tv1, tk0, reinterpret_cast<uint32_t*>(sorted_ids),
-                                                           &ctr->K, cap, ghist + 5 * 256,
-                                                           lbt + (int64_t)L.tile_parts * 256, &ctr->part[7], 8);
-    count_launch();
+    tile_pass(tk0, tv0, tk1, tv1, 0);
+    tile_pass(tk1, tv1, tk0, ids_out, 1);
     final_keys = tk0;
   }
   const int rg_grid = (int)std::min<int64_t>((cap + 255) / 256, (int64_t)nsm * 8);

@@ -32,6 +32,20 @@ gs_status check_launch(const char* what);
 void count_launch(int n = 1);
 int sm_count();  // SMs of the current device (cached per device)
 
+// Lanes of the warp holding the same 8-bit digit as this lane (stable multisplit
+// ranking): 8 bit-sliced ballots instead of __match_any_sync, whose SASS MATCH.ANY
+// measured ~40 cycles/warp of SM throughput on B200.  Invalid lanes
+// are nobody's peers; an invalid lane gets an arbitrary mask (callers ignore it).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
+  uint32_t peers = __ballot_sync(kFull, valid);
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const uint32_t bits = __ballot_sync(kFull, (d >> b) & 1u);
+    peers &= ((d >> b) & 1u) ? bits : ~bits;
+  }
+  return peers;
+}
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

@@ -6,9 +6,9 @@ import subprocess
 import sys
 
 
-def main(rep, regex, n=25):
+def main(rep, regex, n=25, skip=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{regex}",
-                          "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
+                          "--launch-count", "1", "--launch-skip", str(skip), "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr = rows[1]
     data = []
@@ -33,4 +33,5 @@ def main(rep, regex, n=25):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 25,
+         int(sys.argv[4]) if len(sys.argv) > 4 else 0)
