@@ -152,10 +152,16 @@ gs_status gs_bin_tiles(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HO
  * D += z alpha T (R17); finally C += T bg.
  *  rgb: float[3][H][W]   depth, T_final: float[H][W]   n_contrib: int32[H][W]
  *       (1 + position in the tile list of the last composited Gaussian, 0 if none)
- *  blended: nullable u64 counter, += number of composited (pixel, Gaussian) pairs. */
+ *  blended: nullable u64 counter, += number of composited (pixel, Gaussian) pairs.
+ *  key_blocks: nullable uint8[key_capacity]: for every sorted key the forward
+ *       visited, the mask of its tile's 8x4 pixel blocks (bit b: x offset 8 (b & 1),
+ *       y offset 4 (b >> 1)) in which that Gaussian was composited into >= 1 pixel.
+ *       Passing it to the backward lets it skip (tile, Gaussian) pairs that
+ *       contributed nothing (an exact property of this forward pass). */
 gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
                         const int32_t* sorted_ids, const int32_t* tile_ranges, float* rgb, float* depth,
-                        float* T_final, int32_t* n_contrib, unsigned long long* blended, void* stream);
+                        float* T_final, int32_t* n_contrib, unsigned long long* blended, uint8_t* key_blocks,
+                        void* stream);
 
 /* ---------------------------------------------------------------- gs_render_bwd
  * Exact derivative of gs_project + gs_render_fwd (R18) for upstream
@@ -166,13 +172,16 @@ gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  * them to every parameter row.
  *  ws: float[P][12] screen-space gradients (dmu_x, dmu_y, dA, dB, dC, dopacity,
  *      dr, dg, db, dz, pad, pad); >= gs_render_bwd_workspace() bytes; cleared here.
+ *  key_blocks: nullable, the forward's key masks for the SAME forward call (see
+ *      gs_render_fwd); NULL = derive the pixel blocks geometrically.
  *  grad: float[F][P_stride], ACCUMULATED (+=) so that views sum (R21).
  * Float atomics make grad order-dependent in the last bits. */
 size_t gs_render_bwd_workspace(const gs_scene* scene /*HOST*/);
 gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
                         gs_proj proj, const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
-                        const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, void* ws,
-                        size_t ws_bytes, float* grad, void* stream);
+                        const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
+                        const uint8_t* key_blocks /*nullable*/, void* ws, size_t ws_bytes, float* grad,
+                        void* stream);
 
 /* ---------------------------------------------------------------- batched backward
  * gs_render_bwd split in its two halves so that a batch of views (R21) chains the
@@ -194,8 +203,8 @@ gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *    iteration, so that the optimiser need not zero grad). */
 gs_status gs_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
                                const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
-                               const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth, float* sgrad,
-                               void* stream);
+                               const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
+                               const uint8_t* key_blocks /*nullable*/, float* sgrad, void* stream);
 gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views]*/, const gs_scene* scene /*HOST*/,
                                const float* params, const uint8_t* const* flags /*HOST[n_views] of DEVICE*/,
                                float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,

@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
                                                                    float* __restrict__ out_rgb,
                                                                    float* __restrict__ out_d, float* __restrict__ out_T,
                                                                    int32_t* __restrict__ out_n,
-                                                                   unsigned long long* blended) {
+                                                                   unsigned long long* blended,
+                                                                   uint8_t* __restrict__ key_blocks) {
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x * kWarpsPerCta + warp;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
     if (b0 + lane < rg.y) finish_stage(s_rec[warp][buf][lane], ox, oy);
     __syncwarp();
     const int cnt = min(32, rg.y - b0);
+    uint32_t kb_mine = 0;  // lane j: 8x4 blocks in which key b0 + j composited >= 1 pixel
     for (int j = 0; j < cnt; ++j) {
       const StagedRec q = load_staged(s_rec[warp][buf][j]);
       const uint32_t m = q.mask & ~bdone;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
       const int pos1 = b0 + j - rg.x + 1;
       const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
       const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
+      uint32_t lm = 0;  // this lane's composited blocks for this key
       if (kExact) {
 #pragma unroll
         for (int b = 0; b < kPix; ++b) {
@@ -246,6 +249,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
             T[b] = Tn;
             n[b] = pos1;
             ++nblend;
+            lm |= 1u << b;
           }
         }
       } else {
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
             const bool stop = ac[b] && (Tn < kTStop);
             const bool comp = ac[b] && !stop;
             done |= stop ? (1u << b) : 0u;
+            lm |= comp ? (1u << b) : 0u;
             const float w = comp ? al[b] * T[b] : 0.f;
             Cr[b] = fmaf(q.r, w, Cr[b]);
             Cg[b] = fmaf(q.g, w, Cg[b]);
@@ -278,35 +283,38 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
             n[b] = comp ? pos1 : n[b];
             nblend += comp ? 1u : 0u;
           }
-          if ((j & 7) == 7) bdone = blocks_all(done);
-          continue;
-        }
-        // sparse: per block, skipped (warp-uniform) when masked out or no lane passes
+        } else {
+          // sparse: per block, skipped (warp-uniform) when masked out or no lane passes
 #pragma unroll
-        for (int b = 0; b < kPix; ++b) {
-          if (!((m >> b) & 1u)) continue;
-          const Eval& e = (b & 1) ? e1 : e0;
-          const float dy = dy0 - 4.f * (b >> 1);
-          const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
-          const float alpha = fminf(kAlphaCap, q.o * ex2_approx(p2));
-          const bool act = (p2 <= 0.f) && (alpha >= kAlphaMin) && !((done >> b) & 1u);
-          if (!__any_sync(kFull, act)) continue;
-          const float Tn = fmaf(-alpha, T[b], T[b]);
-          const bool stop = act && (Tn < kTStop);
-          const bool comp = act && !stop;
-          done |= stop ? (1u << b) : 0u;
-          const float w = comp ? alpha * T[b] : 0.f;
-          Cr[b] = fmaf(q.r, w, Cr[b]);
-          Cg[b] = fmaf(q.g, w, Cg[b]);
-          Cb[b] = fmaf(q.b, w, Cb[b]);
-          D[b] = fmaf(q.z, w, D[b]);
-          T[b] = comp ? Tn : T[b];
-          n[b] = comp ? pos1 : n[b];
-          nblend += comp ? 1u : 0u;
+          for (int b = 0; b < kPix; ++b) {
+            if (!((m >> b) & 1u)) continue;
+            const Eval& e = (b & 1) ? e1 : e0;
+            const float dy = dy0 - 4.f * (b >> 1);
+            const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
+            const float alpha = fminf(kAlphaCap, q.o * ex2_approx(p2));
+            const bool act = (p2 <= 0.f) && (alpha >= kAlphaMin) && !((done >> b) & 1u);
+            if (!__any_sync(kFull, act)) continue;
+            const float Tn = fmaf(-alpha, T[b], T[b]);
+            const bool stop = act && (Tn < kTStop);
+            const bool comp = act && !stop;
+            done |= stop ? (1u << b) : 0u;
+            lm |= comp ? (1u << b) : 0u;
+            const float w = comp ? alpha * T[b] : 0.f;
+            Cr[b] = fmaf(q.r, w, Cr[b]);
+            Cg[b] = fmaf(q.g, w, Cg[b]);
+            Cb[b] = fmaf(q.b, w, Cb[b]);
+            D[b] = fmaf(q.z, w, D[b]);
+            T[b] = comp ? Tn : T[b];
+            n[b] = comp ? pos1 : n[b];
+            nblend += comp ? 1u : 0u;
+          }
         }
       }
+      const uint32_t cm = __reduce_or_sync(kFull, lm);
+      kb_mine = (lane == j) ? cm : kb_mine;
       if ((j & 7) == 7) bdone = blocks_all(done);
     }
+    if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = (uint8_t)kb_mine;
     bdone = blocks_all(done);
     __syncwarp();
   }
@@ -383,6 +391,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
                                                                    const int32_t* __restrict__ n_contrib,
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
+                                                                   const uint8_t* __restrict__ key_blocks,
                                                                    float* __restrict__ sgrad) {
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   __shared__ int s_gid[kWarpsPerCta][2][32];
@@ -418,47 +427,60 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
     bmaxn[b] = __reduce_max_sync(kFull, n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
-  // double-buffered staging (back to front): ids two batches ahead, records one ahead
+  // double-buffered staging (back to front): ids + key masks two batches ahead,
+  // records one ahead.  With the forward's key masks, keys that composited nothing
+  // in this tile are neither gathered nor visited.
   int hi = rg.x + maxn;
-  if (hi > rg.x) {
-    const int l0 = max(rg.x, hi - 32);
-    if (l0 + lane < hi) {
-      const int g = ids[l0 + lane];
-      s_gid[warp][0][lane] = g;
-      gather_rec_async(rec, g, s_rec[warp][0][lane]);
+  auto load_key = [&](int h, int& id, uint32_t& kb) {
+    id = -1, kb = 0;
+    if (h > rg.x) {
+      const int l = max(rg.x, h - 32);
+      if (l + lane < h) {
+        id = ids[l + lane];
+        kb = key_blocks ? (uint32_t)key_blocks[l + lane] : 0xffu;
+      }
     }
-  }
+  };
+  auto stage = [&](int b, int id, uint32_t kb) {
+    if (id >= 0 && kb) {
+      s_gid[warp][b][lane] = id;
+      gather_rec_async(rec, id, s_rec[warp][b][lane]);
+    }
+  };
+  int id1;
+  uint32_t kb_cur, kb1;
+  load_key(hi, id1, kb_cur);
+  stage(0, id1, kb_cur);
   cp_async_commit();
-  int nxt_id = -1;
-  if (hi - 32 > rg.x) {
-    const int l1 = max(rg.x, hi - 64);
-    if (l1 + lane < hi - 32) nxt_id = ids[l1 + lane];
-  }
+  load_key(hi - 32, id1, kb1);
   int buf = 0;
   for (; hi > rg.x; hi -= 32, buf ^= 1) {
     const int lo = max(rg.x, hi - 32);
-    if (nxt_id >= 0) {
-      s_gid[warp][buf ^ 1][lane] = nxt_id;
-      gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
-    }
+    stage(buf ^ 1, id1, kb1);
     cp_async_commit();
-    nxt_id = -1;
-    if (hi - 64 > rg.x) {
-      const int l2 = max(rg.x, hi - 96);
-      if (l2 + lane < hi - 64) nxt_id = ids[l2 + lane];
-    }
+    int id2;
+    uint32_t kb2;
+    load_key(hi - 64, id2, kb2);
     cp_async_wait<1>();
     __syncwarp();
-    if (lo + lane < hi) finish_stage(s_rec[warp][buf][lane], ox, oy);
+    if (!key_blocks && lo + lane < hi) finish_stage(s_rec[warp][buf][lane], ox, oy);
     __syncwarp();
-    for (int j = hi - 1 - lo; j >= 0; --j) {
+    uint32_t live = __ballot_sync(kFull, kb_cur != 0);
+    while (live) {
+      const int j = 31 - __clz(live);  // back to front
+      live &= ~(1u << j);
       const StagedRec q = load_staged(s_rec[warp][buf][j]);
       const int pos = lo + j - rg.x;
-      uint32_t m = q.mask;
+      uint32_t m;
+      if (key_blocks) {
+        m = __shfl_sync(kFull, kb_cur, j);  // blocks the forward composited this key in
+      } else {
+        m = q.mask;
 #pragma unroll
-      for (int b = 0; b < kPix; ++b)
-        if (pos >= bmaxn[b]) m &= ~(1u << b);
-      if (m == 0) continue;
+        for (int b = 0; b < kPix; ++b)
+          if (pos >= bmaxn[b]) m &= ~(1u << b);
+        if (m == 0) continue;
+      }
       const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
       const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
       float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f, acc_o = 0.f;
@@ -561,28 +583,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
       }
     }
     __syncwarp();
+    kb_cur = kb1, id1 = id2, kb1 = kb2;
   }
+  cp_async_wait<0>();
 }
 
 }  // namespace
 
 void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
-                       cudaStream_t s) {
+                       uint8_t* key_blocks, cudaStream_t s) {
   const int NT = cam.TX * cam.TY;
   k_render_fwd<<<ceil_div(NT, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), rgb, depth, T_final,
-      n_contrib, blended);
+      n_contrib, blended, key_blocks);
   count_launch();
 }
 
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
                        const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                       float* sgrad, cudaStream_t s) {
+                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
   const int NT = cam.TX * cam.TY;
   k_render_bwd<<<ceil_div(NT, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), T_final, n_contrib,
-      g_rgb, g_depth, sgrad);
+      g_rgb, g_depth, key_blocks, sgrad);
   count_launch();
 }
 

@@ -95,11 +95,11 @@ class Library:
         lib.gs_bin_tiles_workspace.argtypes = [vp, i64, i64]
         lib.gs_bin_tiles_workspace.restype = C.c_size_t
         lib.gs_bin_tiles.argtypes = [vp, vp, GsProj, vp, C.c_size_t, i64, vp, vp, vp, vp, vp]
-        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_render_bwd_workspace.argtypes = [vp]
         lib.gs_render_bwd_workspace.restype = C.c_size_t
-        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
-        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
@@ -139,26 +139,26 @@ class Library:
         return (int(k_host.value) if sync else None), st
 
     def render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
-                   stream=None):
+                   key_blocks=None, stream=None):
         return self._check("gs_render_fwd", self.lib.gs_render_fwd(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(rgb), _ptr(depth),
-            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _stream(stream)))
+            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _ptr(key_blocks), _stream(stream)))
 
     def render_bwd_workspace(self, sc: GsScene) -> int:
         return int(self.lib.gs_render_bwd_workspace(C.byref(sc)))
 
     def render_bwd(self, cam, sc, params, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, ws,
-                   grad, stream=None):
+                   grad, key_blocks=None, stream=None):
         return self._check("gs_render_bwd", self.lib.gs_render_bwd(
             C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final),
-            _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(ws), ws.numel() * ws.element_size(), _ptr(grad),
-            _stream(stream)))
+            _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(ws),
+            ws.numel() * ws.element_size(), _ptr(grad), _stream(stream)))
 
     def render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, sgrad,
-                          stream=None):
+                          key_blocks=None, stream=None):
         return self._check("gs_render_bwd_screen", self.lib.gs_render_bwd_screen(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
-            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _stream(stream)))
+            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
 
     def project_bwd_views(self, cams, sc, params, flags, sgrads, grad, accumulate=True, stream=None):
         """cams: list of GsCamera; flags / sgrads: lists of device tensors (one per view)."""

@@ -55,6 +55,7 @@ class ViewBuffers:
         self.bin_ws = torch.empty(lib.bin_tiles_workspace(gcam, P, key_capacity) // 4 + 4, dtype=torch.int32,
                                   device=device)
         self.sorted_ids = torch.empty(max(key_capacity, 1), dtype=torch.int32, device=device)
+        self.key_blocks = torch.empty(max(key_capacity, 1) + 16, dtype=torch.uint8, device=device)
         self.ranges = torch.empty((self.NT, 2), dtype=torch.int32, device=device)
         npx = self.W * self.H
         self.rgb = torch.empty((3, self.H, self.W), dtype=torch.float32, device=device)
@@ -138,12 +139,13 @@ class Trainer:
         lib.bin_tiles(gcam, m.desc, proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
                       num_keys_dev=self.num_keys[v:v + 1])
         self._hook("render_fwd", "begin")
-        lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=self.blended)
+        lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=self.blended,
+                       key_blocks=b.key_blocks)
         self._hook("render_fwd", "end")
         lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
         self._hook("render_bwd", "begin")
         lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
-                              self.sgrad[slot])
+                              self.sgrad[slot], key_blocks=b.key_blocks)
         self._hook("render_bwd", "end")
         return gcam
 

@@ -1,0 +1,91 @@
+"""The forward's per-key block masks (gs_render_fwd key_blocks) used by the backward
+give the same gradients as the geometric block masks, and both match the oracle
+(-m gpu).  Also checks the mask semantics directly: a key's bit b is set iff the
+Gaussian was composited into >= 1 pixel of 8x4 block b of its tile."""
+import numpy as np
+import pytest
+import torch
+
+import scenegen
+from oracle import gsref
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2408_12677_b200 import gsr
+    from gpu_helpers import DEV, gpu_bin, gpu_project, grad_mismatch
+
+
+def _run(name, seed=3):
+    lib = gsr.load()
+    kw = {"num_views": 1} if name in ("replica", "scannetpp") else {}
+    w = scenegen.make(name, **kw)
+    cam, scene = w.cameras[0], w.scene
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    K = b["K"]
+    H, W = cam.height, cam.width
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    rgb = torch.empty((3, H, W), device=DEV)
+    dep = torch.empty((H, W), device=DEV)
+    T = torch.empty((H, W), device=DEV)
+    n = torch.empty((H, W), dtype=torch.int32, device=DEV)
+    kb = torch.full((max(K, 1) + 16,), 0xAB, dtype=torch.uint8, device=DEV)
+    lib.render_fwd(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], rgb, dep, T, n, key_blocks=kb)
+    g_rgb, g_d = (torch.from_numpy(a).to(DEV) for a in scenegen.upstream_fields(seed, W, H))
+    out = {}
+    for mode in ("geometric", "keymask"):
+        ws = torch.zeros(scene.P * 12, device=DEV)
+        grad = torch.zeros((scene.F, scene.P_stride), device=DEV)
+        lib.render_bwd(gsr.camera(cam), sc, params, proj, b["sorted_ids"], b["ranges"], T, n, g_rgb, g_d, ws, grad,
+                       key_blocks=kb if mode == "keymask" else None)
+        torch.cuda.synchronize()
+        out[mode] = grad[:, :scene.P].cpu().numpy().astype(np.float64)
+    return w, cam, scene, b, n, kb, out, g_rgb, g_d
+
+
+@pytest.mark.parametrize("name", ["tiny", "small"])
+def test_keymask_backward_equals_geometric_and_oracle(name):
+    w, cam, scene, b, n, kb, out, g_rgb, g_d = _run(name)
+    # same composited sets; only the float-atomic summation order differs
+    assert grad_mismatch(out["keymask"], out["geometric"]).mean() <= 1e-4
+    ref, _ = gsref.render_bwd(cam, scene, g_rgb.cpu().numpy(), g_d.cpu().numpy(), mode=gsref.MIXED)
+    assert grad_mismatch(out["keymask"], ref).mean() <= 1e-3
+
+
+def test_keymask_semantics_small():
+    """Bit b of a key set  <=>  the oracle composites that Gaussian into >= 1 pixel of
+    block b of that tile (checked on every visited key of the small config)."""
+    w, cam, scene, b, n, kb, out, _, _ = _run("small")
+    ids = b["sorted_ids"].cpu().numpy()
+    ranges = b["ranges"].cpu().numpy()
+    kbn = kb.cpu().numpy()
+    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    pr = gsref.project(cam, scene, gsref.F32)
+    nref = ref["n_contrib"]
+    checked = 0
+    for t in range(0, cam.num_tiles, 7):
+        s, e = ranges[t]
+        ty, tx = divmod(t, cam.tiles_x)
+        tile_n = nref[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16]
+        maxn = int(tile_n.max())
+        for pos in range(maxn):
+            i = ids[s + pos]
+            want = 0
+            for blk in range(8):
+                x0, y0 = tx * 16 + 8 * (blk & 1), ty * 16 + 4 * (blk >> 1)
+                for yy in range(y0, min(y0 + 4, cam.height)):
+                    for xx in range(x0, min(x0 + 8, cam.width)):
+                        if pos >= nref[yy, xx]:
+                            continue
+                        dx, dy = pr["mu_x"][i] - xx, pr["mu_y"][i] - yy
+                        pw = -0.5 * (pr["conic_A"][i] * dx * dx + pr["conic_C"][i] * dy * dy) - pr["conic_B"][i] * dx * dy
+                        a = min(0.99, pr["opacity"][i] * np.exp(pw))
+                        if pw <= 0 and a >= 1 / 255:
+                            want |= 1 << blk
+                            break
+                    if want >> blk & 1:
+                        break
+            assert kbn[s + pos] == want, (t, pos, kbn[s + pos], want)
+            checked += 1
+    assert checked > 1000
