@@ -187,15 +187,22 @@ def main():
     del tgt_model, tg
     torch.cuda.empty_cache()
 
+    # scannetpp / large: a batch of views per iteration, sharded over ranks, gradient
+    # all-reduced (strong scaling).  tiny / small / replica: one view per iteration
+    # (PAPER.md:149), cycling through the poses; N > 1 runs independent replicas.
+    batched = args.config in ("scannetpp", "large")
     allreduce = None
-    if world > 1:
+    if world > 1 and batched:
         allreduce = lambda g: dist.all_reduce(g, op=dist.ReduceOp.SUM)  # noqa: E731
+
+    def step_views(i):
+        return my_views if batched else [my_views[i % len(my_views)]]
     tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce)
     stream = torch.cuda.current_stream()
 
     # --- warm-up
-    for _ in range(args.warmup):
-        tr.step(my_views)
+    for i in range(args.warmup):
+        tr.step(step_views(i))
     torch.cuda.synchronize()
 
     # --- timed region (device time, CUDA events, max over ranks)
@@ -224,8 +231,11 @@ def main():
     e0.record(stream)
     if args.profile:
         torch.cuda.nvtx.range_push("timed")
-    for _ in range(args.steps):
-        tr.step(my_views)
+    views_done = 0
+    for i in range(args.steps):
+        sv = step_views(args.warmup + i)
+        tr.step(sv)
+        views_done += len(sv)
     e1.record(stream)
     if args.profile:
         torch.cuda.nvtx.range_pop()
@@ -258,7 +268,7 @@ def main():
     if not args.no_e2e and not args.profile:
         host_t = {v: (targets[v][0].cpu().pin_memory(), targets[v][1].cpu().pin_memory()) for v in my_views}
         dev_t = {v: (torch.empty_like(targets[v][0]), torch.empty_like(targets[v][1])) for v in my_views}
-        h2d = sum(a.numel() * 4 + b.numel() * 4 for a, b in host_t.values())
+        h2d = sum(host_t[v][0].numel() * 4 + host_t[v][1].numel() * 4 for v in step_views(0))
         loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
         tr.blended.zero_()
         if world > 1:
@@ -266,12 +276,13 @@ def main():
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for _ in range(args.steps):
-            for v in my_views:
+        for i in range(args.steps):
+            sv = step_views(i)
+            for v in sv:
                 dev_t[v][0].copy_(host_t[v][0], non_blocking=True)
                 dev_t[v][1].copy_(host_t[v][1], non_blocking=True)
             tr.loss.zero_()
-            tr.step(my_views, targets_override=dev_t)
+            tr.step(sv, targets_override=dev_t)
             loss_host.copy_(tr.loss, non_blocking=True)
         s1.record(stream)
         torch.cuda.synchronize()
@@ -298,10 +309,11 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    n_views = len(my_views) * args.steps
+    n_views = views_done
     # evaluated pairs of the backward = sum of n_contrib over the views (untimed re-render)
     evaluated = 0
-    for v in my_views:
+    eval_views = my_views[:8]
+    for v in eval_views:
         pipeline.render(lib, model, cams[v], tr.buf)
         evaluated += int(tr.buf.n.sum().item())
     traffic = None
@@ -309,7 +321,7 @@ def main():
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get("k_render_bwd")
     except (OSError, ValueError):
         pass
-    roof = roofline(dev, peaks, clk, stage_ms, blended / max(world, 1) / n_views, evaluated / len(my_views), traffic)
+    roof = roofline(dev, peaks, clk, stage_ms, blended / max(world, 1) / n_views, evaluated / len(eval_views), traffic)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -327,10 +339,10 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "iters_per_s": iters, "higher_is_better": True,
-        "scaling": "strong" if args.config in ("scannetpp", "large") else "replicas",
+        "scaling": "strong" if batched else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "views_per_step": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
-                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}",
+        "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
+                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}" if batched else f"replicas x{world}",
                    "key_capacity": cap, "max_keys_per_view": kmax,
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
