@@ -34,6 +34,7 @@ def parse():
     ap.add_argument("--impl", default="gsr", choices=["gsr", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-morton", action="store_true", help="keep the generated Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
     return ap.parse_args()
@@ -177,6 +178,9 @@ def main():
     my_views = scenegen.shard_views(B, rank, world)
     model = pipeline.GaussianModel(w.scene, dev)
     tgt_model = pipeline.GaussianModel(w.target_scene, dev)
+    if not args.no_morton:  # setup-time layout: Gaussians in Morton order of their means
+        pipeline.spatially_order(lib, model)
+        pipeline.spatially_order(lib, tgt_model)
     my_cams = [cams[v] for v in my_views]
     K0 = max(pipeline.measure_keys(lib, model, my_cams, dev), pipeline.measure_keys(lib, tgt_model, my_cams, dev))
     cap = pipeline.default_capacity(K0)
@@ -344,6 +348,7 @@ def main():
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}" if batched else f"replicas x{world}",
                    "key_capacity": cap, "max_keys_per_view": kmax,
+                   "gaussian_order": "generated" if args.no_morton else "morton",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),

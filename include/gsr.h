@@ -220,6 +220,19 @@ gs_status gs_adam_step(const gs_scene* scene /*HOST*/, float* params, float* gra
                        const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
                        int zero_grad, void* stream);
 
+/* ---------------------------------------------------------------- layout (setup)
+ * gs_spatial_order: params_out = params_in with the Gaussians (columns) permuted into
+ * Morton (Z-curve) order of their means, 10 bits per axis inside the means'
+ * bounding box; ties keep the input order.  perm (nullable) int32[P] receives, for
+ * each new index, the old index.  A one-off layout transform (not a step of the
+ * method): the visible subset of a view then occupies contiguous sectors of every
+ * SoA row, which is what the per-view projection kernels stream.  Synchronous only
+ * in the sense of stream order; params_in and params_out must not alias.
+ *  ws: >= gs_spatial_order_workspace() bytes. */
+size_t gs_spatial_order_workspace(const gs_scene* scene /*HOST*/);
+gs_status gs_spatial_order(const gs_scene* scene /*HOST*/, const float* params_in, float* params_out, int32_t* perm,
+                           void* ws, size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- harness: Eq. 12
  * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
  * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */

@@ -294,6 +294,25 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams, const gs_scen
   return check_launch("gs_project_bwd_views");
 }
 
+size_t gs_spatial_order_workspace(const gs_scene* scene) {
+  if (!scene || scene->P < 0) return 0;
+  return spatial_order_workspace_bytes(scene->P);
+}
+
+gs_status gs_spatial_order(const gs_scene* scene, const float* params_in, float* params_out, int32_t* perm, void* ws,
+                           size_t ws_bytes, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_spatial_order"));
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_spatial_order", {{params_in, "params_in"}, {params_out, "params_out"}, {ws, "ws"}}));
+  if (params_in == params_out) {
+    set_error("gs_spatial_order: params_in and params_out must not alias");
+    return GS_ERR_ARG;
+  }
+  return launch_spatial_order(rows_of(scene), scene->P, scene->P_stride, params_in, params_out, perm, ws, ws_bytes,
+                              static_cast<cudaStream_t>(stream));
+}
+
 gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float* m, float* v, const float* lr_per_row,
                        float beta1, float beta2, float eps, int64_t step, int zero_grad, void* stream) {
   g_err[0] = 0;

@@ -623,4 +623,174 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   return GS_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// gs_spatial_order: permute the Gaussian store into Morton (Z-curve) order of the
+// means (10 bits per axis inside the means' bounding box).  A setup-time layout
+// transform: per-view SoA reads of the visible subset then touch contiguous
+// sectors instead of every sector of every row.  Reuses the onesweep passes.
+// ---------------------------------------------------------------------------
+namespace {
+
+__device__ __forceinline__ uint32_t f2ord(float f) {  // order-preserving float -> uint
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {  // 10 bits -> every third bit
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+struct OrderCtr {
+  uint32_t bmin[3], bmax[3];
+  uint32_t part[4];
+  unsigned long long n;
+};
+
+__global__ void __launch_bounds__(256) k_bbox(int64_t P, int64_t S, const float* __restrict__ prm, OrderCtr* ctr) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) ctr->n = (unsigned long long)P;
+  uint32_t mn[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, mx[3] = {0u, 0u, 0u};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = prm[a * S + i];
+      if (isfinite(v)) {
+        const uint32_t o = f2ord(v);
+        mn[a] = min(mn[a], o);
+        mx[a] = max(mx[a], o);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    mn[a] = __reduce_min_sync(kFull, mn[a]);
+    mx[a] = __reduce_max_sync(kFull, mx[a]);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&ctr->bmin[a], mn[a]);
+      atomicMax(&ctr->bmax[a], mx[a]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_morton(int64_t P, int64_t S, const float* __restrict__ prm,
+                                                const OrderCtr* __restrict__ ctr, uint32_t* __restrict__ keys,
+                                                uint32_t* __restrict__ vals, uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t s_hist[4][256];
+  for (int t = threadIdx.x; t < 1024; t += 256) (&s_hist[0][0])[t] = 0;
+  __syncthreads();
+  float lo[3], sc[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = ord2f(ctr->bmin[a]);
+    const float ext = ord2f(ctr->bmax[a]) - lo[a];
+    sc[a] = ext > 0.f ? 1023.99f / ext : 0.f;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t code = 0;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = prm[a * S + i];
+      const float q = isfinite(v) ? fminf(fmaxf((v - lo[a]) * sc[a], 0.f), 1023.f) : 1023.f;
+      code |= spread10((uint32_t)q) << a;
+    }
+    keys[i] = code;
+    vals[i] = (uint32_t)i;
+    atomicAdd(&s_hist[0][code & 255], 1u);
+    atomicAdd(&s_hist[1][(code >> 8) & 255], 1u);
+    atomicAdd(&s_hist[2][(code >> 16) & 255], 1u);
+    atomicAdd(&s_hist[3][code >> 24], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 1024; t += 256) {
+    const uint32_t c = (&s_hist[0][0])[t];
+    if (c) atomicAdd(&ghist[t], c);
+  }
+}
+
+// params_out[r][j] = params_in[r][perm[j]] for j < P; padding columns zeroed.
+__global__ void __launch_bounds__(256) k_gather_rows(int64_t F, int64_t P, int64_t S, const float* __restrict__ in,
+                                                     const uint32_t* __restrict__ perm, float* __restrict__ out) {
+  const int64_t n = F * S;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = k / S, j = k - r * S;
+    out[k] = j < P ? in[r * S + perm[j]] : 0.f;
+  }
+}
+
+struct OrderLayout {
+  size_t ctr, ghist, lb, zero_end, k0, k1, v0, v1, total;
+  int64_t parts;
+};
+
+OrderLayout order_layout(int64_t P) {
+  OrderLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  L.parts = (P + kRsTileDepth - 1) / kRsTileDepth + 1;
+  L.ctr = take(sizeof(OrderCtr));
+  L.ghist = take(4 * 256 * sizeof(uint32_t));
+  L.lb = take(4 * L.parts * 256 * sizeof(uint32_t));
+  L.zero_end = o;
+  L.k0 = take(P * 4);
+  L.k1 = take(P * 4);
+  L.v0 = take(P * 4);
+  L.v1 = take(P * 4);
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+size_t spatial_order_workspace_bytes(int64_t P) { return order_layout(P).total; }
+
+gs_status launch_spatial_order(int64_t F, int64_t P, int64_t S, const float* params_in, float* params_out,
+                               int32_t* perm, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const OrderLayout L = order_layout(P);
+  if (ws_bytes < L.total) {
+    set_error("gs_spatial_order: workspace %zu B < required %zu B", ws_bytes, L.total);
+    return GS_ERR_ARG;
+  }
+  char* w = static_cast<char*>(ws);
+  OrderCtr* ctr = reinterpret_cast<OrderCtr*>(w + L.ctr);
+  uint32_t* ghist = reinterpret_cast<uint32_t*>(w + L.ghist);
+  if (cudaMemsetAsync(w, 0, L.zero_end, s) != cudaSuccess) return check_launch("gs_spatial_order memset");
+  if (cudaMemsetAsync(ctr->bmin, 0xff, sizeof(ctr->bmin), s) != cudaSuccess)  // bmax, part = 0 from above
+    return check_launch("gs_spatial_order init");
+  const int nsm = sm_count();
+  const int grid = (int)std::min<int64_t>((P + 255) / 256, (int64_t)nsm * 8);
+  uint32_t* kin = reinterpret_cast<uint32_t*>(w + L.k0);
+  uint32_t* kout = reinterpret_cast<uint32_t*>(w + L.k1);
+  uint32_t* vin = reinterpret_cast<uint32_t*>(w + L.v0);
+  uint32_t* vout = reinterpret_cast<uint32_t*>(w + L.v1);
+  k_bbox<<<grid, 256, 0, s>>>(P, S, params_in, ctr);
+  k_morton<<<grid, 256, 0, s>>>(P, S, params_in, ctr, kin, vin, ghist);
+  count_launch(2);
+  const int rs_grid = (int)std::min<int64_t>((P + kRsTileDepth - 1) / kRsTileDepth, (int64_t)nsm * 3);
+  for (int pass = 0; pass < 4; ++pass) {  // stable: equal codes keep index order
+    k_onesweep<uint32_t, kRsItemsDepth><<<rs_grid, kRsThreads, 0, s>>>(
+        kin, vin, kout, vout, &ctr->n, P, ghist + pass * 256, reinterpret_cast<uint32_t*>(w + L.lb) + (int64_t)pass * L.parts * 256,
+        &ctr->part[pass], 8 * pass);
+    count_launch();
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  k_gather_rows<<<(int)std::min<int64_t>((F * S + 255) / 256, (int64_t)nsm * 16), 256, 0, s>>>(F, P, S, params_in, vin,
+                                                                                               params_out);
+  count_launch();
+  if (perm && cudaMemcpyAsync(perm, vin, (size_t)P * 4, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return check_launch("gs_spatial_order perm");
+  return check_launch("gs_spatial_order");
+}
+
 }  // namespace gsr

@@ -62,6 +62,9 @@ size_t bin_workspace_bytes(int64_t P, int64_t key_capacity, int num_tiles);
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes,
                            int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges, int64_t* num_keys_dev,
                            int64_t* num_keys_host, cudaStream_t s);
+size_t spatial_order_workspace_bytes(int64_t P);
+gs_status launch_spatial_order(int64_t F, int64_t P, int64_t S, const float* params_in, float* params_out,
+                               int32_t* perm, void* ws, size_t ws_bytes, cudaStream_t s);
 // render.cu
 void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,

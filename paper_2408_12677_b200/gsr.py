@@ -102,9 +102,12 @@ class Library:
         lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
+        lib.gs_spatial_order_workspace.argtypes = [vp]
+        lib.gs_spatial_order_workspace.restype = C.c_size_t
+        lib.gs_spatial_order.argtypes = [vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
-                   "gs_project_bwd_views", "gs_adam_step", "gs_l1_loss_grad"):
+                   "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -168,6 +171,12 @@ class Library:
         sg = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in sgrads])
         return self._check("gs_project_bwd_views", self.lib.gs_project_bwd_views(
             n, cam_arr, C.byref(sc), _ptr(params), fl, sg, _ptr(grad), 1 if accumulate else 0, _stream(stream)))
+
+    def spatial_order(self, sc, params_in, params_out, perm=None, stream=None):
+        ws = torch.empty(max(int(self.lib.gs_spatial_order_workspace(C.byref(sc))), 16), dtype=torch.uint8,
+                         device=params_in.device)
+        return self._check("gs_spatial_order", self.lib.gs_spatial_order(
+            C.byref(sc), _ptr(params_in), _ptr(params_out), _ptr(perm), _ptr(ws), ws.numel(), _stream(stream)))
 
     def adam_step(self, sc, params, grad, m, v, lr_per_row, step, beta1=0.9, beta2=0.999, eps=1e-15, zero_grad=True,
                   stream=None):

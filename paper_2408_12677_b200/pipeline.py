@@ -42,6 +42,16 @@ class GaussianModel:
         return 4 * self.params.numel()
 
 
+def spatially_order(lib, model: GaussianModel):
+    """Permute the model's Gaussians into Morton order of their means (gs_spatial_order):
+    a setup-time layout transform; returns the permutation (new index -> old index)."""
+    out = torch.empty_like(model.params)
+    perm = torch.empty(max(model.P, 1), dtype=torch.int32, device=model.params.device)
+    lib.spatial_order(model.desc, model.params, out, perm)
+    model.params = out
+    return perm[:model.P]
+
+
 class ViewBuffers:
     """Device buffers for one view in flight (reused across views of equal size)."""
 
