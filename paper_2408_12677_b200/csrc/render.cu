@@ -4,83 +4,70 @@
 // eight 8x4 pixel blocks; lane (lx, ly) owns pixel (lx + 8 (b & 1), ly + 4 (b >> 1))
 // of every block b.  A warp gathers 32 of its tile's Gaussian records (48 B each, by
 // id, from L2) into shared memory with cp.async, one batch ahead of the one being
-// composited; on arrival each lane computes, for its record, the 8-bit mask of the
-// blocks the record's alpha >= 1/255 support can reach (exact ellipse-rectangle
-// test).  Blocks outside the mask, and blocks whose pixels have all terminated, are
-// skipped warp-uniformly; records reaching >= 3 blocks run a branch-free path over
-// all 8 blocks (8 independent chains), the others a per-block path.  Each lane's two
-// columns share x, so the x part of the exponent (A dx^2, B dx) is computed once per
-// record and a pixel costs one FADD + two FFMA + one MUFU.EX2.  The backward reverses the composite
-// with T_k = T_{k+1} / (1 - alpha_k), keeps the suffix term as one scalar per pixel
-// (Q = sum_ch g_ch S^C_ch + g_D S^D), accumulates the 10 screen-space gradient
-// components of the current Gaussian over the lane's 8 pixels in registers, and
-// reduces them across the warp (= the whole tile) with a 13-shuffle transpose
-// reduction so that 10 lanes issue ONE red.global.add.f32 instruction per (tile,
-// Gaussian): one atomic per warp per component, as the north_star asks.
+// composited; on arrival each lane rewrites its record into the form the inner loops
+// consume and computes the 8-bit mask of the blocks the record's alpha >= 1/255
+// support can reach (exact ellipse-rectangle test).  Only keys whose mask meets a
+// block with live pixels are visited; records reaching >= kDenseBlocks blocks run a
+// branch-free path over all 8 blocks (8 independent chains), the others a per-block
+// path skipped warp-uniformly where no lane passes.
 //
-// GSR_EXACT_EXP builds (libgsr_exact.so) evaluate the exponent, alpha, transmittance
-// and accumulation in the oracle's fp32 operation order with exp computed in double
-// (reading R9): the forward is then bit-identical to the fp32 oracle.
+// The inner loops are shaped by the measured B200 issue rates (profiles/r01/
+// pipe_rates.txt): FP32 FMA-pipe 1 warp-instruction/clk/SMSP, ALU pipe (compares,
+// selects, logic, FMNMX) 1/2, MUFU 1/8, and FFMA2 no faster than two FFMAs.  So:
+//  * log2(alpha) = lo2 + Ah dx^2 + Bh dx dy + Ch dy^2 with lo2 = log2(o) folded in
+//    (one FADD + two FFMA + one MUFU.EX2 per pixel, no FMUL by o);
+//  * a terminated pixel is marked by the sign of T (T := -|T|), which makes every
+//    later T - alpha T negative and so fails the same T >= 1e-4 test that decides
+//    compositing: no per-pixel "done" bit tests or selects;
+//  * the composite updates are predicated on one compare; the blended count is
+//    popc of the per-key lane mask, not a per-pixel add;
+//  * opacity <= 0.9 records skip the 0.99 cap (alpha cannot reach it), positive-
+//    definite conics skip the "power > 0" test (it cannot fire in exact arithmetic:
+//    reading R27); the rare others take a general per-block path with both.
+// The backward reverses the composite with T_k = T_{k+1} / (1 - alpha_k), keeps the
+// suffix term as one scalar per pixel (Q = sum_ch g_ch S^C_ch + g_D S^D), accumulates
+// the moments of dL/dpower over the lane's pixels per column (sum dp, dp dy, dp dy^2)
+// and forms the 10 screen-space gradient components once per key, reduces them across
+// the warp (= the whole tile) with a 13-shuffle transpose reduction so that 10 lanes
+// issue ONE red.global.add.f32 instruction per (tile, Gaussian).
+//
+// GSR_EXACT_EXP builds (libgsr_exact.so) run separate kernels that evaluate the
+// exponent, alpha, transmittance and accumulation in the oracle's fp32 operation
+// order with exp computed in double (reading R9): the forward is then bit-identical
+// to the fp32 oracle.
 #include "gsr_internal.cuh"
 
 namespace gsr {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
-constexpr int kPix = 8;  // pixels per lane
+constexpr int kPix = 8;             // pixels per lane
 constexpr int kDenseBlocks = 3;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
-constexpr int kDenseBlocksBwd = 6;  // bwd: same (its per-block body is ~4x longer)
+constexpr int kDenseBlocksBwd = 6;  // bwd: same (its per-block body is ~2x longer)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kTStop = 1e-4f;
 constexpr float kAlphaCap = 0.99f;
-
-#ifdef GSR_EXACT_EXP
-constexpr bool kExact = true;
-#else
-constexpr bool kExact = false;
-#endif
+constexpr float kUncappedO = 0.9f;         // o <= this: alpha = o exp(power) < 0.99 (no cap)
+constexpr uint32_t kFlagGeneral = 1u << 8;  // conic not positive definite: keep the power > 0 test
+constexpr uint32_t kFlagCap = 1u << 9;      // o > kUncappedO: the 0.99 cap may bind
+constexpr float kHalfL2e = -0.5f * kLog2e;  // Ah = kHalfL2e A, Ch = kHalfL2e C
+constexpr float kNegL2e = -kLog2e;          // Bh = kNegL2e B
 
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-
-// Per-(record, lane) constants for evaluating the Gaussian on the lane's column.
-struct Eval {
-  float a0, b0, c2;  // fast path: p2 = a0 + dy (b0 + c2 dy) = log2(e) * power
-  float A, B, C, dx; // exact path
-};
-
-__device__ __forceinline__ Eval make_eval(float mx, float A, float B, float C, float pxf) {
-  Eval e;
-  e.dx = mx - pxf;
-  e.A = A, e.B = B, e.C = C;
-  if (!kExact) {
-    e.a0 = (-0.5f * kLog2e) * A * e.dx * e.dx;
-    e.b0 = (-kLog2e * B) * e.dx;
-    e.c2 = -0.5f * kLog2e * C;
-  }
-  return e;
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-
-// Returns the power test result ("power <= 0") and G = exp(power).
-__device__ __forceinline__ bool eval_gauss(const Eval& e, float my, float pyf, float& G, float& dy) {
-  if (kExact) {
-    const float dxx = e.dx;
-    dy = __fsub_rn(my, pyf);
-    const float power = __fsub_rn(
-        __fmul_rn(-0.5f, __fadd_rn(__fmul_rn(__fmul_rn(e.A, dxx), dxx), __fmul_rn(__fmul_rn(e.C, dy), dy))),
-        __fmul_rn(__fmul_rn(e.B, dxx), dy));
-    G = (float)exp((double)power);
-    return !(power > 0.f);
-  } else {
-    dy = my - pyf;
-    const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
-    G = ex2_approx(p2);
-    return !(p2 > 0.f);
-  }
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // Support box of alpha >= 1/255: {d : 0.5 d^T Sigma_hat^{-1} d <= ln(255 o)} has
@@ -131,23 +118,9 @@ __device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, floa
   return m;
 }
 
-struct StagedRec {
-  float mx, my, z, o, A, B, C, r, g, b;
-  uint32_t mask;
-};
-
-__device__ __forceinline__ StagedRec load_staged(const float4* s) {
-  const float4 q0 = s[0], q1 = s[1], q2 = s[2];
-  StagedRec r;
-  r.mx = q0.x, r.my = q0.y, r.z = q0.z, r.o = q0.w;
-  r.A = q1.x, r.B = q1.y, r.C = q1.z, r.r = q1.w;
-  r.g = q2.x, r.b = q2.y, r.mask = __float_as_uint(q2.w);
-  return r;
-}
-
 // Asynchronous gather of one 48-B record into shared memory (cp.async, L2 -> SMEM,
 // bypassing registers) so that batch k+1's gathers are in flight while batch k is
-// composited; finish_stage then replaces the rect word with the block mask.
+// composited.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
@@ -163,189 +136,7 @@ __device__ __forceinline__ void gather_rec_async(const float4* __restrict__ rec,
   cp_async16(dst + 1, src + 1);
   cp_async16(dst + 2, src + 2);
 }
-__device__ __forceinline__ void finish_stage(float4* dst, int ox, int oy) {
-  const float4 q0 = dst[0], q1 = dst[1];
-  reinterpret_cast<float*>(dst + 2)[3] = __uint_as_float(block_mask(q0.x, q0.y, q1.x, q1.y, q1.z, q0.w, ox, oy));
-}
 
-// Blocks (8x4) all of whose pixels in this warp have bit set in `bits`.
-__device__ __forceinline__ uint32_t blocks_all(uint32_t bits) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int b = 0; b < 8; ++b) m |= __all_sync(kFull, (bits >> b) & 1u) ? (1u << b) : 0u;
-  return m;
-}
-
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
-                                                                   const int32_t* __restrict__ ids,
-                                                                   const int2* __restrict__ ranges,
-                                                                   float* __restrict__ out_rgb,
-                                                                   float* __restrict__ out_d, float* __restrict__ out_T,
-                                                                   int32_t* __restrict__ out_n,
-                                                                   unsigned long long* blended,
-                                                                   uint8_t* __restrict__ key_blocks) {
-  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarpsPerCta + warp;
-  if (tile >= cam.TX * cam.TY) return;
-  const int tx = tile % cam.TX, ty = tile / cam.TX;
-  const int ox = tx * kTile, oy = ty * kTile;
-  const int lx = lane & 7, ly = lane >> 3;
-  // pixel b of this lane: x = ox + lx + 8 (b & 1), y = oy + ly + 4 (b >> 1)
-  const float pxf0 = (float)(ox + lx), pxf1 = pxf0 + 8.f, pyf0 = (float)(oy + ly);
-  const int2 rg = ranges[tile];
-
-  float T[kPix], Cr[kPix], Cg[kPix], Cb[kPix], D[kPix];
-  int n[kPix];
-  uint32_t done = 0;
-#pragma unroll
-  for (int b = 0; b < kPix; ++b) {
-    T[b] = 1.f, Cr[b] = Cg[b] = Cb[b] = D[b] = 0.f, n[b] = 0;
-    if (ox + lx + 8 * (b & 1) >= cam.W || oy + ly + 4 * (b >> 1) >= cam.H) done |= 1u << b;
-  }
-  uint32_t nblend = 0;
-  uint32_t bdone = blocks_all(done);
-  // double-buffered staging: ids two batches ahead, records one batch ahead
-  if (rg.x + lane < rg.y) gather_rec_async(rec, ids[rg.x + lane], s_rec[warp][0][lane]);
-  cp_async_commit();
-  int nxt_id = (rg.x + 32 + lane < rg.y) ? ids[rg.x + 32 + lane] : -1;
-  int buf = 0;
-  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32, buf ^= 1) {
-    if (nxt_id >= 0) gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
-    cp_async_commit();
-    nxt_id = (b0 + 64 + lane < rg.y) ? ids[b0 + 64 + lane] : -1;
-    cp_async_wait<1>();
-    __syncwarp();
-    if (b0 + lane < rg.y) finish_stage(s_rec[warp][buf][lane], ox, oy);
-    __syncwarp();
-    const int cnt = min(32, rg.y - b0);
-    uint32_t kb_mine = 0;  // lane j: 8x4 blocks in which key b0 + j composited >= 1 pixel
-    for (int j = 0; j < cnt; ++j) {
-      const StagedRec q = load_staged(s_rec[warp][buf][j]);
-      const uint32_t m = q.mask & ~bdone;
-      if (m == 0) continue;
-      const int pos1 = b0 + j - rg.x + 1;
-      const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
-      const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
-      uint32_t lm = 0;  // this lane's composited blocks for this key
-      if (kExact) {
-#pragma unroll
-        for (int b = 0; b < kPix; ++b) {
-          if (!((m >> b) & 1u)) continue;
-          float G, dy;
-          const bool pok = eval_gauss((b & 1) ? e1 : e0, q.my, pyf0 + 4.f * (b >> 1), G, dy);
-          const float alpha = fminf(kAlphaCap, __fmul_rn(q.o, G));
-          const bool act = !((done >> b) & 1u) && pok && !(alpha < kAlphaMin);
-          const float Tn = __fmul_rn(T[b], __fsub_rn(1.f, alpha));
-          const bool stop = act && (Tn < kTStop);
-          if (stop) done |= 1u << b;
-          if (act && !stop) {
-            const float w = __fmul_rn(alpha, T[b]);
-            Cr[b] = __fadd_rn(Cr[b], __fmul_rn(q.r, w));
-            Cg[b] = __fadd_rn(Cg[b], __fmul_rn(q.g, w));
-            Cb[b] = __fadd_rn(Cb[b], __fmul_rn(q.b, w));
-            D[b] = __fadd_rn(D[b], __fmul_rn(q.z, w));
-            T[b] = Tn;
-            n[b] = pos1;
-            ++nblend;
-            lm |= 1u << b;
-          }
-        }
-      } else {
-        const float dy0 = q.my - pyf0;
-        if (__popc(m) >= kDenseBlocks) {
-          // dense: all 8 blocks without branches (8 independent chains for the
-          // scheduler); masked-out blocks and failing pixels contribute exact zeros
-          float al[kPix];
-          bool ac[kPix];
-#pragma unroll
-          for (int b = 0; b < kPix; ++b) {
-            const Eval& e = (b & 1) ? e1 : e0;
-            const float dy = dy0 - 4.f * (b >> 1);
-            const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
-            al[b] = fminf(kAlphaCap, q.o * ex2_approx(p2));
-            ac[b] = ((m >> b) & 1u) && (p2 <= 0.f) && (al[b] >= kAlphaMin) && !((done >> b) & 1u);
-          }
-#pragma unroll
-          for (int b = 0; b < kPix; ++b) {
-            const float Tn = fmaf(-al[b], T[b], T[b]);
-            const bool stop = ac[b] && (Tn < kTStop);
-            const bool comp = ac[b] && !stop;
-            done |= stop ? (1u << b) : 0u;
-            lm |= comp ? (1u << b) : 0u;
-            const float w = comp ? al[b] * T[b] : 0.f;
-            Cr[b] = fmaf(q.r, w, Cr[b]);
-            Cg[b] = fmaf(q.g, w, Cg[b]);
-            Cb[b] = fmaf(q.b, w, Cb[b]);
-            D[b] = fmaf(q.z, w, D[b]);
-            T[b] = comp ? Tn : T[b];
-            n[b] = comp ? pos1 : n[b];
-            nblend += comp ? 1u : 0u;
-          }
-        } else {
-          // sparse: per block, skipped (warp-uniform) when masked out or no lane passes
-#pragma unroll
-          for (int b = 0; b < kPix; ++b) {
-            if (!((m >> b) & 1u)) continue;
-            const Eval& e = (b & 1) ? e1 : e0;
-            const float dy = dy0 - 4.f * (b >> 1);
-            const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
-            const float alpha = fminf(kAlphaCap, q.o * ex2_approx(p2));
-            const bool act = (p2 <= 0.f) && (alpha >= kAlphaMin) && !((done >> b) & 1u);
-            if (!__any_sync(kFull, act)) continue;
-            const float Tn = fmaf(-alpha, T[b], T[b]);
-            const bool stop = act && (Tn < kTStop);
-            const bool comp = act && !stop;
-            done |= stop ? (1u << b) : 0u;
-            lm |= comp ? (1u << b) : 0u;
-            const float w = comp ? alpha * T[b] : 0.f;
-            Cr[b] = fmaf(q.r, w, Cr[b]);
-            Cg[b] = fmaf(q.g, w, Cg[b]);
-            Cb[b] = fmaf(q.b, w, Cb[b]);
-            D[b] = fmaf(q.z, w, D[b]);
-            T[b] = comp ? Tn : T[b];
-            n[b] = comp ? pos1 : n[b];
-            nblend += comp ? 1u : 0u;
-          }
-        }
-      }
-      const uint32_t cm = __reduce_or_sync(kFull, lm);
-      kb_mine = (lane == j) ? cm : kb_mine;
-      if ((j & 7) == 7) bdone = blocks_all(done);
-    }
-    if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = (uint8_t)kb_mine;
-    bdone = blocks_all(done);
-    __syncwarp();
-  }
-  cp_async_wait<0>();
-  const int64_t npix = (int64_t)cam.W * cam.H;
-#pragma unroll
-  for (int b = 0; b < kPix; ++b) {
-    const int px = ox + lx + 8 * (b & 1), py = oy + ly + 4 * (b >> 1);
-    if (px < cam.W && py < cam.H) {
-      const int64_t p = (int64_t)py * cam.W + px;
-      if (kExact) {
-        out_rgb[p] = __fadd_rn(Cr[b], __fmul_rn(T[b], cam.bg[0]));
-        out_rgb[npix + p] = __fadd_rn(Cg[b], __fmul_rn(T[b], cam.bg[1]));
-        out_rgb[2 * npix + p] = __fadd_rn(Cb[b], __fmul_rn(T[b], cam.bg[2]));
-      } else {
-        out_rgb[p] = fmaf(T[b], cam.bg[0], Cr[b]);
-        out_rgb[npix + p] = fmaf(T[b], cam.bg[1], Cg[b]);
-        out_rgb[2 * npix + p] = fmaf(T[b], cam.bg[2], Cb[b]);
-      }
-      out_d[p] = D[b];
-      out_T[p] = T[b];
-      out_n[p] = n[b];
-    }
-  }
-  if (blended) {
-    const uint32_t tot = __reduce_add_sync(kFull, nblend);
-    if (lane == 0 && tot) atomicAdd(blended, (unsigned long long)tot);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Transpose reduction of 10 per-lane values over the warp: 13 shuffles (vs 50 for
 // ten butterfly reductions).  On return, the 10 lanes with slot >= 0 hold the warp
 // total of component `slot`.
@@ -384,6 +175,313 @@ __device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, fl
   slot = (gi < 3 && s < 10 && !(lane & 1)) ? s : -1;
 }
 
+#ifndef GSR_EXACT_EXP
+// ===========================================================================
+// Fast path (libgsr.so)
+// ===========================================================================
+
+// Staged record (3 x float4 in shared memory), rewritten in place by its lane:
+//   (mx, my, z, lo2) (Ah, Bh, Ch, r) (g, b, o, mask | flags)
+// lo2 = log2(o), Ah = -log2(e)/2 A, Bh = -log2(e) B, Ch = -log2(e)/2 C, so that
+// log2(alpha) = lo2 + Ah dx^2 + Bh dx dy + Ch dy^2 = lo2 + log2(e) power.  Every value
+// is computed by one fixed instruction sequence, so the forward and the backward
+// take identical decisions.
+template <bool kMask>
+__device__ __forceinline__ void stage_fast(float4* dst, int ox, int oy) {
+  const float4 q0 = dst[0], q1 = dst[1];
+  const float A = q1.x, B = q1.y, C = q1.z, o = q0.w;
+  uint32_t fl = kMask ? block_mask(q0.x, q0.y, A, B, C, o, ox, oy) : 0xffu;
+  const float detc = __fsub_rn(__fmul_rn(A, C), __fmul_rn(B, B));
+  if (!(detc > 0.f && A > 0.f && C > 0.f)) fl |= kFlagGeneral;
+  if (!(o <= kUncappedO)) fl |= kFlagCap;
+  dst[0].w = lg2_approx(o);
+  dst[1] = make_float4(__fmul_rn(kHalfL2e, A), __fmul_rn(kNegL2e, B), __fmul_rn(kHalfL2e, C), q1.w);
+  float* q2 = reinterpret_cast<float*>(dst + 2);
+  q2[2] = o;
+  q2[3] = __uint_as_float(fl);
+}
+
+// Per (key, lane): the column terms of log2(alpha) for the lane's two pixel columns
+// and the four row offsets.  p2(b) = fma(dy_r, fma(Ch, dy_r, b0_e), a0_e), e = b & 1,
+// r = b >> 1.
+struct Geo {
+  float dx[2], a0[2], b0[2], dy[4];
+};
+__device__ __forceinline__ Geo make_geo(const float4& q0, const float4& q1, float pxf0, float pyf0) {
+  Geo g;
+  g.dx[0] = __fsub_rn(q0.x, pxf0);
+  g.dx[1] = __fsub_rn(g.dx[0], 8.f);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    g.a0[e] = __fmaf_rn(__fmul_rn(q1.x, g.dx[e]), g.dx[e], q0.w);
+    g.b0[e] = __fmul_rn(q1.y, g.dx[e]);
+  }
+  g.dy[0] = __fsub_rn(q0.y, pyf0);
+#pragma unroll
+  for (int r = 1; r < 4; ++r) g.dy[r] = __fsub_rn(g.dy[0], 4.f * r);
+  return g;
+}
+__device__ __forceinline__ float geo_p2(const Geo& g, float Ch, int b) {
+  const float dy = g.dy[b >> 1];
+  return __fmaf_rn(dy, __fmaf_rn(Ch, dy, g.b0[b & 1]), g.a0[b & 1]);
+}
+
+struct FwdPix {
+  float T[kPix], Cr[kPix], Cg[kPix], Cb[kPix], D[kPix];  // T < 0: terminated (|T| final)
+  int n[kPix];
+};
+
+// alpha of pixel b and the composite test "alpha >= 1/255 (and power <= 0)".
+template <bool kCap, bool kGen>
+__device__ __forceinline__ bool fwd_alpha(float p2, float lo2, float& al) {
+  al = ex2_approx(p2);
+  if (kCap) al = fminf(al, kAlphaCap);
+  bool c = al >= kAlphaMin;
+  if (kGen) c = c && (p2 <= lo2);
+  return c;
+}
+
+// Front-to-back step for pixel b: composite if T - alpha T stays >= 1e-4, else stop
+// the pixel (R16).  A terminated pixel (T < 0) fails the test forever.
+__device__ __forceinline__ void fwd_blend(FwdPix& px, int b, bool cond, float al, const float4& q0, float r,
+                                          float g, float bl, int pos1, uint32_t& lm) {
+  // Predicated PTX (the C form compiles to branches): with c = cond,
+  //   Tn = T - alpha T;  comp = c && Tn >= 1e-4;
+  //   if comp: C += col alpha T, D += z alpha T, n = pos1, lm |= bit
+  //   if c:    T = comp ? Tn : -|T|
+  asm("{\n\t"
+      ".reg .pred pc, pcomp, pstop;\n\t"
+      ".reg .f32 tn, w, na, ta;\n\t"
+      "setp.ne.u32 pc, %7, 0;\n\t"
+      "neg.f32 na, %8;\n\t"
+      "fma.rn.f32 tn, na, %0, %0;\n\t"
+      "setp.ge.and.f32 pcomp|pstop, tn, 0f38D1B717, pc;\n\t"
+      "mul.f32 w, %8, %0;\n\t"
+      "@pcomp fma.rn.f32 %1, %9, w, %1;\n\t"
+      "@pcomp fma.rn.f32 %2, %10, w, %2;\n\t"
+      "@pcomp fma.rn.f32 %3, %11, w, %3;\n\t"
+      "@pcomp fma.rn.f32 %4, %12, w, %4;\n\t"
+      "@pcomp mov.b32 %5, %13;\n\t"
+      "@pcomp or.b32 %6, %6, %14;\n\t"
+      "abs.f32 ta, %0;\n\t"
+      "neg.f32 ta, ta;\n\t"
+      "@pc selp.f32 %0, tn, ta, pcomp;\n\t"
+      "}"
+      : "+f"(px.T[b]), "+f"(px.Cr[b]), "+f"(px.Cg[b]), "+f"(px.Cb[b]), "+f"(px.D[b]), "+r"(px.n[b]), "+r"(lm)
+      : "r"((uint32_t)cond), "f"(al), "f"(r), "f"(g), "f"(bl), "f"(q0.z), "r"(pos1), "r"(1u << b));
+}
+
+template <bool kCap>
+__device__ __forceinline__ void fwd_dense(FwdPix& px, const Geo& g, const float4& q0, const float4& q1,
+                                          const float4& q2, int pos1, uint32_t& lm) {
+  float al[kPix];
+  bool c[kPix];
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) c[b] = fwd_alpha<kCap, false>(geo_p2(g, q1.z, b), q0.w, al[b]);
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) fwd_blend(px, b, c[b], al[b], q0, q1.w, q2.x, q2.y, pos1, lm);
+}
+
+template <bool kGen>
+__device__ __forceinline__ void fwd_sparse(FwdPix& px, uint32_t m, const Geo& g, const float4& q0, const float4& q1,
+                                           const float4& q2, int pos1, uint32_t& lm) {
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    if (!((m >> b) & 1u)) continue;
+    float al;
+    const bool c = fwd_alpha<true, kGen>(geo_p2(g, q1.z, b), q0.w, al);
+    if (!__any_sync(kFull, c)) continue;
+    fwd_blend(px, b, c, al, q0, q1.w, q2.x, q2.y, pos1, lm);
+  }
+}
+
+// Blocks (8x4) all of whose pixels in this warp have terminated.
+__device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
+  uint32_t d = 0;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) d |= (__float_as_uint(px.T[b]) >> 31) << b;
+  return __reduce_and_sync(kFull, d);
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
+                                                                   const int32_t* __restrict__ ids,
+                                                                   const int2* __restrict__ ranges,
+                                                                   float* __restrict__ out_rgb,
+                                                                   float* __restrict__ out_d, float* __restrict__ out_T,
+                                                                   int32_t* __restrict__ out_n,
+                                                                   unsigned long long* blended,
+                                                                   uint8_t* __restrict__ key_blocks) {
+  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarpsPerCta + warp;
+  if (tile >= cam.TX * cam.TY) return;
+  const int tx = tile % cam.TX, ty = tile / cam.TX;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int lx = lane & 7, ly = lane >> 3;
+  // pixel b of this lane: x = ox + lx + 8 (b & 1), y = oy + ly + 4 (b >> 1)
+  const float pxf0 = (float)(ox + lx), pyf0 = (float)(oy + ly);
+  const int2 rg = ranges[tile];
+
+  FwdPix px;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    const bool inside = ox + lx + 8 * (b & 1) < cam.W && oy + ly + 4 * (b >> 1) < cam.H;
+    px.T[b] = inside ? 1.f : -1.f;  // pixels outside the image start terminated
+    px.Cr[b] = px.Cg[b] = px.Cb[b] = px.D[b] = 0.f;
+    px.n[b] = 0;
+  }
+  uint32_t nblend = 0;
+  uint32_t bdone = dead_blocks(px);
+  // double-buffered staging: ids two batches ahead, records one batch ahead
+  if (rg.x + lane < rg.y) gather_rec_async(rec, ids[rg.x + lane], s_rec[warp][0][lane]);
+  cp_async_commit();
+  int nxt_id = (rg.x + 32 + lane < rg.y) ? ids[rg.x + 32 + lane] : -1;
+  int buf = 0;
+  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32, buf ^= 1) {
+    if (nxt_id >= 0) gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
+    cp_async_commit();
+    nxt_id = (b0 + 64 + lane < rg.y) ? ids[b0 + 64 + lane] : -1;
+    cp_async_wait<1>();
+    __syncwarp();
+    uint32_t my_fl = 0;
+    if (b0 + lane < rg.y) {
+      stage_fast<true>(s_rec[warp][buf][lane], ox, oy);
+      my_fl = __float_as_uint(reinterpret_cast<const float*>(&s_rec[warp][buf][lane][2])[3]);
+    }
+    __syncwarp();
+    uint32_t live = __ballot_sync(kFull, (my_fl & ~bdone & 0xffu) != 0u);
+    uint32_t kb_mine = 0;  // lane j: 8x4 blocks in which key b0 + j composited >= 1 pixel
+    int since = 0;
+    while (live) {
+      const int j = __ffs(live) - 1;
+      live &= live - 1;
+      const float4 q0 = s_rec[warp][buf][j][0], q1 = s_rec[warp][buf][j][1], q2 = s_rec[warp][buf][j][2];
+      const uint32_t fl = __float_as_uint(q2.w);
+      const uint32_t m = fl & ~bdone & 0xffu;
+      if (m == 0) continue;
+      const int pos1 = b0 + j - rg.x + 1;
+      const Geo g = make_geo(q0, q1, pxf0, pyf0);
+      uint32_t lm = 0;  // this lane's composited pixels (bit b = block b) for this key
+      if (fl & kFlagGeneral) {
+        fwd_sparse<true>(px, m, g, q0, q1, q2, pos1, lm);
+      } else if (__popc(m) >= kDenseBlocks) {
+        if (fl & kFlagCap)
+          fwd_dense<true>(px, g, q0, q1, q2, pos1, lm);
+        else
+          fwd_dense<false>(px, g, q0, q1, q2, pos1, lm);
+      } else {
+        fwd_sparse<false>(px, m, g, q0, q1, q2, pos1, lm);
+      }
+      nblend += __popc(lm);
+      const uint32_t cm = __reduce_or_sync(kFull, lm);
+      kb_mine = (lane == j) ? cm : kb_mine;
+      if (++since == 8) {
+        since = 0;
+        bdone = dead_blocks(px);
+        if (bdone == 0xffu) break;
+      }
+    }
+    if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = (uint8_t)kb_mine;
+    bdone = dead_blocks(px);
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  const int64_t npix = (int64_t)cam.W * cam.H;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
+    if (x < cam.W && y < cam.H) {
+      const int64_t p = (int64_t)y * cam.W + x;
+      const float T = fabsf(px.T[b]);
+      out_rgb[p] = fmaf(T, cam.bg[0], px.Cr[b]);
+      out_rgb[npix + p] = fmaf(T, cam.bg[1], px.Cg[b]);
+      out_rgb[2 * npix + p] = fmaf(T, cam.bg[2], px.Cb[b]);
+      out_d[p] = px.D[b];
+      out_T[p] = T;
+      out_n[p] = px.n[b];
+    }
+  }
+  if (blended) {
+    const uint32_t tot = __reduce_add_sync(kFull, nblend);
+    if (lane == 0 && tot) atomicAdd(blended, (unsigned long long)tot);
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct BwdPix {
+  float T[kPix], Q[kPix], gr[kPix], gg[kPix], gb[kPix], gd[kPix];
+  int n[kPix];
+};
+struct BwdAcc {
+  float r, g, b, z;       // sum_pixels g_ch w
+  float s0[2], s1[2], s2;  // per column: sum dp, sum dp dy; sum dp dy^2  (dp = dL/dpower)
+};
+
+// One pixel's reverse step (alpha_k, T_{k+1} = T, suffix Q): dL/dalpha =
+// (T u - Q) / (1 - alpha) with u = g . (c, z); capped alpha has no derivative (R18).
+template <bool kCap>
+__device__ __forceinline__ void bwd_pixel(BwdPix& px, int b, bool valid, float raw, float dy, float dy2,
+                                          const float4& q0, const float4& q1, const float4& q2, BwdAcc& a) {
+  const float al = kCap ? fminf(raw, kAlphaCap) : raw;
+  const float inv = rcp_approx(1.f - al);
+  const float ai = al * inv;
+  const float T = px.T[b];
+  const float Tk = T * inv;
+  const float u = fmaf(px.gr[b], q1.w, fmaf(px.gg[b], q2.x, fmaf(px.gb[b], q2.y, px.gd[b] * q0.z)));
+  const float x = fmaf(T, u, -px.Q[b]);
+  float dp = ai * x;
+  if (kCap) dp = (raw > kAlphaCap) ? 0.f : dp;
+  const float w = ai * T;
+  // predicated PTX (the C form compiles to branches)
+  asm("{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.u32 p, %9, 0;\n\t"
+      "@p fma.rn.f32 %0, %10, %11, %0;\n\t"
+      "@p mov.b32 %1, %12;\n\t"
+      "@p fma.rn.f32 %2, %13, %10, %2;\n\t"
+      "@p fma.rn.f32 %3, %14, %10, %3;\n\t"
+      "@p fma.rn.f32 %4, %15, %10, %4;\n\t"
+      "@p fma.rn.f32 %5, %16, %10, %5;\n\t"
+      "@p add.f32 %6, %6, %17;\n\t"
+      "@p fma.rn.f32 %7, %17, %18, %7;\n\t"
+      "@p fma.rn.f32 %8, %17, %19, %8;\n\t"
+      "}"
+      : "+f"(px.Q[b]), "+f"(px.T[b]), "+f"(a.r), "+f"(a.g), "+f"(a.b), "+f"(a.z), "+f"(a.s0[b & 1]),
+        "+f"(a.s1[b & 1]), "+f"(a.s2)
+      : "r"((uint32_t)valid), "f"(w), "f"(u), "f"(Tk), "f"(px.gr[b]), "f"(px.gg[b]), "f"(px.gb[b]), "f"(px.gd[b]),
+        "f"(dp), "f"(dy), "f"(dy2));
+}
+
+template <bool kCap>
+__device__ __forceinline__ bool bwd_dense(BwdPix& px, int pos, const Geo& g, const float (&dy2)[4], const float4& q0,
+                                          const float4& q1, const float4& q2, BwdAcc& a) {
+  float raw[kPix];
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) raw[b] = ex2_approx(geo_p2(g, q1.z, b));
+#pragma unroll
+  for (int b = 0; b < kPix; ++b)
+    bwd_pixel<kCap>(px, b, pos < px.n[b] && raw[b] >= kAlphaMin, raw[b], g.dy[b >> 1], dy2[b >> 1], q0, q1, q2, a);
+  return true;  // dense keys (>= 6 blocks composited in the forward) practically always contribute
+}
+
+template <bool kGen>
+__device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, const Geo& g, const float (&dy2)[4],
+                                           const float4& q0, const float4& q1, const float4& q2, BwdAcc& a) {
+  bool any = false;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    if (!((m >> b) & 1u)) continue;
+    const float p2 = geo_p2(g, q1.z, b);
+    const float raw = ex2_approx(p2);
+    bool valid = pos < px.n[b] && raw >= kAlphaMin;
+    if (kGen) valid = valid && (p2 <= q0.w);
+    if (!__any_sync(kFull, valid)) continue;
+    any = true;
+    bwd_pixel<true>(px, b, valid, raw, g.dy[b >> 1], dy2[b >> 1], q0, q1, q2, a);
+  }
+  return any;
+}
+
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges,
@@ -401,30 +499,29 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
   const int lx = lane & 7, ly = lane >> 3;
-  const float pxf0 = (float)(ox + lx), pxf1 = pxf0 + 8.f, pyf0 = (float)(oy + ly);
+  const float pxf0 = (float)(ox + lx), pyf0 = (float)(oy + ly);
   const int2 rg = ranges[tile];
   const int64_t npix = (int64_t)cam.W * cam.H;
 
-  float T[kPix], Q[kPix], gr[kPix], gg[kPix], gb[kPix], gd[kPix];
-  int n[kPix];
+  BwdPix px;
   int bmaxn[kPix];  // per 8x4 block: max n_contrib over its 32 pixels (warp-uniform)
   int maxn = 0;
 #pragma unroll
   for (int b = 0; b < kPix; ++b) {
-    const int px = ox + lx + 8 * (b & 1), py = oy + ly + 4 * (b >> 1);
-    if (px < cam.W && py < cam.H) {
-      const int64_t p = (int64_t)py * cam.W + px;
-      T[b] = T_final[p];
-      n[b] = n_contrib[p];
-      gr[b] = g_rgb[p];
-      gg[b] = g_rgb[npix + p];
-      gb[b] = g_rgb[2 * npix + p];
-      gd[b] = g_dep ? g_dep[p] : 0.f;
+    const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
+    if (x < cam.W && y < cam.H) {
+      const int64_t p = (int64_t)y * cam.W + x;
+      px.T[b] = T_final[p];
+      px.n[b] = n_contrib[p];
+      px.gr[b] = g_rgb[p];
+      px.gg[b] = g_rgb[npix + p];
+      px.gb[b] = g_rgb[2 * npix + p];
+      px.gd[b] = g_dep ? g_dep[p] : 0.f;
     } else {
-      T[b] = 1.f, n[b] = 0, gr[b] = gg[b] = gb[b] = gd[b] = 0.f;
+      px.T[b] = 1.f, px.n[b] = 0, px.gr[b] = px.gg[b] = px.gb[b] = px.gd[b] = 0.f;
     }
-    Q[b] = T[b] * (gr[b] * cam.bg[0] + gg[b] * cam.bg[1] + gb[b] * cam.bg[2]);
-    bmaxn[b] = __reduce_max_sync(kFull, n[b]);
+    px.Q[b] = px.T[b] * (px.gr[b] * cam.bg[0] + px.gg[b] * cam.bg[1] + px.gb[b] * cam.bg[2]);
+    bmaxn[b] = __reduce_max_sync(kFull, px.n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
   // double-buffered staging (back to front): ids + key masks two batches ahead,
@@ -463,17 +560,303 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
     load_key(hi - 64, id2, kb2);
     cp_async_wait<1>();
     __syncwarp();
-    if (!key_blocks && lo + lane < hi) finish_stage(s_rec[warp][buf][lane], ox, oy);
+    if (lo + lane < hi && kb_cur) {
+      if (key_blocks)
+        stage_fast<false>(s_rec[warp][buf][lane], ox, oy);
+      else
+        stage_fast<true>(s_rec[warp][buf][lane], ox, oy);
+    }
     __syncwarp();
     uint32_t live = __ballot_sync(kFull, kb_cur != 0);
     while (live) {
       const int j = 31 - __clz(live);  // back to front
       live &= ~(1u << j);
-      const StagedRec q = load_staged(s_rec[warp][buf][j]);
+      const float4 q0 = s_rec[warp][buf][j][0], q1 = s_rec[warp][buf][j][1], q2 = s_rec[warp][buf][j][2];
+      const uint32_t fl = __float_as_uint(q2.w);
       const int pos = lo + j - rg.x;
       uint32_t m;
       if (key_blocks) {
         m = __shfl_sync(kFull, kb_cur, j);  // blocks the forward composited this key in
+      } else {
+        m = fl & 0xffu;
+#pragma unroll
+        for (int b = 0; b < kPix; ++b)
+          if (pos >= bmaxn[b]) m &= ~(1u << b);
+        if (m == 0) continue;
+      }
+      const Geo g = make_geo(q0, q1, pxf0, pyf0);
+      float dy2[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) dy2[r] = g.dy[r] * g.dy[r];
+      BwdAcc a;
+      a.r = a.g = a.b = a.z = a.s2 = 0.f;
+      a.s0[0] = a.s0[1] = a.s1[0] = a.s1[1] = 0.f;
+      bool any;
+      if (fl & kFlagGeneral)
+        any = bwd_sparse<true>(px, m, pos, g, dy2, q0, q1, q2, a);
+      else if (__popc(m) >= kDenseBlocksBwd)
+        any = (fl & kFlagCap) ? bwd_dense<true>(px, pos, g, dy2, q0, q1, q2, a)
+                              : bwd_dense<false>(px, pos, g, dy2, q0, q1, q2, a);
+      else
+        any = bwd_sparse<false>(px, m, pos, g, dy2, q0, q1, q2, a);
+      if (any) {
+        // conic and mean gradients from the moments of dp over the tile:
+        // dpower/dA = -dx^2/2, dpower/dB = -dx dy, dpower/dC = -dy^2/2,
+        // dpower/dmu = -(A dx + B dy, B dx + C dy)
+        const float A = q1.x * (1.f / kHalfL2e), B = q1.y * (1.f / kNegL2e), C = q1.z * (1.f / kHalfL2e);
+        const float dx0 = g.dx[0], dx1 = g.dx[1];
+        const float sx = dx0 * a.s0[0] + dx1 * a.s0[1];
+        const float sxx = dx0 * dx0 * a.s0[0] + dx1 * dx1 * a.s0[1];
+        const float sy = a.s1[0] + a.s1[1];
+        const float sxy = dx0 * a.s1[0] + dx1 * a.s1[1];
+        float v[10];
+        v[0] = -(A * sx + B * sy);
+        v[1] = -(B * sx + C * sy);
+        v[2] = -0.5f * sxx;
+        v[3] = -sxy;
+        v[4] = -0.5f * a.s2;
+        v[5] = __fdividef(a.s0[0] + a.s0[1], q2.z);  // dalpha/do = exp(power) = alpha / o
+        v[6] = a.r;
+        v[7] = a.g;
+        v[8] = a.b;
+        v[9] = a.z;
+        float out;
+        int slot;
+        warp_reduce10(v, lane, out, slot);
+        if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
+      }
+    }
+    __syncwarp();
+    kb_cur = kb1, id1 = id2, kb1 = kb2;
+  }
+  cp_async_wait<0>();
+}
+
+#else  // GSR_EXACT_EXP
+// ===========================================================================
+// Exact path (libgsr_exact.so): the oracle's fp32 operation order, exp in double.
+// ===========================================================================
+struct StagedRec {
+  float mx, my, z, o, A, B, C, r, g, b;
+  uint32_t mask;
+};
+
+__device__ __forceinline__ StagedRec load_staged(const float4* s) {
+  const float4 q0 = s[0], q1 = s[1], q2 = s[2];
+  StagedRec r;
+  r.mx = q0.x, r.my = q0.y, r.z = q0.z, r.o = q0.w;
+  r.A = q1.x, r.B = q1.y, r.C = q1.z, r.r = q1.w;
+  r.g = q2.x, r.b = q2.y, r.mask = __float_as_uint(q2.w);
+  return r;
+}
+
+// replaces the rect word with the block mask
+__device__ __forceinline__ void finish_stage(float4* dst, int ox, int oy) {
+  const float4 q0 = dst[0], q1 = dst[1];
+  reinterpret_cast<float*>(dst + 2)[3] = __uint_as_float(block_mask(q0.x, q0.y, q1.x, q1.y, q1.z, q0.w, ox, oy));
+}
+
+// Blocks (8x4) all of whose pixels in this warp have bit set in `bits`.
+__device__ __forceinline__ uint32_t blocks_all(uint32_t bits) { return __reduce_and_sync(kFull, bits); }
+
+// power in the oracle's order; returns the "power <= 0" test and G = exp(power)
+__device__ __forceinline__ bool eval_gauss(float mx, float my, float A, float B, float C, float pxf, float pyf,
+                                           float& G, float& dx, float& dy) {
+  dx = __fsub_rn(mx, pxf);
+  dy = __fsub_rn(my, pyf);
+  const float power =
+      __fsub_rn(__fmul_rn(-0.5f, __fadd_rn(__fmul_rn(__fmul_rn(A, dx), dx), __fmul_rn(__fmul_rn(C, dy), dy))),
+                __fmul_rn(__fmul_rn(B, dx), dy));
+  G = (float)exp((double)power);
+  return !(power > 0.f);
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
+                                                                   const int32_t* __restrict__ ids,
+                                                                   const int2* __restrict__ ranges,
+                                                                   float* __restrict__ out_rgb,
+                                                                   float* __restrict__ out_d, float* __restrict__ out_T,
+                                                                   int32_t* __restrict__ out_n,
+                                                                   unsigned long long* blended,
+                                                                   uint8_t* __restrict__ key_blocks) {
+  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarpsPerCta + warp;
+  if (tile >= cam.TX * cam.TY) return;
+  const int tx = tile % cam.TX, ty = tile / cam.TX;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int lx = lane & 7, ly = lane >> 3;
+  const float pxf0 = (float)(ox + lx), pyf0 = (float)(oy + ly);
+  const int2 rg = ranges[tile];
+
+  float T[kPix], Cr[kPix], Cg[kPix], Cb[kPix], D[kPix];
+  int n[kPix];
+  uint32_t done = 0;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    T[b] = 1.f, Cr[b] = Cg[b] = Cb[b] = D[b] = 0.f, n[b] = 0;
+    if (ox + lx + 8 * (b & 1) >= cam.W || oy + ly + 4 * (b >> 1) >= cam.H) done |= 1u << b;
+  }
+  uint32_t nblend = 0;
+  uint32_t bdone = blocks_all(done);
+  if (rg.x + lane < rg.y) gather_rec_async(rec, ids[rg.x + lane], s_rec[warp][0][lane]);
+  cp_async_commit();
+  int nxt_id = (rg.x + 32 + lane < rg.y) ? ids[rg.x + 32 + lane] : -1;
+  int buf = 0;
+  for (int b0 = rg.x; b0 < rg.y && bdone != 0xffu; b0 += 32, buf ^= 1) {
+    if (nxt_id >= 0) gather_rec_async(rec, nxt_id, s_rec[warp][buf ^ 1][lane]);
+    cp_async_commit();
+    nxt_id = (b0 + 64 + lane < rg.y) ? ids[b0 + 64 + lane] : -1;
+    cp_async_wait<1>();
+    __syncwarp();
+    if (b0 + lane < rg.y) finish_stage(s_rec[warp][buf][lane], ox, oy);
+    __syncwarp();
+    const int cnt = min(32, rg.y - b0);
+    uint32_t kb_mine = 0;
+    for (int j = 0; j < cnt; ++j) {
+      const StagedRec q = load_staged(s_rec[warp][buf][j]);
+      const uint32_t m = q.mask & ~bdone;
+      if (m == 0) continue;
+      const int pos1 = b0 + j - rg.x + 1;
+      uint32_t lm = 0;
+#pragma unroll
+      for (int b = 0; b < kPix; ++b) {
+        if (!((m >> b) & 1u)) continue;
+        float G, dx, dy;
+        const bool pok = eval_gauss(q.mx, q.my, q.A, q.B, q.C, pxf0 + 8.f * (b & 1), pyf0 + 4.f * (b >> 1), G, dx, dy);
+        const float alpha = fminf(kAlphaCap, __fmul_rn(q.o, G));
+        const bool act = !((done >> b) & 1u) && pok && !(alpha < kAlphaMin);
+        const float Tn = __fmul_rn(T[b], __fsub_rn(1.f, alpha));
+        const bool stop = act && (Tn < kTStop);
+        if (stop) done |= 1u << b;
+        if (act && !stop) {
+          const float w = __fmul_rn(alpha, T[b]);
+          Cr[b] = __fadd_rn(Cr[b], __fmul_rn(q.r, w));
+          Cg[b] = __fadd_rn(Cg[b], __fmul_rn(q.g, w));
+          Cb[b] = __fadd_rn(Cb[b], __fmul_rn(q.b, w));
+          D[b] = __fadd_rn(D[b], __fmul_rn(q.z, w));
+          T[b] = Tn;
+          n[b] = pos1;
+          ++nblend;
+          lm |= 1u << b;
+        }
+      }
+      const uint32_t cm = __reduce_or_sync(kFull, lm);
+      kb_mine = (lane == j) ? cm : kb_mine;
+      if ((j & 7) == 7) bdone = blocks_all(done);
+    }
+    if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = (uint8_t)kb_mine;
+    bdone = blocks_all(done);
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+  const int64_t npix = (int64_t)cam.W * cam.H;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
+    if (x < cam.W && y < cam.H) {
+      const int64_t p = (int64_t)y * cam.W + x;
+      out_rgb[p] = __fadd_rn(Cr[b], __fmul_rn(T[b], cam.bg[0]));
+      out_rgb[npix + p] = __fadd_rn(Cg[b], __fmul_rn(T[b], cam.bg[1]));
+      out_rgb[2 * npix + p] = __fadd_rn(Cb[b], __fmul_rn(T[b], cam.bg[2]));
+      out_d[p] = D[b];
+      out_T[p] = T[b];
+      out_n[p] = n[b];
+    }
+  }
+  if (blended) {
+    const uint32_t tot = __reduce_add_sync(kFull, nblend);
+    if (lane == 0 && tot) atomicAdd(blended, (unsigned long long)tot);
+  }
+}
+
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
+                                                                   const int32_t* __restrict__ ids,
+                                                                   const int2* __restrict__ ranges,
+                                                                   const float* __restrict__ T_final,
+                                                                   const int32_t* __restrict__ n_contrib,
+                                                                   const float* __restrict__ g_rgb,
+                                                                   const float* __restrict__ g_dep,
+                                                                   const uint8_t* __restrict__ key_blocks,
+                                                                   float* __restrict__ sgrad) {
+  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
+  __shared__ int s_gid[kWarpsPerCta][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x * kWarpsPerCta + warp;
+  if (tile >= cam.TX * cam.TY) return;
+  const int tx = tile % cam.TX, ty = tile / cam.TX;
+  const int ox = tx * kTile, oy = ty * kTile;
+  const int lx = lane & 7, ly = lane >> 3;
+  const float pxf0 = (float)(ox + lx), pyf0 = (float)(oy + ly);
+  const int2 rg = ranges[tile];
+  const int64_t npix = (int64_t)cam.W * cam.H;
+
+  float T[kPix], Q[kPix], gr[kPix], gg[kPix], gb[kPix], gd[kPix];
+  int n[kPix];
+  int bmaxn[kPix];
+  int maxn = 0;
+#pragma unroll
+  for (int b = 0; b < kPix; ++b) {
+    const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
+    if (x < cam.W && y < cam.H) {
+      const int64_t p = (int64_t)y * cam.W + x;
+      T[b] = T_final[p];
+      n[b] = n_contrib[p];
+      gr[b] = g_rgb[p];
+      gg[b] = g_rgb[npix + p];
+      gb[b] = g_rgb[2 * npix + p];
+      gd[b] = g_dep ? g_dep[p] : 0.f;
+    } else {
+      T[b] = 1.f, n[b] = 0, gr[b] = gg[b] = gb[b] = gd[b] = 0.f;
+    }
+    Q[b] = T[b] * (gr[b] * cam.bg[0] + gg[b] * cam.bg[1] + gb[b] * cam.bg[2]);
+    bmaxn[b] = __reduce_max_sync(kFull, n[b]);
+    maxn = max(maxn, bmaxn[b]);
+  }
+  int hi = rg.x + maxn;
+  auto load_key = [&](int h, int& id, uint32_t& kb) {
+    id = -1, kb = 0;
+    if (h > rg.x) {
+      const int l = max(rg.x, h - 32);
+      if (l + lane < h) {
+        id = ids[l + lane];
+        kb = key_blocks ? (uint32_t)key_blocks[l + lane] : 0xffu;
+      }
+    }
+  };
+  auto stage = [&](int b, int id, uint32_t kb) {
+    if (id >= 0 && kb) {
+      s_gid[warp][b][lane] = id;
+      gather_rec_async(rec, id, s_rec[warp][b][lane]);
+    }
+  };
+  int id1;
+  uint32_t kb_cur, kb1;
+  load_key(hi, id1, kb_cur);
+  stage(0, id1, kb_cur);
+  cp_async_commit();
+  load_key(hi - 32, id1, kb1);
+  int buf = 0;
+  for (; hi > rg.x; hi -= 32, buf ^= 1) {
+    const int lo = max(rg.x, hi - 32);
+    stage(buf ^ 1, id1, kb1);
+    cp_async_commit();
+    int id2;
+    uint32_t kb2;
+    load_key(hi - 64, id2, kb2);
+    cp_async_wait<1>();
+    __syncwarp();
+    if (!key_blocks && lo + lane < hi) finish_stage(s_rec[warp][buf][lane], ox, oy);
+    __syncwarp();
+    uint32_t live = __ballot_sync(kFull, kb_cur != 0);
+    while (live) {
+      const int j = 31 - __clz(live);
+      live &= ~(1u << j);
+      const StagedRec q = load_staged(s_rec[warp][buf][j]);
+      const int pos = lo + j - rg.x;
+      uint32_t m;
+      if (key_blocks) {
+        m = __shfl_sync(kFull, kb_cur, j);
       } else {
         m = q.mask;
 #pragma unroll
@@ -481,65 +864,19 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
           if (pos >= bmaxn[b]) m &= ~(1u << b);
         if (m == 0) continue;
       }
-      const Eval e0 = make_eval(q.mx, q.A, q.B, q.C, pxf0);
-      const Eval e1 = make_eval(q.mx, q.A, q.B, q.C, pxf1);
       float acc_r = 0.f, acc_g = 0.f, acc_b = 0.f, acc_z = 0.f, acc_o = 0.f;
       float s0[2] = {0.f, 0.f}, s1[2] = {0.f, 0.f}, s2 = 0.f;
-      bool any = false;  // warp-uniform
-      if (!kExact && __popc(m) >= kDenseBlocksBwd) {
-        // dense: all 8 blocks without branches; invalid pixels contribute exact zeros
-        const float dy0 = q.my - pyf0;
-        float Gv[kPix], rawv[kPix];
-        bool vv[kPix];
-        bool lane_any = false;
-#pragma unroll
-        for (int b = 0; b < kPix; ++b) {
-          const Eval& e = (b & 1) ? e1 : e0;
-          const float dy = dy0 - 4.f * (b >> 1);
-          const float p2 = fmaf(dy, fmaf(e.c2, dy, e.b0), e.a0);
-          Gv[b] = ex2_approx(p2);
-          rawv[b] = q.o * Gv[b];
-          vv[b] = ((m >> b) & 1u) && pos < n[b] && (p2 <= 0.f) && (fminf(kAlphaCap, rawv[b]) >= kAlphaMin);
-          lane_any |= vv[b];
-        }
-#pragma unroll
-        for (int b = 0; b < kPix; ++b) {
-          const bool valid = vv[b];
-          const float dy = dy0 - 4.f * (b >> 1);
-          const float alpha = fminf(kAlphaCap, rawv[b]);
-          const float inv = __fdividef(1.f, 1.f - alpha);
-          const float Tk = T[b] * inv;
-          const float w = valid ? alpha * Tk : 0.f;
-          const float u = fmaf(gr[b], q.r, fmaf(gg[b], q.g, fmaf(gb[b], q.b, gd[b] * q.z)));
-          const bool unc = valid && !(rawv[b] > kAlphaCap);
-          const float dal = unc ? (Tk * u - inv * Q[b]) : 0.f;
-          Q[b] = fmaf(w, u, Q[b]);
-          T[b] = valid ? Tk : T[b];
-          acc_r = fmaf(gr[b], w, acc_r);
-          acc_g = fmaf(gg[b], w, acc_g);
-          acc_b = fmaf(gb[b], w, acc_b);
-          acc_z = fmaf(gd[b], w, acc_z);
-          acc_o = fmaf(Gv[b], dal, acc_o);
-          const float dp = rawv[b] * dal;
-          const float t = dp * dy;
-          s0[b & 1] += dp;
-          s1[b & 1] += t;
-          s2 = fmaf(t, dy, s2);
-        }
-        any = __any_sync(kFull, lane_any);
-        m = 0;  // skip the sparse loop below
-      }
+      bool any = false;
 #pragma unroll
       for (int b = 0; b < kPix; ++b) {
         if (!((m >> b) & 1u)) continue;
-        float G, dy;
-        const bool pok = eval_gauss((b & 1) ? e1 : e0, q.my, pyf0 + 4.f * (b >> 1), G, dy);
-        const float raw = kExact ? __fmul_rn(q.o, G) : q.o * G;
+        float G, dx, dy;
+        const bool pok = eval_gauss(q.mx, q.my, q.A, q.B, q.C, pxf0 + 8.f * (b & 1), pyf0 + 4.f * (b >> 1), G, dx, dy);
+        const float raw = __fmul_rn(q.o, G);
         const float alpha = fminf(kAlphaCap, raw);
         const bool valid = pos < n[b] && pok && !(alpha < kAlphaMin);
         if (!__any_sync(kFull, valid)) continue;
         any = true;
-        // predicated body: invalid lanes contribute exact zeros and keep their state
         const float inv = __fdividef(1.f, 1.f - alpha);
         const float Tk = T[b] * inv;
         const float w = valid ? alpha * Tk : 0.f;
@@ -560,11 +897,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
         s2 = fmaf(t, dy, s2);
       }
       if (any) {
-        const float dx0 = e0.dx, dx1 = e1.dx;
-        const float sx = dx0 * s0[0] + dx1 * s0[1];        // sum dp dx
-        const float sxx = dx0 * dx0 * s0[0] + dx1 * dx1 * s0[1];  // sum dp dx^2
-        const float sy = s1[0] + s1[1];                      // sum dp dy
-        const float sxy = dx0 * s1[0] + dx1 * s1[1];         // sum dp dx dy
+        const float dx0 = __fsub_rn(q.mx, pxf0), dx1 = __fsub_rn(q.mx, pxf0 + 8.f);
+        const float sx = dx0 * s0[0] + dx1 * s0[1];
+        const float sxx = dx0 * dx0 * s0[0] + dx1 * dx1 * s0[1];
+        const float sy = s1[0] + s1[1];
+        const float sxy = dx0 * s1[0] + dx1 * s1[1];
         float v[10];
         v[0] = -(q.A * sx + q.B * sy);
         v[1] = -(q.B * sx + q.C * sy);
@@ -587,6 +924,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   }
   cp_async_wait<0>();
 }
+#endif  // GSR_EXACT_EXP
 
 }  // namespace
 
