@@ -118,6 +118,52 @@ __device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, floa
   return m;
 }
 
+// Same contract as block_mask (a superset of the blocks holding a pixel with alpha >=
+// 1/255, the same 1% margin), computed per row of blocks instead of per block: the
+// ellipse E = {q(d) <= qmax} meets the horizontal slab y in [y0, y1] exactly over
+// the x-interval [xl, xr] with xr = hx if the rightmost point of E (y = -B hx / C) lies
+// in the slab, else the larger right end of E's chords on the slab's two edge lines
+// (x_right(y) is concave, so off its peak it is monotone on the slab); xl likewise.
+// Five edge-line chords (one sqrt each) serve the four block rows: ~1/2 the
+// instructions of block_mask's per-block edge minimisation.
+__device__ __forceinline__ uint32_t block_mask_rows(float mx, float my, float A, float B, float C, float o, int ox,
+                                                    int oy) {
+  const float L = __logf(255.f * o);
+  if (!(L >= -1e-3f)) return 0u;  // o < 1/255: alpha can never reach 1/255
+  const float det = A * C - B * B;
+  if (!(det > 0.f) || !(A > 0.f) || !(C > 0.f)) return 0xffu;
+  const float qmax = 2.f * fmaxf(L, 0.f) * 1.0201f + 1e-3f;  // (1.01)^2 margin, as block_mask
+  const float idet = __fdividef(1.f, det), iA = __fdividef(1.f, A);
+  const float hx = sqrtf(qmax * C * idet), hy = sqrtf(qmax * A * idet);
+  if (!(hx < 1e6f) || !(hy < 1e6f)) return 0xffu;
+  const float yR = -B * hx * __fdividef(1.f, C);  // y of the rightmost point; leftmost at -yR
+  const float fx0 = (float)ox - 0.5f - mx, fy0 = (float)oy - 0.5f - my;
+  const float kSlack = 1e-2f;  // px, on top of the 1% quadratic margin
+  float xr[5], xl[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const float y = fy0 + 4.f * k;
+    const float s = sqrtf(fmaxf(fmaf(-det, y * y, A * qmax), 0.f));
+    const bool in = fabsf(y) <= hy + kSlack;
+    xr[k] = in ? (s - B * y) * iA : -3.4e38f;
+    xl[k] = in ? (-s - B * y) * iA : 3.4e38f;
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float y0 = fy0 + 4.f * r, y1 = y0 + 4.f;
+    if (!(y1 >= -hy - kSlack && y0 <= hy + kSlack)) continue;
+    const float r_hi = (yR >= y0 && yR <= y1) ? hx : fmaxf(xr[r], xr[r + 1]);
+    const float l_lo = (-yR >= y0 && -yR <= y1) ? -hx : fminf(xl[r], xl[r + 1]);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const float x0 = fx0 + 8.f * c, x1 = x0 + 8.f;
+      if (r_hi + kSlack >= x0 && l_lo - kSlack <= x1) m |= 1u << (2 * r + c);
+    }
+  }
+  return m;
+}
+
 // Asynchronous gather of one 48-B record into shared memory (cp.async, L2 -> SMEM,
 // bypassing registers) so that batch k+1's gathers are in flight while batch k is
 // composited.
@@ -190,7 +236,7 @@ template <bool kMask>
 __device__ __forceinline__ void stage_fast(float4* dst, int ox, int oy) {
   const float4 q0 = dst[0], q1 = dst[1];
   const float A = q1.x, B = q1.y, C = q1.z, o = q0.w;
-  uint32_t fl = kMask ? block_mask(q0.x, q0.y, A, B, C, o, ox, oy) : 0xffu;
+  uint32_t fl = kMask ? block_mask_rows(q0.x, q0.y, A, B, C, o, ox, oy) : 0xffu;
   const float detc = __fsub_rn(__fmul_rn(A, C), __fmul_rn(B, B));
   if (!(detc > 0.f && A > 0.f && C > 0.f)) fl |= kFlagGeneral;
   if (!(o <= kUncappedO)) fl |= kFlagCap;
@@ -303,7 +349,8 @@ __device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
   return __reduce_and_sync(kFull, d);
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges,
                                                                    float* __restrict__ out_rgb,
@@ -311,9 +358,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
                                                                    int32_t* __restrict__ out_n,
                                                                    unsigned long long* blended,
                                                                    uint8_t* __restrict__ key_blocks) {
-  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
+  __shared__ float4 s_rec[WPC][2][32][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarpsPerCta + warp;
+  const int tile = blockIdx.x * WPC + warp;
   if (tile >= cam.TX * cam.TY) return;
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
@@ -482,7 +529,8 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
   return any;
 }
 
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
+template <int WPC>
+__global__ void __launch_bounds__(WPC * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges,
                                                                    const float* __restrict__ T_final,
@@ -491,10 +539,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
                                                                    const float* __restrict__ g_dep,
                                                                    const uint8_t* __restrict__ key_blocks,
                                                                    float* __restrict__ sgrad) {
-  __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
-  __shared__ int s_gid[kWarpsPerCta][2][32];
+  __shared__ float4 s_rec[WPC][2][32][3];
+  __shared__ int s_gid[WPC][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarpsPerCta + warp;
+  const int tile = blockIdx.x * WPC + warp;
   if (tile >= cam.TX * cam.TY) return;
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
@@ -926,25 +974,71 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
 }
 #endif  // GSR_EXACT_EXP
 
+#ifndef GSR_EXACT_EXP
+// Warps (= tiles) per CTA of the fast kernels.  Tile work is very uneven (list lengths
+// and early termination), and a CTA's slot is held until its slowest warp ends, so
+// small CTAs let the block scheduler balance tiles dynamically.  GSR_RENDER_WPC
+// (1, 2 or 4) overrides the default for A/B runs.
+int render_wpc() {
+  static const int wpc = [] {
+    const char* e = getenv("GSR_RENDER_WPC");
+    const int v = e ? atoi(e) : 1;
+    return (v == 2 || v == 4) ? v : 1;
+  }();
+  return wpc;
+}
+
+template <int WPC>
+void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+                    float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
+                    uint8_t* key_blocks, cudaStream_t s) {
+  k_render_fwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), rgb, depth, T_final,
+      n_contrib, blended, key_blocks);
+}
+template <int WPC>
+void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+                    const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
+                    const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
+  k_render_bwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), T_final, n_contrib,
+      g_rgb, g_depth, key_blocks, sgrad);
+}
+#endif
+
 }  // namespace
 
 void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                        uint8_t* key_blocks, cudaStream_t s) {
-  const int NT = cam.TX * cam.TY;
-  k_render_fwd<<<ceil_div(NT, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
+#ifndef GSR_EXACT_EXP
+  switch (render_wpc()) {
+    case 4: launch_fwd_wpc<4>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
+    case 2: launch_fwd_wpc<2>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
+    default: launch_fwd_wpc<1>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s);
+  }
+#else
+  k_render_fwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), rgb, depth, T_final,
       n_contrib, blended, key_blocks);
+#endif
   count_launch();
 }
 
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
                        const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                        const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
-  const int NT = cam.TX * cam.TY;
-  k_render_bwd<<<ceil_div(NT, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
+#ifndef GSR_EXACT_EXP
+  switch (render_wpc()) {
+    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
+    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
+    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s);
+  }
+#else
+  k_render_bwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), T_final, n_contrib,
       g_rgb, g_depth, key_blocks, sgrad);
+#endif
   count_launch();
 }
 
