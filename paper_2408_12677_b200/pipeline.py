@@ -141,7 +141,7 @@ class Trainer:
         if self.hooks is not None:
             self.hooks(stage, what)
 
-    def _view(self, v: int, slot: int, t_rgb, t_depth):
+    def _view(self, v: int, slot: int, t_rgb, t_depth, targets_ready=None, targets_consumed=None):
         lib, m, b, cam = self.lib, self.model, self.buf, self.cameras[v]
         gcam = gsr.camera(cam)
         proj = gsr.GsProj(b.proj.rec, b.proj.radius, b.proj.tiles, self.flags[slot].data_ptr())
@@ -152,7 +152,11 @@ class Trainer:
         lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=self.blended,
                        key_blocks=b.key_blocks)
         self._hook("render_fwd", "end")
+        if targets_ready is not None:
+            torch.cuda.current_stream().wait_event(targets_ready)
         lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
+        if targets_consumed is not None:
+            targets_consumed.record()
         self._hook("render_bwd", "begin")
         lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
                               self.sgrad[slot], key_blocks=b.key_blocks)
@@ -161,12 +165,56 @@ class Trainer:
 
     def step(self, views, targets_override=None):
         """One iteration over ``views``; targets_override: {v: (rgb, depth)} device tensors."""
+        def targets(k, v):
+            t = targets_override[v] if targets_override is not None else self.targets[v]
+            return t[0], t[1], None, None
+        self._run(views, targets, None)
+
+    def step_host(self, views, host_targets):
+        """One iteration with the targets streamed from (pinned) host memory:
+        host_targets {v: (rgb [3][H][W], depth [H][W])} CPU tensors.  View k's targets
+        are copied on a side stream into one of two device slots while view k-1 is
+        being rendered, and gs_l1_loss_grad of view k waits for its copy only; the
+        copy into a slot waits until the loss that last read it has run."""
+        dev = self.device
+        if getattr(self, "_slots", None) is None:
+            r0, d0 = host_targets[views[0]]
+            self._slots = [(torch.empty(r0.shape, dtype=torch.float32, device=dev),
+                            torch.empty(d0.shape, dtype=torch.float32, device=dev)) for _ in range(2)]
+            self._copy_stream = torch.cuda.Stream(device=dev)
+            self._ready = [torch.cuda.Event() for _ in range(2)]
+            self._free = [torch.cuda.Event() for _ in range(2)]
+
+        def issue(k):
+            s = k % 2
+            with torch.cuda.stream(self._copy_stream):
+                self._copy_stream.wait_event(self._free[s])
+                r, d = host_targets[views[k]]
+                self._slots[s][0].copy_(r, non_blocking=True)
+                self._slots[s][1].copy_(d, non_blocking=True)
+                self._ready[s].record(self._copy_stream)
+
+        def targets(k, v):
+            s = k % 2
+            return self._slots[s][0], self._slots[s][1], self._ready[s], self._free[s]
+
+        def after_view(k):
+            if k + 2 < len(views):
+                issue(k + 2)
+
+        for k in range(min(2, len(views))):
+            issue(k)
+        self._run(views, targets, after_view)
+
+    def _run(self, views, targets, after_view):
         m = self.model
         pending = []
         first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
-        for v in views:
-            t_rgb, t_depth = (targets_override[v] if targets_override is not None else self.targets[v])
-            pending.append(self._view(v, len(pending), t_rgb, t_depth))
+        for k, v in enumerate(views):
+            t_rgb, t_depth, ready, consumed = targets(k, v)
+            pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed))
+            if after_view is not None:
+                after_view(k)
             if len(pending) == self.chunk:
                 self._chain(pending, accumulate=not first)
                 pending, first = [], False

@@ -418,6 +418,30 @@ def test_trainer_step_runs_and_decreases_loss(lib):
     assert losses[-1] < losses[0]
 
 
+def test_trainer_step_host_matches_step(lib):
+    """Targets streamed from pinned host memory on the copy stream (Trainer.step_host,
+    the bench's e2e path) give the same iteration as device-resident targets."""
+    w = workload("small")
+    models = [pipeline.GaussianModel(w.scene, DEV) for _ in range(2)]
+    tgt_model = pipeline.GaussianModel(w.target_scene, DEV)
+    K = pipeline.measure_keys(lib, models[0], w.cameras, DEV)
+    cap = pipeline.default_capacity(K)
+    cams = [w.cameras[0]] * 5  # 5 views through 2 slots: slot reuse within one step
+    targets = pipeline.render_targets(lib, tgt_model, cams, DEV, cap)
+    host = {v: (targets[v][0].cpu().pin_memory(), targets[v][1].cpu().pin_memory()) for v in range(len(cams))}
+    trs = [pipeline.Trainer(lib, m, cams, targets, DEV, cap) for m in models]
+    for it in range(3):
+        trs[0].loss.zero_()
+        trs[1].loss.zero_()
+        trs[0].step(list(range(len(cams))))
+        trs[1].step_host(list(range(len(cams))), host)
+        torch.cuda.synchronize()
+        assert trs[1].loss.item() == pytest.approx(trs[0].loss.item(), rel=1e-5)
+    # float atomics reorder the gradient sums: compare elementwise up to that
+    p0, p1 = (m.params.cpu().numpy().astype(np.float64) for m in models)
+    assert grad_mismatch(p1, p0, rtol=1e-4, atol=1e-6).mean() <= 1e-3
+
+
 def test_batched_views_backward_matches_per_view(lib):
     """gs_render_bwd_screen x n + gs_project_bwd_views == sum of per-view gs_render_bwd
     (and the sgrad buffers are left zero)."""
