@@ -465,15 +465,225 @@ __global__ void k_ranges(const uint16_t* __restrict__ skeys, const Counters* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4' (default when the per-tile counters fit in shared memory): stable bucket
+// placement of the depth-ordered tile keys by tile id, replacing the two 8-bit radix
+// passes.  The K keys are cut into C equal chunks (one CTA each, 8 warps, each warp
+// a contiguous sub-chunk):
+//   k_tcount:   per chunk and tile, the key count           -> chist[c][t]
+//   k_tscan:    per tile, exclusive prefix over the chunks   -> chist[c][t], tot[t]
+//   k_tscatter: per chunk: the exclusive prefix of tot over the tiles (tile starts;
+//               chunk 0 writes tile_ranges), per-warp tile counts, their prefix over the
+//               warps, then each warp walks its keys in order and places key k of
+//               tile t at  start(t) + chist[c][t] + (warp prefix) + (earlier keys of
+//               t in this warp), ranking equal tiles within 32 keys by bit-sliced
+//               ballots.  Keys of a tile thus keep their depth order: the output is
+//               the same stable sort, in ~3 passes of 2-6 B/key and no look-back.
+// ---------------------------------------------------------------------------
+constexpr int kBkThreads = 256, kBkWarps = kBkThreads / 32;
+constexpr int kBkMaxChunks = 512;  // chist capacity (workspace); C = min(this, SMs x CTAs/SM)
+
+__device__ __forceinline__ void chunk_bounds(int64_t K, int C, int c, int w, int64_t& a, int64_t& b) {
+  const int64_t chunk = (K + C - 1) / C;
+  const int64_t k0 = min(K, (int64_t)c * chunk), k1 = min(K, k0 + chunk);
+  const int64_t sub = (k1 - k0 + kBkWarps - 1) / kBkWarps;
+  a = min(k1, k0 + (int64_t)w * sub);
+  b = min(k1, a + sub);
+}
+
+__global__ void __launch_bounds__(kBkThreads) k_tcount(const uint16_t* __restrict__ tkeys,
+                                                       const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
+                                                       uint32_t* __restrict__ chist) {
+  extern __shared__ uint32_t s_cnt[];  // [NT]
+  for (int t = threadIdx.x; t < NT; t += kBkThreads) s_cnt[t] = 0;
+  __syncthreads();
+  int64_t K = (int64_t)ctr->K;
+  if (K > cap) K = 0;
+  int64_t a, b;
+  chunk_bounds(K, C, blockIdx.x, 0, a, b);
+  const int64_t k0 = a;
+  chunk_bounds(K, C, blockIdx.x, kBkWarps - 1, a, b);
+  const int64_t k1 = b;
+  constexpr int G = 8;
+  for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += (int64_t)kBkThreads * G) {
+    uint32_t tt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t k = kb + (int64_t)kBkThreads * g;
+      tt[g] = k < k1 ? (uint32_t)tkeys[k] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (tt[g] != 0xffffffffu) atomicAdd(&s_cnt[tt[g]], 1u);
+  }
+  __syncthreads();
+  uint32_t* out = chist + (int64_t)blockIdx.x * NT;
+  for (int t = threadIdx.x; t < NT; t += kBkThreads) out[t] = s_cnt[t];
+}
+
+// CTA = 32 tiles x 8 warps; warp w scans chunks [w Cw, (w+1) Cw) of its lane's tile.
+__global__ void __launch_bounds__(kBkThreads) k_tscan(uint32_t* __restrict__ chist, int NT, int C,
+                                                      uint32_t* __restrict__ tot) {
+  __shared__ uint32_t s_part[kBkWarps][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int Cw = (C + kBkWarps - 1) / kBkWarps;
+  const int c0 = min(C, warp * Cw), c1 = min(C, c0 + Cw);
+  uint32_t s = 0;
+  if (t < NT)
+    for (int c = c0; c < c1; ++c) s += chist[(int64_t)c * NT + t];
+  s_part[warp][lane] = s;
+  __syncthreads();
+  uint32_t run = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kBkWarps; ++w) {
+    const uint32_t v = s_part[w][lane];
+    run += (w < warp) ? v : 0u;
+    all += v;
+  }
+  if (t < NT) {
+    for (int c = c0; c < c1; ++c) {
+      uint32_t* p = chist + (int64_t)c * NT + t;
+      const uint32_t v = *p;
+      *p = run;
+      run += v;
+    }
+    if (warp == 0) tot[t] = all;
+  }
+}
+
+// Lanes of the warp holding the same tile id (bits: id width); invalid lanes match nobody.
+__device__ __forceinline__ uint32_t tile_peers(uint32_t t, bool valid, int bits) {
+  uint32_t peers = __ballot_sync(kFull, valid);
+  for (int b = 0; b < bits; ++b) {
+    const uint32_t m = __ballot_sync(kFull, (t >> b) & 1u);
+    peers &= ((t >> b) & 1u) ? m : ~m;
+  }
+  return peers;
+}
+
+// Every CTA: s_base[t] := exclusive prefix of tot over the tiles (= start of tile t);
+// CTA 0 also writes tile_ranges.  Warp w scans tiles [w NT/8, (w+1) NT/8) 32 at a time.
+__device__ __forceinline__ void tile_starts(const uint32_t* __restrict__ tot, int NT, uint32_t* s_base,
+                                            uint32_t* s_wsum /*[8]*/, int2* __restrict__ ranges) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int per = (NT + kBkWarps - 1) / kBkWarps;
+  const int t0 = min(NT, warp * per), t1 = min(NT, t0 + per);
+  uint32_t sum = 0;
+  for (int t = t0 + lane; t < t1; t += 32) {
+    const uint32_t v = tot[t];
+    s_base[t] = v;
+    sum += v;
+  }
+  sum = __reduce_add_sync(kFull, sum);
+  if (lane == 0) s_wsum[warp] = sum;
+  __syncthreads();
+  uint32_t run = 0;
+  for (int w = 0; w < warp; ++w) run += s_wsum[w];
+  for (int tb = t0; tb < t1; tb += 32) {
+    const int t = tb + lane;
+    const uint32_t v = t < t1 ? s_base[t] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t start = run + x - v;
+    if (t < t1) {
+      s_base[t] = start;
+      if (blockIdx.x == 0) ranges[t] = make_int2((int)start, (int)(start + v));
+    }
+    run += __shfl_sync(kFull, x, 31);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restrict__ tkeys,
+                                                         const uint32_t* __restrict__ tvals,
+                                                         const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
+                                                         int tile_bits, const uint32_t* __restrict__ chist,
+                                                         const uint32_t* __restrict__ tot, int2* __restrict__ ranges,
+                                                         int32_t* __restrict__ out) {
+  extern __shared__ uint32_t s_dyn[];
+  __shared__ uint32_t s_wsum[kBkWarps];
+  uint32_t* s_base = s_dyn;                                // [NT] global position of this chunk's first key of t
+  const int NTp = (NT + 1) & ~1;                           // even row stride: 4-B aligned rows
+  uint16_t* s_w = reinterpret_cast<uint16_t*>(s_dyn + NT);  // [8][NTp] per-warp count, then running offset
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < NTp * kBkWarps / 2; i += kBkThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
+  tile_starts(tot, NT, s_base, s_wsum, ranges);  // (synchronises the CTA)
+  int64_t K = (int64_t)ctr->K;
+  if (K > cap) return;  // tot is all zero then: tile_ranges are empty
+  const uint32_t* ch = chist + (int64_t)blockIdx.x * NT;
+  for (int t = threadIdx.x; t < NT; t += kBkThreads) s_base[t] += ch[t];
+  int64_t a, b;
+  chunk_bounds(K, C, blockIdx.x, warp, a, b);
+  uint16_t* my = s_w + (int64_t)warp * NTp;
+  // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
+  constexpr int G = 8;  // 32-key groups in flight per warp
+  for (int64_t kb = a; kb < b; kb += 32 * G) {
+    uint32_t tt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t k = kb + 32 * g + lane;
+      tt[g] = k < b ? (uint32_t)tkeys[k] : 0xffffffffu;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (tt[g] != 0xffffffffu) atomicAdd(reinterpret_cast<uint32_t*>(my) + (tt[g] >> 1), 1u << (16 * (tt[g] & 1)));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < NT; t += kBkThreads) {
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < kBkWarps; ++w) {
+      const uint32_t v = s_w[w * NTp + t];
+      s_w[w * NTp + t] = (uint16_t)run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  const uint32_t lt = lanemask_lt();
+  for (int64_t kb = a; kb < b; kb += 32 * G) {
+    uint32_t tt[G], ii[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int64_t k = kb + 32 * g + lane;
+      const bool valid = k < b;
+      tt[g] = valid ? (uint32_t)tkeys[k] : 0xffffffffu;
+      ii[g] = valid ? tvals[k] : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (kb + 32 * g >= b) break;  // warp-uniform
+      const bool valid = tt[g] != 0xffffffffu;
+      const uint32_t t = valid ? tt[g] : 0u;
+      const uint32_t peers = tile_peers(t, valid, tile_bits);
+      const uint32_t r = __popc(peers & lt);
+      uint32_t run = 0;
+      if (valid) run = my[t];
+      __syncwarp();
+      if (valid && r == 0) my[t] = (uint16_t)(run + __popc(peers));
+      __syncwarp();
+      if (valid) out[s_base[t] + run + r] = (int32_t)ii[g];
+    }
+  }
+}
+
+// Shared memory of k_tscatter for NT tiles; bucket placement is used when it fits.
+size_t tscatter_smem(int NT) { return (size_t)NT * 4 + (size_t)((NT + 1) & ~1) * kBkWarps * 2; }
+constexpr size_t kSmemOptIn = 227 * 1024 - 1024;  // dynamic opt-in (static smem of the kernels < 1 KB)
+
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
-  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, total;
+  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, chist, tot, total;
   int64_t depth_parts, tile_parts;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-Layout make_layout(int64_t P, int64_t cap) {
+Layout make_layout(int64_t P, int64_t cap, int NT) {
   Layout L{};
   size_t o = 0;
   auto take = [&](size_t bytes) {
@@ -500,8 +710,18 @@ Layout make_layout(int64_t P, int64_t cap) {
   L.tk1 = take(cap * 2);
   L.tv0 = take(cap * 4);
   L.tv1 = take(cap * 4);
+  L.chist = take((size_t)kBkMaxChunks * NT * 4);
+  L.tot = take((size_t)NT * 4);
   L.total = o;
   return L;
+}
+
+// Tile placement: "bucket" (K4', default when its shared memory fits) or "radix"
+// (two onesweep / reduce-then-scan 8-bit passes; GSR_TILE_SORT=radix forces it).
+bool use_bucket(int NT) {
+  const char* e = std::getenv("GSR_TILE_SORT");
+  if (e && std::strcmp(e, "radix") == 0) return false;
+  return tscatter_smem(NT) <= kSmemOptIn;
 }
 
 }  // namespace
@@ -514,12 +734,15 @@ bool use_rts() {
   return e && std::strcmp(e, "rts") == 0;
 }
 
-size_t bin_workspace_bytes(int64_t P, int64_t cap, int /*num_tiles*/) { return make_layout(P, cap).total; }
+size_t bin_workspace_bytes(int64_t P, int64_t cap, int num_tiles) { return make_layout(P, cap, num_tiles).total; }
+
+gs_status finish_bin(const void* ctr, int64_t cap, int64_t* num_keys_host, cudaStream_t s);
 
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes, int64_t cap,
                            int32_t* sorted_ids, int32_t* tile_ranges, int64_t* num_keys_dev, int64_t* num_keys_host,
                            cudaStream_t s) {
-  const Layout L = make_layout(P, cap);
+  const int NT = cam.TX * cam.TY;
+  const Layout L = make_layout(P, cap, NT);
   if (ws_bytes < L.total) {
     set_error("gs_bin_tiles: workspace %zu B < required %zu B", ws_bytes, L.total);
     return GS_ERR_ARG;
@@ -527,7 +750,6 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   char* w = static_cast<char*>(ws);
   Counters* ctr = reinterpret_cast<Counters*>(w + L.ctr);
   uint32_t* ghist = reinterpret_cast<uint32_t*>(w + L.ghist);
-  const int NT = cam.TX * cam.TY;
   if (cudaMemsetAsync(w, 0, L.zero_end, s) != cudaSuccess || cudaMemsetAsync(tile_ranges, 0, (size_t)NT * 8, s) != cudaSuccess)
     return check_launch("gs_bin_tiles memset");
   if (P == 0) {
@@ -581,6 +803,33 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * 4);
   k_emit<<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0, ghist + 4 * 256);
   count_launch();
+  if (use_bucket(NT)) {
+    // chunks: a multiple of the SMs (CTAs resident per SM by shared memory), each < 2^16 keys
+    const size_t smem = tscatter_smem(NT);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, kSmemOptIn / (smem + 1024)));
+    const int64_t need = (cap + 65000 - 1) / 65000;
+    const int C = (int)std::max<int64_t>(std::min<int64_t>((int64_t)nsm * per_sm, kBkMaxChunks), need);
+    if (C <= kBkMaxChunks) {
+      uint32_t* chist = reinterpret_cast<uint32_t*>(w + L.chist);
+      uint32_t* tot = reinterpret_cast<uint32_t*>(w + L.tot);
+      int2* rng = reinterpret_cast<int2*>(tile_ranges);
+      int tile_bits = 1;
+      while ((1 << tile_bits) < NT) ++tile_bits;
+      static bool attr_set = false;  // opt-in shared memory above 48 KB (once per process)
+      if (!attr_set) {
+        if (cudaFuncSetAttribute(k_tscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_tcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) != cudaSuccess)
+          return check_launch("gs_bin_tiles smem opt-in");
+        attr_set = true;
+      }
+      k_tcount<<<C, kBkThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, chist);
+      k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, tot);
+      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, tot, rng, sorted_ids);
+      count_launch(3);
+      return finish_bin(ctr, cap, num_keys_host, s);
+    }
+  }
   const int rs_grid_t = (int)std::max<int64_t>(1, std::min<int64_t>((cap + kRsTileKeys - 1) / kRsTileKeys, (int64_t)nsm * 3));
   const uint16_t* final_keys;
   uint32_t* lbt1 = lbt + (int64_t)L.tile_parts * 256;
@@ -608,6 +857,11 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   const int rg_grid = (int)std::min<int64_t>((cap + 255) / 256, (int64_t)nsm * 8);
   k_ranges<<<std::max(rg_grid, 1), 256, 0, s>>>(final_keys, ctr, cap, reinterpret_cast<int2*>(tile_ranges));
   count_launch();
+  return finish_bin(ctr, cap, num_keys_host, s);
+}
+
+gs_status finish_bin(const void* ctr_v, int64_t cap, int64_t* num_keys_host, cudaStream_t s) {
+  const Counters* ctr = static_cast<const Counters*>(ctr_v);
   gs_status st = check_launch("gs_bin_tiles");
   if (st != GS_OK) return st;
   if (num_keys_host) {

@@ -35,6 +35,8 @@
 // exponent, alpha, transmittance and accumulation in the oracle's fp32 operation
 // order with exp computed in double (reading R9): the forward is then bit-identical
 // to the fp32 oracle.
+#include <cstdlib>
+
 #include "gsr_internal.cuh"
 
 namespace gsr {
