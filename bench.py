@@ -36,22 +36,55 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true", help="keep the generated Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML (the library
+    nvidia-smi reads) polled every 10 ms from a thread, so that even a ~100 ms timed
+    region gets ~10 samples; nvidia-smi -lms 200 is the fallback when NVML is absent."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
-        self.index, self.samples, self.proc = index, [], None
+        self.index, self.samples, self.proc, self.nvml = index, [], None, None
+        self.stop_flag = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        ent = vis.split(",")[self.index].strip() if vis else str(self.index)
+        if ent.isdigit():
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(int(ent))
+        return pynvml, pynvml.nvmlDeviceGetHandleByUUID(ent)
 
     def start(self):
+        try:
+            nv, h = self._nvml_handle()
+            self.nvml = (nv, h)
+            bits = [nv.nvmlClocksThrottleReasonHwSlowdown, nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    nv.nvmlClocksThrottleReasonSwThermalSlowdown, nv.nvmlClocksThrottleReasonSwPowerCap]
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_flag.is_set():
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append([str(sm), str(self.max_mhz), "", ""] +
+                                        ["Active" if r & b else "Not Active" for b in bits])
+                    time.sleep(0.01)
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:  # noqa: BLE001  (no NVML: fall back to nvidia-smi)
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -68,21 +101,27 @@ class ClockSampler:
                 self.samples.append(parts)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=1)
+            src = "nvml (10 ms poll)"
+        elif self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            src = "nvidia-smi -lms 200"
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[4 + k].lower() == "active"})
+        reasons = sorted({self.NAMES[k] for s in self.samples for k in range(4) if s[4 + k].lower() == "active"})
         sm.sort()
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "sm_min_mhz": sm[0] if sm else None, "reasons": reasons, "samples": len(self.samples),
+                "source": src}
 
 
 # ----------------------------------------------------------------------------- CPU oracle legs
@@ -300,6 +339,39 @@ def main():
         e2e = {"value": eb / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
                "iters_per_s": args.steps / (ems / 1000.0)}
 
+    # --- K13: the straightforward per-pixel GPU port (north_star's >= 10x target), same
+    # steps with gs_naive_render_fwd / gs_naive_render_bwd_screen, device-timed the same way
+    naive = None
+    if not args.no_naive and not args.profile:
+        tr.naive = True
+        tr.step(step_views(0))
+        tr.blended.zero_()
+        nsteps = min(args.steps, 3)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record(stream)
+        for i in range(nsteps):
+            tr.step(step_views(args.warmup + i))
+        n1.record(stream)
+        torch.cuda.synchronize()
+        tr.naive = False
+        nms = n0.elapsed_time(n1)
+        nb = int(tr.blended.item())
+        st = torch.tensor([nms, float(nb)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = st.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = st.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            nms, nb = float(mx[0]), int(sm[1])
+        nval = nb / (nms / 1000.0)
+        naive = {"value": nval, "unit": UNIT, "ms_per_step": nms / nsteps, "steps": nsteps,
+                 "speedup": value / nval,
+                 "what": "K13: same project/bin/project-bwd/Adam; render fwd and bwd one thread per pixel, "
+                         "records read from global memory, 10 atomicAdd per composited pair"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -351,7 +423,7 @@ def main():
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),
         "stage_ms": stage_ms,
-        "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu,
+        "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

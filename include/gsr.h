@@ -210,6 +210,22 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views
                                float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
                                void* stream);
 
+/* ---------------------------------------------------------------- K13 comparison baseline
+ * The "straightforward per-pixel GPU port" the north_star's >= 10x target is measured
+ * against (BASELINE.json north_star).  NOT the product path: drop-in
+ * replacements of gs_render_fwd (without key_blocks) and gs_render_bwd_screen with the
+ * same arguments, layouts, outputs and error behaviour, computed by one thread per
+ * pixel that reads every Gaussian record from global memory (no shared-memory staging,
+ * no warp cooperation) and, in the backward, issues 10 atomicAdd per composited
+ * (pixel, Gaussian) pair.  Results equal the product calls up to fp32 rounding. */
+gs_status gs_naive_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
+                              const int32_t* sorted_ids, const int32_t* tile_ranges, float* rgb, float* depth,
+                              float* T_final, int32_t* n_contrib, unsigned long long* blended, void* stream);
+gs_status gs_naive_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
+                                     const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                                     const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
+                                     float* sgrad, void* stream);
+
 /* ---------------------------------------------------------------- gs_adam_step
  * Dense bias-corrected Adam over all F * P scalars (R20):
  *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;

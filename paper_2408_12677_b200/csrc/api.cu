@@ -258,6 +258,40 @@ gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_p
   return check_launch("gs_render_bwd_screen");
 }
 
+gs_status gs_naive_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
+                              const int32_t* tile_ranges, float* rgb, float* depth, float* T_final,
+                              int32_t* n_contrib, unsigned long long* blended, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_naive_render_fwd"));
+  GS_TRY(check_scene(scene, "gs_naive_render_fwd"));
+  GS_TRY(check_ptrs("gs_naive_render_fwd", {{tile_ranges, "tile_ranges"}, {rgb, "rgb"}, {depth, "depth"},
+                                            {T_final, "T_final"}, {n_contrib, "n_contrib"}}));
+  if (scene->P > 0) GS_TRY(check_ptrs("gs_naive_render_fwd", {{proj.rec, "proj.rec"}}));
+  if (blended && (reinterpret_cast<uintptr_t>(blended) & 7u)) {
+    set_error("gs_naive_render_fwd: blended is not 8-byte aligned");
+    return GS_ERR_ALIGN;
+  }
+  launch_naive_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended,
+                   static_cast<cudaStream_t>(stream));
+  return check_launch("gs_naive_render_fwd");
+}
+
+gs_status gs_naive_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_proj proj,
+                                     const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                                     const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
+                                     float* sgrad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_naive_render_bwd_screen"));
+  GS_TRY(check_scene(scene, "gs_naive_render_bwd_screen"));
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_naive_render_bwd_screen", {{proj.rec, "proj.rec"}, {tile_ranges, "tile_ranges"},
+                                                   {T_final, "T_final"}, {n_contrib, "n_contrib"},
+                                                   {dL_drgb, "dL_drgb"}, {sgrad, "sgrad"}}));
+  launch_naive_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
+                   sgrad, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_naive_render_bwd_screen");
+}
+
 gs_status gs_project_bwd_views(int n_views, const gs_camera* cams, const gs_scene* scene, const float* params,
                                const uint8_t* const* flags, float* const* sgrads, float* grad, int accumulate,
                                void* stream) {

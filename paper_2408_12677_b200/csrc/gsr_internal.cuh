@@ -72,6 +72,12 @@ void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, 
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
                        const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                        const uint8_t* key_blocks, float* sgrad, cudaStream_t s);
+// naive.cu (K13 comparison baseline, not the product path)
+void launch_naive_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+                      float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended, cudaStream_t s);
+void launch_naive_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+                      const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
+                      float* sgrad, cudaStream_t s);
 // optim.cu
 void launch_adam(int64_t F, int64_t P_stride, float* params, float* grad, float* m, float* v, const float* lr,
                  float beta1, float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s);

@@ -100,6 +100,8 @@ class Library:
         lib.gs_render_bwd_workspace.restype = C.c_size_t
         lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
         lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
         lib.gs_spatial_order_workspace.argtypes = [vp]
@@ -107,7 +109,8 @@ class Library:
         lib.gs_spatial_order.argtypes = [vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
-                   "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad"):
+                   "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -162,6 +165,19 @@ class Library:
         return self._check("gs_render_bwd_screen", self.lib.gs_render_bwd_screen(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
             _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
+
+    # -- K13 comparison baseline (per-pixel port; not the product path) ---
+    def naive_render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
+                         stream=None):
+        return self._check("gs_naive_render_fwd", self.lib.gs_naive_render_fwd(
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(rgb), _ptr(depth),
+            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _stream(stream)))
+
+    def naive_render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
+                                sgrad, stream=None):
+        return self._check("gs_naive_render_bwd_screen", self.lib.gs_naive_render_bwd_screen(
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
+            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _stream(stream)))
 
     def project_bwd_views(self, cams, sc, params, flags, sgrads, grad, accumulate=True, stream=None):
         """cams: list of GsCamera; flags / sgrads: lists of device tensors (one per view)."""

@@ -136,6 +136,9 @@ class Trainer:
         self.blended = torch.zeros(1, dtype=torch.int64, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
         self.hooks = None
+        # K13 comparison baseline (bench.py only): per-pixel render kernels, no
+        # block masks; projection, binning, projection backward and Adam unchanged
+        self.naive = False
 
     def _hook(self, stage, what):
         if self.hooks is not None:
@@ -145,12 +148,20 @@ class Trainer:
         lib, m, b, cam = self.lib, self.model, self.buf, self.cameras[v]
         gcam = gsr.camera(cam)
         proj = gsr.GsProj(b.proj.rec, b.proj.radius, b.proj.tiles, self.flags[slot].data_ptr())
+        self._hook("project", "begin")
         lib.project(gcam, m.desc, m.params, proj)
+        self._hook("project", "end")
+        self._hook("bin", "begin")
         lib.bin_tiles(gcam, m.desc, proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
                       num_keys_dev=self.num_keys[v:v + 1])
+        self._hook("bin", "end")
         self._hook("render_fwd", "begin")
-        lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n, blended=self.blended,
-                       key_blocks=b.key_blocks)
+        if self.naive:
+            lib.naive_render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n,
+                                 blended=self.blended)
+        else:
+            lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n,
+                           blended=self.blended, key_blocks=b.key_blocks)
         self._hook("render_fwd", "end")
         if targets_ready is not None:
             torch.cuda.current_stream().wait_event(targets_ready)
@@ -158,8 +169,12 @@ class Trainer:
         if targets_consumed is not None:
             targets_consumed.record()
         self._hook("render_bwd", "begin")
-        lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
-                              self.sgrad[slot], key_blocks=b.key_blocks)
+        if self.naive:
+            lib.naive_render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
+                                        self.sgrad[slot])
+        else:
+            lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
+                                  self.sgrad[slot], key_blocks=b.key_blocks)
         self._hook("render_bwd", "end")
         return gcam
 
