@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true", help="keep the generated Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
+                    help="views in flight (one CUDA stream + buffer set each)")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
     return ap.parse_args()
@@ -240,7 +242,8 @@ def main():
 
     def step_views(i):
         return my_views if batched else [my_views[i % len(my_views)]]
-    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce)
+    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce,
+                          streams=args.streams if batched else 1)
     stream = torch.cuda.current_stream()
 
     # --- warm-up
@@ -254,12 +257,12 @@ def main():
         clocks.start()
     tr.blended.zero_()
     tr.num_keys.zero_()
-    stage_ev = {"render_fwd": [], "render_bwd": [], "project_bwd": []}
+    stage_ev = {"project": [], "bin": [], "render_fwd": [], "render_bwd": [], "project_bwd": []}
     open_ev = {}
 
     def hooks(stage, what):
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(stream)
+        ev.record(torch.cuda.current_stream())  # the stream the stage is launched on
         if what == "begin":
             open_ev[stage] = ev
         else:
@@ -290,11 +293,29 @@ def main():
     clk = clocks.stop() if not args.profile else None
     ms = e0.elapsed_time(e1)
     stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(v), 1) for k, v in stage_ev.items()}
-    fwd_ms, bwd_ms = stage_ms["render_fwd"], stage_ms["render_bwd"]
+    # Per-kernel rooflines need each stage's own duration: with views in flight on
+    # several streams the stages overlap, so an extra serialised pass (streams = 1,
+    # same steps, CUDA events on the launching stream) times them in isolation.
+    blended_timed = int(tr.blended.item())
+    stage_ms_overlapped = None
+    if tr._streams is not None and not args.profile:
+        stage_ms_overlapped = stage_ms
+        tr.serial = True
+        tr.step(step_views(0))
+        for v in stage_ev.values():
+            v.clear()
+        tr.hooks = hooks
+        for i in range(min(args.steps, 5)):
+            tr.step(step_views(args.warmup + i))
+        tr.hooks = None
+        torch.cuda.synchronize()
+        tr.serial = False
+        stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(v), 1) for k, v in stage_ev.items()}
     kmax = int(tr.num_keys.max().item())
     if kmax > cap:
         raise RuntimeError(f"key capacity overflow during the timed region: K={kmax} > {cap}")
-    blended = int(tr.blended.item())
+    blended = blended_timed
+    fwd_ms, bwd_ms = stage_ms["render_fwd"], stage_ms["render_bwd"]
     stats = torch.tensor([ms, float(blended), fwd_ms, bwd_ms], dtype=torch.float64, device=dev)
     if world > 1:
         mx = stats.clone()
@@ -385,17 +406,25 @@ def main():
         pass
     n_views = views_done
     # evaluated pairs of the backward = sum of n_contrib over the views (untimed re-render)
-    evaluated = 0
+    evaluated, vis, keys = 0, 0, 0
     eval_views = my_views[:8]
     for v in eval_views:
-        pipeline.render(lib, model, cams[v], tr.buf)
+        keys += pipeline.render(lib, model, cams[v], tr.buf, sync_keys=True)
         evaluated += int(tr.buf.n.sum().item())
+        vis += int((tr.buf.proj_t["tiles"][:model.P] > 0).sum().item())
+    nv = len(eval_views)
+    hbm = stage_hbm(peaks, stage_ms, model.P, w.scene.sh_degree, vis / nv, keys / nv, cams[0].num_tiles)
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config, {}).get("k_render_bwd")
     except (OSError, ValueError):
         pass
     roof = roofline(dev, peaks, clk, stage_ms, blended / max(world, 1) / n_views, evaluated / len(eval_views), traffic)
+    roof["timing"] = ("CUDA events around each launch on its stream, serialised pass (streams=1) of the same steps "
+                      "right after the timed region" if stage_ms_overlapped is not None else
+                      "CUDA events around each launch on its stream, inside the timed region")
+    if stage_ms_overlapped is not None:
+        roof["launch_ms_overlapped"] = stage_ms_overlapped["render_bwd"]
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -417,17 +446,38 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}" if batched else f"replicas x{world}",
-                   "key_capacity": cap, "max_keys_per_view": kmax,
+                   "key_capacity": cap, "streams": args.streams if batched else 1, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),
-        "stage_ms": stage_ms,
+        "stage_ms": stage_ms, "stage_ms_overlapped": stage_ms_overlapped, "stage_hbm": hbm,
         "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def stage_hbm(peaks, stage_ms, P, deg, V, K, NT):
+    """HBM roofline of the projection and binning stages (north_star: >= 50% of HBM
+    peak on project/bin), each against its COMPULSORY bytes: inputs
+    read once and outputs written once, no intermediate traffic counted.
+      project: P (12 B mean + 9 B radius/tiles/flags) + V (32 B scale/quat/logit +
+               12 (deg+1)^2 B SH + 48 B record)
+      bin:     P 4 B tiles + V 12 B (depth, rect) + K 4 B sorted ids + NT 8 B ranges
+    V = visible Gaussians, K = keys, per view (means over the measured views)."""
+    peak = peaks.get("hbm_gbs") or 6556.2
+    S = (deg + 1) ** 2
+    out = {}
+    for st, by in (("project", P * 21 + V * (32 + 12 * S + 48)), ("bin", P * 4 + V * 12 + K * 4 + NT * 8)):
+        ms = stage_ms.get(st)
+        if ms:
+            gbs = by / (ms / 1e3) / 1e9
+            out[st] = {"ms": ms, "compulsory_bytes": int(by), "achieved": gbs, "peak": peak, "unit": "GB/s",
+                       "frac": gbs / peak}
+    out["V_per_view"], out["K_per_view"] = int(V), int(K)
+    return out
 
 
 def roofline(dev, peaks, clk, stage_ms, blended_per_view, evaluated_per_view, traffic):

@@ -121,11 +121,18 @@ class Trainer:
     by bench.py to time them with CUDA events on the launching stream)."""
 
     def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
-                 w_depth: float = 1.0, allreduce=None, chunk: int = 8):
+                 w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1):
         self.lib, self.model, self.cameras, self.targets = lib, model, cameras, targets
         self.device, self.w_depth, self.allreduce = device, w_depth, allreduce
         self.chunk = max(1, min(8, int(chunk)))
-        self.buf = ViewBuffers(lib, cameras[0], model.P, key_capacity, device)
+        # views in flight: view k of a step runs on stream k % streams with its own
+        # buffers, so that one view's latency-bound projection / binning kernels overlap
+        # another view's rendering (the views of a batch are independent until the
+        # projection backward sums them, R21)
+        n_streams = max(1, int(streams))
+        self.bufs = [ViewBuffers(lib, cameras[0], model.P, key_capacity, device) for _ in range(n_streams)]
+        self.buf = self.bufs[0]
+        self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
         P = max(model.P, 1)
         # per in-flight view: projection flags and screen-space gradients (zeroed once;
         # gs_project_bwd_views leaves them zero again)
@@ -139,13 +146,16 @@ class Trainer:
         # K13 comparison baseline (bench.py only): per-pixel render kernels, no
         # block masks; projection, binning, projection backward and Adam unchanged
         self.naive = False
+        # serial = True runs the views on the caller's stream only (bench.py's isolated
+        # kernel-timing pass)
+        self.serial = False
 
     def _hook(self, stage, what):
         if self.hooks is not None:
             self.hooks(stage, what)
 
-    def _view(self, v: int, slot: int, t_rgb, t_depth, targets_ready=None, targets_consumed=None):
-        lib, m, b, cam = self.lib, self.model, self.buf, self.cameras[v]
+    def _view(self, v: int, slot: int, t_rgb, t_depth, targets_ready=None, targets_consumed=None, buf=None):
+        lib, m, b, cam = self.lib, self.model, buf if buf is not None else self.buf, self.cameras[v]
         gcam = gsr.camera(cam)
         proj = gsr.GsProj(b.proj.rec, b.proj.radius, b.proj.tiles, self.flags[slot].data_ptr())
         self._hook("project", "begin")
@@ -223,16 +233,42 @@ class Trainer:
 
     def _run(self, views, targets, after_view):
         m = self.model
-        pending = []
+        main = torch.cuda.current_stream()
+        S = 1 if self.serial else len(self.bufs)
+        if S > 1:  # side streams start after the previous step's Adam / chains
+            start = torch.cuda.Event()
+            start.record(main)
+            for s in self._streams:
+                s.wait_event(start)
+        pending, done = [], []
+        chain_ev = None
         first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
         for k, v in enumerate(views):
             t_rgb, t_depth, ready, consumed = targets(k, v)
-            pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed))
+            if S == 1:
+                pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed))
+            else:
+                s = self._streams[k % S]
+                if chain_ev is not None:  # this view's flags / sgrad slot was consumed by that chain
+                    s.wait_event(chain_ev)
+                with torch.cuda.stream(s):
+                    pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed, self.bufs[k % S]))
+                    ev = torch.cuda.Event()
+                    ev.record(s)
+                    done.append(ev)
             if after_view is not None:
                 after_view(k)
             if len(pending) == self.chunk:
+                for ev in done:
+                    main.wait_event(ev)
+                done = []
                 self._chain(pending, accumulate=not first)
                 pending, first = [], False
+                if S > 1:
+                    chain_ev = torch.cuda.Event()
+                    chain_ev.record(main)
+        for ev in done:
+            main.wait_event(ev)
         if pending or first:
             self._chain(pending, accumulate=not first)
         if self.allreduce is not None:
@@ -250,7 +286,7 @@ class Trainer:
     def check_capacity(self) -> int:
         """Max K seen since construction (host sync); raises if any view overflowed."""
         k = int(self.num_keys.max().item())
-        if k > self.buf.key_capacity:
+        if k > self.buf.key_capacity:  # every view buffer has the same capacity
             raise gsr.GsError("gs_bin_tiles", gsr.GS_ERR_CAPACITY, f"K={k} > capacity {self.buf.key_capacity}")
         return k
 
