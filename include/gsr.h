@@ -145,6 +145,15 @@ gs_status gs_bin_tiles(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HO
                        size_t ws_bytes, int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges,
                        int64_t* num_keys_dev, int64_t* num_keys_host /*HOST*/, void* stream);
 
+/* ---------------------------------------------------------------- gs_tile_order
+ * Scheduling order of the tiles for the render calls: the tile ids sorted by
+ * decreasing key count (min(count, 4095) / 4 buckets; order inside a bucket is
+ * unspecified), so that the longest tiles start first and the short ones fill the
+ * tail (longest-processing-time-first).  Not a step of the method: a work order.
+ *  tile_ranges: int32[num_tiles][2] from gs_bin_tiles (same stream)
+ *  tile_order:  int32[num_tiles] output permutation.  num_tiles <= 65536. */
+gs_status gs_tile_order(const gs_camera* cam /*HOST*/, const int32_t* tile_ranges, int32_t* tile_order, void* stream);
+
 /* ---------------------------------------------------------------- gs_render_fwd
  * Eq. 11 per pixel over its tile's depth-sorted list, front to back: alpha =
  * min(0.99, o exp(power)), skip alpha < 1/255 (and power > 0), stop before a
@@ -157,9 +166,12 @@ gs_status gs_bin_tiles(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HO
  *       visited, the mask of its tile's 8x4 pixel blocks (bit b: x offset 8 (b & 1),
  *       y offset 4 (b >> 1)) in which that Gaussian was composited into >= 1 pixel.
  *       Passing it to the backward lets it skip (tile, Gaussian) pairs that
- *       contributed nothing (an exact property of this forward pass). */
+ *       contributed nothing (an exact property of this forward pass).
+ *  tile_order: nullable int32[num_tiles], a permutation of the tile ids: the order in
+ *       which tiles are scheduled (gs_tile_order).  Results do not depend on it. */
 gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
-                        const int32_t* sorted_ids, const int32_t* tile_ranges, float* rgb, float* depth,
+                        const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order /*nullable*/,
+                        float* rgb, float* depth,
                         float* T_final, int32_t* n_contrib, unsigned long long* blended, uint8_t* key_blocks,
                         void* stream);
 
@@ -174,11 +186,13 @@ gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *      dr, dg, db, dz, pad, pad); >= gs_render_bwd_workspace() bytes; cleared here.
  *  key_blocks: nullable, the forward's key masks for the SAME forward call (see
  *      gs_render_fwd); NULL = derive the pixel blocks geometrically.
+ *  tile_order: nullable, as in gs_render_fwd.
  *  grad: float[F][P_stride], ACCUMULATED (+=) so that views sum (R21).
  * Float atomics make grad order-dependent in the last bits. */
 size_t gs_render_bwd_workspace(const gs_scene* scene /*HOST*/);
 gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
-                        gs_proj proj, const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                        gs_proj proj, const int32_t* sorted_ids, const int32_t* tile_ranges,
+                        const int32_t* tile_order /*nullable*/, const float* T_final,
                         const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
                         const uint8_t* key_blocks /*nullable*/, void* ws, size_t ws_bytes, float* grad,
                         void* stream);
@@ -202,7 +216,8 @@ gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *    (every row of every Gaussian written, none read -- the first batch of an
  *    iteration, so that the optimiser need not zero grad). */
 gs_status gs_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
-                               const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                               const int32_t* sorted_ids, const int32_t* tile_ranges,
+                               const int32_t* tile_order /*nullable*/, const float* T_final,
                                const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
                                const uint8_t* key_blocks /*nullable*/, float* sgrad, void* stream);
 gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views]*/, const gs_scene* scene /*HOST*/,

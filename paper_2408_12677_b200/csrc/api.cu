@@ -185,7 +185,7 @@ gs_status gs_bin_tiles(const gs_camera* cam, const gs_scene* scene, gs_proj proj
 }
 
 gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
-                        const int32_t* tile_ranges, float* rgb, float* depth, float* T_final, int32_t* n_contrib,
+                        const int32_t* tile_ranges, const int32_t* tile_order, float* rgb, float* depth, float* T_final, int32_t* n_contrib,
                         unsigned long long* blended, uint8_t* key_blocks, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_render_fwd"));
@@ -197,7 +197,7 @@ gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj pro
     set_error("gs_render_fwd: blended is not 8-byte aligned");
     return GS_ERR_ALIGN;
   }
-  launch_render_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended,
+  launch_render_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, rgb, depth, T_final, n_contrib, blended,
                     key_blocks, static_cast<cudaStream_t>(stream));
   return check_launch("gs_render_fwd");
 }
@@ -208,7 +208,8 @@ size_t gs_render_bwd_workspace(const gs_scene* scene) {
 }
 
 gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float* params, gs_proj proj,
-                        const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
+                        const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
+                        const float* T_final,
                         const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
                         const uint8_t* key_blocks, void* ws, size_t ws_bytes, float* grad, void* stream) {
   g_err[0] = 0;
@@ -230,7 +231,7 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(ws, 0, need, s) != cudaSuccess) return check_launch("gs_render_bwd memset");
   const DevCam dc = make_devcam(*cam);
-  launch_render_bwd(dc, proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, key_blocks,
+  launch_render_bwd(dc, proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth, key_blocks,
                     static_cast<float*>(ws), s);
   const uint8_t* fl = proj.flags;
   float* sg = static_cast<float*>(ws);
@@ -239,7 +240,7 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
 }
 
 gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
-                               const int32_t* tile_ranges, const float* T_final, const int32_t* n_contrib,
+                               const int32_t* tile_ranges, const int32_t* tile_order, const float* T_final, const int32_t* n_contrib,
                                const float* dL_drgb, const float* dL_ddepth, const uint8_t* key_blocks, float* sgrad,
                                void* stream) {
   g_err[0] = 0;
@@ -253,9 +254,18 @@ gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_p
     set_error("gs_render_bwd_screen: dL_ddepth is not 16-byte aligned");
     return GS_ERR_ALIGN;
   }
-  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
+  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth,
                     key_blocks, sgrad, static_cast<cudaStream_t>(stream));
   return check_launch("gs_render_bwd_screen");
+}
+
+gs_status gs_tile_order(const gs_camera* cam, const int32_t* tile_ranges, int32_t* tile_order, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_tile_order"));
+  GS_TRY(check_ptrs("gs_tile_order", {{tile_ranges, "tile_ranges"}, {tile_order, "tile_order"}}));
+  const DevCam dc = make_devcam(*cam);
+  launch_tile_order(dc.TX * dc.TY, tile_ranges, tile_order, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_tile_order");
 }
 
 gs_status gs_naive_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,

@@ -62,15 +62,17 @@ size_t bin_workspace_bytes(int64_t P, int64_t key_capacity, int num_tiles);
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes,
                            int64_t key_capacity, int32_t* sorted_ids, int32_t* tile_ranges, int64_t* num_keys_dev,
                            int64_t* num_keys_host, cudaStream_t s);
+void launch_tile_order(int NT, const int32_t* tile_ranges, int32_t* order, cudaStream_t s);
 size_t spatial_order_workspace_bytes(int64_t P);
 gs_status launch_spatial_order(int64_t F, int64_t P, int64_t S, const float* params_in, float* params_out,
                                int32_t* perm, void* ws, size_t ws_bytes, cudaStream_t s);
 // render.cu
-void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+                       const int32_t* order, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                        uint8_t* key_blocks, cudaStream_t s);
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
-                       const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
+                       const int32_t* order, const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                        const uint8_t* key_blocks, float* sgrad, cudaStream_t s);
 // naive.cu (K13 comparison baseline, not the product path)
 void launch_naive_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,

@@ -354,7 +354,7 @@ __device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
 template <int WPC>
 __global__ void __launch_bounds__(WPC * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
-                                                                   const int2* __restrict__ ranges,
+                                                                   const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    float* __restrict__ out_rgb,
                                                                    float* __restrict__ out_d, float* __restrict__ out_T,
                                                                    int32_t* __restrict__ out_n,
@@ -362,8 +362,9 @@ __global__ void __launch_bounds__(WPC * 32) k_render_fwd(DevCam cam, const float
                                                                    uint8_t* __restrict__ key_blocks) {
   __shared__ float4 s_rec[WPC][2][32][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * WPC + warp;
-  if (tile >= cam.TX * cam.TY) return;
+  const int wslot = blockIdx.x * WPC + warp;
+  if (wslot >= cam.TX * cam.TY) return;
+  const int tile = order ? order[wslot] : wslot;  // work order (gs_tile_order)
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
   const int lx = lane & 7, ly = lane >> 3;
@@ -534,7 +535,7 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
 template <int WPC>
 __global__ void __launch_bounds__(WPC * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
-                                                                   const int2* __restrict__ ranges,
+                                                                   const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    const float* __restrict__ T_final,
                                                                    const int32_t* __restrict__ n_contrib,
                                                                    const float* __restrict__ g_rgb,
@@ -544,8 +545,9 @@ __global__ void __launch_bounds__(WPC * 32) k_render_bwd(DevCam cam, const float
   __shared__ float4 s_rec[WPC][2][32][3];
   __shared__ int s_gid[WPC][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * WPC + warp;
-  if (tile >= cam.TX * cam.TY) return;
+  const int wslot = blockIdx.x * WPC + warp;
+  if (wslot >= cam.TX * cam.TY) return;
+  const int tile = order ? order[wslot] : wslot;  // work order (gs_tile_order)
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
   const int lx = lane & 7, ly = lane >> 3;
@@ -723,7 +725,7 @@ __device__ __forceinline__ bool eval_gauss(float mx, float my, float A, float B,
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
-                                                                   const int2* __restrict__ ranges,
+                                                                   const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    float* __restrict__ out_rgb,
                                                                    float* __restrict__ out_d, float* __restrict__ out_T,
                                                                    int32_t* __restrict__ out_n,
@@ -731,8 +733,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
                                                                    uint8_t* __restrict__ key_blocks) {
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarpsPerCta + warp;
-  if (tile >= cam.TX * cam.TY) return;
+  const int wslot = blockIdx.x * kWarpsPerCta + warp;
+  if (wslot >= cam.TX * cam.TY) return;
+  const int tile = order ? order[wslot] : wslot;  // work order (gs_tile_order)
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
   const int lx = lane & 7, ly = lane >> 3;
@@ -822,7 +825,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_fwd(DevCam cam, co
 
 __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
-                                                                   const int2* __restrict__ ranges,
+                                                                   const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    const float* __restrict__ T_final,
                                                                    const int32_t* __restrict__ n_contrib,
                                                                    const float* __restrict__ g_rgb,
@@ -832,8 +835,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   __shared__ int s_gid[kWarpsPerCta][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x * kWarpsPerCta + warp;
-  if (tile >= cam.TX * cam.TY) return;
+  const int wslot = blockIdx.x * kWarpsPerCta + warp;
+  if (wslot >= cam.TX * cam.TY) return;
+  const int tile = order ? order[wslot] : wslot;  // work order (gs_tile_order)
   const int tx = tile % cam.TX, ty = tile / cam.TX;
   const int ox = tx * kTile, oy = ty * kTile;
   const int lx = lane & 7, ly = lane >> 3;
@@ -991,54 +995,54 @@ int render_wpc() {
 }
 
 template <int WPC>
-void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order, float* rgb,
                     float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                     uint8_t* key_blocks, cudaStream_t s) {
   k_render_fwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
-      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), rgb, depth, T_final,
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, rgb, depth, T_final,
       n_contrib, blended, key_blocks);
 }
 template <int WPC>
-void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                     const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
   k_render_bwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
-      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), T_final, n_contrib,
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
       g_rgb, g_depth, key_blocks, sgrad);
 }
 #endif
 
 }  // namespace
 
-void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
+void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                        uint8_t* key_blocks, cudaStream_t s) {
 #ifndef GSR_EXACT_EXP
   switch (render_wpc()) {
-    case 4: launch_fwd_wpc<4>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
-    case 2: launch_fwd_wpc<2>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
-    default: launch_fwd_wpc<1>(cam, rec, ids, ranges, rgb, depth, T_final, n_contrib, blended, key_blocks, s);
+    case 4: launch_fwd_wpc<4>(cam, rec, ids, ranges, order, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
+    case 2: launch_fwd_wpc<2>(cam, rec, ids, ranges, order, rgb, depth, T_final, n_contrib, blended, key_blocks, s); break;
+    default: launch_fwd_wpc<1>(cam, rec, ids, ranges, order, rgb, depth, T_final, n_contrib, blended, key_blocks, s);
   }
 #else
   k_render_fwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
-      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), rgb, depth, T_final,
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, rgb, depth, T_final,
       n_contrib, blended, key_blocks);
 #endif
   count_launch();
 }
 
-void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
+void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                        const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                        const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
 #ifndef GSR_EXACT_EXP
   switch (render_wpc()) {
-    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
-    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
-    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s);
+    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
+    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
+    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s);
   }
 #else
   k_render_bwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
-      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), T_final, n_contrib,
+      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
       g_rgb, g_depth, key_blocks, sgrad);
 #endif
   count_launch();

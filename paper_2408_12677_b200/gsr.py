@@ -95,11 +95,12 @@ class Library:
         lib.gs_bin_tiles_workspace.argtypes = [vp, i64, i64]
         lib.gs_bin_tiles_workspace.restype = C.c_size_t
         lib.gs_bin_tiles.argtypes = [vp, vp, GsProj, vp, C.c_size_t, i64, vp, vp, vp, vp, vp]
-        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_render_bwd_workspace.argtypes = [vp]
         lib.gs_render_bwd_workspace.restype = C.c_size_t
-        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
-        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
+        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_tile_order.argtypes = [vp, vp, vp, vp]
         lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
@@ -110,7 +111,7 @@ class Library:
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -144,26 +145,33 @@ class Library:
         self._check("gs_bin_tiles", st, allow=(GS_ERR_CAPACITY,) if allow_capacity else ())
         return (int(k_host.value) if sync else None), st
 
+    def tile_order(self, cam, tile_ranges, tile_order, stream=None):
+        return self._check("gs_tile_order", self.lib.gs_tile_order(C.byref(cam), _ptr(tile_ranges), _ptr(tile_order),
+                                                                   _stream(stream)))
+
     def render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
-                   key_blocks=None, stream=None):
+                   key_blocks=None, stream=None, tile_order=None):
         return self._check("gs_render_fwd", self.lib.gs_render_fwd(
-            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(rgb), _ptr(depth),
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(rgb),
+            _ptr(depth),
             _ptr(T_final), _ptr(n_contrib), _ptr(blended), _ptr(key_blocks), _stream(stream)))
 
     def render_bwd_workspace(self, sc: GsScene) -> int:
         return int(self.lib.gs_render_bwd_workspace(C.byref(sc)))
 
     def render_bwd(self, cam, sc, params, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, ws,
-                   grad, key_blocks=None, stream=None):
+                   grad, key_blocks=None, stream=None, tile_order=None):
         return self._check("gs_render_bwd", self.lib.gs_render_bwd(
-            C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final),
+            C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
+            _ptr(T_final),
             _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(ws),
             ws.numel() * ws.element_size(), _ptr(grad), _stream(stream)))
 
     def render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, sgrad,
-                          key_blocks=None, stream=None):
+                          key_blocks=None, stream=None, tile_order=None):
         return self._check("gs_render_bwd_screen", self.lib.gs_render_bwd_screen(
-            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(T_final),
+            _ptr(n_contrib),
             _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
 
     # -- K13 comparison baseline (per-pixel port; not the product path) ---

@@ -510,3 +510,37 @@ def test_trainer_streams_match_single_stream(lib, host):
     assert grad_mismatch(p1, p0, rtol=1e-4, atol=1e-6).mean() <= 1e-3
     for sg in trs[1].sgrad:
         assert int(torch.count_nonzero(sg)) == 0
+
+
+def test_tile_order_permutation_and_invariance(lib):
+    """gs_tile_order is a permutation of the tiles by non-increasing key count
+    (bucketed by count / 4); rendering in that order gives bit-identical forward
+    outputs and the same gradients up to atomic reordering."""
+    w = workload("replica")
+    cam, scene = w.cameras[0], w.scene
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    gcam = gsr.camera(cam)
+    order = torch.full((cam.num_tiles,), -1, dtype=torch.int32, device=DEV)
+    lib.tile_order(gcam, b["ranges"], order)
+    torch.cuda.synchronize()
+    o = order.cpu().numpy()
+    assert np.array_equal(np.sort(o), np.arange(cam.num_tiles))
+    r = b["ranges"].cpu().numpy()
+    lens = np.minimum(r[:, 1] - r[:, 0], 4095) // 4
+    assert np.all(np.diff(lens[o]) <= 0)
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    outs = []
+    for tord in (None, order):
+        H, W = cam.height, cam.width
+        rgb, dep, T = (torch.zeros(s, device=DEV) for s in ((3, H, W), (H, W), (H, W)))
+        n = torch.zeros((H, W), dtype=torch.int32, device=DEV)
+        lib.render_fwd(gcam, sc, proj, b["sorted_ids"], b["ranges"], rgb, dep, T, n, tile_order=tord)
+        g_rgb, g_d = (torch.from_numpy(a).to(DEV) for a in scenegen.upstream_fields(5, W, H))
+        sg = torch.zeros((scene.P, 12), device=DEV)
+        lib.render_bwd_screen(gcam, sc, proj, b["sorted_ids"], b["ranges"], T, n, g_rgb, g_d, sg, tile_order=tord)
+        torch.cuda.synchronize()
+        outs.append((rgb.cpu().numpy(), dep.cpu().numpy(), n.cpu().numpy(), sg.cpu().numpy().astype(np.float64)))
+    for a, c in zip(outs[0][:3], outs[1][:3]):
+        assert np.array_equal(a, c)
+    assert grad_mismatch(outs[1][3], outs[0][3], rtol=1e-4, atol=1e-6).mean() <= 1e-4
