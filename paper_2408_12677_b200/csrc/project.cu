@@ -10,7 +10,10 @@
 // (reading R9), so that mu, z, conic, opacity, radius, rect and tile counts are
 // bit-identical to the fp32 CPU oracle.  The colour (SH) and the backward are free
 // to use FMA contraction: their parity is a tolerance.
+#include <cstdlib>
+
 #include "gsr_internal.cuh"
+#include "bulk_copy.cuh"
 #include "sh_basis.cuh"
 
 namespace gsr {
@@ -39,7 +42,110 @@ __device__ __forceinline__ void quat_to_rot(float w, float x, float y, float z, 
 __device__ __forceinline__ bool finitef(float v) { return isfinite(v); }
 
 // ---------------------------------------------------------------------------
-// K1a: geometry of the projection (O1-O7).  Reads rows 0-10 only.
+// O1-O7 for one Gaussian (mean already read): the fixed-order fp32 chain of R9.
+// fetch(row) returns parameter row 3..10 of this Gaussian (read only if z_c > z_near).
+// ---------------------------------------------------------------------------
+struct Geom {
+  float4 q0, q1;  // (mu_x, mu_y, z, opacity), (conic A, B, C, -)
+  uint32_t rx, ry;
+  int32_t rad, ntiles;
+  uint8_t flags;
+};
+
+template <class Fetch>
+__device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, float py, float pz, Fetch fetch) {
+  Geom g;
+  // O3: p_c = W p + t  (Eq. 4)
+  const float* W = cam.R;
+  const float xc = FA(FA(FA(FM(W[0], px), FM(W[1], py)), FM(W[2], pz)), cam.t[0]);
+  const float yc = FA(FA(FA(FM(W[3], px), FM(W[4], py)), FM(W[5], pz)), cam.t[1]);
+  const float zc = FA(FA(FA(FM(W[6], px), FM(W[7], py)), FM(W[8], pz)), cam.t[2]);
+  g.rad = 0, g.ntiles = 0;
+  g.flags = GS_FLAG_CULLED;
+  do {
+    if (!(zc > cam.z_near)) break;  // R6, R23
+    // O1: activations (R3-R5, R9)
+    const float l0 = fetch(3), l1 = fetch(4), l2 = fetch(5);
+    const float qw = fetch(6), qx = fetch(7), qy = fetch(8), qz = fetch(9);
+    const float logit = fetch(10);
+    float s[3];
+    s[0] = act_exp(l0);
+    s[1] = act_exp(l1);
+    s[2] = act_exp(l2);
+    const float qn = __fsqrt_rn(FA(FA(FA(FM(qw, qw), FM(qx, qx)), FM(qy, qy)), FM(qz, qz)));
+    if (!(qn > 0.f) || !finitef(qn)) break;
+    const float opa = act_sigmoid(logit);
+    float R[3][3];
+    quat_to_rot(FD(qw, qn), FD(qx, qn), FD(qy, qn), FD(qz, qn), R);
+    // O2: Sigma = (R S)(R S)^T  (Eq. 2)
+    float M[3][3], Sig[3][3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) M[r][c] = FM(R[r][c], s[c]);
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) Sig[r][c] = FA(FA(FM(M[r][0], M[c][0]), FM(M[r][1], M[c][1])), FM(M[r][2], M[c][2]));
+    // O4: mean projection (Eq. 4), R1
+    const float ux = FD(xc, zc), uy = FD(yc, zc);
+    const float mux = FA(FM(cam.fx, ux), cam.cx);
+    const float muy = FA(FM(cam.fy, uy), cam.cy);
+    // O5: EWA (Eq. 5) with the 1.3x tangent clamp (R7) and the 0.3 low-pass (R8)
+    const float limx = FM(1.3f, FD((float)cam.W, FM(2.f, cam.fx)));
+    const float limy = FM(1.3f, FD((float)cam.H, FM(2.f, cam.fy)));
+    const float uxc = fminf(fmaxf(ux, -limx), limx);
+    const float uyc = fminf(fmaxf(uy, -limy), limy);
+    const float J00 = FD(cam.fx, zc), J02 = FD(-FM(cam.fx, uxc), zc);
+    const float J11 = FD(cam.fy, zc), J12 = FD(-FM(cam.fy, uyc), zc);
+    float T[2][3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      T[0][c] = FA(FM(J00, W[c]), FM(J02, W[6 + c]));
+      T[1][c] = FA(FM(J11, W[3 + c]), FM(J12, W[6 + c]));
+    }
+    float MT[2][3];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) MT[r][c] = FA(FA(FM(T[r][0], Sig[0][c]), FM(T[r][1], Sig[1][c])), FM(T[r][2], Sig[2][c]));
+    const float a = FA(FA(FA(FM(MT[0][0], T[0][0]), FM(MT[0][1], T[0][1])), FM(MT[0][2], T[0][2])), 0.3f);
+    const float b = FA(FA(FM(MT[0][0], T[1][0]), FM(MT[0][1], T[1][1])), FM(MT[0][2], T[1][2]));
+    const float c = FA(FA(FA(FM(MT[1][0], T[1][0]), FM(MT[1][1], T[1][1])), FM(MT[1][2], T[1][2])), 0.3f);
+    // O6: conic
+    const float det = FS(FM(a, c), FM(b, b));
+    if (!(det > 0.f) || !finitef(det)) break;
+    const float cA = FD(c, det), cB = FD(-b, det), cC = FD(a, det);
+    if (!finitef(cA) || !finitef(cB) || !finitef(cC) || !finitef(mux) || !finitef(muy)) break;
+    // O7: radius and tile rectangle (R10, R11)
+    const float mid = FM(0.5f, FA(a, c));
+    const float disc = FS(FM(mid, mid), det);
+    const float lam = FA(mid, __fsqrt_rn(fmaxf(disc, 0.f)));
+    const float rf = ceilf(FM(3.f, __fsqrt_rn(lam)));
+    float xlo = ceilf(FS(mux, rf)), xhi = floorf(FA(mux, rf));
+    float ylo = ceilf(FS(muy, rf)), yhi = floorf(FA(muy, rf));
+    xlo = fmaxf(xlo, 0.f);
+    ylo = fmaxf(ylo, 0.f);
+    xhi = fminf(xhi, (float)(cam.W - 1));
+    yhi = fminf(yhi, (float)(cam.H - 1));
+    if (!(xlo <= xhi) || !(ylo <= yhi)) break;
+    const int x0 = (int)xlo / kTile, x1 = (int)xhi / kTile + 1;
+    const int y0 = (int)ylo / kTile, y1 = (int)yhi / kTile + 1;
+    g.rad = (int32_t)fminf(rf, (float)(1 << 30));
+    g.ntiles = (x1 - x0) * (y1 - y0);
+    g.flags = ((uxc != ux) ? GS_FLAG_JCLAMP_X : 0) | ((uyc != uy) ? GS_FLAG_JCLAMP_Y : 0);
+    const uint32_t rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
+    const uint32_t ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
+    g.q0 = make_float4(mux, muy, zc, opa);
+    g.q1 = make_float4(cA, cB, cC, 0.f);
+    g.rx = rx, g.ry = ry;
+  } while (0);
+  return g;
+}
+
+// ---------------------------------------------------------------------------
+// K1a (legacy, GSR_PROJECT=legacy): geometry of the projection (O1-O7), one thread
+// per Gaussian with direct loads; K1b below adds the colour.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256, 3) k_project_geom(DevCam cam, int64_t P, int64_t S, const float* __restrict__ prm,
                                                           float4* __restrict__ rec, int32_t* __restrict__ radius_out,
@@ -48,97 +154,17 @@ __global__ void __launch_bounds__(256, 3) k_project_geom(DevCam cam, int64_t P, 
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
     const float px = __ldg(prm + i), py = __ldg(prm + S + i), pz = __ldg(prm + 2 * S + i);
-    // O3: p_c = W p + t  (Eq. 4)
-    const float* W = cam.R;
-    const float xc = FA(FA(FA(FM(W[0], px), FM(W[1], py)), FM(W[2], pz)), cam.t[0]);
-    const float yc = FA(FA(FA(FM(W[3], px), FM(W[4], py)), FM(W[5], pz)), cam.t[1]);
-    const float zc = FA(FA(FA(FM(W[6], px), FM(W[7], py)), FM(W[8], pz)), cam.t[2]);
-    int32_t rad = 0, ntiles = 0;
-    uint8_t flags = GS_FLAG_CULLED;
-    do {
-      if (!(zc > cam.z_near)) break;  // R6, R23
-      // O1: activations (R3-R5, R9)
-      const float l0 = __ldg(prm + 3 * S + i), l1 = __ldg(prm + 4 * S + i), l2 = __ldg(prm + 5 * S + i);
-      const float qw = __ldg(prm + 6 * S + i), qx = __ldg(prm + 7 * S + i), qy = __ldg(prm + 8 * S + i),
-                  qz = __ldg(prm + 9 * S + i);
-      const float logit = __ldg(prm + 10 * S + i);
-      float s[3];
-      s[0] = act_exp(l0);
-      s[1] = act_exp(l1);
-      s[2] = act_exp(l2);
-      const float qn = __fsqrt_rn(FA(FA(FA(FM(qw, qw), FM(qx, qx)), FM(qy, qy)), FM(qz, qz)));
-      if (!(qn > 0.f) || !finitef(qn)) break;
-      const float opa = act_sigmoid(logit);
-      float R[3][3];
-      quat_to_rot(FD(qw, qn), FD(qx, qn), FD(qy, qn), FD(qz, qn), R);
-      // O2: Sigma = (R S)(R S)^T  (Eq. 2)
-      float M[3][3], Sig[3][3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) M[r][c] = FM(R[r][c], s[c]);
-#pragma unroll
-      for (int r = 0; r < 3; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) Sig[r][c] = FA(FA(FM(M[r][0], M[c][0]), FM(M[r][1], M[c][1])), FM(M[r][2], M[c][2]));
-      // O4: mean projection (Eq. 4), R1
-      const float ux = FD(xc, zc), uy = FD(yc, zc);
-      const float mux = FA(FM(cam.fx, ux), cam.cx);
-      const float muy = FA(FM(cam.fy, uy), cam.cy);
-      // O5: EWA (Eq. 5) with the 1.3x tangent clamp (R7) and the 0.3 low-pass (R8)
-      const float limx = FM(1.3f, FD((float)cam.W, FM(2.f, cam.fx)));
-      const float limy = FM(1.3f, FD((float)cam.H, FM(2.f, cam.fy)));
-      const float uxc = fminf(fmaxf(ux, -limx), limx);
-      const float uyc = fminf(fmaxf(uy, -limy), limy);
-      const float J00 = FD(cam.fx, zc), J02 = FD(-FM(cam.fx, uxc), zc);
-      const float J11 = FD(cam.fy, zc), J12 = FD(-FM(cam.fy, uyc), zc);
-      float T[2][3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        T[0][c] = FA(FM(J00, W[c]), FM(J02, W[6 + c]));
-        T[1][c] = FA(FM(J11, W[3 + c]), FM(J12, W[6 + c]));
-      }
-      float MT[2][3];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) MT[r][c] = FA(FA(FM(T[r][0], Sig[0][c]), FM(T[r][1], Sig[1][c])), FM(T[r][2], Sig[2][c]));
-      const float a = FA(FA(FA(FM(MT[0][0], T[0][0]), FM(MT[0][1], T[0][1])), FM(MT[0][2], T[0][2])), 0.3f);
-      const float b = FA(FA(FM(MT[0][0], T[1][0]), FM(MT[0][1], T[1][1])), FM(MT[0][2], T[1][2]));
-      const float c = FA(FA(FA(FM(MT[1][0], T[1][0]), FM(MT[1][1], T[1][1])), FM(MT[1][2], T[1][2])), 0.3f);
-      // O6: conic
-      const float det = FS(FM(a, c), FM(b, b));
-      if (!(det > 0.f) || !finitef(det)) break;
-      const float cA = FD(c, det), cB = FD(-b, det), cC = FD(a, det);
-      if (!finitef(cA) || !finitef(cB) || !finitef(cC) || !finitef(mux) || !finitef(muy)) break;
-      // O7: radius and tile rectangle (R10, R11)
-      const float mid = FM(0.5f, FA(a, c));
-      const float disc = FS(FM(mid, mid), det);
-      const float lam = FA(mid, __fsqrt_rn(fmaxf(disc, 0.f)));
-      const float rf = ceilf(FM(3.f, __fsqrt_rn(lam)));
-      float xlo = ceilf(FS(mux, rf)), xhi = floorf(FA(mux, rf));
-      float ylo = ceilf(FS(muy, rf)), yhi = floorf(FA(muy, rf));
-      xlo = fmaxf(xlo, 0.f);
-      ylo = fmaxf(ylo, 0.f);
-      xhi = fminf(xhi, (float)(cam.W - 1));
-      yhi = fminf(yhi, (float)(cam.H - 1));
-      if (!(xlo <= xhi) || !(ylo <= yhi)) break;
-      const int x0 = (int)xlo / kTile, x1 = (int)xhi / kTile + 1;
-      const int y0 = (int)ylo / kTile, y1 = (int)yhi / kTile + 1;
-      rad = (int32_t)fminf(rf, (float)(1 << 30));
-      ntiles = (x1 - x0) * (y1 - y0);
-      flags = ((uxc != ux) ? GS_FLAG_JCLAMP_X : 0) | ((uyc != uy) ? GS_FLAG_JCLAMP_Y : 0);
-      const uint32_t rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
-      const uint32_t ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
+    const Geom g = project_geom_one(cam, px, py, pz, [&](int row) { return __ldg(prm + row * S + i); });
+    if (g.rad > 0) {
       float4* r4 = rec + 3 * i;
-      r4[0] = make_float4(mux, muy, zc, opa);
-      reinterpret_cast<float2*>(r4 + 1)[0] = make_float2(cA, cB);
-      reinterpret_cast<float*>(r4 + 1)[2] = cC;
-      reinterpret_cast<float2*>(r4 + 2)[1] = make_float2(__uint_as_float(rx), __uint_as_float(ry));
-    } while (0);
-    radius_out[i] = rad;
-    tiles_out[i] = ntiles;
-    flags_out[i] = flags;
+      r4[0] = g.q0;
+      reinterpret_cast<float2*>(r4 + 1)[0] = make_float2(g.q1.x, g.q1.y);
+      reinterpret_cast<float*>(r4 + 1)[2] = g.q1.z;
+      reinterpret_cast<float2*>(r4 + 2)[1] = make_float2(__uint_as_float(g.rx), __uint_as_float(g.ry));
+    }
+    radius_out[i] = g.rad;
+    tiles_out[i] = g.ntiles;
+    flags_out[i] = g.flags;
   }
 }
 
@@ -179,10 +205,109 @@ __global__ void __launch_bounds__(256, 4) k_project_color(DevCam cam, int64_t P,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1 (default): the whole projection (O1-O8) in one pass.  A CTA owns 128
+// consecutive Gaussians; one thread stages their 11 geometry rows into shared
+// memory with 1-D TMA bulk copies (11 x 512 B in flight per CTA, no register
+// staging), the CTA computes O1-O7, and only if any of its Gaussians is visible
+// (Morton order makes CTAs mostly all-visible or all-culled) it bulk-copies the
+// 3 (deg+1)^2 SH rows and computes the colour (O8).  Each visible Gaussian's 48-B
+// record is written once with three 16-B stores.
+// ---------------------------------------------------------------------------
+constexpr int kPjThreads = 128;
+
+template <int DEG>
+__global__ void __launch_bounds__(kPjThreads) k_project(DevCam cam, int64_t P, int64_t S,
+                                                        const float* __restrict__ prm, float4* __restrict__ rec,
+                                                        int32_t* __restrict__ radius_out,
+                                                        int32_t* __restrict__ tiles_out,
+                                                        uint8_t* __restrict__ flags_out) {
+  constexpr int NK = (DEG + 1) * (DEG + 1), NSH = 3 * NK;
+  __shared__ __align__(16) float s_geo[11][kPjThreads];
+  __shared__ __align__(16) float s_sh[NSH][kPjThreads];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPjThreads;
+  // columns i0 .. i0 + ncol - 1 exist in every row (P_stride = S is a multiple of 4,
+  // so the byte count is a multiple of 16 and every row segment is 16-B aligned)
+  const int64_t ncol = S - i0 < kPjThreads ? S - i0 : (int64_t)kPjThreads;
+  const uint32_t bytes = (uint32_t)ncol * 4u;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, 11u * bytes);
+#pragma unroll 1
+    for (int r = 0; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar);
+  }
+  mbar_wait(&bar, 0);
+  const int64_t i = i0 + tid;
+  Geom g;
+  g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
+  if (i < P) g = project_geom_one(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&](int row) { return s_geo[row][tid]; });
+  const bool vis = g.rad > 0;
+  if (__syncthreads_or(vis)) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)NSH * bytes);
+#pragma unroll 1
+      for (int r = 0; r < NSH; ++r) bulk_g2s(s_sh[r], prm + (11 + r) * S + i0, bytes, &bar);
+    }
+    mbar_wait(&bar, 1);
+    if (vis) {
+      // O8: SH colour at the mean's viewing direction (R13); same arithmetic as K1b
+      const float vx = s_geo[0][tid] - cam.ocam[0], vy = s_geo[1][tid] - cam.ocam[1], vz = s_geo[2][tid] - cam.ocam[2];
+      const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+      const float x = vx * inv, y = vy * inv, z = vz * inv;
+      float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        float Y, gx, gy, gz;
+        sh_term(k, x, y, z, Y, gx, gy, gz);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) acc[ch] = fmaf(s_sh[3 * k + ch][tid], Y, acc[ch]);
+      }
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        acc[ch] += 0.5f;
+        if (acc[ch] < 0.f) g.flags |= (uint8_t)(1u << ch);
+        acc[ch] = fmaxf(acc[ch], 0.f);
+      }
+      float4* r4 = rec + 3 * i;
+      r4[0] = g.q0;
+      r4[1] = make_float4(g.q1.x, g.q1.y, g.q1.z, acc[0]);
+      r4[2] = make_float4(acc[1], acc[2], __uint_as_float(g.rx), __uint_as_float(g.ry));
+    }
+  }
+  if (i < P) {
+    radius_out[i] = g.rad;
+    tiles_out[i] = g.ntiles;
+    flags_out[i] = g.flags;
+  }
+}
+
+bool use_legacy_project() {
+  static const bool legacy = [] {
+    const char* e = getenv("GSR_PROJECT");
+    return e && e[0] == 'l';
+  }();
+  return legacy;
+}
+
 }  // namespace
 
 void launch_project(const DevCam& cam, int64_t P, int64_t S, int deg, const float* params, gs_proj out,
                     cudaStream_t s) {
+  if (!use_legacy_project()) {
+    const int grid = (int)((P + kPjThreads - 1) / kPjThreads);
+    float4* rec = reinterpret_cast<float4*>(out.rec);
+    switch (deg) {
+      case 0: k_project<0><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      case 1: k_project<1><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      case 2: k_project<2><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      default: k_project<3><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags);
+    }
+    count_launch();
+    return;
+  }
   const int block = 256;
   const int grid = (int)std::min<int64_t>((P + block - 1) / block, (int64_t)sm_count() * 12);
   float4* rec = reinterpret_cast<float4*>(out.rec);
