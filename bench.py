@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
                     help="views in flight (one CUDA stream + buffer set each)")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
+    ap.add_argument("--schedule", action="store_true",
+                    help="keyframe-scheduled online + global optimisation run (PAPER.md:149; SURVEY §8(f) NEXT-1)")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
     return ap.parse_args()
 
@@ -190,6 +192,71 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- NEXT-1
+def run_schedule(args):
+    """The keyframe-scheduled online mapping loop of PAPER.md:149 over a config's pose
+    sequence (replica: 100 poses, m = 5, n = 3, 2 random keyframes; scannetpp setting:
+    m = 10, n = 1, every frame in the list; threshold 50, 10 global passes,
+    PAPER.md:174), each planned iteration one fwd + bwd + Adam step on one view.
+    Device time (CUDA events) of the online phase and of the global passes."""
+    import torch
+
+    import scenegen
+    from paper_2408_12677_b200 import gsr, pipeline
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    lib = gsr.load()
+    w = scenegen.make(args.config, args.seed)
+    cams = w.cameras
+    model = pipeline.GaussianModel(w.scene, dev)
+    tgt = pipeline.GaussianModel(w.target_scene, dev)
+    pipeline.spatially_order(lib, model)
+    pipeline.spatially_order(lib, tgt)
+    cap = pipeline.default_capacity(max(pipeline.measure_keys(lib, model, cams, dev),
+                                        pipeline.measure_keys(lib, tgt, cams, dev)))
+    targets = pipeline.render_targets(lib, tgt, cams, dev, cap)
+    del tgt
+    scannet = args.config in ("scannetpp", "large")
+    setting = dict(m=10, n=1, store_all_frames=True) if scannet else dict(m=5, n=3, store_all_frames=False)
+    new = scenegen.new_primitive_counts(len(cams), args.seed)
+    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap)
+    ko = pipeline.KeyframeOptimizer(lib, tr, new, threshold=50, global_iters=10, seed=args.seed, **setting)
+    for v in range(min(args.warmup, len(cams))):
+        tr.step([v])
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = {}
+
+    def mark(i, v, f):
+        if i == 0:
+            ev["start"] = torch.cuda.Event(enable_timing=True)
+            ev["start"].record(stream)
+        if f < 0 and "glob" not in ev:
+            ev["glob"] = torch.cuda.Event(enable_timing=True)
+            ev["glob"].record(stream)
+    tr.blended.zero_()
+    ko.run(mark)
+    end = torch.cuda.Event(enable_timing=True)
+    end.record(stream)
+    torch.cuda.synchronize()
+    n_on = ko.n_online
+    n_gl = len(ko.views) - n_on
+    t_on = ev["start"].elapsed_time(ev.get("glob", end))
+    t_gl = ev["glob"].elapsed_time(end) if "glob" in ev else 0.0
+    tr.check_capacity()
+    line = {"metric": "keyframe-scheduled online mapping: frames/s and ms per iteration (PAPER.md:149)",
+            "value": len(cams) / (t_on / 1e3), "unit": "frames/s (online phase)", "n_gpus": 1,
+            "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.config, "frames": len(cams), "keyframes": int(ko.is_keyframe.sum()),
+                       "threshold": 50, **setting, "global_iters": 10,
+                       "new_primitives": "scenegen.new_primitive_counts (stand-in for the out-of-scope seeding)"},
+            "online": {"iterations": n_on, "ms": t_on, "ms_per_iteration": t_on / max(n_on, 1)},
+            "global": {"iterations": n_gl, "ms": t_gl, "ms_per_iteration": t_gl / max(n_gl, 1)},
+            "blended_per_s": int(tr.blended.item()) / ((t_on + t_gl) / 1e3),
+            "paper_context": "RTX 3060 global optimisation (derived, SURVEY.md §6b): Replica 25.5 ms/iteration (PAPER.md:354-356), ScanNet++ 876x584 17.7 ms/iteration (PAPER.md:314-316)"}
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -198,6 +265,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.schedule:
+        run_schedule(args)
         return
 
     import numpy as np

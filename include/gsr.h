@@ -264,6 +264,34 @@ size_t gs_spatial_order_workspace(const gs_scene* scene /*HOST*/);
 gs_status gs_spatial_order(const gs_scene* scene /*HOST*/, const float* params_in, float* params_out, int32_t* perm,
                            void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- keyframe schedule (host)
+ * The online optimisation strategy of PAPER.md:149 (§III-B3 "Online Optimization")
+ * with the settings of PAPER.md:174, as a plan of iterations; each iteration is then
+ * one fwd + bwd + Adam step over one view.  Frame t is a
+ * keyframe iff new_prims[t] > threshold; keyframes get m iterations on themselves;
+ * non-keyframes get n, plus one iteration on each of the first (m - n) keyframes of
+ * the shuffled keyframe list (the current frame excluded); after the last frame,
+ * global_iters passes over the keyframe list, each in a freshly shuffled order.
+ * store_all_frames != 0 puts every frame in the list (the paper's ScanNet++ setting)
+ * while the m / n split still follows the threshold.  Shuffles: Fisher-Yates with
+ * the counter-based generator documented in DESIGN.md (R31).  All pointers HOST.
+ *  iter_view[i]:  view (frame) optimised by iteration i
+ *  iter_frame[i]: frame during which iteration i runs, -1 for the global passes
+ *  n_iters:       number of iterations of the plan (always written)
+ *  is_keyframe:   nullable uint8[n_frames]
+ * Returns GS_ERR_CAPACITY (n_iters = the required capacity) if capacity is too small,
+ * GS_ERR_ARG on invalid parameters (n > m, negative counts, NULL). */
+typedef struct {
+  int64_t threshold;        /* 50 */
+  int32_t m, n;             /* Replica 5 / 3, ScanNet++ 10 / 1 */
+  int32_t global_iters;     /* 10 */
+  int32_t store_all_frames; /* 1 for the ScanNet++ setting */
+  uint64_t seed;
+} gs_kf_params;
+gs_status gs_keyframe_schedule(const gs_kf_params* prm /*HOST*/, int64_t n_frames, const int64_t* new_prims /*HOST*/,
+                               int32_t* iter_view /*HOST*/, int32_t* iter_frame /*HOST*/, int64_t capacity,
+                               int64_t* n_iters /*HOST*/, uint8_t* is_keyframe /*HOST, nullable*/);
+
 /* ---------------------------------------------------------------- harness: Eq. 12
  * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
  * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */

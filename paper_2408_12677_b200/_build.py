@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["api.cu", "project.cu", "project_bwd.cu", "binning.cu", "render.cu", "optim.cu", "naive.cu"]
+SOURCES = ["api.cu", "project.cu", "project_bwd.cu", "binning.cu", "render.cu", "optim.cu", "naive.cu", "schedule.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIBS = {"libgsr.so": [], "libgsr_exact.so": ["-DGSR_EXACT_EXP"]}
 
@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> list:
         if not (force or _stale(target)):
             continue
         tag = lib.replace(".so", "")
-        objs = [os.path.join(objdir, f"{tag}_{s.replace('.cu', '.o')}") for s in SOURCES]
+        objs = [os.path.join(objdir, f"{tag}_{os.path.splitext(s)[0]}.o") for s in SOURCES]
         jobs.append((target, objs, defines))
     with cf.ThreadPoolExecutor(max_workers=min(10, os.cpu_count() or 4)) as ex:
         futs = [ex.submit(_compile, s, o, d) for (_, objs, d) in jobs for s, o in zip(SOURCES, objs)]

@@ -40,6 +40,11 @@ class GsScene(C.Structure):
     _fields_ = [("P", C.c_int64), ("P_stride", C.c_int64), ("sh_degree", C.c_int32)]
 
 
+class GsKfParams(C.Structure):
+    _fields_ = [("threshold", C.c_int64), ("m", C.c_int32), ("n", C.c_int32), ("global_iters", C.c_int32),
+                ("store_all_frames", C.c_int32), ("seed", C.c_uint64)]
+
+
 class GsProj(C.Structure):
     _fields_ = [("rec", C.c_void_p), ("radius", C.c_void_p), ("tiles", C.c_void_p), ("flags", C.c_void_p)]
 
@@ -109,9 +114,10 @@ class Library:
         lib.gs_spatial_order_workspace.restype = C.c_size_t
         lib.gs_spatial_order.argtypes = [vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
+        lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -208,6 +214,25 @@ class Library:
         return self._check("gs_adam_step", self.lib.gs_adam_step(
             C.byref(sc), _ptr(params), _ptr(grad), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
             1 if zero_grad else 0, _stream(stream)))
+
+    def keyframe_schedule(self, new_prims, threshold=50, m=5, n=3, global_iters=10, store_all_frames=False, seed=0):
+        """gs_keyframe_schedule (host): returns (iter_view, iter_frame, is_keyframe) numpy arrays."""
+        import numpy as np
+        prm = GsKfParams(int(threshold), int(m), int(n), int(global_iters), 1 if store_all_frames else 0, int(seed))
+        counts = np.ascontiguousarray(new_prims, dtype=np.int64)
+        T = counts.shape[0]
+        kf = np.zeros(max(T, 1), np.uint8)
+        need = C.c_int64(0)
+        cp = counts.ctypes.data_as(C.c_void_p)
+        st = self.lib.gs_keyframe_schedule(C.byref(prm), T, cp, None, None, 0, C.byref(need), kf.ctypes.data_as(C.c_void_p))
+        if st not in (GS_OK, GS_ERR_CAPACITY):
+            raise GsError("gs_keyframe_schedule", st, "invalid parameters")
+        views = np.zeros(max(need.value, 1), np.int32)
+        frames = np.zeros(max(need.value, 1), np.int32)
+        self._check("gs_keyframe_schedule", self.lib.gs_keyframe_schedule(
+            C.byref(prm), T, cp, views.ctypes.data_as(C.c_void_p), frames.ctypes.data_as(C.c_void_p), need.value,
+            C.byref(need), kf.ctypes.data_as(C.c_void_p)))
+        return views[:need.value], frames[:need.value], kf[:T].astype(bool)
 
     def l1_loss_grad(self, rgb, depth, t_rgb, t_depth, w_depth, g_rgb, g_depth, loss=None, stream=None):
         return self._check("gs_l1_loss_grad", self.lib.gs_l1_loss_grad(

@@ -318,3 +318,32 @@ def render_targets(lib, target_model: GaussianModel, cameras, device, key_capaci
 
 def default_capacity(K: int) -> int:
     return int(math.ceil(K * 1.3)) + 4096
+
+
+class KeyframeOptimizer:
+    """GSFusion's keyframe-scheduled online optimisation (settings
+    PAPER.md:174) on top of the built path: the plan comes from
+    the library's host scheduler (gs_keyframe_schedule: keyframe if more than
+    ``threshold`` new primitives, m / n iterations, (m - n) shuffled keyframes for
+    non-keyframes, ``global_iters`` passes over the keyframe list after scanning) and
+    every planned iteration is one fwd + bwd + Adam step of ``trainer`` on one view.
+    ``new_prims`` is the per-frame count of newly initialised Gaussians (the output of
+    the out-of-scope seeding stage; scenegen.new_primitive_counts stands in for it)."""
+
+    def __init__(self, lib, trainer: Trainer, new_prims, threshold=50, m=5, n=3, global_iters=10,
+                 store_all_frames=False, seed=0):
+        self.trainer = trainer
+        self.views, self.frames, self.is_keyframe = lib.keyframe_schedule(
+            new_prims, threshold, m, n, global_iters, store_all_frames, seed)
+
+    @property
+    def n_online(self) -> int:
+        return int((self.frames >= 0).sum())
+
+    def run(self, on_iteration=None):
+        """Executes the whole plan (asynchronously on the current stream).
+        on_iteration(i, view, frame) is called before each iteration."""
+        for i, (v, f) in enumerate(zip(self.views.tolist(), self.frames.tolist())):
+            if on_iteration is not None:
+                on_iteration(i, v, f)
+            self.trainer.step([v])

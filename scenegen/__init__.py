@@ -401,3 +401,20 @@ def shard_views(num_views: int, rank: int, world: int):
     lo = (rank * num_views) // world
     hi = ((rank + 1) * num_views) // world
     return list(range(lo, hi))
+
+
+def new_primitive_counts(num_frames: int, seed: int = 0):
+    """Seeded stand-in for the per-frame number of newly initialised Gaussians, the
+    keyframe criterion of PAPER.md:149 (its producer, the TSDF-gated quadtree
+    seeding of PAPER.md:125-135, is out of scope).  Shape of an online scan: early
+    frames see mostly unobserved space (thousands of new primitives, decaying with a
+    15-frame time constant and log-normal spread), later frames mostly revisit (a few
+    new ones) with occasional turns into unseen areas (probability 0.15, 50-800 new).
+    Seed stream: seed + 3.  Returns int64[num_frames]."""
+    rng = np.random.default_rng(seed + 3)
+    t = np.arange(num_frames)
+    base = 4000.0 * np.exp(-t / 15.0) * rng.lognormal(0.0, 0.5, num_frames) + 5.0
+    counts = rng.poisson(base)
+    turns = rng.random(num_frames) < 0.15
+    counts = counts + turns * rng.integers(50, 800, num_frames)
+    return counts.astype(np.int64)

@@ -544,3 +544,31 @@ def test_tile_order_permutation_and_invariance(lib):
     for a, c in zip(outs[0][:3], outs[1][:3]):
         assert np.array_equal(a, c)
     assert grad_mismatch(outs[1][3], outs[0][3], rtol=1e-4, atol=1e-6).mean() <= 1e-4
+
+
+def test_keyframe_optimizer_runs_plan(lib):
+    """NEXT-1: the keyframe-scheduled plan drives the GPU path view by view; every
+    planned iteration is one step (Adam step counter), the loss on the keyframes drops."""
+    w = scenegen.make("small")
+    cams = [scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.02 * (k - 6)), [0.04 * (k - 6), 0.0, 0.0])
+            for k in range(12)]
+    model = pipeline.GaussianModel(w.scene, DEV)
+    tgt = pipeline.GaussianModel(w.target_scene, DEV)
+    cap = pipeline.default_capacity(pipeline.measure_keys(lib, model, cams, DEV))
+    targets = pipeline.render_targets(lib, tgt, cams, DEV, cap)
+    tr = pipeline.Trainer(lib, model, cams, targets, DEV, cap)
+    new = scenegen.new_primitive_counts(len(cams), seed=0)
+    ko = pipeline.KeyframeOptimizer(lib, tr, new, threshold=50, m=5, n=3, global_iters=2, seed=0)
+
+    def kf_loss():
+        tot = 0.0
+        for v in np.flatnonzero(ko.is_keyframe):
+            b = tr.buf
+            pipeline.render(lib, model, cams[v], b)
+            tot += float((b.rgb - targets[v][0]).abs().mean() + (b.depth - targets[v][1]).abs().mean())
+        return tot
+    before = kf_loss()
+    ko.run()
+    torch.cuda.synchronize()
+    assert model.step_count == len(ko.views)
+    assert kf_loss() < before
