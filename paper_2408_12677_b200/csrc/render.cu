@@ -43,6 +43,17 @@ namespace gsr {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
+// Resident warps per SM the fast kernels are compiled for (register cap 65536 /
+// (32 x warps)); the register file is split per SM sub-partition, so 16 warps = 4
+// per SMSP at <= 128 registers, 20 = 5 per SMSP at <= 102 (measured: 16 -> 20 warps
+// gives 7.28 -> 6.92 ms per scannetpp step, 24 spills and loses).  A/B: -DGSR_FWD_MINW=...
+#ifndef GSR_FWD_MINW
+#define GSR_FWD_MINW 20
+#endif
+#ifndef GSR_BWD_MINW
+#define GSR_BWD_MINW 20
+#endif
+constexpr int kFwdMinWarps = GSR_FWD_MINW, kBwdMinWarps = GSR_BWD_MINW;
 constexpr int kPix = 8;             // pixels per lane
 constexpr int kDenseBlocks = 3;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
 constexpr int kDenseBlocksBwd = 6;  // bwd: same (its per-block body is ~2x longer)
@@ -352,7 +363,7 @@ __device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
 }
 
 template <int WPC>
-__global__ void __launch_bounds__(WPC * 32) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    float* __restrict__ out_rgb,
@@ -533,7 +544,7 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
 }
 
 template <int WPC>
-__global__ void __launch_bounds__(WPC * 32) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
+__global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
                                                                    const float* __restrict__ T_final,

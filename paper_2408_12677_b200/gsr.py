@@ -244,7 +244,9 @@ _LIBS = {}
 
 
 def load(exact: bool = False) -> Library:
-    name = "libgsr_exact.so" if exact else "libgsr.so"
+    # GSR_LIB selects an in-tree build variant of the fast library (A/B experiments,
+    # e.g. libgsr_w20.so from tools/build_variant.py); default libgsr.so
+    name = "libgsr_exact.so" if exact else os.environ.get("GSR_LIB", "libgsr.so")
     if name not in _LIBS:
         _LIBS[name] = Library(os.path.join(PKG, name))
     return _LIBS[name]
