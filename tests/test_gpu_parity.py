@@ -59,7 +59,7 @@ def test_libraries_load(lib, lib_exact):
 
 
 # ----------------------------------------------------------------------------- gs_project
-@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp"])
+@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp", "large"])
 def test_project_bitexact(lib, name):
     w = workload(name)
     cam, scene = w.cameras[0], w.scene
@@ -94,7 +94,7 @@ def test_project_bitexact(lib, name):
 
 
 # ----------------------------------------------------------------------------- gs_bin_tiles
-@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp"])
+@pytest.mark.parametrize("name", ["tiny", "small", "replica", "scannetpp", "large"])
 def test_bin_bitexact_stagewise(lib, name):
     w = workload(name)
     cam, scene = w.cameras[0], w.scene
@@ -175,7 +175,7 @@ def test_render_fwd_parity_with_flip_accounting(lib, name):
     assert T.min() >= 1e-4 and T.max() <= 1.0  # R16 invariant on the GPU path
 
 
-@pytest.mark.parametrize("name", ["replica", "scannetpp"])
+@pytest.mark.parametrize("name", ["replica", "scannetpp", "large"])
 def test_render_fwd_sampled_full_size(lib, name):
     """Full-size config, GPU chain project -> bin -> fwd (the bench launch), checked
     on 3000 sampled pixels (random + two complete tiles + the ragged last row/col)."""
@@ -236,7 +236,7 @@ def test_render_bwd_parity_stagewise(lib, name):
     assert frac <= 1e-3, f"{int(bad.sum())}/{bad.size} gradient elements outside tolerance; worst {[(g.ravel()[k], ref.ravel()[k]) for k in worst]}"
 
 
-@pytest.mark.parametrize("name", ["replica", "scannetpp"])
+@pytest.mark.parametrize("name", ["replica", "scannetpp", "large"])
 def test_render_bwd_sampled_full_size(lib, name):
     """Full-size view with upstream gradient on a sampled set of 64 tiles."""
     w = workload(name)
