@@ -522,6 +522,12 @@ def main():
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),
         "stage_ms": stage_ms, "stage_ms_overlapped": stage_ms_overlapped, "stage_hbm": hbm,
+        "work": {"blended_per_view": blended / max(world, 1) / n_views, "evaluated_per_view": evaluated / nv,
+                 "keys_per_view": keys / nv, "views_per_s": views_done * world / (ms / 1e3),
+                 "evaluated_per_s": evaluated / nv * views_done * world / (ms / 1e3),
+                 "keys_per_s": keys / nv * views_done * world / (ms / 1e3),
+                 "note": "evaluated = sum of n_contrib (list entries visited up to each pixel's stop, R24), "
+                         "measured on up to 8 of this rank's views after the timed region"},
         "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive,
     }
     print(json.dumps(line), flush=True)

@@ -480,6 +480,9 @@ __global__ void k_ranges(const uint16_t* __restrict__ skeys, const Counters* __r
 //               ballots.  Keys of a tile thus keep their depth order: the output is
 //               the same stable sort, in ~3 passes of 2-6 B/key and no look-back.
 // ---------------------------------------------------------------------------
+#ifndef GSR_TSCATTER_G
+#define GSR_TSCATTER_G 8
+#endif
 constexpr int kBkThreads = 256, kBkWarps = kBkThreads / 32;
 constexpr int kBkMaxChunks = 512;  // chist capacity (workspace); C = min(this, SMs x CTAs/SM)
 
@@ -621,7 +624,7 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   chunk_bounds(K, C, blockIdx.x, warp, a, b);
   uint16_t* my = s_w + (int64_t)warp * NTp;
   // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
-  constexpr int G = 8;  // 32-key groups in flight per warp
+  constexpr int G = GSR_TSCATTER_G;  // 32-key groups in flight per warp (latency: 8 warps per SM)
   for (int64_t kb = a; kb < b; kb += 32 * G) {
     uint32_t tt[G];
 #pragma unroll

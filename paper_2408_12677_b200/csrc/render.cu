@@ -55,8 +55,14 @@ constexpr int kWarpsPerCta = 4;
 #endif
 constexpr int kFwdMinWarps = GSR_FWD_MINW, kBwdMinWarps = GSR_BWD_MINW;
 constexpr int kPix = 8;             // pixels per lane
-constexpr int kDenseBlocks = 3;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
-constexpr int kDenseBlocksBwd = 6;  // bwd: same (its per-block body is ~2x longer)
+#ifndef GSR_DENSE_FWD
+#define GSR_DENSE_FWD 3
+#endif
+#ifndef GSR_DENSE_BWD
+#define GSR_DENSE_BWD 6
+#endif
+constexpr int kDenseBlocks = GSR_DENSE_FWD;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
+constexpr int kDenseBlocksBwd = GSR_DENSE_BWD;  // bwd: same (its per-block body is ~2x longer)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kAlphaMin = 1.0f / 255.0f;
 constexpr float kTStop = 1e-4f;
