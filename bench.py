@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
                     help="views in flight (one CUDA stream + buffer set each)")
+    ap.add_argument("--optim", default="sharded", choices=["sharded", "replicated"],
+                    help="N > 1: reduce-scatter + sharded Adam + all-gather, or all-reduce + replicated Adam")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--schedule", action="store_true",
                     help="keyframe-scheduled online + global optimisation run (PAPER.md:149; SURVEY §8(f) NEXT-1)")
@@ -312,8 +314,12 @@ def main():
 
     def step_views(i):
         return my_views if batched else [my_views[i % len(my_views)]]
+    optimizer = None
+    if world > 1 and batched and args.optim == "sharded":
+        optimizer = pipeline.ShardedAdam(lib, model)
+        allreduce = None
     tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce,
-                          streams=args.streams if batched else 1)
+                          streams=args.streams if batched else 1, optimizer=optimizer)
     stream = torch.cuda.current_stream()
 
     # --- warm-up
@@ -515,7 +521,7 @@ def main():
         "scaling": "strong" if batched else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
-                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": f"views/dp{world}" if batched else f"replicas x{world}",
+                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({args.optim} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (

@@ -251,6 +251,17 @@ gs_status gs_adam_step(const gs_scene* scene /*HOST*/, float* params, float* gra
                        const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
                        int zero_grad, void* stream);
 
+/* gs_adam_step restricted to the scalars [begin, end) of the flattened [F][P_stride]
+ * arrays (row r = index / P_stride keeps its learning rate): the optimiser half of a
+ * reduce-scatter -> sharded Adam -> all-gather step across ranks (SURVEY.md §8(f)
+ * NEXT-2).  params, m, v: the FULL arrays (only the range is read or
+ * written); grad_range: float[end - begin], the (reduce-scattered) gradient of the
+ * range.  begin and end must be multiples of 4 (GS_ERR_ALIGN).  The gradient is not
+ * zeroed.  Same hyper-parameters and update as gs_adam_step. */
+gs_status gs_adam_step_range(const gs_scene* scene /*HOST*/, float* params, const float* grad_range, float* m, float* v,
+                             const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
+                             int64_t begin, int64_t end, void* stream);
+
 /* ---------------------------------------------------------------- layout (setup)
  * gs_spatial_order: params_out = params_in with the Gaussians (columns) permuted into
  * Morton (Z-curve) order of their means, 10 bits per axis inside the means'

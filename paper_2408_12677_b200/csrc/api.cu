@@ -378,6 +378,31 @@ gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float*
   return check_launch("gs_adam_step");
 }
 
+gs_status gs_adam_step_range(const gs_scene* scene, float* params, const float* grad_range, float* m, float* v,
+                             const float* lr_per_row, float beta1, float beta2, float eps, int64_t step, int64_t begin,
+                             int64_t end, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_adam_step_range"));
+  const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
+  if (!lr_per_row || step < 1 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f) ||
+      begin < 0 || end < begin || end > n) {
+    set_error("gs_adam_step_range: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", (long long)step,
+              (long long)begin, (long long)end, (long long)n);
+    return GS_ERR_ARG;
+  }
+  if ((begin & 3) || (end & 3)) {
+    set_error("gs_adam_step_range: begin/end must be multiples of 4");
+    return GS_ERR_ALIGN;
+  }
+  if (end == begin) return GS_OK;
+  GS_TRY(check_ptrs("gs_adam_step_range", {{params, "params"}, {grad_range, "grad_range"}, {m, "m"}, {v, "v"}}));
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  launch_adam(rows_of(scene), scene->P_stride, params, const_cast<float*>(grad_range), m, v, lr_per_row, beta1, beta2,
+              eps, (float)bc1, (float)bc2, 0, static_cast<cudaStream_t>(stream), begin, end);
+  return check_launch("gs_adam_step_range");
+}
+
 gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
                           const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
                           void* stream) {

@@ -10,13 +10,16 @@ struct LrTable {
   float step[64];  // lr_row / (1 - beta1^t)
 };
 
+// Scalars [4 b4, 4 e4) of the flattened [F][P_stride] arrays; g holds the gradient of
+// that range (g[i - b4]), so a rank of the sharded optimiser passes its reduce-scattered
+// shard and the full step passes b4 = 0, g = grad.
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
-                                              float4* __restrict__ v, int64_t n4, int64_t S4, LrTable lr, float b1,
-                                              float b2, float eps, float rs_bc2, int zero_grad) {
+                                              float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4, LrTable lr,
+                                              float b1, float b2, float eps, float rs_bc2, int zero_grad) {
   const float c1 = 1.f - b1, c2 = 1.f - b2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i = b4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e4; i += (int64_t)gridDim.x * blockDim.x) {
     const float step = lr.step[i / S4];
-    const float4 gg = g[i];
+    const float4 gg = g[i - b4];
     float4 mm = m[i], vv = v[i], pp = p[i];
 #define ADAM_LANE(c)                                              \
   mm.c = b1 * mm.c + c1 * gg.c;                                  \
@@ -27,7 +30,7 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
     p[i] = pp;
     m[i] = mm;
     v[i] = vv;
-    if (zero_grad) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (zero_grad) g[i - b4] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
@@ -57,14 +60,16 @@ __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restric
 }  // namespace
 
 void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
-                 float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s) {
+                 float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s, int64_t begin,
+                 int64_t end) {
   LrTable t{};
   for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
-  const int64_t n4 = F * S / 4;
+  if (end < 0) end = F * S;
+  const int64_t n4 = (end - begin) / 4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
   k_adam<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
-                                           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, S / 4, t,
-                                           beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
+                                           reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
+                                           end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
   count_launch();
 }
 

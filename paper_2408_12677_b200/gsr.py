@@ -114,10 +114,11 @@ class Library:
         lib.gs_spatial_order_workspace.restype = C.c_size_t
         lib.gs_spatial_order.argtypes = [vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
+        lib.gs_adam_step_range.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, i64, i64, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -214,6 +215,13 @@ class Library:
         return self._check("gs_adam_step", self.lib.gs_adam_step(
             C.byref(sc), _ptr(params), _ptr(grad), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
             1 if zero_grad else 0, _stream(stream)))
+
+    def adam_step_range(self, sc, params, grad_range, m, v, lr_per_row, step, begin, end, beta1=0.9, beta2=0.999,
+                        eps=1e-15, stream=None):
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        return self._check("gs_adam_step_range", self.lib.gs_adam_step_range(
+            C.byref(sc), _ptr(params), _ptr(grad_range), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
+            int(begin), int(end), _stream(stream)))
 
     def keyframe_schedule(self, new_prims, threshold=50, m=5, n=3, global_iters=10, store_all_frames=False, seed=0):
         """gs_keyframe_schedule (host): returns (iter_view, iter_frame, is_keyframe) numpy arrays."""

@@ -123,9 +123,13 @@ class Trainer:
     by bench.py to time them with CUDA events on the launching stream)."""
 
     def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
-                 w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1):
+                 w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1, optimizer=None):
         self.lib, self.model, self.cameras, self.targets = lib, model, cameras, targets
         self.device, self.w_depth, self.allreduce = device, w_depth, allreduce
+        # optimizer: None = (allreduce +) replicated gs_adam_step; else an object whose
+        # step() combines the gradient across ranks and updates the parameters
+        # (ShardedAdam); it is called after the step counter is incremented
+        self.optimizer = optimizer
         self.chunk = max(1, min(8, int(chunk)))
         # views in flight: view k of a step runs on stream k % streams with its own
         # buffers, so that one view's latency-bound projection / binning kernels overlap
@@ -283,9 +287,12 @@ class Trainer:
             main.wait_event(ev)
         if pending or first:
             self._chain(pending, accumulate=not first)
+        m.step_count += 1
+        if self.optimizer is not None:
+            self.optimizer.step()
+            return
         if self.allreduce is not None:
             self.allreduce(m.grad)
-        m.step_count += 1
         self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False)
 
     def _chain(self, gcams, accumulate):
@@ -347,3 +354,58 @@ class KeyframeOptimizer:
             if on_iteration is not None:
                 on_iteration(i, v, f)
             self.trainer.step([v])
+
+
+class ShardedAdam:
+    """The gradient exchange + optimiser step of the data-parallel path as
+    reduce-scatter -> Adam on this rank's shard -> all-gather of the parameters
+    (SURVEY.md §8(e) "equivalent alternative", §8(f) NEXT-2): the same wire bytes as
+    the all-reduce, 1/world of the optimiser's HBM traffic per rank, parameters
+    bit-identical on every rank (each scalar is updated by exactly one rank).
+
+    The flattened [F][P_stride] arrays are cut into `world` shards of `shard` scalars
+    (a multiple of 4); model.grad and model.params become views of zero-padded flat
+    buffers of world x shard scalars so the collectives need no copies.
+    adam_range(begin, end, grad_shard) applies the optimiser to scalars [begin, end)
+    (default: the library's gs_adam_step_range on the model's device buffers)."""
+
+    def __init__(self, lib, model: GaussianModel, group=None, adam_range=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.model = model
+        F, S = model.F, model.P_stride
+        self.n = F * S
+        self.shard = ((self.n + self.world - 1) // self.world + 3) // 4 * 4
+        dev = model.params.device
+        self.gpad = torch.zeros(self.world * self.shard, dtype=torch.float32, device=dev)
+        self.ppad = torch.zeros(self.world * self.shard, dtype=torch.float32, device=dev)
+        self.gpad[:self.n].copy_(model.grad.reshape(-1))
+        self.ppad[:self.n].copy_(model.params.reshape(-1))
+        model.grad = self.gpad[:self.n].view(F, S)
+        model.params = self.ppad[:self.n].view(F, S)
+        self.gshard = torch.empty(self.shard, dtype=torch.float32, device=dev)
+        self.pshard = torch.empty(self.shard, dtype=torch.float32, device=dev)
+        self.begin = min(self.rank * self.shard, self.n)
+        self.end = min(self.begin + self.shard, self.n)
+        self.nccl = dist.get_backend(group) == "nccl"
+        if adam_range is None:
+            def adam_range(b, e, g):
+                lib.adam_step_range(model.desc, model.params, g, model.m, model.v, model.lr, model.step_count, b, e)
+        self.adam_range = adam_range
+
+    def step(self):
+        d = self.dist
+        if self.nccl:
+            d.reduce_scatter_tensor(self.gshard, self.gpad, op=d.ReduceOp.SUM, group=self.group)
+        else:  # gloo (CPU tests): no reduce-scatter; all-reduce and keep this rank's shard
+            d.all_reduce(self.gpad, op=d.ReduceOp.SUM, group=self.group)
+            self.gshard.copy_(self.gpad[self.rank * self.shard:(self.rank + 1) * self.shard])
+        if self.end > self.begin:
+            self.adam_range(self.begin, self.end, self.gshard)
+        self.pshard.copy_(self.ppad[self.rank * self.shard:(self.rank + 1) * self.shard])
+        if self.nccl:
+            d.all_gather_into_tensor(self.ppad, self.pshard, group=self.group)
+        else:
+            parts = list(self.ppad.view(self.world, self.shard).unbind(0))
+            d.all_gather(parts, self.pshard, group=self.group)

@@ -572,3 +572,60 @@ def test_keyframe_optimizer_runs_plan(lib):
     torch.cuda.synchronize()
     assert model.step_count == len(ko.views)
     assert kf_loss() < before
+
+
+def test_adam_step_range_matches_full_step(lib):
+    """gs_adam_step_range on [b, e) == gs_adam_step restricted to [b, e); untouched
+    outside; misaligned bounds rejected."""
+    rng = np.random.default_rng(4)
+    P, deg = 999, 1
+    F, S = 11 + 3 * 4, scenegen.pad4(999)
+    sc = gsr.scene_desc(P, S, deg)
+    arrs = [rng.normal(size=(F, S)).astype(np.float32) for _ in range(2)] + \
+           [(rng.uniform(0, 1e-3, size=(F, S))).astype(np.float32), rng.normal(size=(F, S)).astype(np.float32)]
+    lr = pipeline.lr_per_row(deg)
+    full = [torch.from_numpy(a.copy()).to(DEV) for a in arrs]  # p, m, v, g
+    part = [torch.from_numpy(a.copy()).to(DEV) for a in arrs]
+    lib.adam_step(sc, full[0], full[3], full[1], full[2], lr, 3, zero_grad=False)
+    b, e = 4 * 1001, 4 * 3777
+    gr = part[3].view(-1)[b:e].clone()
+    lib.adam_step_range(sc, part[0], gr, part[1], part[2], lr, 3, b, e)
+    torch.cuda.synchronize()
+    for x, y, a in zip(full[:3], part[:3], arrs[:3]):
+        xf, yf = x.view(-1).cpu().numpy(), y.view(-1).cpu().numpy()
+        np.testing.assert_array_equal(yf[b:e], xf[b:e])
+        np.testing.assert_array_equal(np.delete(yf, np.s_[b:e]), np.delete(a.reshape(-1), np.s_[b:e]))
+    with pytest.raises(gsr.GsError):
+        lib.adam_step_range(sc, part[0], gr, part[1], part[2], lr, 3, b + 1, e)
+
+
+def test_sharded_adam_single_rank_nccl(lib):
+    """pipeline.ShardedAdam through a real NCCL process group (world size 1 on this
+    GPU: reduce_scatter_tensor / all_gather_into_tensor + gs_adam_step_range) gives
+    the same parameters as the replicated gs_adam_step."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = workload("small")
+        rng = np.random.default_rng(8)
+        g = torch.from_numpy(rng.normal(size=w.scene.params.shape).astype(np.float32)).to(DEV)
+        ma, mb = pipeline.GaussianModel(w.scene, DEV), pipeline.GaussianModel(w.scene, DEV)
+        opt = pipeline.ShardedAdam(lib, mb)
+        for it in range(3):
+            ma.grad.copy_(g * (it + 1))
+            mb.grad.copy_(g * (it + 1))
+            ma.step_count += 1
+            lib.adam_step(ma.desc, ma.params, ma.grad, ma.m, ma.v, ma.lr, ma.step_count, zero_grad=False)
+            mb.step_count += 1
+            opt.step()
+        torch.cuda.synchronize()
+        assert torch.equal(ma.params, mb.params)
+    finally:
+        dist.destroy_process_group()

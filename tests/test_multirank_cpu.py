@@ -95,3 +95,62 @@ def test_gloo_two_ranks_allreduce_matches_sum():
     np.testing.assert_allclose(out["grad"], ref, rtol=1e-12, atol=1e-15)
     assert out["shards"] == [[0, 1], [2, 3, 4]]
     np.testing.assert_array_equal(out["params"][0], out["params"][1])
+
+
+def _sharded_worker(rank, world, port, out):
+    """pipeline.ShardedAdam on gloo: reduce-scatter (emulated) -> Adam on the rank's
+    shard (here the CPU oracle's Adam restricted to the range) -> all-gather."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import gsref
+    from paper_2408_12677_b200 import pipeline
+    w, _ = _views()
+    model = pipeline.GaussianModel(w.scene, torch.device("cpu"))
+    rng = np.random.default_rng(100 + rank)
+    model.grad.copy_(torch.from_numpy(rng.normal(size=model.grad.shape).astype(np.float32)))
+    lr = np.array(model.lr, np.float32)
+
+    def adam_range(b, e, g):
+        S = model.P_stride
+        p = model.params.numpy().astype(np.float64).reshape(-1).copy()
+        full_g = np.zeros_like(p)
+        full_g[b:e] = g[:e - b].numpy()
+        mm = model.m.numpy().reshape(-1).astype(np.float64)
+        vv = model.v.numpy().reshape(-1).astype(np.float64)
+        p1, m1, v1 = gsref.adam_step(p.reshape(model.F, S), full_g.reshape(model.F, S), mm.reshape(model.F, S),
+                                     vv.reshape(model.F, S), lr, model.step_count, P=S)
+        model.params.view(-1)[b:e] = torch.from_numpy(p1.reshape(-1)[b:e].astype(np.float32))
+        model.m.view(-1)[b:e] = torch.from_numpy(m1.reshape(-1)[b:e].astype(np.float32))
+        model.v.view(-1)[b:e] = torch.from_numpy(v1.reshape(-1)[b:e].astype(np.float32))
+
+    opt = pipeline.ShardedAdam(None, model, adam_range=adam_range)
+    g_local = model.grad.clone()
+    model.step_count += 1
+    opt.step()
+    gathered = [torch.zeros(model.params.numel()) for _ in range(world)]
+    dist.all_gather(gathered, model.params.reshape(-1).contiguous())
+    glist = [torch.zeros(g_local.numel()) for _ in range(world)]
+    dist.all_gather(glist, g_local.reshape(-1).contiguous())
+    if rank == 0:
+        out["params"] = [x.numpy().copy() for x in gathered]
+        out["grads"] = [x.numpy().copy() for x in glist]
+        out["shard"], out["n"] = opt.shard, opt.n
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_sharded_adam_matches_replicated():
+    from oracle import gsref
+    from paper_2408_12677_b200 import pipeline
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    w, _ = _views()
+    F, S = w.scene.params.shape
+    assert out["n"] == F * S and out["shard"] % 4 == 0 and 2 * out["shard"] >= F * S
+    gsum = (out["grads"][0].astype(np.float32) + out["grads"][1].astype(np.float32)).astype(np.float64)
+    z = np.zeros((F, S))
+    ref, _, _ = gsref.adam_step(w.scene.params.astype(np.float64), gsum.reshape(F, S), z, z,
+                                np.array(pipeline.lr_per_row(0), np.float32), 1, P=S)
+    np.testing.assert_array_equal(out["params"][0], out["params"][1])  # bit-identical across ranks
+    np.testing.assert_allclose(out["params"][0].reshape(F, S), ref, rtol=1e-6, atol=1e-7)
