@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
                     help="views in flight (one CUDA stream + buffer set each)")
+    ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "8")),
+                    help="views chained per projection-backward pass (<= 8)")
     ap.add_argument("--optim", default="sharded", choices=["sharded", "replicated"],
                     help="N > 1: reduce-scatter + sharded Adam + all-gather, or all-reduce + replicated Adam")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
@@ -319,7 +321,7 @@ def main():
         optimizer = pipeline.ShardedAdam(lib, model)
         allreduce = None
     tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce,
-                          streams=args.streams if batched else 1, optimizer=optimizer)
+                          streams=args.streams if batched else 1, optimizer=optimizer, chunk=args.chunk)
     stream = torch.cuda.current_stream()
 
     # --- warm-up
@@ -522,7 +524,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({args.optim} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
-                   "key_capacity": cap, "streams": args.streams if batched else 1, "max_keys_per_view": kmax,
+                   "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
