@@ -28,7 +28,10 @@
 namespace gsr {
 namespace {
 
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+#ifndef GSR_SCAN_ITEMS
+#define GSR_SCAN_ITEMS 8
+#endif
+constexpr int kScanThreads = 256, kScanItems = GSR_SCAN_ITEMS, kScanTile = kScanThreads * kScanItems;
 constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32;
 constexpr int kRsItemsKeys = 16, kRsItemsDepth = 4;  // items per thread: tile-key passes / depth passes
 constexpr int kRsTileKeys = kRsThreads * kRsItemsKeys, kRsTileDepth = kRsThreads * kRsItemsDepth;
@@ -87,6 +90,40 @@ __device__ __forceinline__ T block_excl_scan256(T v, T* s_warp /*[8]*/, T& total
   return wpre + x - v;
 }
 
+// Decoupled look-back for the chained scans, run by one whole warp: publishes this
+// partition's aggregate, then examines 32 predecessors per round trip (lane l reads
+// partition part - 1 - l - 32 r), adds every aggregate up to and including the
+// nearest inclusive prefix, and spins only while a needed predecessor has not
+// published yet.  Returns the exclusive prefix (all lanes) and publishes the
+// inclusive one.
+__device__ __forceinline__ unsigned long long warp_lookback(unsigned long long* lookback, int64_t part,
+                                                            unsigned long long total) {
+  const int lane = threadIdx.x & 31;
+  if (part == 0) {
+    if (lane == 0) st_vol(&lookback[0], kScInc | total);
+    return 0ull;
+  }
+  if (lane == 0) st_vol(&lookback[part], kScAgg | total);
+  unsigned long long prefix = 0;
+  int64_t p = part - 1;
+  while (true) {
+    const int64_t q = p - lane;
+    const unsigned long long v = q >= 0 ? ld_vol(&lookback[q]) : kScInc;  // before partition 0: prefix 0
+    const uint32_t inc = __ballot_sync(kFull, (v >> 62) == 2);
+    const uint32_t ready = __ballot_sync(kFull, (v >> 62) != 0);
+    const uint32_t need = inc ? ((inc & (0u - inc)) << 1) - 1u : kFull;  // lanes up to the nearest inclusive
+    if ((ready & need) != need) continue;                                  // someone needed is not ready
+    unsigned long long x = (lane < 32 && ((need >> lane) & 1u)) ? (v & kScMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+    prefix += x;
+    if (inc) break;
+    p -= 32;
+  }
+  if (lane == 0) st_vol(&lookback[part], kScInc | (prefix + total));
+  return prefix;
+}
+
 // ---------------------------------------------------------------------------
 // K2a: order-preserving compaction of the visible set (tiles > 0), fused with the
 // 4 x 256-bin histograms of the depth-key bytes for the depth sort.
@@ -116,23 +153,12 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(int64_t P, const int32
   }
   unsigned long long total;
   const unsigned long long excl = block_excl_scan256<unsigned long long>(cnt, s_warp, total);
-  if (threadIdx.x == 0) {
-    unsigned long long prefix = 0;
-    if (part == 0) {
-      st_vol(&lookback[0], kScInc | total);
-    } else {
-      st_vol(&lookback[part], kScAgg | total);
-      for (int64_t p = part - 1; p >= 0;) {
-        const unsigned long long v = ld_vol(&lookback[p]);
-        if ((v >> 62) == 0) continue;
-        prefix += v & kScMask;
-        if ((v >> 62) == 2) break;
-        --p;
-      }
-      st_vol(&lookback[part], kScInc | (prefix + total));
+  if (threadIdx.x < 32) {
+    const unsigned long long prefix = warp_lookback(lookback, part, total);
+    if (threadIdx.x == 0) {
+      s_prefix = prefix;
+      if ((int64_t)part == num_parts - 1) ctr->V = prefix + total;
     }
-    s_prefix = prefix;
-    if ((int64_t)part == num_parts - 1) ctr->V = prefix + total;
   }
   __syncthreads();
   unsigned long long pos = s_prefix + excl;
@@ -184,25 +210,14 @@ __global__ void __launch_bounds__(kScanThreads) k_offsets(const int32_t* __restr
   }
   unsigned long long total;
   const unsigned long long excl = block_excl_scan256<unsigned long long>(sum, s_warp, total);
-  if (threadIdx.x == 0) {
-    unsigned long long prefix = 0;
-    if (part == 0) {
-      st_vol(&lookback[0], kScInc | total);
-    } else {
-      st_vol(&lookback[part], kScAgg | total);
-      for (int64_t p = part - 1; p >= 0;) {
-        const unsigned long long v = ld_vol(&lookback[p]);
-        if ((v >> 62) == 0) continue;
-        prefix += v & kScMask;
-        if ((v >> 62) == 2) break;
-        --p;
+  if (threadIdx.x < 32) {
+    const unsigned long long prefix = warp_lookback(lookback, part, total);
+    if (threadIdx.x == 0) {
+      s_prefix = prefix;
+      if ((int64_t)part == num_parts - 1) {
+        ctr->K = prefix + total;
+        if (num_keys_dev) *num_keys_dev = (long long)(prefix + total);
       }
-      st_vol(&lookback[part], kScInc | (prefix + total));
-    }
-    s_prefix = prefix;
-    if ((int64_t)part == num_parts - 1) {
-      ctr->K = prefix + total;
-      if (num_keys_dev) *num_keys_dev = (long long)(prefix + total);
     }
   }
   __syncthreads();
