@@ -40,8 +40,10 @@ def parse():
                     help="views in flight (one CUDA stream + buffer set each)")
     ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "8")),
                     help="views chained per projection-backward pass (<= 8)")
-    ap.add_argument("--optim", default="sharded", choices=["sharded", "replicated"],
-                    help="N > 1: reduce-scatter + sharded Adam + all-gather, or all-reduce + replicated Adam")
+    ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated"],
+                    help="N > 1: fused peer-memory reduce-scatter+Adam+all-gather kernel (falls back to 'sharded' if "
+                         "symmetric memory is unavailable), NCCL reduce-scatter + sharded Adam + all-gather, or "
+                         "NCCL all-reduce + replicated Adam")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--schedule", action="store_true",
                     help="keyframe-scheduled online + global optimisation run (PAPER.md:149; SURVEY §8(f) NEXT-1)")
@@ -316,9 +318,16 @@ def main():
 
     def step_views(i):
         return my_views if batched else [my_views[i % len(my_views)]]
-    optimizer = None
-    if world > 1 and batched and args.optim == "sharded":
+    optimizer, optim_used = None, ("replicated" if world > 1 and batched else "local")
+    if world > 1 and batched and args.optim == "peer":
+        try:
+            optimizer, optim_used = pipeline.PeerShardedAdam(lib, model), "peer"
+        except Exception as ex:  # noqa: BLE001  (no symmetric memory / P2P: NCCL path)
+            optim_used = f"sharded (peer unavailable: {type(ex).__name__})"
+    if world > 1 and batched and optimizer is None and args.optim in ("peer", "sharded"):
         optimizer = pipeline.ShardedAdam(lib, model)
+        optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
+    if optimizer is not None:
         allreduce = None
     tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce,
                           streams=args.streams if batched else 1, optimizer=optimizer, chunk=args.chunk)
@@ -328,6 +337,19 @@ def main():
     for i in range(args.warmup):
         tr.step(step_views(i))
     torch.cuda.synchronize()
+    if world > 1 and not pipeline.params_agree_across_ranks(model):
+        if optim_used != "peer":
+            raise RuntimeError(f"parameters differ across ranks after warm-up (optimiser: {optim_used})")
+        # the peer-memory path misbehaved on this machine: resynchronise from rank 0
+        # and continue on the NCCL reduce-scatter path (m, v shards keep their owners)
+        dist.broadcast(model.params, src=0)
+        tr.optimizer = pipeline.ShardedAdam(lib, model)
+        optim_used = "sharded (peer failed the cross-rank check)"
+        for i in range(args.warmup):
+            tr.step(step_views(i))
+        torch.cuda.synchronize()
+        if not pipeline.params_agree_across_ranks(model):
+            raise RuntimeError("parameters differ across ranks after warm-up (sharded)")
 
     # --- timed region (device time, CUDA events, max over ranks)
     clocks = ClockSampler(local)
@@ -523,7 +545,7 @@ def main():
         "scaling": "strong" if batched else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
-                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({args.optim} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
+                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (

@@ -262,6 +262,21 @@ gs_status gs_adam_step_range(const gs_scene* scene /*HOST*/, float* params, cons
                              const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
                              int64_t begin, int64_t end, void* stream);
 
+/* Reduce-scatter + Adam + all-gather fused in ONE kernel over peer memory (SURVEY.md
+ * §8(f) NEXT-2): for the scalars [begin, end) this rank owns, sum every rank's
+ * gradient (P2P loads over NVLink from grad_peers[0..world-1], in rank order), apply
+ * Adam to the local m, v and param_peers[rank], and store the new parameters into
+ * every rank's param_peers[r] (P2P stores).  grad_peers / param_peers: HOST arrays of
+ * world DEVICE pointers to each rank's full [F][P_stride] buffers (symmetric memory
+ * mapped into this process); m, v: this rank's full arrays (only the range is
+ * touched).  world <= 8; begin, end multiples of 4.  The caller must order the ranks
+ * around the call (all gradients final before, all parameter stores done after),
+ * e.g. with a symmetric-memory barrier on the same stream. */
+gs_status gs_adam_step_peers(const gs_scene* scene /*HOST*/, int world, int rank,
+                             const float* const* grad_peers /*HOST[world]*/, float* const* param_peers /*HOST[world]*/,
+                             float* m, float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps,
+                             int64_t step, int64_t begin, int64_t end, void* stream);
+
 /* ---------------------------------------------------------------- layout (setup)
  * gs_spatial_order: params_out = params_in with the Gaussians (columns) permuted into
  * Morton (Z-curve) order of their means, 10 bits per axis inside the means'

@@ -403,6 +403,30 @@ gs_status gs_adam_step_range(const gs_scene* scene, float* params, const float* 
   return check_launch("gs_adam_step_range");
 }
 
+gs_status gs_adam_step_peers(const gs_scene* scene, int world, int rank, const float* const* grad_peers,
+                             float* const* param_peers, float* m, float* v, const float* lr_per_row, float beta1,
+                             float beta2, float eps, int64_t step, int64_t begin, int64_t end, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_adam_step_peers"));
+  const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
+  if (!grad_peers || !param_peers || !lr_per_row || step < 1 || !(beta1 >= 0.f && beta1 < 1.f) ||
+      !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f) || begin < 0 || end < begin || end > n) {
+    set_error("gs_adam_step_peers: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", (long long)step,
+              (long long)begin, (long long)end, (long long)n);
+    return GS_ERR_ARG;
+  }
+  if ((begin & 3) || (end & 3)) {
+    set_error("gs_adam_step_peers: begin/end must be multiples of 4");
+    return GS_ERR_ALIGN;
+  }
+  if (end > begin) GS_TRY(check_ptrs("gs_adam_step_peers", {{m, "m"}, {v, "v"}}));
+  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  GS_TRY(launch_adam_peers(rows_of(scene), scene->P_stride, world, rank, grad_peers, param_peers, m, v, lr_per_row,
+                           beta1, beta2, eps, (float)bc1, (float)bc2, begin, end, static_cast<cudaStream_t>(stream)));
+  return check_launch("gs_adam_step_peers");
+}
+
 gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
                           const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
                           void* stream) {

@@ -34,6 +34,48 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
   }
 }
 
+// Fused reduce-scatter + Adam + all-gather over peer memory (NEXT-2): this rank owns
+// scalars [4 b4, 4 e4) of the flattened arrays; it pulls that range of every rank's
+// gradient over NVLink (P2P loads, summed in rank order: deterministic), applies Adam
+// to its local m, v and parameters, and pushes the new parameters into every rank's
+// parameter buffer (P2P stores).  Peer buffers come from symmetric memory; the caller
+// fences the ranks before (gradients final) and after (parameters delivered).
+constexpr int kMaxPeers = 8;
+struct Peers {
+  const float4* grad[kMaxPeers];
+  float4* param[kMaxPeers];
+  int world, rank;
+};
+
+__global__ void __launch_bounds__(256) k_adam_peers(const __grid_constant__ Peers pr, float4* __restrict__ m,
+                                                    float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4,
+                                                    LrTable lr, float b1, float b2, float eps, float rs_bc2) {
+  const float c1 = 1.f - b1, c2 = 1.f - b2;
+  for (int64_t i = b4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float step = lr.step[i / S4];
+    float4 gs[kMaxPeers];
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < pr.world) gs[r] = pr.grad[r][i];  // all peers' loads in flight at once
+    float4 gg = gs[0];
+#pragma unroll
+    for (int r = 1; r < kMaxPeers; ++r)
+      if (r < pr.world) gg.x += gs[r].x, gg.y += gs[r].y, gg.z += gs[r].z, gg.w += gs[r].w;
+    float4 mm = m[i], vv = v[i], pp = pr.param[pr.rank][i];
+#define ADAM_LANE(c)                                              \
+  mm.c = b1 * mm.c + c1 * gg.c;                                  \
+  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
+  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
+    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
+#undef ADAM_LANE
+    m[i] = mm;
+    v[i] = vv;
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < pr.world) pr.param[r][i] = pp;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restrict__ rgb, const float* __restrict__ dep,
                                             const float* __restrict__ trgb, const float* __restrict__ tdep, float sc,
                                             float sd, float* __restrict__ grgb, float* __restrict__ gdep,
@@ -71,6 +113,35 @@ void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, flo
                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
                                            end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
   count_launch();
+}
+
+gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const float* const* grad_peers,
+                            float* const* param_peers, float* m, float* v, const float* lr, float beta1, float beta2,
+                            float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s) {
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) {
+    set_error("gs_adam_step_peers: world %d / rank %d outside [1, %d]", world, rank, kMaxPeers);
+    return GS_ERR_ARG;
+  }
+  Peers pr{};
+  pr.world = world, pr.rank = rank;
+  for (int r = 0; r < world; ++r) {
+    if (!grad_peers[r] || !param_peers[r] || !aligned16(grad_peers[r]) || !aligned16(param_peers[r])) {
+      set_error("gs_adam_step_peers: peer %d buffers NULL or not 16-byte aligned", r);
+      return GS_ERR_ALIGN;
+    }
+    pr.grad[r] = reinterpret_cast<const float4*>(grad_peers[r]);
+    pr.param[r] = reinterpret_cast<float4*>(param_peers[r]);
+  }
+  LrTable t{};
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
+  const int64_t n4 = (end - begin) / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
+  if (n4 > 0) {
+    k_adam_peers<<<std::max(grid, 1), 256, 0, s>>>(pr, reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
+                                                    begin / 4, end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2));
+    count_launch();
+  }
+  return GS_OK;
 }
 
 void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,

@@ -439,8 +439,15 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       } else {
         fwd_sparse<false>(px, m, g, q0, q1, q2, pos1, lm);
       }
-      nblend += __popc(lm);
       const uint32_t cm = __reduce_or_sync(kFull, lm);
+#ifndef GSR_COUNT_EVAL
+      nblend += __popc(lm);
+#else  // diagnostics build: the blended counter counts work units instead (lane 0)
+      if (lane == 0) {
+        const bool dense = !(fl & kFlagGeneral) && __popc(m) >= kDenseBlocks;
+        nblend += GSR_COUNT_EVAL == 1 ? (dense ? 8u : (uint32_t)__popc(m)) : GSR_COUNT_EVAL == 2 ? 1u : (uint32_t)__popc(cm);
+      }
+#endif
       kb_mine = (lane == j) ? cm : kb_mine;
       if (++since == 8) {
         since = 0;

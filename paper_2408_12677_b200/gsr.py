@@ -115,10 +115,12 @@ class Library:
         lib.gs_spatial_order.argtypes = [vp, vp, vp, vp, vp, C.c_size_t, vp]
         lib.gs_l1_loss_grad.argtypes = [i64, vp, vp, vp, vp, C.c_float, vp, vp, vp, vp]
         lib.gs_adam_step_range.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, i64, i64, vp]
+        lib.gs_adam_step_peers.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float,
+                                           i64, i64, i64, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -222,6 +224,16 @@ class Library:
         return self._check("gs_adam_step_range", self.lib.gs_adam_step_range(
             C.byref(sc), _ptr(params), _ptr(grad_range), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
             int(begin), int(end), _stream(stream)))
+
+    def adam_step_peers(self, sc, world, rank, grad_ptrs, param_ptrs, m, v, lr_per_row, step, begin, end, beta1=0.9,
+                        beta2=0.999, eps=1e-15, stream=None):
+        """grad_ptrs / param_ptrs: lists of `world` device addresses (ints)."""
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        gp = (C.c_void_p * max(world, 1))(*grad_ptrs)
+        pp = (C.c_void_p * max(world, 1))(*param_ptrs)
+        return self._check("gs_adam_step_peers", self.lib.gs_adam_step_peers(
+            C.byref(sc), int(world), int(rank), gp, pp, _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step), int(begin),
+            int(end), _stream(stream)))
 
     def keyframe_schedule(self, new_prims, threshold=50, m=5, n=3, global_iters=10, store_all_frames=False, seed=0):
         """gs_keyframe_schedule (host): returns (iter_view, iter_frame, is_keyframe) numpy arrays."""

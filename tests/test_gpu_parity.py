@@ -629,3 +629,36 @@ def test_sharded_adam_single_rank_nccl(lib):
         assert torch.equal(ma.params, mb.params)
     finally:
         dist.destroy_process_group()
+
+
+def test_peer_sharded_adam_single_rank(lib):
+    """PeerShardedAdam (gs_adam_step_peers over torch symmetric memory, world size 1 on
+    this GPU): the fused kernel's pull / Adam / push path equals gs_adam_step."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = workload("small")
+        rng = np.random.default_rng(9)
+        g = torch.from_numpy(rng.normal(size=w.scene.params.shape).astype(np.float32)).to(DEV)
+        ma, mb = pipeline.GaussianModel(w.scene, DEV), pipeline.GaussianModel(w.scene, DEV)
+        opt = pipeline.PeerShardedAdam(lib, mb)
+        for it in range(3):
+            ma.grad.copy_(g * (it + 1))
+            mb.grad.copy_(g * (it + 1))
+            ma.step_count += 1
+            lib.adam_step(ma.desc, ma.params, ma.grad, ma.m, ma.v, ma.lr, ma.step_count, zero_grad=False)
+            mb.step_count += 1
+            opt.step()
+        torch.cuda.synchronize()
+        assert torch.equal(ma.params, mb.params)
+        assert torch.equal(ma.m, mb.m) and torch.equal(ma.v, mb.v)
+        assert pipeline.params_agree_across_ranks(mb)
+    finally:
+        dist.destroy_process_group()
