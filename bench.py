@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
                     help="views in flight (one CUDA stream + buffer set each)")
+    ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of whole iterations (N = 1)")
     ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "8")),
                     help="views chained per projection-backward pass (<= 8)")
     ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated"],
@@ -368,38 +369,68 @@ def main():
         else:
             stage_ev[stage].append((open_ev.pop(stage), ev))
 
+    # CUDA-graph mode (single rank): each distinct view set of the timed steps is
+    # captured once as a whole iteration and replayed; launches per step are counted
+    # while capturing (a replay does not pass through the library's counter)
+    use_graph = args.graph and world == 1 and not args.profile and tr.optimizer is None
+    graphs, graph_launches = {}, {}
+    if use_graph:
+        for i in range(args.steps):
+            key = tuple(step_views(args.warmup + i))
+            if key not in graphs:
+                c0 = lib.launch_count()
+                graphs[key] = tr.capture(list(key))
+                graph_launches[key] = (lib.launch_count() - c0) // 2  # eager warm-up + captured step
+        torch.cuda.synchronize()
+        tr.blended.zero_()
+        tr.num_keys.zero_()
+
+    def timed_loop(graph_mode):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tr.hooks = None if graph_mode else hooks
+        a.record(stream)
+        if args.profile:
+            torch.cuda.nvtx.range_push("timed")
+        done, nl = 0, 0
+        for i in range(args.steps):
+            sv = step_views(args.warmup + i)
+            if graph_mode:
+                tr.replay(graphs[tuple(sv)])
+                nl += graph_launches[tuple(sv)]
+            else:
+                tr.step(sv)
+            done += len(sv)
+        b.record(stream)
+        if args.profile:
+            torch.cuda.nvtx.range_pop()
+        tr.hooks = None
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return a.elapsed_time(b), done, nl
+
     l0 = lib.launch_count()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tr.hooks = hooks
-    e0.record(stream)
-    if args.profile:
-        torch.cuda.nvtx.range_push("timed")
-    views_done = 0
-    for i in range(args.steps):
-        sv = step_views(args.warmup + i)
-        tr.step(sv)
-        views_done += len(sv)
-    e1.record(stream)
-    if args.profile:
-        torch.cuda.nvtx.range_pop()
-    tr.hooks = None
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    launches = lib.launch_count() - l0
+    ms, views_done, nl = timed_loop(use_graph)
+    launches = nl if use_graph else lib.launch_count() - l0
     clk = clocks.stop() if not args.profile else None
-    ms = e0.elapsed_time(e1)
     stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(v), 1) for k, v in stage_ev.items()}
     # Per-kernel rooflines need each stage's own duration: with views in flight on
     # several streams the stages overlap, so an extra serialised pass (streams = 1,
     # same steps, CUDA events on the launching stream) times them in isolation.
     blended_timed = int(tr.blended.item())
     stage_ms_overlapped = None
-    if tr._streams is not None and not args.profile:
-        stage_ms_overlapped = stage_ms
+    eager = None
+    if use_graph:  # the same steps eager (no graph), for comparison
+        tr.blended.zero_()
+        e_ms, _, _ = timed_loop(False)
+        eager = {"ms_per_step": e_ms / args.steps, "value": int(tr.blended.item()) / (e_ms / 1e3), "unit": UNIT,
+                 "note": "same steps launched eagerly from Python (no CUDA graph)"}
+        stage_ms = {k: sum(a.elapsed_time(b) for a, b in v) / max(len(v), 1) for k, v in stage_ev.items()}
+    if (tr._streams is not None or use_graph) and not args.profile:
+        stage_ms_overlapped = stage_ms if tr._streams is not None else None
         tr.serial = True
         tr.step(step_views(0))
         for v in stage_ev.values():
@@ -521,7 +552,7 @@ def main():
         pass
     roof = roofline(dev, peaks, clk, stage_ms, blended / max(world, 1) / n_views, evaluated / len(eval_views), traffic)
     roof["timing"] = ("CUDA events around each launch on its stream, serialised pass (streams=1) of the same steps "
-                      "right after the timed region" if stage_ms_overlapped is not None else
+                      "right after the timed region" if (stage_ms_overlapped is not None or use_graph) else
                       "CUDA events around each launch on its stream, inside the timed region")
     if stage_ms_overlapped is not None:
         roof["launch_ms_overlapped"] = stage_ms_overlapped["render_bwd"]
@@ -548,6 +579,7 @@ def main():
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
+                   "launch": "CUDA graph per iteration" if use_graph else "eager",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},
         "gpu_launches": int(launches),
@@ -558,7 +590,7 @@ def main():
                  "keys_per_s": keys / nv * views_done * world / (ms / 1e3),
                  "note": "evaluated = sum of n_contrib (list entries visited up to each pixel's stop, R24), "
                          "measured on up to 8 of this rank's views after the timed region"},
-        "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive,
+        "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive, "eager": eager,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

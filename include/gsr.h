@@ -251,6 +251,14 @@ gs_status gs_adam_step(const gs_scene* scene /*HOST*/, float* params, float* gra
                        const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
                        int zero_grad, void* stream);
 
+/* gs_adam_step with the 1-based step counter in DEVICE memory: *step_dev (int64) is
+ * incremented on the stream first and the bias corrections are computed from it on
+ * the device, so the call can be captured in a CUDA graph and replayed (bench.py's
+ * graph mode).  On entry *step_dev = t - 1. */
+gs_status gs_adam_step_dev(const gs_scene* scene /*HOST*/, float* params, float* grad, float* m, float* v,
+                           const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t* step_dev,
+                           int zero_grad, void* stream);
+
 /* gs_adam_step restricted to the scalars [begin, end) of the flattened [F][P_stride]
  * arrays (row r = index / P_stride keeps its learning rate): the optimiser half of a
  * reduce-scatter -> sharded Adam -> all-gather step across ranks (SURVEY.md §8(f)

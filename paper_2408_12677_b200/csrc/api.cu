@@ -378,6 +378,25 @@ gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float*
   return check_launch("gs_adam_step");
 }
 
+gs_status gs_adam_step_dev(const gs_scene* scene, float* params, float* grad, float* m, float* v,
+                           const float* lr_per_row, float beta1, float beta2, float eps, int64_t* step_dev,
+                           int zero_grad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_adam_step_dev"));
+  if (scene->P == 0) {
+    set_error("gs_adam_step_dev: no Gaussians (P == 0)");
+    return GS_ERR_EMPTY;
+  }
+  if (!lr_per_row || !step_dev || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f)) {
+    set_error("gs_adam_step_dev: invalid arguments");
+    return GS_ERR_ARG;
+  }
+  GS_TRY(check_ptrs("gs_adam_step_dev", {{params, "params"}, {grad, "grad"}, {m, "m"}, {v, "v"}}));
+  launch_adam_dev(rows_of(scene), scene->P_stride, params, grad, m, v, lr_per_row, beta1, beta2, eps, step_dev,
+                  zero_grad, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_adam_step_dev");
+}
+
 gs_status gs_adam_step_range(const gs_scene* scene, float* params, const float* grad_range, float* m, float* v,
                              const float* lr_per_row, float beta1, float beta2, float eps, int64_t step, int64_t begin,
                              int64_t end, void* stream) {

@@ -34,6 +34,43 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
   }
 }
 
+// Graph-capturable Adam: the step counter lives on the device (k_step_inc advances it,
+// then every block derives its bias corrections from it), so a captured iteration
+// replays with the right t.  Same arithmetic as k_adam (t in double, rounded to fp32).
+__global__ void k_step_inc(int64_t* t) { *t += 1; }
+
+__global__ void __launch_bounds__(256) k_adam_dev(float4* __restrict__ p, float4* __restrict__ g,
+                                                  float4* __restrict__ m, float4* __restrict__ v, int64_t n4,
+                                                  int64_t S4, LrTable lr_raw, int F, float b1, float b2, float eps,
+                                                  const int64_t* __restrict__ step_dev, int zero_grad) {
+  __shared__ float s_step[64];
+  __shared__ float s_rs;
+  if (threadIdx.x < 64) {
+    const double t = (double)*step_dev;
+    const float bc1 = (float)(1.0 - pow((double)b1, t));
+    s_step[threadIdx.x] = threadIdx.x < F ? lr_raw.step[threadIdx.x] / bc1 : 0.f;
+    if (threadIdx.x == 0) s_rs = 1.f / sqrtf((float)(1.0 - pow((double)b2, t)));
+  }
+  __syncthreads();
+  const float rs_bc2 = s_rs;
+  const float c1 = 1.f - b1, c2 = 1.f - b2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float step = s_step[i / S4];
+    const float4 gg = g[i];
+    float4 mm = m[i], vv = v[i], pp = p[i];
+#define ADAM_LANE(c)                                              \
+  mm.c = b1 * mm.c + c1 * gg.c;                                  \
+  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
+  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
+    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
+#undef ADAM_LANE
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+    if (zero_grad) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
 // Fused reduce-scatter + Adam + all-gather over peer memory (NEXT-2): this rank owns
 // scalars [4 b4, 4 e4) of the flattened arrays; it pulls that range of every rank's
 // gradient over NVLink (P2P loads, summed in rank order: deterministic), applies Adam
@@ -113,6 +150,19 @@ void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, flo
                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
                                            end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
   count_launch();
+}
+
+void launch_adam_dev(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
+                     float beta2, float eps, int64_t* step_dev, int zero_grad, cudaStream_t s) {
+  LrTable t{};
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r];
+  const int64_t n4 = F * S / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
+  k_step_inc<<<1, 1, 0, s>>>(step_dev);
+  k_adam_dev<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
+                                               reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, S / 4, t,
+                                               (int)F, beta1, beta2, eps, step_dev, zero_grad);
+  count_launch(2);
 }
 
 gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const float* const* grad_peers,

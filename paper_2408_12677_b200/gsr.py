@@ -117,10 +117,11 @@ class Library:
         lib.gs_adam_step_range.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, i64, i64, vp]
         lib.gs_adam_step_peers.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float,
                                            i64, i64, i64, vp]
+        lib.gs_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -216,6 +217,13 @@ class Library:
         lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
         return self._check("gs_adam_step", self.lib.gs_adam_step(
             C.byref(sc), _ptr(params), _ptr(grad), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
+            1 if zero_grad else 0, _stream(stream)))
+
+    def adam_step_dev(self, sc, params, grad, m, v, lr_per_row, step_dev, beta1=0.9, beta2=0.999, eps=1e-15,
+                      zero_grad=False, stream=None):
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        return self._check("gs_adam_step_dev", self.lib.gs_adam_step_dev(
+            C.byref(sc), _ptr(params), _ptr(grad), _ptr(m), _ptr(v), lr, beta1, beta2, eps, _ptr(step_dev),
             1 if zero_grad else 0, _stream(stream)))
 
     def adam_step_range(self, sc, params, grad_range, m, v, lr_per_row, step, begin, end, beta1=0.9, beta2=0.999,

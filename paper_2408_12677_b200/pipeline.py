@@ -35,6 +35,8 @@ class GaussianModel:
         self.m = torch.zeros_like(self.params)
         self.v = torch.zeros_like(self.params)
         self.step_count = 0
+        # device copy of the step counter for graph-captured iterations (gs_adam_step_dev)
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=device)
         self.lr = lr_per_row(self.sh_degree)
         self.desc = gsr.scene_desc(self.P, self.P_stride, self.sh_degree)
 
@@ -155,6 +157,8 @@ class Trainer:
         # serial = True runs the views on the caller's stream only (bench.py's isolated
         # kernel-timing pass)
         self.serial = False
+        # device_step = True: Adam reads / advances model.step_dev (graph capture)
+        self.device_step = False
         # render tiles longest-list-first (gs_tile_order): 7% faster render kernels when
         # one view is in flight; with several views in flight the other streams already
         # fill each kernel's tail and the extra launch cost 2% (B200, scannetpp), so the
@@ -293,7 +297,38 @@ class Trainer:
             return
         if self.allreduce is not None:
             self.allreduce(m.grad)
-        self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False)
+        if self.device_step:
+            self.lib.adam_step_dev(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_dev, zero_grad=False)
+        else:
+            self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False)
+
+    def capture(self, views):
+        """One whole iteration over ``views`` (every view's project -> bin -> fwd -> L1 ->
+        bwd on its stream, the projection backward, Adam) captured in a CUDA graph
+        (the launch-bound configs run as one graph per iteration).
+        Binning runs in capacity mode (K stays on the device), Adam takes the step
+        counter from the device.  Returns the graph; replay it with replay()."""
+        if self.optimizer is not None:
+            raise ValueError("graph capture supports the single-rank / all-reduce optimiser path only")
+        m = self.model
+        m.step_dev.fill_(m.step_count)
+        self.device_step = True
+        hooks, self.hooks = self.hooks, None
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step(views)  # one eager iteration on a side stream (lazy allocations)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step(views)
+        m.step_count -= 1  # the captured iteration has not run yet
+        self.hooks = hooks
+        return g
+
+    def replay(self, g):
+        g.replay()
+        self.model.step_count += 1
 
     def _chain(self, gcams, accumulate):
         n = len(gcams)
