@@ -141,8 +141,8 @@ def cpu_window_camera(cam, size=584):
     a bounded sample of the same workload for the CPU oracle."""
     import copy
     c = copy.copy(cam)
-    x0 = (cam.width - size) // 2 // 16 * 16
-    y0 = (cam.height - size) // 2 // 16 * 16
+    x0 = max(0, (cam.width - size) // 2 // 16 * 16)
+    y0 = max(0, (cam.height - size) // 2 // 16 * 16)
     c.width, c.height = min(size, cam.width), min(size, cam.height)
     c.cx, c.cy = cam.cx - x0, cam.cy - y0
     return c

@@ -143,10 +143,14 @@ class Trainer:
         self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
         P = max(model.P, 1)
         # per in-flight view: projection flags and screen-space gradients (zeroed once;
-        # gs_project_bwd_views leaves them zero again)
-        self.flags = [torch.empty(P + 16, dtype=torch.uint8, device=device) for _ in range(self.chunk)]
+        # gs_project_bwd_views leaves them zero again).  Two slot sets when a step has
+        # more views than one chain takes, so that chunk c + 1's views render while
+        # chunk c's projection backward runs (they only wait for chunk c - 1's chain).
+        n_sets = 2 if len(cameras) > self.chunk and n_streams > 1 else 1
+        self.flags = [torch.empty(P + 16, dtype=torch.uint8, device=device) for _ in range(n_sets * self.chunk)]
         self.sgrad = [torch.zeros((P, gsr.SGRAD_FLOATS), dtype=torch.float32, device=device)
-                      for _ in range(self.chunk)]
+                      for _ in range(n_sets * self.chunk)]
+        self._n_sets = n_sets
         self.num_keys = torch.zeros(len(cameras), dtype=torch.int64, device=device)
         self.blended = torch.zeros(1, dtype=torch.int64, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
@@ -261,18 +265,22 @@ class Trainer:
             for s in self._streams:
                 s.wait_event(start)
         pending, done = [], []
-        chain_ev = None
+        n_sets = self._n_sets if S > 1 else 1
+        chain_ev = [None] * n_sets  # per slot set: the chain that last consumed it
         first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
+        n_chain = 0
         for k, v in enumerate(views):
             t_rgb, t_depth, ready, consumed = targets(k, v)
+            base = (n_chain % n_sets) * self.chunk  # slot set of the chunk being filled
             if S == 1:
-                pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed))
+                pending.append(self._view(v, base + len(pending), t_rgb, t_depth, ready, consumed))
             else:
                 s = self._streams[k % S]
-                if chain_ev is not None:  # this view's flags / sgrad slot was consumed by that chain
-                    s.wait_event(chain_ev)
+                if chain_ev[n_chain % n_sets] is not None:  # this slot was consumed by that chain
+                    s.wait_event(chain_ev[n_chain % n_sets])
                 with torch.cuda.stream(s):
-                    pending.append(self._view(v, len(pending), t_rgb, t_depth, ready, consumed, self.bufs[k % S]))
+                    pending.append(self._view(v, base + len(pending), t_rgb, t_depth, ready, consumed,
+                                              self.bufs[k % S]))
                     ev = torch.cuda.Event()
                     ev.record(s)
                     done.append(ev)
@@ -282,15 +290,17 @@ class Trainer:
                 for ev in done:
                     main.wait_event(ev)
                 done = []
-                self._chain(pending, accumulate=not first)
+                self._chain(pending, accumulate=not first, base=base)
                 pending, first = [], False
                 if S > 1:
-                    chain_ev = torch.cuda.Event()
-                    chain_ev.record(main)
+                    ev = torch.cuda.Event()
+                    ev.record(main)
+                    chain_ev[n_chain % n_sets] = ev
+                n_chain += 1
         for ev in done:
             main.wait_event(ev)
         if pending or first:
-            self._chain(pending, accumulate=not first)
+            self._chain(pending, accumulate=not first, base=(n_chain % n_sets) * self.chunk)
         m.step_count += 1
         if self.optimizer is not None:
             self.optimizer.step()
@@ -330,11 +340,11 @@ class Trainer:
         g.replay()
         self.model.step_count += 1
 
-    def _chain(self, gcams, accumulate):
+    def _chain(self, gcams, accumulate, base=0):
         n = len(gcams)
         self._hook("project_bwd", "begin")
-        self.lib.project_bwd_views(gcams, self.model.desc, self.model.params, self.flags[:n], self.sgrad[:n],
-                                   self.model.grad, accumulate=accumulate)
+        self.lib.project_bwd_views(gcams, self.model.desc, self.model.params, self.flags[base:base + n],
+                                   self.sgrad[base:base + n], self.model.grad, accumulate=accumulate)
         self._hook("project_bwd", "end")
 
     def check_capacity(self) -> int:
