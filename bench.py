@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--schedule", action="store_true",
                     help="keyframe-scheduled online + global optimisation run (PAPER.md:149; SURVEY §8(f) NEXT-1)")
+    ap.add_argument("--tsdf", action="store_true",
+                    help="TSDF band allocation + integration over a pose sequence (PAPER.md:105-115; SURVEY §8(f) NEXT-3)")
     ap.add_argument("--profile", action="store_true", help="minimal run for ncu (no e2e / cpu / clocks)")
     return ap.parse_args()
 
@@ -268,6 +270,76 @@ def run_schedule(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- NEXT-3
+def run_tsdf(args):
+    """TSDF fusion (gs_tsdf_allocate + gs_tsdf_integrate, Eqs. 6-9) of a config's pose
+    sequence at 1 cm voxels, eps = 6 cm, w_max 100: `--warmup` frames,
+    then `--steps` timed frames (CUDA events).  Depth frames are synthetic (scenegen.
+    render_depth of the config's surfaces, 2 mm noise, 1% invalid), on the device before
+    the timed region.  Roofline of k_tsdf_integrate: 16 B of voxel state (tsdf + weight,
+    read + write) per allocated voxel per frame, against the HBM peak."""
+    import torch
+
+    import scenegen
+    from paper_2408_12677_b200 import gsr, pipeline
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    lib = gsr.load()
+    n = args.warmup + args.steps
+    cfg = args.config if args.config in ("replica", "scannetpp", "large") else "replica"
+    w = scenegen.make(cfg, args.seed, num_views=n)
+    cams = w.cameras[:n]
+    depths = [torch.from_numpy(scenegen.render_depth(w.faces, c, noise_sigma=0.002, dropout=0.01, seed=k)).to(dev)
+              for k, c in enumerate(cams)]
+    vol = pipeline.TsdfVolume(lib, dev, 1 << 20, voxel_size=0.01, w_max=100.0)
+    for k in range(args.warmup):
+        vol.integrate_frame(cams[k], depths[k])
+    torch.cuda.synchronize()
+    nb0 = int(vol.num_blocks.item())
+    vol.new_blocks.zero_()
+    vol.updated.zero_()
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * args.steps + 1)]
+    ev[0].record(stream)
+    gcams = [gsr.camera(c) for c in cams]
+    for i in range(args.steps):
+        k = args.warmup + i
+        lib.tsdf_allocate(vol.prm, vol.vol, gcams[k], depths[k], vol.new_blocks)
+        ev[3 * i + 1].record(stream)
+        lib.tsdf_integrate(vol.prm, vol.vol, gcams[k], depths[k], vol.updated)
+        ev[3 * i + 2].record(stream)
+        ev[3 * i + 3] = ev[3 * i + 2]
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[-1])
+    alloc_ms = sum(ev[3 * i].elapsed_time(ev[3 * i + 1]) for i in range(args.steps)) / args.steps
+    int_ms = sum(ev[3 * i + 1].elapsed_time(ev[3 * i + 2]) for i in range(args.steps)) / args.steps
+    nb1 = int(vol.num_blocks.item())
+    if nb1 > vol.block_cap:
+        raise RuntimeError("TSDF block pool overflow")
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs") or 6556.2
+    vox_bytes = (nb0 + nb1) / 2 * 512 * 16  # mean allocated voxels x (tsdf, weight) read + write
+    gbs = vox_bytes / (int_ms / 1e3) / 1e9
+    upd = int(vol.updated.item())
+    line = {"metric": "TSDF fusion (band allocation + Eqs. 6-9 integration): frames/s and voxel updates/s",
+            "value": args.steps / (ms / 1e3), "unit": "frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_frame": ms / args.steps, "higher_is_better": True, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": cfg, "resolution": f"{cams[0].width}x{cams[0].height}",
+                                            "voxel_size_m": 0.01, "trunc_m": 0.06, "w_max": 100, "step_m": 0.005,
+                                            "depth": "scenegen.render_depth: 2 mm noise, 1% invalid"},
+            "voxel_updates_per_s": upd / (ms / 1e3), "blocks": {"before": nb0, "after": nb1,
+                                                                 "new_in_timed": int(vol.new_blocks.item())},
+            "stage_ms": {"allocate": alloc_ms, "integrate": int_ms},
+            "roofline": {"kernel": "k_tsdf_integrate", "bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "algorithmic_bytes_per_launch": vox_bytes,
+                         "note": "16 B per allocated voxel (tsdf + weight read and written); depth reads not counted"}}
+    print(json.dumps(line), flush=True)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
@@ -279,6 +351,9 @@ def main():
         return
     if args.schedule:
         run_schedule(args)
+        return
+    if args.tsdf:
+        run_tsdf(args)
         return
 
     import numpy as np

@@ -326,6 +326,63 @@ gs_status gs_keyframe_schedule(const gs_kf_params* prm /*HOST*/, int64_t n_frame
                                int32_t* iter_view /*HOST*/, int32_t* iter_frame /*HOST*/, int64_t capacity,
                                int64_t* n_iters /*HOST*/, uint8_t* is_keyframe /*HOST, nullable*/);
 
+/* ================================================================ TSDF fusion (NEXT-3)
+ * GSFusion's TSDF grid (§III-A1) and its fusion step (PAPER.md:105-115,
+ * §III-B1, Eqs. 6-9) on the GPU: single-resolution voxels
+ * (tsdf, weight) in 8^3-voxel blocks, indexed by the 63-bit Morton code of the block
+ * coordinates through an open-addressing hash table (the octree is used "as a spatial
+ * index" only).  Readings R32-R36 in DESIGN.md.
+ *
+ * Coordinates: voxel index v = floor(p / voxel_size) + origin (per axis, must lie in
+ * [0, 2^21)); block b = v >> 3; voxel centre p_v = (v - origin + 0.5) voxel_size. */
+typedef struct {
+  float voxel_size; /* m (1 cm) */
+  float trunc;      /* epsilon, m (band half-width; default 6 voxels, R33) */
+  float w_max;      /* weight cap of Eq. 8 */
+  float step;       /* allocation ray-march step, m (default voxel_size / 2, R34) */
+  int32_t origin[3];
+} gs_tsdf_params;
+
+/* Caller-owned DEVICE buffers.  keys/slots: int64/int32 [table_cap] (table_cap a power
+ * of two, >= 2 x blocks); pool_keys: uint64 [block_cap] (Morton key of each pool
+ * block); tsdf, weight: float [block_cap][512] (voxel x-fastest inside a block);
+ * num_blocks: int64 counter.  gs_tsdf_reset initialises everything (empty table,
+ * zero voxels); allocated blocks are never freed, so pool entries are zero until
+ * first allocated. */
+typedef struct {
+  uint64_t* keys;
+  int32_t* slots;
+  uint64_t* pool_keys;
+  float* tsdf;
+  float* weight;
+  int64_t table_cap;
+  int64_t block_cap;
+  int64_t* num_blocks;
+} gs_tsdf_volume;
+
+#define GS_TSDF_EMPTY_KEY 0xFFFFFFFFFFFFFFFFull
+
+gs_status gs_tsdf_reset(gs_tsdf_volume vol, void* stream);
+
+/* Band allocation: for every pixel with valid depth d (> 0, metres of
+ * camera z), samples the pixel's line of sight at z = d - eps + k step (k = 0..n, the
+ * last sample clamped to d + eps) and allocates the block of every sample.
+ * depth: float[H][W] DEVICE.  new_blocks: nullable DEVICE int64, += blocks created.
+ * Returns GS_ERR_CAPACITY (synchronising) if the pool or table overflowed; the volume
+ * is then unusable until reset. */
+gs_status gs_tsdf_allocate(const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume vol, const gs_camera* cam /*HOST*/,
+                           const float* depth, int64_t* new_blocks, void* stream);
+
+/* Integration (Eqs. 6-9): every voxel of every allocated block whose
+ * centre projects (camera z > 0, nearest pixel under R1) onto a valid depth d gets
+ * sdf = d - z_c (Eq. 6); voxels with sdf < -eps are skipped (R35); tsdf = min(1,
+ * sdf/eps) if sdf > 0 else max(-1, sdf/eps) (Eq. 7); w_k = min(w_max, w_{k-1} + 1)
+ * (Eq. 8); tsdf_k = (tsdf_{k-1} w_{k-1} + tsdf w_k) / (w_{k-1} + w_k) (Eq. 9).
+ * updated: nullable DEVICE int64, += voxels updated.  fp32 with a fixed operation
+ * order (bit-exact against the oracle). */
+gs_status gs_tsdf_integrate(const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume vol, const gs_camera* cam /*HOST*/,
+                            const float* depth, int64_t* updated, void* stream);
+
 /* ---------------------------------------------------------------- harness: Eq. 12
  * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
  * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */

@@ -45,6 +45,17 @@ class GsKfParams(C.Structure):
                 ("store_all_frames", C.c_int32), ("seed", C.c_uint64)]
 
 
+class GsTsdfParams(C.Structure):
+    _fields_ = [("voxel_size", C.c_float), ("trunc", C.c_float), ("w_max", C.c_float), ("step", C.c_float),
+                ("origin", C.c_int32 * 3)]
+
+
+class GsTsdfVolume(C.Structure):
+    _fields_ = [("keys", C.c_void_p), ("slots", C.c_void_p), ("pool_keys", C.c_void_p), ("tsdf", C.c_void_p),
+                ("weight", C.c_void_p), ("table_cap", C.c_int64), ("block_cap", C.c_int64),
+                ("num_blocks", C.c_void_p)]
+
+
 class GsProj(C.Structure):
     _fields_ = [("rec", C.c_void_p), ("radius", C.c_void_p), ("tiles", C.c_void_p), ("flags", C.c_void_p)]
 
@@ -118,10 +129,14 @@ class Library:
         lib.gs_adam_step_peers.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float,
                                            i64, i64, i64, vp]
         lib.gs_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp]
+        lib.gs_tsdf_reset.argtypes = [GsTsdfVolume, vp]
+        lib.gs_tsdf_allocate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
+        lib.gs_tsdf_integrate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev"):
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
+                   "gs_tsdf_integrate"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -242,6 +257,18 @@ class Library:
         return self._check("gs_adam_step_peers", self.lib.gs_adam_step_peers(
             C.byref(sc), int(world), int(rank), gp, pp, _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step), int(begin),
             int(end), _stream(stream)))
+
+    # -- NEXT-3: TSDF fusion ---------------------------------------------
+    def tsdf_reset(self, vol, stream=None):
+        return self._check("gs_tsdf_reset", self.lib.gs_tsdf_reset(vol, _stream(stream)))
+
+    def tsdf_allocate(self, prm, vol, cam, depth, new_blocks=None, stream=None):
+        return self._check("gs_tsdf_allocate", self.lib.gs_tsdf_allocate(
+            C.byref(prm), vol, C.byref(cam), _ptr(depth), _ptr(new_blocks), _stream(stream)))
+
+    def tsdf_integrate(self, prm, vol, cam, depth, updated=None, stream=None):
+        return self._check("gs_tsdf_integrate", self.lib.gs_tsdf_integrate(
+            C.byref(prm), vol, C.byref(cam), _ptr(depth), _ptr(updated), _stream(stream)))
 
     def keyframe_schedule(self, new_prims, threshold=50, m=5, n=3, global_iters=10, store_all_frames=False, seed=0):
         """gs_keyframe_schedule (host): returns (iter_view, iter_frame, is_keyframe) numpy arrays."""

@@ -510,3 +510,47 @@ def params_agree_across_ranks(model: GaussianModel, group=None) -> bool:
     allv = [torch.zeros_like(sig) for _ in range(dist.get_world_size(group))]
     dist.all_gather(allv, sig, group=group)
     return all(torch.equal(allv[0], x) for x in allv[1:])
+
+
+class TsdfVolume:
+    """Device buffers of the TSDF grid (NEXT-3, gs_tsdf_* calls): hash table of block
+    Morton keys, block pool of 8^3 (tsdf, weight) voxels.  integrate_frame() is one
+    frame of GSFusion's TSDF fusion: band allocation, then Eqs. 6-9."""
+
+    def __init__(self, lib, device, block_cap: int, voxel_size=0.01, trunc=None, w_max=100.0, step=None,
+                 origin=(1 << 20,) * 3):
+        self.lib = lib
+        self.block_cap = int(block_cap)
+        table_cap = 1
+        while table_cap < 2 * self.block_cap:
+            table_cap *= 2
+        self.keys = torch.empty(table_cap, dtype=torch.int64, device=device)
+        self.slots = torch.empty(table_cap, dtype=torch.int32, device=device)
+        self.pool_keys = torch.zeros(self.block_cap, dtype=torch.int64, device=device)
+        self.tsdf = torch.empty((self.block_cap, 512), dtype=torch.float32, device=device)
+        self.weight = torch.empty((self.block_cap, 512), dtype=torch.float32, device=device)
+        self.num_blocks = torch.zeros(1, dtype=torch.int64, device=device)
+        self.new_blocks = torch.zeros(1, dtype=torch.int64, device=device)
+        self.updated = torch.zeros(1, dtype=torch.int64, device=device)
+        self.vol = gsr.GsTsdfVolume(self.keys.data_ptr(), self.slots.data_ptr(), self.pool_keys.data_ptr(),
+                                    self.tsdf.data_ptr(), self.weight.data_ptr(), table_cap, self.block_cap,
+                                    self.num_blocks.data_ptr())
+        self.prm = gsr.GsTsdfParams(float(voxel_size), float(trunc if trunc is not None else 6 * voxel_size),
+                                    float(w_max), float(step if step is not None else voxel_size / 2),
+                                    (gsr.C.c_int32 * 3)(*[int(x) for x in origin]))
+        lib.tsdf_reset(self.vol)
+
+    def integrate_frame(self, cam, depth):
+        gcam = gsr.camera(cam)
+        self.lib.tsdf_allocate(self.prm, self.vol, gcam, depth, self.new_blocks)
+        self.lib.tsdf_integrate(self.prm, self.vol, gcam, depth, self.updated)
+
+    def blocks(self):
+        """(keys uint64 ascending, tsdf [n][512], weight [n][512]) on the host (sync)."""
+        import numpy as np
+        n = int(self.num_blocks.item())
+        if n > self.block_cap:
+            raise gsr.GsError("gs_tsdf_allocate", gsr.GS_ERR_CAPACITY, f"{n} blocks > capacity {self.block_cap}")
+        keys = self.pool_keys[:n].cpu().numpy().view(np.uint64)
+        order = np.argsort(keys)
+        return keys[order], self.tsdf[:n].cpu().numpy()[order], self.weight[:n].cpu().numpy()[order]

@@ -105,6 +105,7 @@ class Workload:
     scene: Scene
     target_scene: Scene  # perturbed parameters used to render the target images
     cameras: list  # list[Camera]; the views of one batch
+    faces: list = None  # surface rectangles the Gaussians were sampled on (depth synthesis)
 
 
 # ---------------------------------------------------------------------------
@@ -295,7 +296,7 @@ def make_replica(seed: int = 0, num_views: int = 100, P: int = 300_000) -> Workl
         pos = [prng.uniform(-3, 3), prng.uniform(-2, 2), 1.5]
         fwd = _yaw_pitch_forward(prng.uniform(0, 2 * math.pi), math.radians(prng.normal(0, 10)))
         cams.append(camera_from_forward(1200, 680, 600.0, 599.5, 339.5, pos, fwd))
-    return Workload("replica", scene, perturb(scene, seed + 1), cams)
+    return Workload("replica", scene, perturb(scene, seed + 1), cams, faces)
 
 
 def make_scannetpp(seed: int = 0, num_views: int = 8, P: int = 1_000_000) -> Workload:
@@ -311,7 +312,7 @@ def make_scannetpp(seed: int = 0, num_views: int = 8, P: int = 1_000_000) -> Wor
         pos = np.array([1.5 * math.cos(ang), 1.5 * math.sin(ang), 1.5])
         fwd = np.array([0.0, 0.0, 1.0]) - pos
         cams.append(camera_from_forward(1752, 1168, 1100.0, 875.5, 583.5, pos, fwd))
-    return Workload("scannetpp", scene, perturb(scene, seed + 1), cams)
+    return Workload("scannetpp", scene, perturb(scene, seed + 1), cams, faces)
 
 
 def make_large(seed: int = 0, num_views: int = 64, P: int = 4_000_000) -> Workload:
@@ -330,7 +331,7 @@ def make_large(seed: int = 0, num_views: int = 64, P: int = 4_000_000) -> Worklo
         pos = [prng.uniform(-14, 14), prng.uniform(-9, 9), 1.5]
         fwd = _yaw_pitch_forward(prng.uniform(0, 2 * math.pi), math.radians(prng.normal(0, 10)))
         cams.append(camera_from_forward(1920, 1440, 1200.0, 959.5, 719.5, pos, fwd))
-    return Workload("large", scene, perturb(scene, seed + 1), cams)
+    return Workload("large", scene, perturb(scene, seed + 1), cams, faces)
 
 
 MAKERS = {
@@ -418,3 +419,62 @@ def new_primitive_counts(num_frames: int, seed: int = 0):
     turns = rng.random(num_frames) < 0.15
     counts = counts + turns * rng.integers(50, 800, num_frames)
     return counts.astype(np.int64)
+
+
+def render_depth(faces, cam, noise_sigma: float = 0.0, dropout: float = 0.0, seed: int = 0):
+    """Synthetic depth frame (metres of camera z, 0 = invalid) of the surface
+    rectangles seen by ``cam``: the input of the TSDF fusion (NEXT-3) in place of a
+    sensor's depth map (Replica / ScanNet++ depth is not available).
+    Pixel (i, j) looks along p(z) = o + z R^T ((i - cx)/fx, (j - cy)/fy, 1) (R1);
+    depth = the smallest z > 0 where the ray meets a rectangle.  Optional Gaussian noise
+    (sigma, m) and random invalid pixels (fraction), seed stream seed + 4.  Input
+    generation only: none of the fusion arithmetic happens here."""
+    R = np.asarray(cam.R_cw, np.float64).reshape(3, 3)
+    t = np.asarray(cam.t_cw, np.float64).reshape(3)
+    o = -R.T @ t
+    jj, ii = np.meshgrid(np.arange(cam.height, dtype=np.float64), np.arange(cam.width, dtype=np.float64),
+                         indexing="ij")
+    dc = np.stack([(ii - cam.cx) / cam.fx, (jj - cam.cy) / cam.fy, np.ones_like(ii)], axis=-1)
+    dw = dc @ R  # rows: R^T dc
+    best = np.full(ii.shape, np.inf)
+    for (O, U, V, N) in faces:
+        O, U, V, N = (np.asarray(x, np.float64) for x in (O, U, V, N))
+        # pixel window: the projected corners' bounding box (whole image if the
+        # rectangle crosses the camera plane); faces entirely behind are skipped
+        corners = np.stack([O, O + U, O + V, O + U + V]) @ R.T + t
+        if np.all(corners[:, 2] <= 1e-6):
+            continue
+        if np.all(corners[:, 2] > 1e-6):
+            u = cam.fx * corners[:, 0] / corners[:, 2] + cam.cx
+            v = cam.fy * corners[:, 1] / corners[:, 2] + cam.cy
+            x0, x1 = max(int(np.floor(u.min())) - 1, 0), min(int(np.ceil(u.max())) + 2, cam.width)
+            y0, y1 = max(int(np.floor(v.min())) - 1, 0), min(int(np.ceil(v.max())) + 2, cam.height)
+            if x0 >= x1 or y0 >= y1:
+                continue
+        else:
+            x0, x1, y0, y1 = 0, cam.width, 0, cam.height
+        dwin = dw[y0:y1, x0:x1]
+        n = np.cross(U, V)
+        den = dwin @ n
+        with np.errstate(divide="ignore", invalid="ignore"):
+            z = ((O - o) @ n) / den
+        ok = np.isfinite(z) & (z > 1e-6)
+        p = o + z[..., None] * dwin - O
+        a = (p @ U) / (U @ U)
+        b = (p @ V) / (V @ V)
+        ok &= (a >= 0) & (a <= 1) & (b >= 0) & (b <= 1)
+        win = best[y0:y1, x0:x1]
+        best[y0:y1, x0:x1] = np.where(ok & (z < win), z, win)
+    depth = np.where(np.isfinite(best), best, 0.0)
+    rng = np.random.default_rng(seed + 4)
+    if noise_sigma > 0:
+        depth = np.where(depth > 0, depth + rng.normal(0.0, noise_sigma, depth.shape), 0.0)
+    if dropout > 0:
+        depth = np.where(rng.random(depth.shape) < dropout, 0.0, depth)
+    return depth.astype(np.float32)
+
+
+def plane_faces(z0: float, half: float = 50.0):
+    """One fronto-parallel rectangle z = z0 (identity camera): TSDF closed-form tests."""
+    o = np.array
+    return [(o([-half, -half, z0]), o([2 * half, 0.0, 0.0]), o([0.0, 2 * half, 0.0]), o([0.0, 0.0, -1.0]))]
