@@ -383,6 +383,32 @@ gs_status gs_tsdf_allocate(const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume vo
 gs_status gs_tsdf_integrate(const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume vol, const gs_camera* cam /*HOST*/,
                             const float* depth, int64_t* updated, void* stream);
 
+/* ================================================================ seeding (NEXT-4)
+ * Quadtree decomposition of the RGB frame and weight-gated Gaussian initialisation
+ * (§III-B2, Eq. 10).  Readings R37-R40.
+ *
+ * gs_quadtree: a cell (x, y, w, h) splits into NW (x, y, w/2, h/2), NE (x + w/2, y,
+ *   w - w/2, h/2), SW, SE (integer halves) iff w > min_cell, h > min_cell and its
+ *   contrast max(L) - min(L) > threshold, L = 0.299 R + 0.587 G + 0.114 B (fp32, in
+ *   that order).  rgb: float[3][H][W] in [0, 1] DEVICE.  leaves: int32[leaf_capacity][4]
+ *   (x, y, w, h) DEVICE, in depth-first NW, NE, SW, SE order; num_leaves: DEVICE int64
+ *   (the full count even if it exceeds the capacity).  ws: gs_quadtree_workspace bytes.
+ * gs_seed_gaussians: for every leaf in order, the centre pixel u = (x + w/2, y + h/2)
+ *   with depth d > 0 is back-projected, p_q = T_WC pi^-1(u, d) (Eq. 10); if the voxel
+ *   containing p_q (TSDF grid of the same frame, fused BEFORE seeding) has weight
+ *   exactly 1, a Gaussian is appended at column scene->P + (index among the accepted
+ *   leaves): mean p_q, log-scale log(s) x 3 with s = |pi^-1(corner (x, y), d) -
+ *   pi^-1(u, d)|, quaternion (1, 0, 0, 0), opacity logit 0 (alpha 0.5), SH DC
+ *   (rgb(u) - 0.5) / Y00, higher SH 0.  Columns past P_stride are not written.
+ *   num_new: DEVICE int64 = accepted count (the keyframe signal of PAPER.md:149); the
+ *   caller advances P. */
+size_t gs_quadtree_workspace(int32_t width, int32_t height, int32_t min_cell);
+gs_status gs_quadtree(int32_t width, int32_t height, const float* rgb, float threshold, int32_t min_cell, void* ws,
+                      size_t ws_bytes, int32_t* leaves, int64_t leaf_capacity, int64_t* num_leaves, void* stream);
+gs_status gs_seed_gaussians(const gs_camera* cam /*HOST*/, const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume vol,
+                            const float* depth, const float* rgb, const int32_t* leaves, const int64_t* num_leaves,
+                            const gs_scene* scene /*HOST*/, float* params, int64_t* num_new, void* stream);
+
 /* ---------------------------------------------------------------- harness: Eq. 12
  * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
  * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */

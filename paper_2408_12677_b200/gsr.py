@@ -132,11 +132,15 @@ class Library:
         lib.gs_tsdf_reset.argtypes = [GsTsdfVolume, vp]
         lib.gs_tsdf_allocate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
         lib.gs_tsdf_integrate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
+        lib.gs_quadtree_workspace.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        lib.gs_quadtree_workspace.restype = C.c_size_t
+        lib.gs_quadtree.argtypes = [C.c_int32, C.c_int32, vp, C.c_float, C.c_int32, vp, C.c_size_t, vp, i64, vp, vp]
+        lib.gs_seed_gaussians.argtypes = [vp, vp, GsTsdfVolume, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
                    "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
-                   "gs_tsdf_integrate"):
+                   "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -269,6 +273,20 @@ class Library:
     def tsdf_integrate(self, prm, vol, cam, depth, updated=None, stream=None):
         return self._check("gs_tsdf_integrate", self.lib.gs_tsdf_integrate(
             C.byref(prm), vol, C.byref(cam), _ptr(depth), _ptr(updated), _stream(stream)))
+
+    # -- NEXT-4: quadtree seeding ------------------------------------------
+    def quadtree_workspace(self, width, height, min_cell) -> int:
+        return int(self.lib.gs_quadtree_workspace(int(width), int(height), int(min_cell)))
+
+    def quadtree(self, width, height, rgb, threshold, min_cell, ws, leaves, num_leaves, stream=None):
+        return self._check("gs_quadtree", self.lib.gs_quadtree(
+            int(width), int(height), _ptr(rgb), float(threshold), int(min_cell), _ptr(ws), ws.numel() * ws.element_size(),
+            _ptr(leaves), leaves.shape[0], _ptr(num_leaves), _stream(stream)))
+
+    def seed_gaussians(self, cam, prm, vol, depth, rgb, leaves, num_leaves, sc, params, num_new, stream=None):
+        return self._check("gs_seed_gaussians", self.lib.gs_seed_gaussians(
+            C.byref(cam), C.byref(prm), vol, _ptr(depth), _ptr(rgb), _ptr(leaves), _ptr(num_leaves), C.byref(sc),
+            _ptr(params), _ptr(num_new), _stream(stream)))
 
     def keyframe_schedule(self, new_prims, threshold=50, m=5, n=3, global_iters=10, store_all_frames=False, seed=0):
         """gs_keyframe_schedule (host): returns (iter_view, iter_frame, is_keyframe) numpy arrays."""

@@ -554,3 +554,46 @@ class TsdfVolume:
         keys = self.pool_keys[:n].cpu().numpy().view(np.uint64)
         order = np.argsort(keys)
         return keys[order], self.tsdf[:n].cpu().numpy()[order], self.weight[:n].cpu().numpy()[order]
+
+
+def empty_model(capacity: int, sh_degree: int, device) -> GaussianModel:
+    """A model with no Gaussians and room for `capacity` (the online map grows into it)."""
+    import numpy as np
+
+    class _S:
+        pass
+    sc = _S()
+    S = (int(capacity) + 3) // 4 * 4
+    sc.P, sc.sh_degree = 0, int(sh_degree)
+    sc.params = np.zeros((11 + 3 * (sh_degree + 1) ** 2, S), np.float32)
+    return GaussianModel(sc, device)
+
+
+class Seeder:
+    """NEXT-4: per frame, the contrast quadtree of the RGB image
+    (gs_quadtree) and the weight-gated initialisation of new Gaussians at the leaves
+    (gs_seed_gaussians, Eq. 10) against the TSDF grid fused with the same frame.
+    seed_frame() appends to `model` and returns the number of new Gaussians (the
+    keyframe signal of PAPER.md:149; one host sync)."""
+
+    def __init__(self, lib, width: int, height: int, device, threshold=0.1, min_cell=4):
+        self.lib, self.W, self.H = lib, int(width), int(height)
+        self.threshold, self.min_cell = float(threshold), int(min_cell)
+        self.ws = torch.empty(lib.quadtree_workspace(self.W, self.H, self.min_cell), dtype=torch.uint8, device=device)
+        cap = (self.W // self.min_cell + 1) * (self.H // self.min_cell + 1) + 16
+        self.leaves = torch.empty((cap, 4), dtype=torch.int32, device=device)
+        self.num_leaves = torch.zeros(1, dtype=torch.int64, device=device)
+        self.num_new = torch.zeros(1, dtype=torch.int64, device=device)
+
+    def leaves_of(self, rgb):
+        self.lib.quadtree(self.W, self.H, rgb, self.threshold, self.min_cell, self.ws, self.leaves, self.num_leaves)
+
+    def seed_frame(self, cam, depth, rgb, tsdf: "TsdfVolume", model: GaussianModel) -> int:
+        self.leaves_of(rgb)
+        self.lib.seed_gaussians(gsr.camera(cam), tsdf.prm, tsdf.vol, depth, rgb, self.leaves, self.num_leaves,
+                                model.desc, model.params, self.num_new)
+        n = int(self.num_new.item())
+        n_fit = min(n, model.P_stride - model.P)
+        model.P += n_fit
+        model.desc = gsr.scene_desc(model.P, model.P_stride, model.sh_degree)
+        return n
