@@ -242,7 +242,8 @@ gs_status gs_naive_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_sce
                                      float* sgrad, void* stream);
 
 /* ---------------------------------------------------------------- gs_adam_step
- * Dense bias-corrected Adam over all F * P scalars (R20):
+ * Dense bias-corrected Adam over all F x P scalars of the live Gaussians [0, P) (R20;
+ * columns P..P_stride-1, the room a growing map has left, are not touched):
  *   m = b1 m + (1-b1) g;  v = b2 v + (1-b2) g^2;
  *   p -= lr_row * (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
  *  lr_per_row: HOST float[F].  step: 1-based t.  zero_grad != 0 also writes grad = 0.

@@ -374,7 +374,7 @@ gs_status gs_adam_step(const gs_scene* scene, float* params, float* grad, float*
   const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
   const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
   launch_adam(rows_of(scene), scene->P_stride, params, grad, m, v, lr_per_row, beta1, beta2, eps, (float)bc1,
-              (float)bc2, zero_grad, static_cast<cudaStream_t>(stream));
+              (float)bc2, zero_grad, static_cast<cudaStream_t>(stream), 0, -1, scene->P);
   return check_launch("gs_adam_step");
 }
 
@@ -393,7 +393,7 @@ gs_status gs_adam_step_dev(const gs_scene* scene, float* params, float* grad, fl
   }
   GS_TRY(check_ptrs("gs_adam_step_dev", {{params, "params"}, {grad, "grad"}, {m, "m"}, {v, "v"}}));
   launch_adam_dev(rows_of(scene), scene->P_stride, params, grad, m, v, lr_per_row, beta1, beta2, eps, step_dev,
-                  zero_grad, static_cast<cudaStream_t>(stream));
+                  zero_grad, static_cast<cudaStream_t>(stream), scene->P);
   return check_launch("gs_adam_step_dev");
 }
 

@@ -13,11 +13,15 @@ struct LrTable {
 // Scalars [4 b4, 4 e4) of the flattened [F][P_stride] arrays; g holds the gradient of
 // that range (g[i - b4]), so a rank of the sharded optimiser passes its reduce-scattered
 // shard and the full step passes b4 = 0, g = grad.
+// cl4 < S4 (full step only): just the first cl4 float4 columns of every row -- the live
+// Gaussians [0, P) of a map that grows into its capacity P_stride.
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
-                                              float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4, LrTable lr,
-                                              float b1, float b2, float eps, float rs_bc2, int zero_grad) {
+                                              float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4, int64_t cl4,
+                                              LrTable lr, float b1, float b2, float eps, float rs_bc2, int zero_grad) {
   const float c1 = 1.f - b1, c2 = 1.f - b2;
-  for (int64_t i = b4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e4; i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t count = cl4 < S4 ? (e4 / S4) * cl4 : e4 - b4;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = cl4 < S4 ? (j / cl4) * S4 + j % cl4 : b4 + j;
     const float step = lr.step[i / S4];
     const float4 gg = g[i - b4];
     float4 mm = m[i], vv = v[i], pp = p[i];
@@ -41,8 +45,8 @@ __global__ void k_step_inc(int64_t* t) { *t += 1; }
 
 __global__ void __launch_bounds__(256) k_adam_dev(float4* __restrict__ p, float4* __restrict__ g,
                                                   float4* __restrict__ m, float4* __restrict__ v, int64_t n4,
-                                                  int64_t S4, LrTable lr_raw, int F, float b1, float b2, float eps,
-                                                  const int64_t* __restrict__ step_dev, int zero_grad) {
+                                                  int64_t S4, int64_t cl4, LrTable lr_raw, int F, float b1, float b2,
+                                                  float eps, const int64_t* __restrict__ step_dev, int zero_grad) {
   __shared__ float s_step[64];
   __shared__ float s_rs;
   if (threadIdx.x < 64) {
@@ -54,7 +58,8 @@ __global__ void __launch_bounds__(256) k_adam_dev(float4* __restrict__ p, float4
   __syncthreads();
   const float rs_bc2 = s_rs;
   const float c1 = 1.f - b1, c2 = 1.f - b2;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n4; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = cl4 < S4 ? (j / cl4) * S4 + j % cl4 : j;
     const float step = s_step[i / S4];
     const float4 gg = g[i];
     float4 mm = m[i], vv = v[i], pp = p[i];
@@ -140,28 +145,33 @@ __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restric
 
 void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
                  float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s, int64_t begin,
-                 int64_t end) {
+                 int64_t end, int64_t live) {
   LrTable t{};
   for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
-  if (end < 0) end = F * S;
-  const int64_t n4 = (end - begin) / 4;
+  int64_t cl4 = S / 4;
+  if (end < 0) {
+    end = F * S;
+    if (live >= 0) cl4 = std::min<int64_t>((live + 3) / 4, S / 4);
+  }
+  const int64_t n4 = cl4 < S / 4 ? F * cl4 : (end - begin) / 4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
   k_adam<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
-                                           end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
+                                           end / 4, S / 4, cl4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
   count_launch();
 }
 
 void launch_adam_dev(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
-                     float beta2, float eps, int64_t* step_dev, int zero_grad, cudaStream_t s) {
+                     float beta2, float eps, int64_t* step_dev, int zero_grad, cudaStream_t s, int64_t live) {
   LrTable t{};
   for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r];
-  const int64_t n4 = F * S / 4;
+  const int64_t cl4 = live >= 0 ? std::min<int64_t>((live + 3) / 4, S / 4) : S / 4;
+  const int64_t n4 = F * cl4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
   k_step_inc<<<1, 1, 0, s>>>(step_dev);
   k_adam_dev<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
-                                               reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, S / 4, t,
-                                               (int)F, beta1, beta2, eps, step_dev, zero_grad);
+                                               reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, S / 4, cl4,
+                                               t, (int)F, beta1, beta2, eps, step_dev, zero_grad);
   count_launch(2);
 }
 

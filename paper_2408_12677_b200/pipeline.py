@@ -125,7 +125,11 @@ class Trainer:
     by bench.py to time them with CUDA events on the launching stream)."""
 
     def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
-                 w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1, optimizer=None):
+                 w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1, optimizer=None,
+                 capacity: int = None):
+        # capacity: the most Gaussians the per-view buffers must hold (a growing online
+        # map passes its P_stride; default the model's current P)
+        cap_p = int(capacity) if capacity is not None else model.P
         self.lib, self.model, self.cameras, self.targets = lib, model, cameras, targets
         self.device, self.w_depth, self.allreduce = device, w_depth, allreduce
         # optimizer: None = (allreduce +) replicated gs_adam_step; else an object whose
@@ -138,10 +142,10 @@ class Trainer:
         # another view's rendering (the views of a batch are independent until the
         # projection backward sums them, R21)
         n_streams = max(1, int(streams))
-        self.bufs = [ViewBuffers(lib, cameras[0], model.P, key_capacity, device) for _ in range(n_streams)]
+        self.bufs = [ViewBuffers(lib, cameras[0], cap_p, key_capacity, device) for _ in range(n_streams)]
         self.buf = self.bufs[0]
         self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
-        P = max(model.P, 1)
+        P = max(cap_p, 1)
         # per in-flight view: projection flags and screen-space gradients (zeroed once;
         # gs_project_bwd_views leaves them zero again).  Two slot sets when a step has
         # more views than one chain takes, so that chunk c + 1's views render while
@@ -597,3 +601,53 @@ class Seeder:
         model.P += n_fit
         model.desc = gsr.scene_desc(model.P, model.P_stride, model.sh_degree)
         return n
+
+
+class OnlineMapper:
+    """GSFusion's incremental mapping loop on the built GPU path, one
+    RGB-D frame at a time:
+      1. TSDF fusion of the depth frame (NEXT-3: band allocation + Eqs. 6-9);
+      2. quadtree seeding of new Gaussians gated by the fused voxel weights (NEXT-4,
+         Eq. 10) -- the number appended is the frame's keyframe signal;
+      3. the keyframe strategy's iterations for this frame (NEXT-1: m on a keyframe, n +
+         (m - n) shuffled keyframes otherwise), each one fwd + bwd + Adam step on one
+         view with the colour L1 loss of Eq. 12 (w_depth = 0);
+    and finish() runs the global passes over the keyframe list after the scan.  The
+    plan of frame t is the host scheduler's plan of the prefix counts[0..t] (causal)."""
+
+    def __init__(self, lib, cameras, device, capacity: int, sh_degree: int = 0, key_capacity: int = 8 << 20,
+                 voxel_size=0.01, block_cap=1 << 20, threshold=0.1, min_cell=4, kf_threshold=50, m=5, n=3,
+                 global_iters=10, store_all_frames=False, seed=0):
+        self.lib, self.cameras, self.device = lib, cameras, device
+        self.tsdf = TsdfVolume(lib, device, block_cap, voxel_size=voxel_size)
+        c0 = cameras[0]
+        self.seeder = Seeder(lib, c0.width, c0.height, device, threshold=threshold, min_cell=min_cell)
+        self.model = empty_model(capacity, sh_degree, device)
+        self.targets = [None] * len(cameras)
+        self.trainer = Trainer(lib, self.model, cameras, self.targets, device, key_capacity, w_depth=0.0,
+                               capacity=self.model.P_stride)
+        self.kf = dict(threshold=kf_threshold, m=m, n=n, store_all_frames=store_all_frames, seed=seed)
+        self.global_iters = global_iters
+        self.counts = []
+        self.iterations = 0
+
+    def add_frame(self, t: int, rgb, depth):
+        """Frame t (cameras[t]) with its colour [3][H][W] and depth [H][W] device images."""
+        cam = self.cameras[t]
+        self.targets[t] = (rgb, depth)
+        self.tsdf.integrate_frame(cam, depth)
+        n_new = self.seeder.seed_frame(cam, depth, rgb, self.tsdf, self.model)
+        self.counts.append(n_new)
+        views, frames, _ = self.lib.keyframe_schedule(self.counts, global_iters=0, **self.kf)
+        if self.model.P > 0:
+            for v in views[frames == t].tolist():
+                self.trainer.step([v])
+                self.iterations += 1
+        return n_new
+
+    def finish(self):
+        views, frames, is_kf = self.lib.keyframe_schedule(self.counts, global_iters=self.global_iters, **self.kf)
+        for v in views[frames < 0].tolist():
+            self.trainer.step([v])
+            self.iterations += 1
+        return is_kf

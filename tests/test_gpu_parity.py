@@ -695,3 +695,28 @@ def test_graph_replay_matches_eager(lib, streams):
         assert b == pytest.approx(a, rel=1e-4)
     p0, p1 = (m.params.cpu().numpy().astype(np.float64) for m in models)
     assert grad_mismatch(p1, p0, rtol=1e-4, atol=1e-6).mean() <= 1e-3
+
+
+def test_adam_touches_live_columns_only(lib):
+    """A map growing into its capacity (P < P_stride): gs_adam_step / gs_adam_step_dev
+    update columns [0, P) as the full step would and leave the spare columns alone."""
+    rng = np.random.default_rng(5)
+    P, S, deg = 999, 1200, 0
+    F = 14
+    arrs = [rng.normal(size=(F, S)).astype(np.float32), (rng.normal(size=(F, S)) * 1e-2).astype(np.float32),
+            rng.uniform(0, 1e-3, size=(F, S)).astype(np.float32), rng.normal(size=(F, S)).astype(np.float32)]
+    lr = pipeline.lr_per_row(deg)
+    full = [torch.from_numpy(a.copy()).to(DEV) for a in arrs]
+    lib.adam_step(gsr.scene_desc(S, S, deg), full[0], full[3], full[1], full[2], lr, 2, zero_grad=False)
+    for dev_step in (False, True):
+        part = [torch.from_numpy(a.copy()).to(DEV) for a in arrs]
+        sc = gsr.scene_desc(P, S, deg)
+        if dev_step:
+            t = torch.ones(1, dtype=torch.int64, device=DEV)
+            lib.adam_step_dev(sc, part[0], part[3], part[1], part[2], lr, t)
+        else:
+            lib.adam_step(sc, part[0], part[3], part[1], part[2], lr, 2, zero_grad=False)
+        torch.cuda.synchronize()
+        for x, y, a in zip(full[:3], part[:3], arrs[:3]):
+            np.testing.assert_allclose(y.cpu().numpy()[:, :P], x.cpu().numpy()[:, :P], rtol=1e-6, atol=1e-7)
+            np.testing.assert_array_equal(y.cpu().numpy()[:, 1000:], a[:, 1000:])

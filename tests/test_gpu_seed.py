@@ -69,3 +69,37 @@ def test_seed_sequence_bitexact(lib):
         np.testing.assert_array_equal(got, ref)
         counts.append(n)
     assert counts[0] > 0 and counts[-1] < counts[0] // 4  # revisited view: mostly already observed
+
+
+def test_online_mapper_grows_and_fits(lib):
+    """The whole incremental loop (TSDF fusion -> seeding -> keyframe-scheduled steps ->
+    global passes) on a small room: the map grows from nothing, new-Gaussian counts drop
+    as the room gets observed, and the colour loss of the mapped views decreases."""
+    w = scenegen.make("replica", num_views=8)
+    cams = [scenegen.camera_from_forward(160, 90, 80.0, 79.5, 44.5, -c.R_cw.T @ c.t_cw, c.R_cw[2]) for c in w.cameras]
+    cams.append(cams[0])  # revisit the first view at the end
+    gt = pipeline.GaussianModel(w.scene, DEV)
+    cap = pipeline.default_capacity(pipeline.measure_keys(lib, gt, cams, DEV))
+    rgbs = [t[0] for t in pipeline.render_targets(lib, gt, cams, DEV, cap)]  # stand-in for the sensor's colour
+    om = pipeline.OnlineMapper(lib, cams, DEV, capacity=60000, sh_degree=0, key_capacity=1 << 21, voxel_size=0.02,
+                               block_cap=1 << 16, min_cell=2, m=5, n=3, global_iters=3)
+    for t, cam in enumerate(cams):
+        depth = torch.from_numpy(scenegen.render_depth(w.faces, cam, noise_sigma=0.002, seed=t)).to(DEV)
+        om.add_frame(t, rgbs[t].contiguous(), depth)
+    P_online = om.model.P
+    tr = om.trainer
+
+    def loss():
+        tot = 0.0
+        for t in range(len(cams)):
+            pipeline.render(lib, om.model, cams[t], tr.buf)
+            tot += float((tr.buf.rgb - rgbs[t]).abs().mean())
+        return tot
+    before = loss()
+    om.finish()
+    torch.cuda.synchronize()
+    tr.check_capacity()
+    assert P_online > 1000 and om.model.P == P_online == sum(om.counts)
+    assert om.counts[-1] < om.counts[0] // 4  # the revisited view adds little (weight gate)
+    assert om.iterations == om.model.step_count > 0
+    assert loss() < before
