@@ -474,6 +474,14 @@ def main():
             optimizer, optim_used = pipeline.PeerShardedAdam(lib, model), "peer"
         except Exception as ex:  # noqa: BLE001  (no symmetric memory / P2P: NCCL path)
             optim_used = f"sharded (peer unavailable: {type(ex).__name__})"
+        ok = torch.tensor([1 if optimizer is not None else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
+        if int(ok.item()) == 0 and optimizer is not None:
+            # another rank could not set up the peer path: undo ours (copy the state out of
+            # the symmetric buffers) and use the NCCL path everywhere
+            model.params = model.params.clone()
+            model.grad = model.grad.clone()
+            optimizer, optim_used = None, "sharded (peer unavailable on another rank)"
     if world > 1 and batched and optimizer is None and args.optim in ("peer", "sharded"):
         optimizer = pipeline.ShardedAdam(lib, model)
         optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
