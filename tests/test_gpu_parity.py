@@ -720,3 +720,39 @@ def test_adam_touches_live_columns_only(lib):
         for x, y, a in zip(full[:3], part[:3], arrs[:3]):
             np.testing.assert_allclose(y.cpu().numpy()[:, :P], x.cpu().numpy()[:, :P], rtol=1e-6, atol=1e-7)
             np.testing.assert_array_equal(y.cpu().numpy()[:, 1000:], a[:, 1000:])
+
+
+def test_bench_launch_configuration_full_size_sampled(lib):
+    """The bench's launch configuration at full size: scannetpp (1M Gaussians, 8 views of
+    1752x1168), Morton layout, 4 views in flight, the whole iteration replayed as a CUDA
+    graph.  After one replay, each stream's buffers hold the render of its last view
+    made with the pre-step parameters: sampled pixels against the oracle (1e-5, flips
+    explained by the decision margin), and the per-view key counts against the oracle's."""
+    w = workload("scannetpp")
+    model = pipeline.GaussianModel(w.scene, DEV)
+    pipeline.spatially_order(lib, model)
+    tgt = pipeline.GaussianModel(w.target_scene, DEV)
+    pipeline.spatially_order(lib, tgt)
+    cams = w.cameras
+    cap = pipeline.default_capacity(max(pipeline.measure_keys(lib, model, cams, DEV),
+                                        pipeline.measure_keys(lib, tgt, cams, DEV)))
+    targets = pipeline.render_targets(lib, tgt, cams, DEV, cap)
+    tr = pipeline.Trainer(lib, model, cams, targets, DEV, cap, streams=4)
+    views = list(range(len(cams)))
+    g = tr.capture(views)
+    snap = model.params.detach().cpu().numpy().copy()
+    tr.num_keys.zero_()
+    tr.replay(g)
+    torch.cuda.synchronize()
+    scene = scenegen.Scene(w.scene.P, w.scene.sh_degree, snap)
+    rng = np.random.default_rng(11)
+    for s in (0, 3):
+        v = 4 + s  # the last view stream s rendered
+        cam = cams[v]
+        px, py = rng.integers(0, cam.width, 1500), rng.integers(0, cam.height, 1500)
+        ref = gsref.render_pixels(cam, scene, px, py, gsref.F32)
+        rgb = tr.bufs[s].rgb.cpu().numpy()[:, py, px]
+        bad = np.abs(rgb - ref["rgb"]).max(0) > 1e-5
+        assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
+        K_ref = int(gsref.project(cam, scene, gsref.F32)["tiles"].sum())
+        assert int(tr.num_keys[v].item()) == K_ref
