@@ -10,7 +10,8 @@
 //  * band allocation: "a ray is marched along the line of sight for each
 //    pixel, and voxel blocks are allocated only if they fall into the specified eps
 //    band around the depth measurement" -- samples at z = d - eps + k step, k = 0..n,
-//    n = ceil(2 eps / step), the last one at z = d + eps (readings R33, R34);
+//    n = ceil(2 eps / step), the last one at z = d + eps, world point o + z R^T (rx, ry, 1)
+//    (readings R33, R34);
 //  * integration, Eqs. 6-9, per voxel of every allocated block:
 //      sdf = D[pi(T^-1 p_v)] - z_v                  (Eq. 6; nearest pixel, R1)
 //      tsdf = min(1, sdf/eps) if sdf > 0 else max(-1, sdf/eps)      (Eq. 7)
@@ -97,6 +98,18 @@ int64_t ref_tsdf_allocate(void* h, const Camera* c, const float* depth) {
       const float z0 = d - P.trunc;
       const float z1 = d + P.trunc;
       const int n = (int)std::ceil((z1 - z0) / P.step);
+      // the same line in the world: p(z) = o + z dw with dw = R^T (rx, ry, 1) and the
+      // camera centre o = -R^T t (double, rounded; reading R34)
+      float dw[3], o[3];
+      for (int a = 0; a < 3; ++a) {
+        const float m0 = c->R_cw[a] * rx;
+        const float m1 = c->R_cw[3 + a] * ry;
+        const float s01 = m0 + m1;
+        dw[a] = s01 + c->R_cw[6 + a];
+        double acc = 0.0;
+        for (int r = 0; r < 3; ++r) acc += (double)c->R_cw[3 * r + a] * (double)c->t_cw[r];
+        o[a] = (float)(-acc);
+      }
       for (int k = 0; k <= n; ++k) {
         float z;
         if (k == n) {
@@ -105,18 +118,11 @@ int64_t ref_tsdf_allocate(void* h, const Camera* c, const float* depth) {
           const float dz = (float)k * P.step;
           z = z0 + dz;
         }
-        const float pc[3] = {rx * z, ry * z, z};
-        // world point p = R^T (p_c - t)
-        float q[3];
-        for (int r = 0; r < 3; ++r) q[r] = pc[r] - c->t_cw[r];
         int64_t blk[3];
         bool inside = true;
         for (int a = 0; a < 3; ++a) {
-          const float m0 = c->R_cw[a] * q[0];
-          const float m1 = c->R_cw[3 + a] * q[1];
-          const float m2 = c->R_cw[6 + a] * q[2];
-          const float s01 = m0 + m1;
-          const float pw = s01 + m2;
+          const float zd = z * dw[a];
+          const float pw = zd + o[a];
           const float cell = std::floor(pw * inv_vs);
           const float vox = cell + (float)P.origin[a];
           if (!(vox >= 0.f && vox < 2097152.f)) inside = false;

@@ -87,38 +87,55 @@ __device__ __forceinline__ int insert_block(const gs_tsdf_volume& vol, uint64_t 
   return 0;
 }
 
+// Two phases per ray so that the warp stays converged: the sample loop only records the
+// distinct blocks its samples fall in (consecutive samples mostly share a block; a
+// per-lane list of up to kRayBlocks), and the insertion loop -- Morton code, hash probe,
+// CAS -- runs once per recorded block with the lanes in step.
+constexpr int kRayBlocks = 8;
+
 __global__ void __launch_bounds__(256) k_tsdf_alloc(TsdfDev tp, gs_tsdf_volume vol, DevCam cam,
                                                      const float* __restrict__ depth,
                                                      unsigned long long* __restrict__ new_blocks) {
   const int64_t npix = (int64_t)cam.W * cam.H;
   uint32_t created = 0;
+  int nb = 0;
+  int bl[kRayBlocks][3];
+  auto flush = [&]() {
+    const int n_max = __reduce_max_sync(__activemask(), nb);
+    for (int q = 0; q < n_max; ++q)
+      if (q < nb) created += insert_block(vol, morton3((uint32_t)bl[q][0], (uint32_t)bl[q][1], (uint32_t)bl[q][2]));
+    nb = 0;
+  };
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npix; p += (int64_t)gridDim.x * blockDim.x) {
     const float d = depth[p];
-    if (!(d > 0.f)) continue;
     const int i = (int)(p % cam.W), j = (int)(p / cam.W);
     const float rx = TD(TS((float)i, cam.cx), cam.fx), ry = TD(TS((float)j, cam.cy), cam.fy);
     const float z0 = TS(d, tp.eps), z1 = TA(d, tp.eps);
-    const int n = (int)ceilf(TD(TS(z1, z0), tp.step));
-    int lb0 = -1, lb1 = -1, lb2 = -1;  // block of the previous sample (consecutive samples share blocks)
+    const int n = d > 0.f ? (int)ceilf(TD(TS(z1, z0), tp.step)) : -1;
+    // the pixel's line of sight in the world: p(z) = o + z dw, dw = R^T (rx, ry, 1),
+    // o = the camera centre (R34: per-pixel direction, two operations per sample axis)
+    float dw[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) dw[a] = TA(TA(TM(cam.R[a], rx), TM(cam.R[3 + a], ry)), cam.R[6 + a]);
+    int lb0 = -1, lb1 = -1, lb2 = -1;  // block of the previous sample
     for (int k = 0; k <= n; ++k) {
       const float z = (k == n) ? z1 : TA(z0, TM((float)k, tp.step));
-      const float pc[3] = {TM(rx, z), TM(ry, z), z};
-      float q[3];
-#pragma unroll
-      for (int r = 0; r < 3; ++r) q[r] = TS(pc[r], cam.t[r]);
       int b[3];
       bool ok = true;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {  // p = R^T (p_c - t); voxel = floor(p * (1 / voxel_size)) (R34)
-        const float pw = TA(TA(TM(cam.R[a], q[0]), TM(cam.R[3 + a], q[1])), TM(cam.R[6 + a], q[2]));
+      for (int a = 0; a < 3; ++a) {  // voxel = floor(p * (1 / voxel_size)) + origin (R34)
+        const float pw = TA(TM(z, dw[a]), cam.ocam[a]);
         const float vv = TA(floorf(TM(pw, tp.inv_vs)), (float)tp.org[a]);
         ok = ok && (vv >= 0.f) && (vv < (float)(1 << kVoxBits));
         b[a] = ok ? ((int)vv >> 3) : 0;
       }
       if (!ok || (b[0] == lb0 && b[1] == lb1 && b[2] == lb2)) continue;
       lb0 = b[0], lb1 = b[1], lb2 = b[2];
-      created += insert_block(vol, morton3((uint32_t)b[0], (uint32_t)b[1], (uint32_t)b[2]));
+      if (nb == kRayBlocks) flush();  // rare: a long band through many blocks
+      bl[nb][0] = b[0], bl[nb][1] = b[1], bl[nb][2] = b[2];
+      ++nb;
     }
+    flush();
   }
   if (new_blocks) {
     const uint32_t tot = __reduce_add_sync(kFull, created);
