@@ -42,7 +42,7 @@
 namespace gsr {
 namespace {
 
-constexpr int kWarpsPerCta = 4;
+[[maybe_unused]] constexpr int kWarpsPerCta = 4;
 // Resident warps per SM the fast kernels are compiled for (register cap 65536 /
 // (32 x warps)); the register file is split per SM sub-partition, so 16 warps = 4
 // per SMSP at <= 128 registers, 20 = 5 per SMSP at <= 102 (measured: 16 -> 20 warps
@@ -53,37 +53,37 @@ constexpr int kWarpsPerCta = 4;
 #ifndef GSR_BWD_MINW
 #define GSR_BWD_MINW 20
 #endif
-constexpr int kFwdMinWarps = GSR_FWD_MINW, kBwdMinWarps = GSR_BWD_MINW;
-constexpr int kPix = 8;             // pixels per lane
+[[maybe_unused]] constexpr int kFwdMinWarps = GSR_FWD_MINW, kBwdMinWarps = GSR_BWD_MINW;
+[[maybe_unused]] constexpr int kPix = 8;             // pixels per lane
 #ifndef GSR_DENSE_FWD
 #define GSR_DENSE_FWD 3
 #endif
 #ifndef GSR_DENSE_BWD
 #define GSR_DENSE_BWD 6
 #endif
-constexpr int kDenseBlocks = GSR_DENSE_FWD;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
-constexpr int kDenseBlocksBwd = GSR_DENSE_BWD;  // bwd: same (its per-block body is ~2x longer)
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr float kAlphaMin = 1.0f / 255.0f;
-constexpr float kTStop = 1e-4f;
-constexpr float kAlphaCap = 0.99f;
-constexpr float kUncappedO = 0.9f;         // o <= this: alpha = o exp(power) < 0.99 (no cap)
-constexpr uint32_t kFlagGeneral = 1u << 8;  // conic not positive definite: keep the power > 0 test
-constexpr uint32_t kFlagCap = 1u << 9;      // o > kUncappedO: the 0.99 cap may bind
-constexpr float kHalfL2e = -0.5f * kLog2e;  // Ah = kHalfL2e A, Ch = kHalfL2e C
-constexpr float kNegL2e = -kLog2e;          // Bh = kNegL2e B
+[[maybe_unused]] constexpr int kDenseBlocks = GSR_DENSE_FWD;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
+[[maybe_unused]] constexpr int kDenseBlocksBwd = GSR_DENSE_BWD;  // bwd: same (its per-block body is ~2x longer)
+[[maybe_unused]] constexpr float kLog2e = 1.4426950408889634f;
+[[maybe_unused]] constexpr float kAlphaMin = 1.0f / 255.0f;
+[[maybe_unused]] constexpr float kTStop = 1e-4f;
+[[maybe_unused]] constexpr float kAlphaCap = 0.99f;
+[[maybe_unused]] constexpr float kUncappedO = 0.9f;         // o <= this: alpha = o exp(power) < 0.99 (no cap)
+[[maybe_unused]] constexpr uint32_t kFlagGeneral = 1u << 8;  // conic not positive definite: keep the power > 0 test
+[[maybe_unused]] constexpr uint32_t kFlagCap = 1u << 9;      // o > kUncappedO: the 0.99 cap may bind
+[[maybe_unused]] constexpr float kHalfL2e = -0.5f * kLog2e;  // Ah = kHalfL2e A, Ch = kHalfL2e C
+[[maybe_unused]] constexpr float kNegL2e = -kLog2e;          // Bh = kNegL2e B
 
-__device__ __forceinline__ float ex2_approx(float x) {
+[[maybe_unused]] __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float lg2_approx(float x) {
+[[maybe_unused]] __device__ __forceinline__ float lg2_approx(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ float rcp_approx(float x) {
+[[maybe_unused]] __device__ __forceinline__ float rcp_approx(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
@@ -95,7 +95,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // offset 4 (b >> 1)) that intersect it, with a relative 1% + 1 px safety margin so
 // that a skipped pixel can never pass the alpha test (the result is identical to
 // evaluating every pixel; the oracle parity tests check it).
-__device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, float B, float C, float o, int ox,
+[[maybe_unused]] __device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, float B, float C, float o, int ox,
                                                int oy) {
   const float L = __logf(255.f * o);
   if (!(L >= -1e-3f)) return 0u;  // o < 1/255: alpha can never reach 1/255
@@ -145,7 +145,7 @@ __device__ __forceinline__ uint32_t block_mask(float mx, float my, float A, floa
 // (x_right(y) is concave, so off its peak it is monotone on the slab); xl likewise.
 // Five edge-line chords (one sqrt each) serve the four block rows: ~1/2 the
 // instructions of block_mask's per-block edge minimisation.
-__device__ __forceinline__ uint32_t block_mask_rows(float mx, float my, float A, float B, float C, float o, int ox,
+[[maybe_unused]] __device__ __forceinline__ uint32_t block_mask_rows(float mx, float my, float A, float B, float C, float o, int ox,
                                                     int oy) {
   const float L = __logf(255.f * o);
   if (!(L >= -1e-3f)) return 0u;  // o < 1/255: alpha can never reach 1/255
