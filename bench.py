@@ -435,8 +435,13 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # GSR_FORCE_DIST=1: run the N > 1 exchange + optimiser path even at world size 1 (a
+    # functional check of that path on a single GPU; the sums then have one term)
+    dist_on = world > 1 or os.environ.get("GSR_FORCE_DIST") == "1"
+    if dist_on:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     lib = gsr.load()
 
     w = scenegen.make(args.config, args.seed)
@@ -463,13 +468,13 @@ def main():
     # (PAPER.md:149), cycling through the poses; N > 1 runs independent replicas.
     batched = args.config in ("scannetpp", "large")
     allreduce = None
-    if world > 1 and batched:
+    if dist_on and batched:
         allreduce = lambda g: dist.all_reduce(g, op=dist.ReduceOp.SUM)  # noqa: E731
 
     def step_views(i):
         return my_views if batched else [my_views[i % len(my_views)]]
-    optimizer, optim_used = None, ("replicated" if world > 1 and batched else "local")
-    if world > 1 and batched and args.optim == "peer":
+    optimizer, optim_used = None, ("replicated" if dist_on and batched else "local")
+    if dist_on and batched and args.optim == "peer":
         try:
             optimizer, optim_used = pipeline.PeerShardedAdam(lib, model), "peer"
         except Exception as ex:  # noqa: BLE001  (no symmetric memory / P2P: NCCL path)
@@ -482,7 +487,7 @@ def main():
             model.params = model.params.clone()
             model.grad = model.grad.clone()
             optimizer, optim_used = None, "sharded (peer unavailable on another rank)"
-    if world > 1 and batched and optimizer is None and args.optim in ("peer", "sharded"):
+    if dist_on and batched and optimizer is None and args.optim in ("peer", "sharded"):
         optimizer = pipeline.ShardedAdam(lib, model)
         optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
     if optimizer is not None:
@@ -495,7 +500,7 @@ def main():
     for i in range(args.warmup):
         tr.step(step_views(i))
     torch.cuda.synchronize()
-    if world > 1 and not pipeline.params_agree_across_ranks(model):
+    if dist_on and not pipeline.params_agree_across_ranks(model):
         if optim_used != "peer":
             raise RuntimeError(f"parameters differ across ranks after warm-up (optimiser: {optim_used})")
         # the peer-memory path misbehaved on this machine: resynchronise from rank 0
@@ -682,7 +687,7 @@ def main():
                          "records read from global memory, 10 atomicAdd per composited pair"}
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return
 
@@ -733,7 +738,7 @@ def main():
         "scaling": "strong" if batched else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
-                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if world > 1 else "")) if batched else f"replicas x{world}",
+                   "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if dist_on else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "launch": "CUDA graph per iteration" if use_graph else "eager",
@@ -750,7 +755,7 @@ def main():
         "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive, "eager": eager,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
