@@ -241,6 +241,21 @@ gs_status gs_naive_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_sce
                                      const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
                                      float* sgrad, void* stream);
 
+/* gs_render_bwd_screen with the harness loss of Eq. 12 fused in: the upstream gradient
+ * of every pixel is computed inside the backward from the rendered rgb / depth (as
+ * written by gs_render_fwd) and the target images, with exactly the values
+ * gs_l1_loss_grad writes (sign(residual) / (3 npix) per colour channel, w_depth
+ * sign / npix for depth, sign(0) = 0), and the loss (nullable DEVICE float) += L.
+ * One kernel instead of gs_l1_loss_grad + gs_render_bwd_screen; no dL/d-image buffers.
+ * P == 0 is valid (background-only images; the loss is still accumulated). */
+gs_status gs_render_bwd_screen_l1(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
+                                  const int32_t* sorted_ids, const int32_t* tile_ranges,
+                                  const int32_t* tile_order /*nullable*/, const float* T_final,
+                                  const int32_t* n_contrib, const float* rgb, const float* depth,
+                                  const float* target_rgb, const float* target_depth, float w_depth,
+                                  float* loss /*nullable*/, const uint8_t* key_blocks /*nullable*/, float* sgrad,
+                                  void* stream);
+
 /* ---------------------------------------------------------------- gs_adam_step
  * Dense bias-corrected Adam over all F x P scalars of the live Gaussians [0, P) (R20;
  * columns P..P_stride-1, the room a growing map has left, are not touched):

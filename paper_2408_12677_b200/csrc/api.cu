@@ -259,6 +259,25 @@ gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_p
   return check_launch("gs_render_bwd_screen");
 }
 
+gs_status gs_render_bwd_screen_l1(const gs_camera* cam, const gs_scene* scene, gs_proj proj,
+                                  const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
+                                  const float* T_final, const int32_t* n_contrib, const float* rgb, const float* depth,
+                                  const float* target_rgb, const float* target_depth, float w_depth, float* loss,
+                                  const uint8_t* key_blocks, float* sgrad, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_camera(cam, "gs_render_bwd_screen_l1"));
+  GS_TRY(check_scene(scene, "gs_render_bwd_screen_l1"));
+  GS_TRY(check_ptrs("gs_render_bwd_screen_l1", {{tile_ranges, "tile_ranges"}, {T_final, "T_final"},
+                                                {n_contrib, "n_contrib"}, {rgb, "rgb"}, {depth, "depth"},
+                                                {target_rgb, "target_rgb"}, {target_depth, "target_depth"},
+                                                {sgrad, "sgrad"}}));
+  if (scene->P > 0) GS_TRY(check_ptrs("gs_render_bwd_screen_l1", {{proj.rec, "proj.rec"}}));
+  const L1Targets l1{rgb, depth, target_rgb, target_depth, w_depth, loss};
+  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, nullptr,
+                    nullptr, key_blocks, sgrad, static_cast<cudaStream_t>(stream), &l1);
+  return check_launch("gs_render_bwd_screen_l1");
+}
+
 gs_status gs_tile_order(const gs_camera* cam, const int32_t* tile_ranges, int32_t* tile_order, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_tile_order"));

@@ -71,9 +71,16 @@ void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, 
                        const int32_t* order, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                        uint8_t* key_blocks, cudaStream_t s);
+// Fused Eq. 12 upstream for the backward (gs_render_bwd_screen_l1): rendered and target
+// images, the depth weight and the loss accumulator.
+struct L1Targets {
+  const float *rgb, *depth, *target_rgb, *target_depth;
+  float w_depth;
+  float* loss;
+};
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
                        const int32_t* order, const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s);
+                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Targets* l1 = nullptr);
 // naive.cu (K13 comparison baseline, not the product path)
 void launch_naive_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
                       float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended, cudaStream_t s);

@@ -240,6 +240,37 @@ __device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, fl
   slot = (gi < 3 && s < 10 && !(lane & 1)) ? s : -1;
 }
 
+
+// Upstream gradient of one pixel: dL/drgb, dL/ddepth read from the caller's buffers, or,
+// with the fused Eq. 12 loss (gs_render_bwd_screen_l1), computed here from the rendered
+// and target images exactly as gs_l1_loss_grad does (sign(residual) x 1/(3 npix), x
+// w_depth/npix for depth, sign(0) = 0), the pixel's loss terms added to `lsum`.
+struct L1Fuse {
+  const float *rgb, *depth, *trgb, *tdep;
+  float sc, sd;
+  float* loss;
+};
+__device__ __forceinline__ float l1_sign(float r, float s) { return r > 0.f ? s : (r < 0.f ? -s : 0.f); }
+__device__ __forceinline__ void upstream(const L1Fuse& l1, const float* __restrict__ g_rgb,
+                                         const float* __restrict__ g_dep, int64_t npix, int64_t p, float& gr,
+                                         float& gg, float& gb, float& gd, float& lsum) {
+  if (l1.trgb) {
+    const float r0 = l1.rgb[p] - l1.trgb[p], r1 = l1.rgb[npix + p] - l1.trgb[npix + p];
+    const float r2 = l1.rgb[2 * npix + p] - l1.trgb[2 * npix + p], rd = l1.depth[p] - l1.tdep[p];
+    gr = l1_sign(r0, l1.sc), gg = l1_sign(r1, l1.sc), gb = l1_sign(r2, l1.sc), gd = l1_sign(rd, l1.sd);
+    lsum += fabsf(r0) * l1.sc + fabsf(r1) * l1.sc + fabsf(r2) * l1.sc + fabsf(rd) * l1.sd;
+  } else {
+    gr = g_rgb[p], gg = g_rgb[npix + p], gb = g_rgb[2 * npix + p];
+    gd = g_dep ? g_dep[p] : 0.f;
+  }
+}
+__device__ __forceinline__ void l1_commit(const L1Fuse& l1, float lsum, int lane) {
+  if (l1.loss) {
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+    if (lane == 0 && lsum != 0.f) atomicAdd(l1.loss, lsum);
+  }
+}
+
 #ifndef GSR_EXACT_EXP
 // ===========================================================================
 // Fast path (libgsr.so)
@@ -565,7 +596,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
                                                                    const uint8_t* __restrict__ key_blocks,
-                                                                   float* __restrict__ sgrad) {
+                                                                   float* __restrict__ sgrad, L1Fuse l1) {
   __shared__ float4 s_rec[WPC][2][32][3];
   __shared__ int s_gid[WPC][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -582,6 +613,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
   BwdPix px;
   int bmaxn[kPix];  // per 8x4 block: max n_contrib over its 32 pixels (warp-uniform)
   int maxn = 0;
+  float lsum = 0.f;
 #pragma unroll
   for (int b = 0; b < kPix; ++b) {
     const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
@@ -589,10 +621,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       const int64_t p = (int64_t)y * cam.W + x;
       px.T[b] = T_final[p];
       px.n[b] = n_contrib[p];
-      px.gr[b] = g_rgb[p];
-      px.gg[b] = g_rgb[npix + p];
-      px.gb[b] = g_rgb[2 * npix + p];
-      px.gd[b] = g_dep ? g_dep[p] : 0.f;
+      upstream(l1, g_rgb, g_dep, npix, p, px.gr[b], px.gg[b], px.gb[b], px.gd[b], lsum);
     } else {
       px.T[b] = 1.f, px.n[b] = 0, px.gr[b] = px.gg[b] = px.gb[b] = px.gd[b] = 0.f;
     }
@@ -600,6 +629,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
     bmaxn[b] = __reduce_max_sync(kFull, px.n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
+  l1_commit(l1, lsum, lane);
   // double-buffered staging (back to front): ids + key masks two batches ahead,
   // records one ahead.  With the forward's key masks, keys that composited nothing
   // in this tile are neither gathered nor visited.
@@ -855,7 +885,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
                                                                    const uint8_t* __restrict__ key_blocks,
-                                                                   float* __restrict__ sgrad) {
+                                                                   float* __restrict__ sgrad, L1Fuse l1) {
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   __shared__ int s_gid[kWarpsPerCta][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -873,6 +903,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   int n[kPix];
   int bmaxn[kPix];
   int maxn = 0;
+  float lsum = 0.f;
 #pragma unroll
   for (int b = 0; b < kPix; ++b) {
     const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
@@ -880,10 +911,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
       const int64_t p = (int64_t)y * cam.W + x;
       T[b] = T_final[p];
       n[b] = n_contrib[p];
-      gr[b] = g_rgb[p];
-      gg[b] = g_rgb[npix + p];
-      gb[b] = g_rgb[2 * npix + p];
-      gd[b] = g_dep ? g_dep[p] : 0.f;
+      upstream(l1, g_rgb, g_dep, npix, p, gr[b], gg[b], gb[b], gd[b], lsum);
     } else {
       T[b] = 1.f, n[b] = 0, gr[b] = gg[b] = gb[b] = gd[b] = 0.f;
     }
@@ -891,6 +919,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
     bmaxn[b] = __reduce_max_sync(kFull, n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
+  l1_commit(l1, lsum, lane);
   int hi = rg.x + maxn;
   auto load_key = [&](int h, int& id, uint32_t& kb) {
     id = -1, kb = 0;
@@ -1029,10 +1058,10 @@ void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, con
 template <int WPC>
 void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                    const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
+                    const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1) {
   k_render_bwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-      g_rgb, g_depth, key_blocks, sgrad);
+      g_rgb, g_depth, key_blocks, sgrad, l1);
 }
 #endif
 
@@ -1057,17 +1086,25 @@ void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, 
 
 void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                        const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s) {
+                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Targets* l1t) {
+  L1Fuse l1{};
+  if (l1t) {
+    const int64_t npix = (int64_t)cam.W * cam.H;
+    l1.rgb = l1t->rgb, l1.depth = l1t->depth, l1.trgb = l1t->target_rgb, l1.tdep = l1t->target_depth;
+    l1.sc = (float)(1.0 / (3.0 * (double)npix));  // as launch_l1
+    l1.sd = (float)((double)l1t->w_depth / (double)npix);
+    l1.loss = l1t->loss;
+  }
 #ifndef GSR_EXACT_EXP
   switch (render_wpc()) {
-    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
-    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s); break;
-    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s);
+    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1); break;
+    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1); break;
+    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1);
   }
 #else
   k_render_bwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-      g_rgb, g_depth, key_blocks, sgrad);
+      g_rgb, g_depth, key_blocks, sgrad, l1);
 #endif
   count_launch();
 }

@@ -117,6 +117,8 @@ class Library:
         lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
         lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_tile_order.argtypes = [vp, vp, vp, vp]
+        lib.gs_render_bwd_screen_l1.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_float, vp,
+                                                vp, vp, vp]
         lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
@@ -137,9 +139,9 @@ class Library:
         lib.gs_quadtree.argtypes = [C.c_int32, C.c_int32, vp, C.c_float, C.c_int32, vp, C.c_size_t, vp, i64, vp, vp]
         lib.gs_seed_gaussians.argtypes = [vp, vp, GsTsdfVolume, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
-        for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",
+        for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",  # noqa: E501
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
                    "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians"):
             getattr(lib, fn).restype = i32
         self.lib = lib
@@ -215,6 +217,13 @@ class Library:
         return self._check("gs_naive_render_bwd_screen", self.lib.gs_naive_render_bwd_screen(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
             _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _stream(stream)))
+
+    def render_bwd_screen_l1(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, rgb, depth, t_rgb,
+                             t_depth, w_depth, sgrad, loss=None, key_blocks=None, stream=None, tile_order=None):
+        return self._check("gs_render_bwd_screen_l1", self.lib.gs_render_bwd_screen_l1(
+            C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(T_final),
+            _ptr(n_contrib), _ptr(rgb), _ptr(depth), _ptr(t_rgb), _ptr(t_depth), float(w_depth), _ptr(loss),
+            _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
 
     def project_bwd_views(self, cams, sc, params, flags, sgrads, grad, accumulate=True, stream=None):
         """cams: list of GsCamera; flags / sgrads: lists of device tensors (one per view)."""

@@ -167,6 +167,9 @@ class Trainer:
         self.serial = False
         # device_step = True: Adam reads / advances model.step_dev (graph capture)
         self.device_step = False
+        # fuse_l1: the L1 upstream (Eq. 12) computed inside the backward kernel
+        # (gs_render_bwd_screen_l1) instead of a gs_l1_loss_grad pass; GSR_FUSE_L1=0 for A/B
+        self.fuse_l1 = os.environ.get("GSR_FUSE_L1", "1") != "0"
         # render tiles longest-list-first (gs_tile_order): 7% faster render kernels when
         # one view is in flight; with several views in flight the other streams already
         # fill each kernel's tail and the extra launch cost 2% (B200, scannetpp), so the
@@ -203,13 +206,20 @@ class Trainer:
         self._hook("render_fwd", "end")
         if targets_ready is not None:
             torch.cuda.current_stream().wait_event(targets_ready)
-        lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
-        if targets_consumed is not None:
-            targets_consumed.record()
+        if self.naive or not self.fuse_l1:
+            lib.l1_loss_grad(b.rgb, b.depth, t_rgb, t_depth, self.w_depth, b.g_rgb, b.g_depth, loss=self.loss)
+            if targets_consumed is not None:
+                targets_consumed.record()
         self._hook("render_bwd", "begin")
         if self.naive:
             lib.naive_render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
                                         self.sgrad[slot])
+        elif self.fuse_l1:  # Eq. 12's upstream computed inside the backward (one kernel)
+            lib.render_bwd_screen_l1(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.rgb, b.depth, t_rgb,
+                                     t_depth, self.w_depth, self.sgrad[slot], loss=self.loss, key_blocks=b.key_blocks,
+                                     tile_order=order)
+            if targets_consumed is not None:
+                targets_consumed.record()
         else:
             lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
                                   self.sgrad[slot], key_blocks=b.key_blocks, tile_order=order)

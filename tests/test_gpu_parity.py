@@ -756,3 +756,32 @@ def test_bench_launch_configuration_full_size_sampled(lib):
         assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
         K_ref = int(gsref.project(cam, scene, gsref.F32)["tiles"].sum())
         assert int(tr.num_keys[v].item()) == K_ref
+
+
+def test_fused_l1_backward_matches_separate(lib):
+    """gs_render_bwd_screen_l1 (Eq. 12 upstream inside the backward) gives the same
+    screen-space gradients and loss as gs_l1_loss_grad + gs_render_bwd_screen."""
+    w = workload("small")
+    cam, scene = w.cameras[0], w.scene
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+    tw = scenegen.make("small").target_scene
+    tproj, _, _ = gpu_project(lib, cam, tw)
+    tb = gpu_bin(lib, cam, tw, tproj)
+    tgt = gpu_render(lib, cam, tw, tproj, tb["sorted_ids"], tb["ranges"])
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    gcam = gsr.camera(cam)
+    g_rgb, g_d = torch.empty_like(out["rgb"]), torch.empty_like(out["depth"])
+    loss_a, loss_b = torch.zeros(1, device=DEV), torch.zeros(1, device=DEV)
+    lib.l1_loss_grad(out["rgb"], out["depth"], tgt["rgb"], tgt["depth"], 0.7, g_rgb, g_d, loss_a)
+    sa = torch.zeros((scene.P, 12), device=DEV)
+    lib.render_bwd_screen(gcam, sc, proj, b["sorted_ids"], b["ranges"], out["T_final"], out["n_contrib"], g_rgb, g_d, sa)
+    sb = torch.zeros((scene.P, 12), device=DEV)
+    lib.render_bwd_screen_l1(gcam, sc, proj, b["sorted_ids"], b["ranges"], out["T_final"], out["n_contrib"],
+                             out["rgb"], out["depth"], tgt["rgb"], tgt["depth"], 0.7, sb, loss=loss_b)
+    torch.cuda.synchronize()
+    assert loss_b.item() == pytest.approx(loss_a.item(), rel=1e-5)
+    a, c = sa.cpu().numpy().astype(np.float64), sb.cpu().numpy().astype(np.float64)
+    assert np.abs(a).max() > 0
+    assert grad_mismatch(c, a, rtol=1e-5, atol=1e-9).mean() <= 1e-4
