@@ -409,6 +409,9 @@ gs_status gs_tsdf_integrate(const gs_tsdf_params* prm /*HOST*/, gs_tsdf_volume v
  *   that order).  rgb: float[3][H][W] in [0, 1] DEVICE.  leaves: int32[leaf_capacity][4]
  *   (x, y, w, h) DEVICE, in depth-first NW, NE, SW, SE order; num_leaves: DEVICE int64
  *   (the full count even if it exceeds the capacity).  ws: gs_quadtree_workspace bytes.
+ *   A leaf side is at least ceil((min_cell + 1) / 2) pixels, so (W / s + 1)(H / s + 1)
+ *   leaves with that s always fit; gs_seed_gaussians reads num_leaves leaves, so size
+ *   the buffer for that bound.
  * gs_seed_gaussians: for every leaf in order, the centre pixel u = (x + w/2, y + h/2)
  *   with depth d > 0 is back-projected, p_q = T_WC pi^-1(u, d) (Eq. 10); if the voxel
  *   containing p_q (TSDF grid of the same frame, fused BEFORE seeding) has weight

@@ -594,7 +594,11 @@ class Seeder:
         self.lib, self.W, self.H = lib, int(width), int(height)
         self.threshold, self.min_cell = float(threshold), int(min_cell)
         self.ws = torch.empty(lib.quadtree_workspace(self.W, self.H, self.min_cell), dtype=torch.uint8, device=device)
-        cap = (self.W // self.min_cell + 1) * (self.H // self.min_cell + 1) + 16
+        # worst case: a cell splits only while both sides exceed min_cell, so a leaf side
+        # is at least ceil((min_cell + 1) / 2) pixels (gs_seed_gaussians reads every leaf
+        # gs_quadtree counted, so the buffer must hold them all)
+        side = (self.min_cell + 2) // 2
+        cap = (self.W // side + 1) * (self.H // side + 1) + 16
         self.leaves = torch.empty((cap, 4), dtype=torch.int32, device=device)
         self.num_leaves = torch.zeros(1, dtype=torch.int64, device=device)
         self.num_new = torch.zeros(1, dtype=torch.int64, device=device)
