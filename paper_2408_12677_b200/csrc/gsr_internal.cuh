@@ -46,6 +46,16 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid) {
   return peers;
 }
 
+// One Adam update of a scalar (R20), in a fixed fp32 operation order shared by every
+// kernel that applies it (k_adam, k_adam_dev, k_adam_peers), so the single-rank,
+// graph and multi-GPU paths give bit-identical parameters.
+__device__ __forceinline__ void adam_update(float& p, float& m, float& v, float g, float b1, float b2, float c1,
+                                            float c2, float step, float rs_bc2, float eps) {
+  m = __fmaf_rn(b1, m, __fmul_rn(c1, g));
+  v = __fmaf_rn(b2, v, __fmul_rn(__fmul_rn(c2, g), g));
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(step, m), __fmaf_rn(__fsqrt_rn(v), rs_bc2, eps)));
+}
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

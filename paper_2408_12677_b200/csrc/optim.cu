@@ -25,12 +25,10 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
     const float step = lr.step[i / S4];
     const float4 gg = g[i - b4];
     float4 mm = m[i], vv = v[i], pp = p[i];
-#define ADAM_LANE(c)                                              \
-  mm.c = b1 * mm.c + c1 * gg.c;                                  \
-  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
-  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
-    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
-#undef ADAM_LANE
+    adam_update(pp.x, mm.x, vv.x, gg.x, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.y, mm.y, vv.y, gg.y, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.z, mm.z, vv.z, gg.z, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.w, mm.w, vv.w, gg.w, b1, b2, c1, c2, step, rs_bc2, eps);
     p[i] = pp;
     m[i] = mm;
     v[i] = vv;
@@ -63,12 +61,10 @@ __global__ void __launch_bounds__(256) k_adam_dev(float4* __restrict__ p, float4
     const float step = s_step[i / S4];
     const float4 gg = g[i];
     float4 mm = m[i], vv = v[i], pp = p[i];
-#define ADAM_LANE(c)                                              \
-  mm.c = b1 * mm.c + c1 * gg.c;                                  \
-  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
-  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
-    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
-#undef ADAM_LANE
+    adam_update(pp.x, mm.x, vv.x, gg.x, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.y, mm.y, vv.y, gg.y, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.z, mm.z, vv.z, gg.z, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.w, mm.w, vv.w, gg.w, b1, b2, c1, c2, step, rs_bc2, eps);
     p[i] = pp;
     m[i] = mm;
     v[i] = vv;
@@ -104,12 +100,10 @@ __global__ void __launch_bounds__(256) k_adam_peers(const __grid_constant__ Peer
     for (int r = 1; r < kMaxPeers; ++r)
       if (r < pr.world) gg.x += gs[r].x, gg.y += gs[r].y, gg.z += gs[r].z, gg.w += gs[r].w;
     float4 mm = m[i], vv = v[i], pp = pr.param[pr.rank][i];
-#define ADAM_LANE(c)                                              \
-  mm.c = b1 * mm.c + c1 * gg.c;                                  \
-  vv.c = b2 * vv.c + c2 * gg.c * gg.c;                           \
-  pp.c -= step * mm.c / (sqrtf(vv.c) * rs_bc2 + eps);
-    ADAM_LANE(x) ADAM_LANE(y) ADAM_LANE(z) ADAM_LANE(w)
-#undef ADAM_LANE
+    adam_update(pp.x, mm.x, vv.x, gg.x, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.y, mm.y, vv.y, gg.y, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.z, mm.z, vv.z, gg.z, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.w, mm.w, vv.w, gg.w, b1, b2, c1, c2, step, rs_bc2, eps);
     m[i] = mm;
     v[i] = vv;
 #pragma unroll
