@@ -236,36 +236,42 @@ class Trainer:
     def step_host(self, views, host_targets):
         """One iteration with the targets streamed from (pinned) host memory:
         host_targets {v: (rgb [3][H][W], depth [H][W])} CPU tensors.  View k's targets
-        are copied on a side stream into one of two device slots while view k-1 is
-        being rendered, and gs_l1_loss_grad of view k waits for its copy only; the
-        copy into a slot waits until the loss that last read it has run."""
+        are copied on a side stream into device slot k % n (n = 2 x the views in flight,
+        so every in-flight view has its slot and the next ones are already loading);
+        the loss of view k waits for its copy only, and the copy into a slot waits until
+        the loss that last read it has run.  The host enqueues ahead of the GPU, so the
+        next iteration's first copies overlap this one's tail."""
         dev = self.device
+        n_slots = max(2, 2 * len(self.bufs))
         if getattr(self, "_slots", None) is None:
             r0, d0 = host_targets[views[0]]
             self._slots = [(torch.empty(r0.shape, dtype=torch.float32, device=dev),
-                            torch.empty(d0.shape, dtype=torch.float32, device=dev)) for _ in range(2)]
-            self._copy_stream = torch.cuda.Stream(device=dev)
-            self._ready = [torch.cuda.Event() for _ in range(2)]
-            self._free = [torch.cuda.Event() for _ in range(2)]
+                            torch.empty(d0.shape, dtype=torch.float32, device=dev)) for _ in range(n_slots)]
+            n_cs = int(os.environ.get("GSR_COPY_STREAMS", "1"))  # 2-3 measured no faster
+            self._copy_streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, n_cs))]
+            self._ready = [torch.cuda.Event() for _ in range(n_slots)]
+            self._free = [torch.cuda.Event() for _ in range(n_slots)]
+        n_slots = len(self._slots)
 
         def issue(k):
-            s = k % 2
-            with torch.cuda.stream(self._copy_stream):
-                self._copy_stream.wait_event(self._free[s])
+            s = k % n_slots
+            cs = self._copy_streams[k % len(self._copy_streams)]  # copies alternate DMA queues
+            with torch.cuda.stream(cs):
+                cs.wait_event(self._free[s])
                 r, d = host_targets[views[k]]
                 self._slots[s][0].copy_(r, non_blocking=True)
                 self._slots[s][1].copy_(d, non_blocking=True)
-                self._ready[s].record(self._copy_stream)
+                self._ready[s].record(cs)
 
         def targets(k, v):
-            s = k % 2
+            s = k % n_slots
             return self._slots[s][0], self._slots[s][1], self._ready[s], self._free[s]
 
         def after_view(k):
-            if k + 2 < len(views):
-                issue(k + 2)
+            if k + n_slots < len(views):
+                issue(k + n_slots)
 
-        for k in range(min(2, len(views))):
+        for k in range(min(n_slots, len(views))):
             issue(k)
         self._run(views, targets, after_view)
 
