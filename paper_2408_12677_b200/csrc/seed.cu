@@ -23,9 +23,11 @@
 #include <vector>
 
 #include "gsr_internal.cuh"
+#include "tsdf_hash.cuh"
 
 namespace gsr {
 namespace {
+using namespace tsdfhash;
 
 #define QM(a, b) __fmul_rn((a), (b))
 #define QA(a, b) __fadd_rn((a), (b))
@@ -154,34 +156,6 @@ __global__ void __launch_bounds__(1024) k_qt_emit(QtGeom g, const uint8_t* const
 }
 
 // ---------------------------------------------------------------- seeding
-__device__ __forceinline__ uint64_t spread3s(uint32_t x) {
-  uint64_t v = x & 0x1fffffu;
-  v = (v | (v << 32)) & 0x1f00000000ffffull;
-  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
-  v = (v | (v << 8)) & 0x100f00f00f00f00full;
-  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v << 2)) & 0x1249249249249249ull;
-  return v;
-}
-__device__ __forceinline__ uint64_t mix64s(uint64_t x) {
-  x ^= x >> 33;
-  x *= 0xff51afd7ed558ccdull;
-  x ^= x >> 33;
-  x *= 0xc4ceb9fe1a85ec53ull;
-  return x ^ (x >> 33);
-}
-// pool index of a block key, -1 if not allocated
-__device__ __forceinline__ int64_t find_block(const gs_tsdf_volume& vol, uint64_t key) {
-  const uint64_t mask = (uint64_t)vol.table_cap - 1;
-  uint64_t h = mix64s(key) & mask;
-  for (int64_t probe = 0; probe < vol.table_cap; ++probe, h = (h + 1) & mask) {
-    const uint64_t k = vol.keys[h];
-    if (k == key) return vol.slots[h];
-    if (k == GS_TSDF_EMPTY_KEY) return -1;
-  }
-  return -1;
-}
-
 struct SeedCtx {
   float vs, inv_vs;
   int org[3];
@@ -228,8 +202,8 @@ __global__ void __launch_bounds__(1024) k_seed(SeedCtx sc, gs_tsdf_volume vol, D
           vox[a] = ok ? (int)vv : 0;
         }
         if (ok) {
-          const uint64_t key = spread3s((uint32_t)(vox[0] >> 3)) | (spread3s((uint32_t)(vox[1] >> 3)) << 1) |
-                               (spread3s((uint32_t)(vox[2] >> 3)) << 2);
+          const uint64_t key = spread3((uint32_t)(vox[0] >> 3)) | (spread3((uint32_t)(vox[1] >> 3)) << 1) |
+                               (spread3((uint32_t)(vox[2] >> 3)) << 2);
           const int64_t blk = find_block(vol, key);
           if (blk >= 0 && blk < vol.block_cap) {
             const int loc = (vox[0] & 7) + 8 * (vox[1] & 7) + 64 * (vox[2] & 7);

@@ -17,9 +17,11 @@
 // projection does, reading R9) so that block sets, tsdf and weights are bit-identical
 // to the CPU oracle (oracle/tsdf_ref.cpp).
 #include "gsr_internal.cuh"
+#include "tsdf_hash.cuh"
 
 namespace gsr {
 namespace {
+using namespace tsdfhash;
 
 #define TM(a, b) __fmul_rn((a), (b))
 #define TA(a, b) __fadd_rn((a), (b))
@@ -29,63 +31,10 @@ namespace {
 constexpr int kVoxBits = 21;  // per axis in the 63-bit Morton code
 constexpr int kIntThreads = 128;
 
-__device__ __forceinline__ uint64_t spread3(uint32_t x) {  // 21 bits -> every third bit
-  uint64_t v = x & 0x1fffffu;
-  v = (v | (v << 32)) & 0x1f00000000ffffull;
-  v = (v | (v << 16)) & 0x1f0000ff0000ffull;
-  v = (v | (v << 8)) & 0x100f00f00f00f00full;
-  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v << 2)) & 0x1249249249249249ull;
-  return v;
-}
-__device__ __forceinline__ uint32_t compact3(uint64_t v) {
-  v &= 0x1249249249249249ull;
-  v = (v | (v >> 2)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v >> 4)) & 0x100f00f00f00f00full;
-  v = (v | (v >> 8)) & 0x1f0000ff0000ffull;
-  v = (v | (v >> 16)) & 0x1f00000000ffffull;
-  v = (v | (v >> 32)) & 0x1fffffull;
-  return (uint32_t)v;
-}
-__device__ __forceinline__ uint64_t morton3(uint32_t x, uint32_t y, uint32_t z) {
-  return spread3(x) | (spread3(y) << 1) | (spread3(z) << 2);
-}
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x ^= x >> 33;
-  x *= 0xff51afd7ed558ccdull;
-  x ^= x >> 33;
-  x *= 0xc4ceb9fe1a85ec53ull;
-  return x ^ (x >> 33);
-}
-
 struct TsdfDev {
   float vs, inv_vs, eps, wmax, step;
   int org[3];
 };
-
-// Insert a block key; returns 1 if this call created the block.
-__device__ __forceinline__ int insert_block(const gs_tsdf_volume& vol, uint64_t key) {
-  const uint64_t mask = (uint64_t)vol.table_cap - 1;
-  uint64_t h = mix64(key) & mask;
-  for (int64_t probe = 0; probe < vol.table_cap; ++probe, h = (h + 1) & mask) {
-    uint64_t k = vol.keys[h];
-    if (k == key) return 0;
-    if (k == GS_TSDF_EMPTY_KEY) {
-      k = atomicCAS(reinterpret_cast<unsigned long long*>(vol.keys + h), (unsigned long long)GS_TSDF_EMPTY_KEY,
-                    (unsigned long long)key);
-      if (k == GS_TSDF_EMPTY_KEY) {
-        const long long idx = atomicAdd(reinterpret_cast<unsigned long long*>(vol.num_blocks), 1ull);
-        vol.slots[h] = (int32_t)(idx < (long long)INT32_MAX ? idx : (long long)INT32_MAX);
-        if (idx < vol.block_cap) vol.pool_keys[idx] = key;
-        return 1;
-      }
-      if (k == key) return 0;
-    }
-  }
-  // table full: poison the block counter so that the overflow is visible (> block_cap)
-  atomicAdd(reinterpret_cast<unsigned long long*>(vol.num_blocks), (unsigned long long)vol.block_cap + 1ull);
-  return 0;
-}
 
 // Two phases per ray so that the warp stays converged: the sample loop only records the
 // distinct blocks its samples fall in (consecutive samples mostly share a block; a
