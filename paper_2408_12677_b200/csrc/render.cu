@@ -55,6 +55,9 @@ namespace {
 #endif
 [[maybe_unused]] constexpr int kFwdMinWarps = GSR_FWD_MINW, kBwdMinWarps = GSR_BWD_MINW;
 [[maybe_unused]] constexpr int kPix = 8;             // pixels per lane
+#ifndef GSR_BWD_PAIR
+#define GSR_BWD_PAIR 1
+#endif
 #ifndef GSR_DENSE_FWD
 #define GSR_DENSE_FWD 3
 #endif
@@ -240,6 +243,49 @@ __device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, fl
   slot = (gi < 3 && s < 10 && !(lane & 1)) ? s : -1;
 }
 
+// Two keys' 10-component reductions in one transpose (GSR_BWD_PAIR): the first stage
+// (xor 16) of each key alone -- 5 shuffles, leaving components k (lanes with bit 4
+// clear) or k + 5 (set) -- then both keys' 5 + 5 halves together (xor 8, 4, 2, 1: 11
+// shuffles), 21 in all instead of 26, and one RED instruction for both keys' 20 values.
+__device__ __forceinline__ void reduce_half10(const float (&v)[10], int lane, float (&h)[5]) {
+  const bool b4 = lane & 16;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const float send = b4 ? v[k] : v[k + 5], keep = b4 ? v[k + 5] : v[k];
+    h[k] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+}
+// Keys a (gid ga) and b (gid gb; gb < 0: none) reduced to their warp totals and added to
+// the screen gradients: 20 lanes, component (bit 4 ? 5 : 0) + d of key (bit 3 ? b : a).
+__device__ __forceinline__ void reduce_pair_commit(const float (&a)[5], const float (&b)[5], int ga, int gb, int lane,
+                                                   float* __restrict__ sgrad) {
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
+  float d[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const float send = b3 ? a[k] : b[k], keep = b3 ? b[k] : a[k];
+    d[k] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  float e[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float lo = d[k], hi = (k + 3 < 5) ? d[k + 3] : 0.f;
+    const float send = b2 ? lo : hi, keep = b2 ? hi : lo;
+    e[k] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  float f[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float lo = e[k], hi = (k + 2 < 3) ? e[k + 2] : 0.f;
+    const float send = b1 ? lo : hi, keep = b1 ? hi : lo;
+    f[k] = keep + __shfl_xor_sync(kFull, send, 2);
+  }
+  const float send = b0 ? f[0] : f[1], keep = b0 ? f[1] : f[0];
+  const float out = keep + __shfl_xor_sync(kFull, send, 1);
+  const int ei = (b1 ? 2 : 0) + (b0 ? 1 : 0), di = (b2 ? 3 : 0) + ei;
+  const int g = b3 ? gb : ga;
+  if (ei < 3 && di < 5 && g >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * g + ((lane & 16) ? 5 : 0) + di, out);
+}
 
 // Upstream gradient of one pixel: dL/drgb, dL/ddepth read from the caller's buffers, or,
 // with the fused Eq. 12 loss (gs_render_bwd_screen_l1), computed here from the rendered
@@ -650,6 +696,10 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       gather_rec_async(rec, id, s_rec[warp][b][lane]);
     }
   };
+#if GSR_BWD_PAIR
+  float h_p[5];  // first stage of the pending key's reduction (gid_p >= 0)
+  int gid_p = -1;
+#endif
   int id1;
   uint32_t kb_cur, kb1;
   load_key(hi, id1, kb_cur);
@@ -726,16 +776,36 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
         v[7] = a.g;
         v[8] = a.b;
         v[9] = a.z;
+#if GSR_BWD_PAIR
+        float h[5];
+        reduce_half10(v, lane, h);
+        const int gid = s_gid[warp][buf][j];
+        if (gid_p >= 0) {
+          reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
+          gid_p = -1;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 5; ++k) h_p[k] = h[k];
+          gid_p = gid;
+        }
+#else
         float out;
         int slot;
         warp_reduce10(v, lane, out, slot);
         if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
+#endif
       }
     }
     __syncwarp();
     kb_cur = kb1, id1 = id2, kb1 = kb2;
   }
   cp_async_wait<0>();
+#if GSR_BWD_PAIR
+  if (gid_p >= 0) {
+    const float z[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    reduce_pair_commit(h_p, z, gid_p, -1, lane, sgrad);
+  }
+#endif
 }
 
 #else  // GSR_EXACT_EXP

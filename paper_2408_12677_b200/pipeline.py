@@ -144,6 +144,7 @@ class Trainer:
         n_streams = max(1, int(streams))
         self.bufs = [ViewBuffers(lib, cameras[0], cap_p, key_capacity, device) for _ in range(n_streams)]
         self.buf = self.bufs[0]
+        # (equal priorities: staggering the streams' priorities measured 4% slower)
         self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
         P = max(cap_p, 1)
         # per in-flight view: projection flags and screen-space gradients (zeroed once;
