@@ -397,6 +397,21 @@ def upstream_fields(seed: int, width: int, height: int, kind: str = "normal"):
     return g_rgb.astype(np.float32), g_d.astype(np.float32)
 
 
+DEPTH_SCALE = 1e-3  # metres per 16-bit depth unit of the synthetic sensor frames (millimetres)
+
+
+def quantize_frame(rgb, depth, depth_scale: float = DEPTH_SCALE):
+    """Sensor form of a float RGB-D frame, as an RGB-D camera / dataset delivers it
+    (input generation, R41): uint8 [H][W][3] = round(clip(rgb, 0, 1) x 255) re-laid out
+    interleaved, uint16 [H][W] = round(clip(depth / depth_scale, 0, 65535)); rgb
+    [3][H][W] and depth [H][W] float arrays."""
+    rgb = np.asarray(rgb, np.float64)
+    depth = np.asarray(depth, np.float64)
+    c = np.rint(np.clip(rgb, 0.0, 1.0) * 255.0).astype(np.uint8)
+    d = np.rint(np.clip(depth / depth_scale, 0.0, 65535.0)).astype(np.uint16)
+    return np.ascontiguousarray(np.transpose(c, (1, 2, 0))), d
+
+
 def shard_views(num_views: int, rank: int, world: int):
     """Contiguous view shard of rank ``rank``: [r*B/R, (r+1)*B/R)."""
     lo = (rank * num_views) // world
