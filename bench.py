@@ -161,8 +161,12 @@ def oracle_step_sample(w, view=0, size=584, tgt=None):
     from paper_2408_12677_b200.pipeline import lr_per_row
     cam = cpu_window_camera(w.cameras[view], size)
     t0 = time.perf_counter()
-    if tgt is None:
+    if tgt is None:  # the target scene's render as a sensor frame (R41), decoded
+        import scenegen
+        from oracle import frame
         tgt = gsref.render_fwd(cam, w.target_scene, gsref.F32)
+        c8, d16 = scenegen.quantize_frame(tgt["rgb"], tgt["depth"])
+        tgt["rgb"], tgt["depth"] = frame.decode_rgbd(c8, d16, scenegen.DEPTH_SCALE)
     t1 = time.perf_counter()
     f = gsref.render_fwd(cam, w.scene, gsref.F32)
     L, g_rgb, g_d = gsref.l1_loss_grad(f["rgb"], f["depth"], tgt["rgb"].astype(np.float32),
@@ -457,8 +461,15 @@ def main():
     K0 = max(pipeline.measure_keys(lib, model, my_cams, dev), pipeline.measure_keys(lib, tgt_model, my_cams, dev))
     cap = pipeline.default_capacity(K0)
     tg = pipeline.render_targets(lib, tgt_model, my_cams, dev, cap)
+    # the targets as an RGB-D sensor delivers them (R41): 8-bit colour and
+    # 16-bit depth in mm.  The host frames feed the e2e leg; the device-resident float
+    # targets of the timed region are decoded from the same frames (gs_decode_rgbd).
     targets = [None] * B
+    frames = {}
     for v, t in zip(my_views, tg):
+        c8, d16 = scenegen.quantize_frame(t[0].cpu().numpy(), t[1].cpu().numpy())
+        frames[v] = (torch.from_numpy(c8), torch.from_numpy(d16.view(np.int16)))
+        lib.decode_rgbd(frames[v][0].to(dev), frames[v][1].to(dev), scenegen.DEPTH_SCALE, t[0], t[1])
         targets[v] = t
     del tgt_model, tg
     torch.cuda.empty_cache()
@@ -623,10 +634,12 @@ def main():
     # --- end to end: targets from pinned host memory every step, loss read back
     e2e = None
     if not args.no_e2e and not args.profile:
-        host_t = {v: (targets[v][0].cpu().pin_memory(), targets[v][1].cpu().pin_memory()) for v in my_views}
-        h2d = sum(host_t[v][0].numel() * 4 + host_t[v][1].numel() * 4 for v in step_views(0))
+        # sensor frames (uint8 rgb, 16-bit depth) from pinned host memory, decoded on the GPU
+        host_t = {v: (frames[v][0].pin_memory(), frames[v][1].pin_memory()) for v in my_views}
+        h2d = sum(host_t[v][0].numel() * host_t[v][0].element_size() +
+                  host_t[v][1].numel() * host_t[v][1].element_size() for v in step_views(0))
         loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
-        tr.step_host(step_views(0), host_t)  # allocate the target slots + copy stream (untimed)
+        tr.step_host(step_views(0), host_t, scenegen.DEPTH_SCALE)  # allocate the slots + copy stream (untimed)
         torch.cuda.synchronize()
         tr.blended.zero_()
         if world > 1:
@@ -637,7 +650,7 @@ def main():
         for i in range(args.steps):
             sv = step_views(i)
             tr.loss.zero_()
-            tr.step_host(sv, host_t)  # every view's targets: pinned host -> device inside the step
+            tr.step_host(sv, host_t, scenegen.DEPTH_SCALE)  # every view's frame: host -> device + decode
             loss_host.copy_(tr.loss, non_blocking=True)
         s1.record(stream)
         torch.cuda.synchronize()
@@ -651,7 +664,9 @@ def main():
             dist.all_reduce(sm, op=dist.ReduceOp.SUM)
             ems, eb = float(mx[0]), int(sm[1])
         e2e = {"value": eb / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
-               "iters_per_s": args.steps / (ems / 1000.0)}
+               "iters_per_s": args.steps / (ems / 1000.0),
+               "inputs": "per view an RGB-D sensor frame (uint8 [H][W][3] + uint16 mm [H][W]) from pinned host "
+                         "memory, copied and decoded (gs_decode_rgbd) inside the step; loss read back"}
 
     # --- K13: the straightforward per-pixel GPU port (north_star's >= 10x target), same
     # steps with gs_naive_render_fwd / gs_naive_render_bwd_screen, device-timed the same way
@@ -741,6 +756,8 @@ def main():
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if dist_on else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
+                   "targets": "renders of the target scene quantised to RGB-D sensor frames (8-bit colour, 16-bit mm "
+                              "depth) and decoded on the GPU",
                    "launch": "CUDA graph per iteration" if use_graph else "eager",
                    "l2": "inputs larger than L2 (params+grad+m+v %.0f MB, targets %.0f MB per rank)" % (
                        4 * model.nbytes / 1e6, sum(t[0].numel() * 4 + t[1].numel() * 4 for t in targets if t) / 1e6)},

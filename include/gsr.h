@@ -435,6 +435,23 @@ gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, co
                           const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
                           void* stream);
 
+/* ---------------------------------------------------------------- harness: input frames
+ * The method "takes a pair of RGB-D images as input" at every time step (PAPER.md:58,
+ * Fig. 2); Eq. 12's C* and D* and the depth map D_k of Eqs. 6 and 10 are that frame.
+ * A sensor frame is an 8-bit RGB image and a 16-bit depth image whose units times
+ * depth_scale are metres, 0 = invalid (reading R41).  This call turns
+ * one frame, as it arrives from the host, into the planar float images the other calls
+ * take:  out_rgb[c][y][x] = rgb[y][x][c] / 255 (IEEE division, correctly rounded),
+ * out_depth[y][x] = depth[y][x] * depth_scale (one rounded fp32 product; 0 stays 0).
+ *   rgb       DEVICE uint8 [H][W][3] (interleaved, as decoded from the sensor / file)
+ *   depth     DEVICE uint16 [H][W]
+ *   out_rgb   DEVICE float [3][H][W];  out_depth DEVICE float [H][W]  (caller-owned)
+ * width, height > 0 and depth_scale > 0 (finite), else GS_ERR_ARG.  Vectorised 4 pixels
+ * per thread when W*H % 4 == 0 and the buffers are 16-B (rgb 4-B, depth 8-B) aligned,
+ * else one pixel per thread; same values either way. */
+gs_status gs_decode_rgbd(int32_t width, int32_t height, const uint8_t* rgb, const uint16_t* depth,
+                         float depth_scale, float* out_rgb, float* out_depth, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

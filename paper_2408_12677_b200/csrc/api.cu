@@ -481,4 +481,23 @@ gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, co
   return check_launch("gs_l1_loss_grad");
 }
 
+gs_status gs_decode_rgbd(int32_t width, int32_t height, const uint8_t* rgb, const uint16_t* depth, float depth_scale,
+                         float* out_rgb, float* out_depth, void* stream) {
+  g_err[0] = 0;
+  if (width <= 0 || height <= 0 || !(depth_scale > 0.f) || !std::isfinite(depth_scale)) {
+    set_error("gs_decode_rgbd: width=%d height=%d depth_scale=%g", width, height, (double)depth_scale);
+    return GS_ERR_ARG;
+  }
+  // any alignment is accepted (the aligned case takes the vectorised kernel)
+  for (const auto& p : {std::make_pair((const void*)rgb, "rgb"), std::make_pair((const void*)depth, "depth"),
+                        std::make_pair((const void*)out_rgb, "out_rgb"), std::make_pair((const void*)out_depth, "out_depth")})
+    if (!p.first) {
+      set_error("gs_decode_rgbd: %s is NULL", p.second);
+      return GS_ERR_ARG;
+    }
+  launch_decode_rgbd((int64_t)width * height, rgb, depth, depth_scale, out_rgb, out_depth,
+                     static_cast<cudaStream_t>(stream));
+  return check_launch("gs_decode_rgbd");
+}
+
 }  // extern "C"

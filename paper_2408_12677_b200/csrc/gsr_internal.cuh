@@ -109,4 +109,8 @@ gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const flo
 void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
                float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s);
 
+// frame.cu
+void launch_decode_rgbd(int64_t npix, const uint8_t* rgb, const uint16_t* depth, float scale, float* out_rgb,
+                        float* out_d, cudaStream_t s);
+
 }  // namespace gsr

@@ -208,7 +208,7 @@ __device__ __forceinline__ void gather_rec_async(const float4* __restrict__ rec,
 // Transpose reduction of 10 per-lane values over the warp: 13 shuffles (vs 50 for
 // ten butterfly reductions).  On return, the 10 lanes with slot >= 0 hold the warp
 // total of component `slot`.
-__device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, float& out, int& slot) {
+[[maybe_unused]] __device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, float& out, int& slot) {
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
   float w6[6];
 #pragma unroll
@@ -242,6 +242,41 @@ __device__ __forceinline__ void warp_reduce10(const float (&v)[10], int lane, fl
   out = w1;
   slot = (gi < 3 && s < 10 && !(lane & 1)) ? s : -1;
 }
+
+// Upstream gradient of one pixel: dL/drgb, dL/ddepth read from the caller's buffers, or,
+// with the fused Eq. 12 loss (gs_render_bwd_screen_l1), computed here from the rendered
+// and target images exactly as gs_l1_loss_grad does (sign(residual) x 1/(3 npix), x
+// w_depth/npix for depth, sign(0) = 0), the pixel's loss terms added to `lsum`.
+struct L1Fuse {
+  const float *rgb, *depth, *trgb, *tdep;
+  float sc, sd;
+  float* loss;
+};
+__device__ __forceinline__ float l1_sign(float r, float s) { return r > 0.f ? s : (r < 0.f ? -s : 0.f); }
+__device__ __forceinline__ void upstream(const L1Fuse& l1, const float* __restrict__ g_rgb,
+                                         const float* __restrict__ g_dep, int64_t npix, int64_t p, float& gr,
+                                         float& gg, float& gb, float& gd, float& lsum) {
+  if (l1.trgb) {
+    const float r0 = l1.rgb[p] - l1.trgb[p], r1 = l1.rgb[npix + p] - l1.trgb[npix + p];
+    const float r2 = l1.rgb[2 * npix + p] - l1.trgb[2 * npix + p], rd = l1.depth[p] - l1.tdep[p];
+    gr = l1_sign(r0, l1.sc), gg = l1_sign(r1, l1.sc), gb = l1_sign(r2, l1.sc), gd = l1_sign(rd, l1.sd);
+    lsum += fabsf(r0) * l1.sc + fabsf(r1) * l1.sc + fabsf(r2) * l1.sc + fabsf(rd) * l1.sd;
+  } else {
+    gr = g_rgb[p], gg = g_rgb[npix + p], gb = g_rgb[2 * npix + p];
+    gd = g_dep ? g_dep[p] : 0.f;
+  }
+}
+__device__ __forceinline__ void l1_commit(const L1Fuse& l1, float lsum, int lane) {
+  if (l1.loss) {
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
+    if (lane == 0 && lsum != 0.f) atomicAdd(l1.loss, lsum);
+  }
+}
+
+#ifndef GSR_EXACT_EXP
+// ===========================================================================
+// Fast path (libgsr.so)
+// ===========================================================================
 
 // Two keys' 10-component reductions in one transpose (GSR_BWD_PAIR): the first stage
 // (xor 16) of each key alone -- 5 shuffles, leaving components k (lanes with bit 4
@@ -286,41 +321,6 @@ __device__ __forceinline__ void reduce_pair_commit(const float (&a)[5], const fl
   const int g = b3 ? gb : ga;
   if (ei < 3 && di < 5 && g >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * g + ((lane & 16) ? 5 : 0) + di, out);
 }
-
-// Upstream gradient of one pixel: dL/drgb, dL/ddepth read from the caller's buffers, or,
-// with the fused Eq. 12 loss (gs_render_bwd_screen_l1), computed here from the rendered
-// and target images exactly as gs_l1_loss_grad does (sign(residual) x 1/(3 npix), x
-// w_depth/npix for depth, sign(0) = 0), the pixel's loss terms added to `lsum`.
-struct L1Fuse {
-  const float *rgb, *depth, *trgb, *tdep;
-  float sc, sd;
-  float* loss;
-};
-__device__ __forceinline__ float l1_sign(float r, float s) { return r > 0.f ? s : (r < 0.f ? -s : 0.f); }
-__device__ __forceinline__ void upstream(const L1Fuse& l1, const float* __restrict__ g_rgb,
-                                         const float* __restrict__ g_dep, int64_t npix, int64_t p, float& gr,
-                                         float& gg, float& gb, float& gd, float& lsum) {
-  if (l1.trgb) {
-    const float r0 = l1.rgb[p] - l1.trgb[p], r1 = l1.rgb[npix + p] - l1.trgb[npix + p];
-    const float r2 = l1.rgb[2 * npix + p] - l1.trgb[2 * npix + p], rd = l1.depth[p] - l1.tdep[p];
-    gr = l1_sign(r0, l1.sc), gg = l1_sign(r1, l1.sc), gb = l1_sign(r2, l1.sc), gd = l1_sign(rd, l1.sd);
-    lsum += fabsf(r0) * l1.sc + fabsf(r1) * l1.sc + fabsf(r2) * l1.sc + fabsf(rd) * l1.sd;
-  } else {
-    gr = g_rgb[p], gg = g_rgb[npix + p], gb = g_rgb[2 * npix + p];
-    gd = g_dep ? g_dep[p] : 0.f;
-  }
-}
-__device__ __forceinline__ void l1_commit(const L1Fuse& l1, float lsum, int lane) {
-  if (l1.loss) {
-    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(kFull, lsum, o);
-    if (lane == 0 && lsum != 0.f) atomicAdd(l1.loss, lsum);
-  }
-}
-
-#ifndef GSR_EXACT_EXP
-// ===========================================================================
-// Fast path (libgsr.so)
-// ===========================================================================
 
 // Staged record (3 x float4 in shared memory), rewritten in place by its lane:
 //   (mx, my, z, lo2) (Ah, Bh, Ch, r) (g, b, o, mask | flags)

@@ -139,10 +139,11 @@ class Library:
         lib.gs_quadtree.argtypes = [C.c_int32, C.c_int32, vp, C.c_float, C.c_int32, vp, C.c_size_t, vp, i64, vp, vp]
         lib.gs_seed_gaussians.argtypes = [vp, vp, GsTsdfVolume, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
+        lib.gs_decode_rgbd.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_float, vp, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",  # noqa: E501
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
                    "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
-                   "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians"):
+                   "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -320,6 +321,16 @@ class Library:
         return self._check("gs_l1_loss_grad", self.lib.gs_l1_loss_grad(
             int(depth.numel()), _ptr(rgb), _ptr(depth), _ptr(t_rgb), _ptr(t_depth), float(w_depth), _ptr(g_rgb),
             _ptr(g_depth), _ptr(loss), _stream(stream)))
+
+    def decode_rgbd(self, rgb_u8, depth_u16, depth_scale, out_rgb, out_depth, stream=None):
+        """Sensor frame (uint8 [H][W][3], uint16 [H][W] -- or int16 holding the same bits)
+        -> float [3][H][W] rgb / 255 and [H][W] depth x depth_scale (gs_decode_rgbd)."""
+        H, W = int(depth_u16.shape[0]), int(depth_u16.shape[1])
+        if tuple(rgb_u8.shape) != (H, W, 3) or rgb_u8.element_size() != 1 or depth_u16.element_size() != 2:
+            raise ValueError("decode_rgbd: rgb must be uint8 [H][W][3] and depth 16-bit [H][W]")
+        return self._check("gs_decode_rgbd", self.lib.gs_decode_rgbd(
+            W, H, _ptr(rgb_u8), _ptr(depth_u16), float(depth_scale), _ptr(out_rgb), _ptr(out_depth),
+            _stream(stream)))
 
 
 _LIBS = {}

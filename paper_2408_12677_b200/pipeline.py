@@ -234,20 +234,32 @@ class Trainer:
             return t[0], t[1], None, None
         self._run(views, targets, None)
 
-    def step_host(self, views, host_targets):
+    def step_host(self, views, host_targets, depth_scale=None):
         """One iteration with the targets streamed from (pinned) host memory:
-        host_targets {v: (rgb [3][H][W], depth [H][W])} CPU tensors.  View k's targets
-        are copied on a side stream into device slot k % n (n = 2 x the views in flight,
-        so every in-flight view has its slot and the next ones are already loading);
-        the loss of view k waits for its copy only, and the copy into a slot waits until
-        the loss that last read it has run.  The host enqueues ahead of the GPU, so the
-        next iteration's first copies overlap this one's tail."""
+        host_targets {v: (rgb, depth)} CPU tensors, either float32 rgb [3][H][W] + depth
+        [H][W], or a sensor frame (R41): uint8 rgb [H][W][3] + 16-bit
+        depth [H][W] in units of ``depth_scale`` metres, shipped as is (5 B/px instead
+        of 16) and decoded on the device (gs_decode_rgbd) right after its copy.  View
+        k's targets are copied on a side stream into device slot k % n (n = 2 x the
+        views in flight, so every in-flight view has its slot and the next ones are
+        already loading); the loss of view k waits for its copy only, and the copy into
+        a slot waits until the loss that last read it has run.  The host enqueues ahead
+        of the GPU, so the next iteration's first copies overlap this one's tail."""
         dev = self.device
         n_slots = max(2, 2 * len(self.bufs))
-        if getattr(self, "_slots", None) is None:
-            r0, d0 = host_targets[views[0]]
-            self._slots = [(torch.empty(r0.shape, dtype=torch.float32, device=dev),
-                            torch.empty(d0.shape, dtype=torch.float32, device=dev)) for _ in range(n_slots)]
+        r0, d0 = host_targets[views[0]]
+        sensor = r0.dtype == torch.uint8
+        if sensor and depth_scale is None:
+            raise ValueError("step_host: sensor frames (uint8 rgb) need depth_scale")
+        if getattr(self, "_slots", None) is None or self._sensor != sensor:
+            H, W = int(d0.shape[0]), int(d0.shape[1])
+            self._slots = [(torch.empty((3, H, W), dtype=torch.float32, device=dev),
+                            torch.empty((H, W), dtype=torch.float32, device=dev)) for _ in range(n_slots)]
+            # sensor frames land in raw slots first (uint8 [H][W][3], 16-bit [H][W])
+            self._raw = ([(torch.empty((H, W, 3), dtype=torch.uint8, device=dev),
+                           torch.empty((H, W), dtype=d0.dtype, device=dev)) for _ in range(n_slots)]
+                         if sensor else None)
+            self._sensor = sensor
             n_cs = int(os.environ.get("GSR_COPY_STREAMS", "1"))  # 2-3 measured no faster
             self._copy_streams = [torch.cuda.Stream(device=dev) for _ in range(max(1, n_cs))]
             self._ready = [torch.cuda.Event() for _ in range(n_slots)]
@@ -260,8 +272,14 @@ class Trainer:
             with torch.cuda.stream(cs):
                 cs.wait_event(self._free[s])
                 r, d = host_targets[views[k]]
-                self._slots[s][0].copy_(r, non_blocking=True)
-                self._slots[s][1].copy_(d, non_blocking=True)
+                if sensor:
+                    self._raw[s][0].copy_(r, non_blocking=True)
+                    self._raw[s][1].copy_(d, non_blocking=True)
+                    self.lib.decode_rgbd(self._raw[s][0], self._raw[s][1], depth_scale, self._slots[s][0],
+                                         self._slots[s][1])
+                else:
+                    self._slots[s][0].copy_(r, non_blocking=True)
+                    self._slots[s][1].copy_(d, non_blocking=True)
                 self._ready[s].record(cs)
 
         def targets(k, v):
