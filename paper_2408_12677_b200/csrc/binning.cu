@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
                                                          const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
                                                          int tile_bits, const uint32_t* __restrict__ chist,
                                                          const uint32_t* __restrict__ tot, int2* __restrict__ ranges,
-                                                         int32_t* __restrict__ out) {
+                                                         int32_t* __restrict__ out, int own_bits) {
   extern __shared__ uint32_t s_dyn[];
   __shared__ uint32_t s_wsum[kBkWarps];
   uint32_t* s_base = s_dyn;                                // [NT] global position of this chunk's first key of t
@@ -638,6 +638,9 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   int64_t a, b;
   chunk_bounds(K, C, blockIdx.x, warp, a, b);
   uint16_t* my = s_w + (int64_t)warp * NTp;
+  // per-warp tile -> lane arbitration slots (hashed by the low own_bits of the tile id)
+  uint8_t* own = reinterpret_cast<uint8_t*>(s_w + (int64_t)kBkWarps * NTp) + ((int64_t)warp << own_bits);
+  const uint32_t omask = (1u << own_bits) - 1u;
   // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
   constexpr int G = GSR_TSCATTER_G;  // 32-key groups in flight per warp (latency: 8 warps per SM)
   for (int64_t kb = a; kb < b; kb += 32 * G) {
@@ -677,6 +680,20 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
       if (kb + 32 * g >= b) break;  // warp-uniform
       const bool valid = tt[g] != 0xffffffffu;
       const uint32_t t = valid ? tt[g] : 0u;
+      // Fast path: every lane writes its lane id into its tile's slot; if every lane
+      // reads its own id back, the group's tiles are distinct (rank 0, count 1 each) --
+      // the common case, since a group spans ~2 Gaussians whose keys are distinct tiles.
+      // Otherwise (a repeated tile or a hash collision) the exact ballot ranking below.
+      if (valid) own[t & omask] = (uint8_t)lane;
+      __syncwarp();
+      if (__all_sync(kFull, !valid || own[t & omask] == (uint8_t)lane)) {
+        if (valid) {
+          const uint32_t run = my[t];
+          my[t] = (uint16_t)(run + 1u);
+          out[s_base[t] + run] = (int32_t)ii[g];
+        }
+        continue;
+      }
       const uint32_t peers = tile_peers(t, valid, tile_bits);
       const uint32_t r = __popc(peers & lt);
       uint32_t run = 0;
@@ -690,8 +707,15 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
 }
 
 // Shared memory of k_tscatter for NT tiles; bucket placement is used when it fits.
-size_t tscatter_smem(int NT) { return (size_t)NT * 4 + (size_t)((NT + 1) & ~1) * kBkWarps * 2; }
 constexpr size_t kSmemOptIn = 227 * 1024 - 1024;  // dynamic opt-in (static smem of the kernels < 1 KB)
+size_t tscatter_smem_base(int NT) { return (size_t)NT * 4 + (size_t)((NT + 1) & ~1) * kBkWarps * 2; }
+// arbitration slots per warp: 2^own_bits, the most (<= 4096) that still fit
+int tscatter_own_bits(int NT) {
+  int bits = 12;
+  while (bits > 5 && tscatter_smem_base(NT) + ((size_t)kBkWarps << bits) > kSmemOptIn) --bits;
+  return bits;
+}
+size_t tscatter_smem(int NT) { return tscatter_smem_base(NT) + ((size_t)kBkWarps << tscatter_own_bits(NT)); }
 
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
@@ -843,7 +867,8 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
       }
       k_tcount<<<C, kBkThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, chist);
       k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, tot);
-      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, tot, rng, sorted_ids);
+      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, tot, rng, sorted_ids,
+                                             tscatter_own_bits(NT));
       count_launch(3);
       return finish_bin(ctr, cap, num_keys_host, s);
     }
