@@ -486,27 +486,65 @@ __global__ void k_ranges(const uint16_t* __restrict__ skeys, const Counters* __r
 // passes.  The K keys are cut into C equal chunks (one CTA each, 8 warps, each warp
 // a contiguous sub-chunk):
 //   k_tcount:   per chunk and tile, the key count           -> chist[c][t]
-//   k_tscan:    per tile, exclusive prefix over the chunks   -> chist[c][t], tot[t]
-//   k_tscatter: per chunk: the exclusive prefix of tot over the tiles (tile starts;
-//               chunk 0 writes tile_ranges), per-warp tile counts, their prefix over the
+//   k_tscan:    per tile, exclusive prefix over the chunks plus the tile's start (the
+//               tile totals chained by look-back)  -> chist[c][t], tile_ranges
+//   k_tscatter: per chunk: per-warp tile counts, their prefix over the
 //               warps, then each warp walks its keys in order and places key k of
 //               tile t at  start(t) + chist[c][t] + (warp prefix) + (earlier keys of
 //               t in this warp), ranking equal tiles within 32 keys by bit-sliced
 //               ballots.  Keys of a tile thus keep their depth order: the output is
 //               the same stable sort, in ~3 passes of 2-6 B/key and no look-back.
 // ---------------------------------------------------------------------------
-#ifndef GSR_TSCATTER_G
-#define GSR_TSCATTER_G 8
-#endif
 constexpr int kBkThreads = 256, kBkWarps = kBkThreads / 32;
 constexpr int kBkMaxChunks = 512;  // chist capacity (workspace); C = min(this, SMs x CTAs/SM)
 
+constexpr int kBkBatch = 256;  // keys per staged batch of a warp (32 lanes x 8 keys)
+// Chunk c = keys [c chunk, (c + 1) chunk), cut into 8 warp sub-chunks; chunk and
+// sub-chunk sizes are multiples of kBkBatch, so every sub-chunk starts 16-B aligned in
+// the key (u16) and value (u32) arrays (vector loads, cp.async staging).
 __device__ __forceinline__ void chunk_bounds(int64_t K, int C, int c, int w, int64_t& a, int64_t& b) {
-  const int64_t chunk = (K + C - 1) / C;
+  constexpr int64_t q = (int64_t)kBkWarps * kBkBatch;
+  const int64_t chunk = ((K + C - 1) / C + q - 1) / q * q;
   const int64_t k0 = min(K, (int64_t)c * chunk), k1 = min(K, k0 + chunk);
-  const int64_t sub = (k1 - k0 + kBkWarps - 1) / kBkWarps;
+  const int64_t sub = chunk / kBkWarps;
   a = min(k1, k0 + (int64_t)w * sub);
   b = min(k1, a + sub);
+}
+
+// Count the tile keys [a, b) (a % 8 == 0) into packed 16-bit (pk16) or 32-bit counters:
+// one 16-B load (8 keys) per thread and step; key 0xffff marks past-the-end.
+template <bool kPk16>
+__device__ __forceinline__ void count_keys(const uint16_t* __restrict__ tkeys, int64_t a, int64_t b, int tid,
+                                           int nthreads, uint32_t* cnt) {
+  constexpr int U = 4;  // 16-B loads in flight per thread
+  for (int64_t kb = a + 8 * (int64_t)tid; kb < b; kb += 8 * (int64_t)nthreads * U) {
+    uint4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + 8 * (int64_t)nthreads * u;
+      q[u] = k < b ? *reinterpret_cast<const uint4*>(tkeys + k) : make_uint4(~0u, ~0u, ~0u, ~0u);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + 8 * (int64_t)nthreads * u;
+      const uint32_t w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const uint32_t t = (w[e >> 1] >> (16 * (e & 1))) & 0xffffu;
+        if (k + e < b) {
+          if (kPk16)
+            atomicAdd(cnt + (t >> 1), 1u << (16 * (t & 1)));
+          else
+            atomicAdd(cnt + t, 1u);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16_bin(void* smem, const void* gmem) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
 __global__ void __launch_bounds__(kBkThreads) k_tcount(const uint16_t* __restrict__ tkeys,
@@ -522,34 +560,35 @@ __global__ void __launch_bounds__(kBkThreads) k_tcount(const uint16_t* __restric
   const int64_t k0 = a;
   chunk_bounds(K, C, blockIdx.x, kBkWarps - 1, a, b);
   const int64_t k1 = b;
-  constexpr int G = 8;
-  for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += (int64_t)kBkThreads * G) {
-    uint32_t tt[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t k = kb + (int64_t)kBkThreads * g;
-      tt[g] = k < k1 ? (uint32_t)tkeys[k] : 0xffffffffu;
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (tt[g] != 0xffffffffu) atomicAdd(&s_cnt[tt[g]], 1u);
-  }
+  count_keys<false>(tkeys, k0, k1, threadIdx.x, kBkThreads, s_cnt);
   __syncthreads();
-  uint32_t* out = chist + (int64_t)blockIdx.x * NT;
+  uint32_t* out = chist + (int64_t)blockIdx.x * ((NT + 3) & ~3);  // rows padded to 16 B
   for (int t = threadIdx.x; t < NT; t += kBkThreads) out[t] = s_cnt[t];
 }
 
 // CTA = 32 tiles x 8 warps; warp w scans chunks [w Cw, (w+1) Cw) of its lane's tile.
+// The CTAs take their 32 tiles in launch order (partition counter) and chain the tile
+// totals by decoupled look-back, so every chist[c][t] leaves as the global position of
+// chunk c's first key of tile t (tile start + keys of t in earlier chunks), and
+// tile_ranges are written here once.
 __global__ void __launch_bounds__(kBkThreads) k_tscan(uint32_t* __restrict__ chist, int NT, int C,
-                                                      uint32_t* __restrict__ tot) {
+                                                      Counters* __restrict__ ctr,
+                                                      unsigned long long* __restrict__ lookback,
+                                                      int2* __restrict__ ranges) {
   __shared__ uint32_t s_part[kBkWarps][32];
+  __shared__ uint32_t s_blk;
+  __shared__ unsigned long long s_prefix;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
+  if (threadIdx.x == 0) s_blk = atomicAdd(&ctr->part[6], 1u);
+  __syncthreads();
+  const int blk = (int)s_blk;
+  const int t = blk * 32 + lane;
+  const int NS = (NT + 3) & ~3;  // chist row stride
   const int Cw = (C + kBkWarps - 1) / kBkWarps;
   const int c0 = min(C, warp * Cw), c1 = min(C, c0 + Cw);
   uint32_t s = 0;
   if (t < NT)
-    for (int c = c0; c < c1; ++c) s += chist[(int64_t)c * NT + t];
+    for (int c = c0; c < c1; ++c) s += chist[(int64_t)c * NS + t];
   s_part[warp][lane] = s;
   __syncthreads();
   uint32_t run = 0, all = 0;
@@ -559,14 +598,28 @@ __global__ void __launch_bounds__(kBkThreads) k_tscan(uint32_t* __restrict__ chi
     run += (w < warp) ? v : 0u;
     all += v;
   }
+  // tile starts: exclusive scan of the 32 tile totals, plus the preceding CTAs' keys
+  uint32_t incl = all;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (warp == 0) {
+    const unsigned long long pre = warp_lookback(lookback, blk, (unsigned long long)__shfl_sync(kFull, incl, 31));
+    if (lane == 0) s_prefix = pre;
+  }
+  __syncthreads();
+  const uint32_t start = (uint32_t)s_prefix + incl - all;
   if (t < NT) {
+    run += start;
     for (int c = c0; c < c1; ++c) {
-      uint32_t* p = chist + (int64_t)c * NT + t;
+      uint32_t* p = chist + (int64_t)c * NS + t;
       const uint32_t v = *p;
       *p = run;
       run += v;
     }
-    if (warp == 0) tot[t] = all;
+    if (warp == 0) ranges[t] = make_int2((int)start, (int)(start + all));
   }
 }
 
@@ -580,80 +633,57 @@ __device__ __forceinline__ uint32_t tile_peers(uint32_t t, bool valid, int bits)
   return peers;
 }
 
-// Every CTA: s_base[t] := exclusive prefix of tot over the tiles (= start of tile t);
-// CTA 0 also writes tile_ranges.  Warp w scans tiles [w NT/8, (w+1) NT/8) 32 at a time.
-__device__ __forceinline__ void tile_starts(const uint32_t* __restrict__ tot, int NT, uint32_t* s_base,
-                                            uint32_t* s_wsum /*[8]*/, int2* __restrict__ ranges) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int per = (NT + kBkWarps - 1) / kBkWarps;
-  const int t0 = min(NT, warp * per), t1 = min(NT, t0 + per);
-  uint32_t sum = 0;
-  for (int t = t0 + lane; t < t1; t += 32) {
-    const uint32_t v = tot[t];
-    s_base[t] = v;
-    sum += v;
-  }
-  sum = __reduce_add_sync(kFull, sum);
-  if (lane == 0) s_wsum[warp] = sum;
-  __syncthreads();
-  uint32_t run = 0;
-  for (int w = 0; w < warp; ++w) run += s_wsum[w];
-  for (int tb = t0; tb < t1; tb += 32) {
-    const int t = tb + lane;
-    const uint32_t v = t < t1 ? s_base[t] : 0u;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, x, o);
-      if (lane >= o) x += y;
-    }
-    const uint32_t start = run + x - v;
-    if (t < t1) {
-      s_base[t] = start;
-      if (blockIdx.x == 0) ranges[t] = make_int2((int)start, (int)(start + v));
-    }
-    run += __shfl_sync(kFull, x, 31);
-  }
-  __syncthreads();
-}
-
 __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restrict__ tkeys,
                                                          const uint32_t* __restrict__ tvals,
                                                          const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
                                                          int tile_bits, const uint32_t* __restrict__ chist,
-                                                         const uint32_t* __restrict__ tot, int2* __restrict__ ranges,
                                                          int32_t* __restrict__ out, int own_bits) {
-  extern __shared__ uint32_t s_dyn[];
-  __shared__ uint32_t s_wsum[kBkWarps];
-  uint32_t* s_base = s_dyn;                                // [NT] global position of this chunk's first key of t
-  const int NTp = (NT + 1) & ~1;                           // even row stride: 4-B aligned rows
-  uint16_t* s_w = reinterpret_cast<uint16_t*>(s_dyn + NT);  // [8][NTp] per-warp count, then running offset
+  extern __shared__ __align__(16) uint32_t s_dyn[];
+  // dynamic layout (tscatter_layout): s_base [NT] u32 | s_w [8][NTp] u16 | stage [8][2] x
+  // (256 u16 keys, 256 u32 values) | own [8][2^own_bits] u8
+  // tables carry 32 dummy tiles NT + lane for the lanes past the end of the last group
+  // (branch-free fast path; their counters are never read back)
+  uint32_t* s_base = s_dyn;                                // [NT + 32] global position of this chunk's first key of t
+  const int NTx = NT + 32;
+  const int NTp = (NTx + 1) & ~1;                          // even row stride: 4-B aligned rows
+  const size_t off_w = ((size_t)NTx * 4 + 15) & ~size_t(15);
+  const size_t off_stage = (off_w + (size_t)NTp * kBkWarps * 2 + 15) & ~size_t(15);
+  const size_t off_own = off_stage + (size_t)kBkWarps * 2 * kBkBatch * 6;
+  char* s_bytes = reinterpret_cast<char*>(s_dyn);
+  uint16_t* s_w = reinterpret_cast<uint16_t*>(s_bytes + off_w);  // [8][NTp] per-warp count, then running offset
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < NTp * kBkWarps / 2; i += kBkThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
-  tile_starts(tot, NT, s_base, s_wsum, ranges);  // (synchronises the CTA)
   int64_t K = (int64_t)ctr->K;
-  if (K > cap) return;  // tot is all zero then: tile_ranges are empty
-  const uint32_t* ch = chist + (int64_t)blockIdx.x * NT;
-  for (int t = threadIdx.x; t < NT; t += kBkThreads) s_base[t] += ch[t];
+  if (K > cap) return;  // chist is all zero then: tile_ranges (k_tscan) are empty
+  // this chunk's row of global positions (k_tscan) -> s_base: all 16-B pieces in flight
+  // at once (cp.async) instead of one L2 round trip per loop iteration
+  const uint32_t* ch = chist + (int64_t)blockIdx.x * ((NT + 3) & ~3);
+  for (int i = threadIdx.x; i < (NT + 3) / 4; i += kBkThreads) cp_async16_bin(s_base + 4 * i, ch + 4 * i);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int i = threadIdx.x; i < NTp * kBkWarps / 2; i += kBkThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
   int64_t a, b;
   chunk_bounds(K, C, blockIdx.x, warp, a, b);
   uint16_t* my = s_w + (int64_t)warp * NTp;
   // per-warp tile -> lane arbitration slots (hashed by the low own_bits of the tile id)
-  uint8_t* own = reinterpret_cast<uint8_t*>(s_w + (int64_t)kBkWarps * NTp) + ((int64_t)warp << own_bits);
+  uint8_t* own = reinterpret_cast<uint8_t*>(s_bytes + off_own) + ((int64_t)warp << own_bits);
   const uint32_t omask = (1u << own_bits) - 1u;
-  // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
-  constexpr int G = GSR_TSCATTER_G;  // 32-key groups in flight per warp (latency: 8 warps per SM)
-  for (int64_t kb = a; kb < b; kb += 32 * G) {
-    uint32_t tt[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t k = kb + 32 * g + lane;
-      tt[g] = k < b ? (uint32_t)tkeys[k] : 0xffffffffu;
+  uint16_t* stk = reinterpret_cast<uint16_t*>(s_bytes + off_stage + (size_t)warp * 2 * kBkBatch * 6);  // [2][256]
+  uint32_t* stv = reinterpret_cast<uint32_t*>(stk + 2 * kBkBatch);                                     // [2][256]
+  // stage batch [kb, kb + 256) of this warp's keys and values into buffer sb (cp.async;
+  // a 16-B piece starting past b is skipped, the keys past b are masked when read)
+  auto stage = [&](int64_t kb, int sb) {
+    const int64_t k = kb + 8 * lane;
+    if (k < b) {
+      cp_async16_bin(stk + sb * kBkBatch + 8 * lane, tkeys + k);
+      cp_async16_bin(stv + sb * kBkBatch + 8 * lane, tvals + k);
+      cp_async16_bin(stv + sb * kBkBatch + 8 * lane + 4, tvals + k + 4);
     }
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (tt[g] != 0xffffffffu) atomicAdd(reinterpret_cast<uint32_t*>(my) + (tt[g] >> 1), 1u << (16 * (tt[g] & 1)));
-  }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();          // s_w zeroed, s_base loaded
+  if (a < b) stage(a, 0);   // in flight during the counting pass
+  // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
+  count_keys<true>(tkeys, a, b, lane, 32, reinterpret_cast<uint32_t*>(my));
   __syncthreads();
   for (int t = threadIdx.x; t < NT; t += kBkThreads) {
     uint32_t run = 0;
@@ -666,32 +696,29 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   }
   __syncthreads();
   const uint32_t lt = lanemask_lt();
-  for (int64_t kb = a; kb < b; kb += 32 * G) {
-    uint32_t tt[G], ii[G];
+  int sb = 0;
+  for (int64_t kb = a; kb < b; kb += kBkBatch, sb ^= 1) {
+    if (kb + kBkBatch < b) stage(kb + kBkBatch, sb ^ 1);  // next batch in flight
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+    const int rem = (int)min((int64_t)kBkBatch, b - kb);  // keys of this batch
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int64_t k = kb + 32 * g + lane;
-      const bool valid = k < b;
-      tt[g] = valid ? (uint32_t)tkeys[k] : 0xffffffffu;
-      ii[g] = valid ? tvals[k] : 0u;
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (kb + 32 * g >= b) break;  // warp-uniform
-      const bool valid = tt[g] != 0xffffffffu;
-      const uint32_t t = valid ? tt[g] : 0u;
+    for (int g = 0; g < kBkBatch / 32; ++g) {
+      if (32 * g >= rem) break;  // warp-uniform
+      const bool valid = 32 * g + lane < rem;
+      const uint32_t t = valid ? (uint32_t)stk[sb * kBkBatch + 32 * g + lane] : (uint32_t)NT + lane;
+      const uint32_t id = stv[sb * kBkBatch + 32 * g + lane];
       // Fast path: every lane writes its lane id into its tile's slot; if every lane
       // reads its own id back, the group's tiles are distinct (rank 0, count 1 each) --
       // the common case, since a group spans ~2 Gaussians whose keys are distinct tiles.
       // Otherwise (a repeated tile or a hash collision) the exact ballot ranking below.
-      if (valid) own[t & omask] = (uint8_t)lane;
+      own[t & omask] = (uint8_t)lane;
       __syncwarp();
-      if (__all_sync(kFull, !valid || own[t & omask] == (uint8_t)lane)) {
-        if (valid) {
-          const uint32_t run = my[t];
-          my[t] = (uint16_t)(run + 1u);
-          out[s_base[t] + run] = (int32_t)ii[g];
-        }
+      if (__all_sync(kFull, own[t & omask] == (uint8_t)lane)) {
+        const uint32_t run = my[t];
+        my[t] = (uint16_t)(run + 1u);
+        if (valid) out[s_base[t] + run] = (int32_t)id;
         continue;
       }
       const uint32_t peers = tile_peers(t, valid, tile_bits);
@@ -701,14 +728,20 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
       __syncwarp();
       if (valid && r == 0) my[t] = (uint16_t)(run + __popc(peers));
       __syncwarp();
-      if (valid) out[s_base[t] + run + r] = (int32_t)ii[g];
+      if (valid) out[s_base[t] + run + r] = (int32_t)id;
     }
+    __syncwarp();  // buffer sb is restaged two batches from now
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Shared memory of k_tscatter for NT tiles; bucket placement is used when it fits.
 constexpr size_t kSmemOptIn = 227 * 1024 - 1024;  // dynamic opt-in (static smem of the kernels < 1 KB)
-size_t tscatter_smem_base(int NT) { return (size_t)NT * 4 + (size_t)((NT + 1) & ~1) * kBkWarps * 2; }
+size_t tscatter_smem_base(int NT) {
+  const size_t off_w = ((size_t)(NT + 32) * 4 + 15) & ~size_t(15);
+  const size_t off_stage = (off_w + (size_t)((NT + 33) & ~1) * kBkWarps * 2 + 15) & ~size_t(15);
+  return off_stage + (size_t)kBkWarps * 2 * kBkBatch * 6;
+}
 // arbitration slots per warp: 2^own_bits, the most (<= 4096) that still fit
 int tscatter_own_bits(int NT) {
   int bits = 12;
@@ -719,7 +752,7 @@ size_t tscatter_smem(int NT) { return tscatter_smem_base(NT) + ((size_t)kBkWarps
 
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
-  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, chist, tot, total;
+  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, chist, total;
   int64_t depth_parts, tile_parts;
 };
 
@@ -741,7 +774,8 @@ Layout make_layout(int64_t P, int64_t cap, int NT) {
   L.lb_scan0 = take(scan_parts * 8);
   L.lb_scan1 = take(scan_parts * 8);
   L.lb_depth = take(4 * L.depth_parts * 256 * sizeof(uint32_t));
-  L.lb_tile = take(2 * L.tile_parts * 256 * sizeof(uint32_t));
+  // tile passes' look-back (radix mode) or k_tscan's tile-total chain (bucket mode)
+  L.lb_tile = take(std::max<size_t>(2 * L.tile_parts * 256 * sizeof(uint32_t), ((size_t)NT / 32 + 2) * 8));
   L.zero_end = o;
   L.dk0 = take(P * 4);
   L.dk1 = take(P * 4);
@@ -752,8 +786,7 @@ Layout make_layout(int64_t P, int64_t cap, int NT) {
   L.tk1 = take(cap * 2);
   L.tv0 = take(cap * 4);
   L.tv1 = take(cap * 4);
-  L.chist = take((size_t)kBkMaxChunks * NT * 4);
-  L.tot = take((size_t)NT * 4);
+  L.chist = take((size_t)kBkMaxChunks * ((NT + 3) & ~3) * 4);
   L.total = o;
   return L;
 }
@@ -849,11 +882,10 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
     // chunks: a multiple of the SMs (CTAs resident per SM by shared memory), each < 2^16 keys
     const size_t smem = tscatter_smem(NT);
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, kSmemOptIn / (smem + 1024)));
-    const int64_t need = (cap + 65000 - 1) / 65000;
+    const int64_t need = (cap + 63000 - 1) / 63000;  // chunks (rounded up to 2048 keys) stay < 2^16 keys
     const int C = (int)std::max<int64_t>(std::min<int64_t>((int64_t)nsm * per_sm, kBkMaxChunks), need);
     if (C <= kBkMaxChunks) {
       uint32_t* chist = reinterpret_cast<uint32_t*>(w + L.chist);
-      uint32_t* tot = reinterpret_cast<uint32_t*>(w + L.tot);
       int2* rng = reinterpret_cast<int2*>(tile_ranges);
       int tile_bits = 1;
       while ((1 << tile_bits) < NT) ++tile_bits;
@@ -866,8 +898,9 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
         attr_set = true;
       }
       k_tcount<<<C, kBkThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, chist);
-      k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, tot);
-      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, tot, rng, sorted_ids,
+      k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, ctr, reinterpret_cast<unsigned long long*>(lbt),
+                                                    rng);
+      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
                                              tscatter_own_bits(NT));
       count_launch(3);
       return finish_bin(ctr, cap, num_keys_host, s);
