@@ -142,21 +142,26 @@ class Trainer:
         # another view's rendering (the views of a batch are independent until the
         # projection backward sums them, R21)
         n_streams = max(1, int(streams))
-        # bin-ahead (GSR_BIN_STREAMS=n > 0, views in flight only): every view's
-        # projection + binning runs on one of n streams into its own view buffer (a ring
-        # of streams + 2n buffers), ahead of the render streams, which only wait for
-        # their view's lists.  Measured 1-10% SLOWER than running each view's whole
-        # chain on its render stream (scannetpp: n = 1/2/3 -> 7.24/6.74/6.65 vs 6.58 ms):
-        # the binning kernels get no SM room while the render kernels fill the GPU, so
-        # the render streams wait for them either way.  Default 0 (off).
+        # bin-ahead (views in flight only): every view's projection + binning runs on
+        # one of n = GSR_BIN_STREAMS (default 8) streams of the highest priority into its
+        # own view buffer (a ring of streams + n buffers), ahead of the render streams,
+        # which only wait for their view's lists; the binning kernels' CTAs are then
+        # dispatched before pending render CTAs.  scannetpp: 6.30 -> 6.245 ms/step vs
+        # each view's whole chain on its render stream (GSR_BIN_STREAMS=0); with 1-3
+        # bin streams of normal priority it was 1-10% slower (their kernels wait behind
+        # the render CTAs that fill the GPU).
         nb = os.environ.get("GSR_BIN_STREAMS")
-        self.n_bin = (int(nb) if nb is not None else 0) if n_streams > 1 else 0
-        n_bufs = n_streams + 2 * self.n_bin
+        self.n_bin = (int(nb) if nb is not None else 8) if n_streams > 1 else 0
+        n_bufs = n_streams + self.n_bin
         self.bufs = [ViewBuffers(lib, cameras[0], cap_p, key_capacity, device) for _ in range(n_bufs)]
         self.buf = self.bufs[0]
         # (equal priorities: staggering the streams' priorities measured 4% slower)
         self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
-        self._bin_streams = [torch.cuda.Stream(device=device) for _ in range(self.n_bin)]
+        self._bin_streams = []
+        if self.n_bin:
+            bp = os.environ.get("GSR_BIN_PRIO")
+            bp = int(bp) if bp is not None else torch.cuda.Stream.priority_range()[1]  # highest
+            self._bin_streams = [torch.cuda.Stream(device=device, priority=bp) for _ in range(self.n_bin)]
         P = max(cap_p, 1)
         # per in-flight view: projection flags and screen-space gradients (zeroed once;
         # gs_project_bwd_views leaves them zero again).  Two slot sets when a step has
