@@ -480,11 +480,15 @@ def test_batched_views_backward_matches_per_view(lib):
         assert int(torch.count_nonzero(sg)) == 0
 
 
-@pytest.mark.parametrize("host", [False, True])
-def test_trainer_streams_match_single_stream(lib, host):
+@pytest.mark.parametrize("host,bins", [(False, None), (True, None), (False, "0"), (False, "2")])
+def test_trainer_streams_match_single_stream(lib, host, bins, monkeypatch):
     """Views in flight on 3 streams (own buffers each) give the same iteration as one
     stream: 11 distinct views, chunks of 4, so sgrad / flag slots are reused across
-    projection-backward chains within a step; host=True also streams the targets."""
+    projection-backward chains within a step; host=True also streams the targets.
+    bins: GSR_BIN_STREAMS (None = the default bin-ahead streams; "0" = each view's whole
+    chain on its render stream; "2" = a ring of 5 view buffers, reused within a step)."""
+    if bins is not None:
+        monkeypatch.setenv("GSR_BIN_STREAMS", bins)
     w = workload("small")
     cams = [scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.03 * (k - 5)),
                                [0.05 * (k - 5), 0.02 * k, 0.0]) for k in range(11)]
