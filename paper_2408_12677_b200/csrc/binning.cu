@@ -496,6 +496,10 @@ __global__ void k_ranges(const uint16_t* __restrict__ skeys, const Counters* __r
 //               the same stable sort, in ~3 passes of 2-6 B/key and no look-back.
 // ---------------------------------------------------------------------------
 constexpr int kBkThreads = 256, kBkWarps = kBkThreads / 32;
+#ifndef GSR_TSC_WARPS
+#define GSR_TSC_WARPS 8
+#endif
+constexpr int kTsWarps = GSR_TSC_WARPS, kTsThreads = 32 * kTsWarps;  // k_tscatter: warps (sub-chunks) per chunk
 constexpr int kBkMaxChunks = 512;  // chist capacity (workspace); C = min(this, SMs x CTAs/SM)
 
 constexpr int kBkBatch = 256;  // keys per staged batch of a warp (32 lanes x 8 keys)
@@ -503,10 +507,10 @@ constexpr int kBkBatch = 256;  // keys per staged batch of a warp (32 lanes x 8 
 // sub-chunk sizes are multiples of kBkBatch, so every sub-chunk starts 16-B aligned in
 // the key (u16) and value (u32) arrays (vector loads, cp.async staging).
 __device__ __forceinline__ void chunk_bounds(int64_t K, int C, int c, int w, int64_t& a, int64_t& b) {
-  constexpr int64_t q = (int64_t)kBkWarps * kBkBatch;
+  constexpr int64_t q = (int64_t)kTsWarps * kBkBatch;
   const int64_t chunk = ((K + C - 1) / C + q - 1) / q * q;
   const int64_t k0 = min(K, (int64_t)c * chunk), k1 = min(K, k0 + chunk);
-  const int64_t sub = chunk / kBkWarps;
+  const int64_t sub = chunk / kTsWarps;
   a = min(k1, k0 + (int64_t)w * sub);
   b = min(k1, a + sub);
 }
@@ -562,7 +566,7 @@ __global__ void __launch_bounds__(kTcThreads) k_tcount(const uint16_t* __restric
   int64_t a, b;
   chunk_bounds(K, C, blockIdx.x, 0, a, b);
   const int64_t k0 = a;
-  chunk_bounds(K, C, blockIdx.x, kBkWarps - 1, a, b);
+  chunk_bounds(K, C, blockIdx.x, kTsWarps - 1, a, b);
   const int64_t k1 = b;
   count_keys<false>(tkeys, k0, k1, threadIdx.x, kTcThreads, s_cnt);
   __syncthreads();
@@ -637,7 +641,7 @@ __device__ __forceinline__ uint32_t tile_peers(uint32_t t, bool valid, int bits)
   return peers;
 }
 
-__global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restrict__ tkeys,
+__global__ void __launch_bounds__(kTsThreads) k_tscatter(const uint16_t* __restrict__ tkeys,
                                                          const uint32_t* __restrict__ tvals,
                                                          const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
                                                          int tile_bits, const uint32_t* __restrict__ chist,
@@ -651,8 +655,8 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   const int NTx = NT + 32;
   const int NTp = (NTx + 1) & ~1;                          // even row stride: 4-B aligned rows
   const size_t off_w = ((size_t)NTx * 4 + 15) & ~size_t(15);
-  const size_t off_stage = (off_w + (size_t)NTp * kBkWarps * 2 + 15) & ~size_t(15);
-  const size_t off_own = off_stage + (size_t)kBkWarps * 2 * kBkBatch * 6;
+  const size_t off_stage = (off_w + (size_t)NTp * kTsWarps * 2 + 15) & ~size_t(15);
+  const size_t off_own = off_stage + (size_t)kTsWarps * 2 * kBkBatch * 6;
   char* s_bytes = reinterpret_cast<char*>(s_dyn);
   uint16_t* s_w = reinterpret_cast<uint16_t*>(s_bytes + off_w);  // [8][NTp] per-warp count, then running offset
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -661,9 +665,9 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   // this chunk's row of global positions (k_tscan) -> s_base: all 16-B pieces in flight
   // at once (cp.async) instead of one L2 round trip per loop iteration
   const uint32_t* ch = chist + (int64_t)blockIdx.x * ((NT + 3) & ~3);
-  for (int i = threadIdx.x; i < (NT + 3) / 4; i += kBkThreads) cp_async16_bin(s_base + 4 * i, ch + 4 * i);
+  for (int i = threadIdx.x; i < (NT + 3) / 4; i += kTsThreads) cp_async16_bin(s_base + 4 * i, ch + 4 * i);
   asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int i = threadIdx.x; i < NTp * kBkWarps / 2; i += kBkThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
+  for (int i = threadIdx.x; i < NTp * kTsWarps / 2; i += kTsThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
   int64_t a, b;
   chunk_bounds(K, C, blockIdx.x, warp, a, b);
   uint16_t* my = s_w + (int64_t)warp * NTp;
@@ -689,10 +693,10 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
   // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
   count_keys<true>(tkeys, a, b, lane, 32, reinterpret_cast<uint32_t*>(my));
   __syncthreads();
-  for (int t = threadIdx.x; t < NT; t += kBkThreads) {
+  for (int t = threadIdx.x; t < NT; t += kTsThreads) {
     uint32_t run = 0;
 #pragma unroll
-    for (int w = 0; w < kBkWarps; ++w) {
+    for (int w = 0; w < kTsWarps; ++w) {
       const uint32_t v = s_w[w * NTp + t];
       s_w[w * NTp + t] = (uint16_t)run;
       run += v;
@@ -743,16 +747,16 @@ __global__ void __launch_bounds__(kBkThreads) k_tscatter(const uint16_t* __restr
 constexpr size_t kSmemOptIn = 227 * 1024 - 1024;  // dynamic opt-in (static smem of the kernels < 1 KB)
 size_t tscatter_smem_base(int NT) {
   const size_t off_w = ((size_t)(NT + 32) * 4 + 15) & ~size_t(15);
-  const size_t off_stage = (off_w + (size_t)((NT + 33) & ~1) * kBkWarps * 2 + 15) & ~size_t(15);
-  return off_stage + (size_t)kBkWarps * 2 * kBkBatch * 6;
+  const size_t off_stage = (off_w + (size_t)((NT + 33) & ~1) * kTsWarps * 2 + 15) & ~size_t(15);
+  return off_stage + (size_t)kTsWarps * 2 * kBkBatch * 6;
 }
 // arbitration slots per warp: 2^own_bits, the most (<= 4096) that still fit
 int tscatter_own_bits(int NT) {
   int bits = 12;
-  while (bits > 5 && tscatter_smem_base(NT) + ((size_t)kBkWarps << bits) > kSmemOptIn) --bits;
+  while (bits > 5 && tscatter_smem_base(NT) + ((size_t)kTsWarps << bits) > kSmemOptIn) --bits;
   return bits;
 }
-size_t tscatter_smem(int NT) { return tscatter_smem_base(NT) + ((size_t)kBkWarps << tscatter_own_bits(NT)); }
+size_t tscatter_smem(int NT) { return tscatter_smem_base(NT) + ((size_t)kTsWarps << tscatter_own_bits(NT)); }
 
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
@@ -904,7 +908,7 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
       k_tcount<<<C, kTcThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, chist);
       k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, ctr, reinterpret_cast<unsigned long long*>(lbt),
                                                     rng);
-      k_tscatter<<<C, kBkThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
+      k_tscatter<<<C, kTsThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
                                              tscatter_own_bits(NT));
       count_launch(3);
       return finish_bin(ctr, cap, num_keys_host, s);
