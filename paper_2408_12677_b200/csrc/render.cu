@@ -633,7 +633,9 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
   return any;
 }
 
-template <int WPC>
+// kMasks: the forward's per-key block masks are given (key_blocks != NULL; the
+// product path) -- a compile-time switch, so the key loop carries no test for it.
+template <int WPC, bool kMasks>
 __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
@@ -686,7 +688,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       const int l = max(rg.x, h - 32);
       if (l + lane < h) {
         id = ids[l + lane];
-        kb = key_blocks ? (uint32_t)key_blocks[l + lane] : 0xffu;
+        kb = kMasks ? (uint32_t)key_blocks[l + lane] : 0xffu;
       }
     }
   };
@@ -717,10 +719,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
     cp_async_wait<1>();
     __syncwarp();
     if (lo + lane < hi && kb_cur) {
-      if (key_blocks)
-        stage_fast<false>(s_rec[warp][buf][lane], ox, oy);
-      else
-        stage_fast<true>(s_rec[warp][buf][lane], ox, oy);
+      stage_fast<!kMasks>(s_rec[warp][buf][lane], ox, oy);
     }
     __syncwarp();
     uint32_t live = __ballot_sync(kFull, kb_cur != 0);
@@ -731,7 +730,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       const uint32_t fl = __float_as_uint(q2.w);
       const int pos = lo + j - rg.x;
       uint32_t m;
-      if (key_blocks) {
+      if constexpr (kMasks) {
         m = __shfl_sync(kFull, kb_cur, j);  // blocks the forward composited this key in
       } else {
         m = fl & 0xffu;
@@ -1129,9 +1128,14 @@ template <int WPC>
 void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                     const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1) {
-  k_render_bwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
-      cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-      g_rgb, g_depth, key_blocks, sgrad, l1);
+  if (key_blocks)
+    k_render_bwd<WPC, true><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+        cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
+        g_rgb, g_depth, key_blocks, sgrad, l1);
+  else
+    k_render_bwd<WPC, false><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+        cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
+        g_rgb, g_depth, key_blocks, sgrad, l1);
 }
 #endif
 
