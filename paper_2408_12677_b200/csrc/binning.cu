@@ -496,21 +496,18 @@ __global__ void k_ranges(const uint16_t* __restrict__ skeys, const Counters* __r
 //               the same stable sort, in ~3 passes of 2-6 B/key and no look-back.
 // ---------------------------------------------------------------------------
 constexpr int kBkThreads = 256, kBkWarps = kBkThreads / 32;
-#ifndef GSR_TSC_WARPS
-#define GSR_TSC_WARPS 8
-#endif
-constexpr int kTsWarps = GSR_TSC_WARPS, kTsThreads = 32 * kTsWarps;  // k_tscatter: warps (sub-chunks) per chunk
+// k_tscatter runs W = 8 warps (sub-chunks) per chunk (GSR_TSC_WARPS=4: 4, A/B only).
 constexpr int kBkMaxChunks = 512;  // chist capacity (workspace); C = min(this, SMs x CTAs/SM)
 
 constexpr int kBkBatch = 256;  // keys per staged batch of a warp (32 lanes x 8 keys)
 // Chunk c = keys [c chunk, (c + 1) chunk), cut into 8 warp sub-chunks; chunk and
 // sub-chunk sizes are multiples of kBkBatch, so every sub-chunk starts 16-B aligned in
 // the key (u16) and value (u32) arrays (vector loads, cp.async staging).
-__device__ __forceinline__ void chunk_bounds(int64_t K, int C, int c, int w, int64_t& a, int64_t& b) {
-  constexpr int64_t q = (int64_t)kTsWarps * kBkBatch;
+__device__ __forceinline__ void chunk_bounds(int64_t K, int C, int W, int c, int w, int64_t& a, int64_t& b) {
+  const int64_t q = (int64_t)W * kBkBatch;
   const int64_t chunk = ((K + C - 1) / C + q - 1) / q * q;
   const int64_t k0 = min(K, (int64_t)c * chunk), k1 = min(K, k0 + chunk);
-  const int64_t sub = chunk / kTsWarps;
+  const int64_t sub = chunk / W;
   a = min(k1, k0 + (int64_t)w * sub);
   b = min(k1, a + sub);
 }
@@ -557,16 +554,16 @@ constexpr int kTcThreads = 1024;
 
 __global__ void __launch_bounds__(kTcThreads) k_tcount(const uint16_t* __restrict__ tkeys,
                                                        const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
-                                                       uint32_t* __restrict__ chist) {
+                                                       int W, uint32_t* __restrict__ chist) {
   extern __shared__ uint32_t s_cnt[];  // [NT]
   for (int t = threadIdx.x; t < NT; t += kTcThreads) s_cnt[t] = 0;
   __syncthreads();
   int64_t K = (int64_t)ctr->K;
   if (K > cap) K = 0;
   int64_t a, b;
-  chunk_bounds(K, C, blockIdx.x, 0, a, b);
+  chunk_bounds(K, C, W, blockIdx.x, 0, a, b);
   const int64_t k0 = a;
-  chunk_bounds(K, C, blockIdx.x, kTsWarps - 1, a, b);
+  chunk_bounds(K, C, W, blockIdx.x, W - 1, a, b);
   const int64_t k1 = b;
   count_keys<false>(tkeys, k0, k1, threadIdx.x, kTcThreads, s_cnt);
   __syncthreads();
@@ -641,7 +638,8 @@ __device__ __forceinline__ uint32_t tile_peers(uint32_t t, bool valid, int bits)
   return peers;
 }
 
-__global__ void __launch_bounds__(kTsThreads) k_tscatter(const uint16_t* __restrict__ tkeys,
+template <int kTsWarps>
+__global__ void __launch_bounds__(32 * kTsWarps) k_tscatter(const uint16_t* __restrict__ tkeys,
                                                          const uint32_t* __restrict__ tvals,
                                                          const Counters* __restrict__ ctr, int64_t cap, int NT, int C,
                                                          int tile_bits, const uint32_t* __restrict__ chist,
@@ -665,11 +663,11 @@ __global__ void __launch_bounds__(kTsThreads) k_tscatter(const uint16_t* __restr
   // this chunk's row of global positions (k_tscan) -> s_base: all 16-B pieces in flight
   // at once (cp.async) instead of one L2 round trip per loop iteration
   const uint32_t* ch = chist + (int64_t)blockIdx.x * ((NT + 3) & ~3);
-  for (int i = threadIdx.x; i < (NT + 3) / 4; i += kTsThreads) cp_async16_bin(s_base + 4 * i, ch + 4 * i);
+  for (int i = threadIdx.x; i < (NT + 3) / 4; i += (32 * kTsWarps)) cp_async16_bin(s_base + 4 * i, ch + 4 * i);
   asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int i = threadIdx.x; i < NTp * kTsWarps / 2; i += kTsThreads) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
+  for (int i = threadIdx.x; i < NTp * kTsWarps / 2; i += (32 * kTsWarps)) reinterpret_cast<uint32_t*>(s_w)[i] = 0;
   int64_t a, b;
-  chunk_bounds(K, C, blockIdx.x, warp, a, b);
+  chunk_bounds(K, C, kTsWarps, blockIdx.x, warp, a, b);
   uint16_t* my = s_w + (int64_t)warp * NTp;
   // per-warp tile -> lane arbitration slots (hashed by the low own_bits of the tile id)
   uint8_t* own = reinterpret_cast<uint8_t*>(s_bytes + off_own) + ((int64_t)warp << own_bits);
@@ -693,7 +691,7 @@ __global__ void __launch_bounds__(kTsThreads) k_tscatter(const uint16_t* __restr
   // per-warp counts: packed 16-bit increments on 32-bit words (a chunk has < 2^16 keys)
   count_keys<true>(tkeys, a, b, lane, 32, reinterpret_cast<uint32_t*>(my));
   __syncthreads();
-  for (int t = threadIdx.x; t < NT; t += kTsThreads) {
+  for (int t = threadIdx.x; t < NT; t += (32 * kTsWarps)) {
     uint32_t run = 0;
 #pragma unroll
     for (int w = 0; w < kTsWarps; ++w) {
@@ -745,18 +743,26 @@ __global__ void __launch_bounds__(kTsThreads) k_tscatter(const uint16_t* __restr
 
 // Shared memory of k_tscatter for NT tiles; bucket placement is used when it fits.
 constexpr size_t kSmemOptIn = 227 * 1024 - 1024;  // dynamic opt-in (static smem of the kernels < 1 KB)
-size_t tscatter_smem_base(int NT) {
+size_t tscatter_smem_base(int NT, int W) {
   const size_t off_w = ((size_t)(NT + 32) * 4 + 15) & ~size_t(15);
-  const size_t off_stage = (off_w + (size_t)((NT + 33) & ~1) * kTsWarps * 2 + 15) & ~size_t(15);
-  return off_stage + (size_t)kTsWarps * 2 * kBkBatch * 6;
+  const size_t off_stage = (off_w + (size_t)((NT + 33) & ~1) * W * 2 + 15) & ~size_t(15);
+  return off_stage + (size_t)W * 2 * kBkBatch * 6;
 }
-// arbitration slots per warp: 2^own_bits, the most (<= 4096) that still fit
-int tscatter_own_bits(int NT) {
+// arbitration slots per warp: 2^own_bits, the most (<= 4096) that still fit (0: none fit)
+int tscatter_own_bits(int NT, int W) {
   int bits = 12;
-  while (bits > 5 && tscatter_smem_base(NT) + ((size_t)kTsWarps << bits) > kSmemOptIn) --bits;
-  return bits;
+  while (bits >= 10 && tscatter_smem_base(NT, W) + ((size_t)W << bits) > kSmemOptIn) --bits;
+  return bits >= 10 ? bits : 0;
 }
-size_t tscatter_smem(int NT) { return tscatter_smem_base(NT) + ((size_t)kTsWarps << tscatter_own_bits(NT)); }
+size_t tscatter_smem(int NT, int W) { return tscatter_smem_base(NT, W) + ((size_t)W << tscatter_own_bits(NT, W)); }
+// warps per tscatter CTA: 8 if it fits with >= 1024 slots per warp, else 0 (radix tile
+// passes).  GSR_TSC_WARPS=4 forces 4 warps where they fit -- measured slower than 8
+// (scannetpp) and than the radix passes (config 4: bin 340 vs 288 us/view).
+int tscatter_warps(int NT) {
+  const char* e = std::getenv("GSR_TSC_WARPS");
+  if (e && std::strcmp(e, "4") == 0) return tscatter_own_bits(NT, 4) ? 4 : 0;
+  return tscatter_own_bits(NT, 8) ? 8 : 0;
+}
 
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
@@ -804,7 +810,7 @@ Layout make_layout(int64_t P, int64_t cap, int NT) {
 bool use_bucket(int NT) {
   const char* e = std::getenv("GSR_TILE_SORT");
   if (e && std::strcmp(e, "radix") == 0) return false;
-  return tscatter_smem(NT) <= kSmemOptIn;
+  return tscatter_warps(NT) > 0;
 }
 
 }  // namespace
@@ -888,7 +894,8 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   count_launch();
   if (use_bucket(NT)) {
     // chunks: a multiple of the SMs (CTAs resident per SM by shared memory), each < 2^16 keys
-    const size_t smem = tscatter_smem(NT);
+    const int W = tscatter_warps(NT);
+    const size_t smem = tscatter_smem(NT, W);
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(4, kSmemOptIn / (smem + 1024)));
     const int64_t need = (cap + 63000 - 1) / 63000;  // chunks (rounded up to 2048 keys) stay < 2^16 keys
     const int C = (int)std::max<int64_t>(std::min<int64_t>((int64_t)nsm * per_sm, kBkMaxChunks), need);
@@ -899,17 +906,23 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
       while ((1 << tile_bits) < NT) ++tile_bits;
       static bool attr_set = false;  // opt-in shared memory above 48 KB (once per process)
       if (!attr_set) {
-        if (cudaFuncSetAttribute(k_tscatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) !=
+        if (cudaFuncSetAttribute(k_tscatter<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_tscatter<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) !=
                 cudaSuccess ||
             cudaFuncSetAttribute(k_tcount, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemOptIn) != cudaSuccess)
           return check_launch("gs_bin_tiles smem opt-in");
         attr_set = true;
       }
-      k_tcount<<<C, kTcThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, chist);
+      k_tcount<<<C, kTcThreads, (size_t)NT * 4, s>>>(tk0, ctr, cap, NT, C, W, chist);
       k_tscan<<<(NT + 31) / 32, kBkThreads, 0, s>>>(chist, NT, C, ctr, reinterpret_cast<unsigned long long*>(lbt),
                                                     rng);
-      k_tscatter<<<C, kTsThreads, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
-                                             tscatter_own_bits(NT));
+      if (W == 8)
+        k_tscatter<8><<<C, 256, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
+                                           tscatter_own_bits(NT, 8));
+      else
+        k_tscatter<4><<<C, 128, smem, s>>>(tk0, tv0, ctr, cap, NT, C, tile_bits, chist, sorted_ids,
+                                           tscatter_own_bits(NT, 4));
       count_launch(3);
       return finish_bin(ctr, cap, num_keys_host, s);
     }
