@@ -41,10 +41,11 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of whole iterations (N = 1)")
     ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "8")),
                     help="views chained per projection-backward pass (<= 8)")
-    ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated"],
+    ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated", "sparse"],
                     help="N > 1: fused peer-memory reduce-scatter+Adam+all-gather kernel (falls back to 'sharded' if "
-                         "symmetric memory is unavailable), NCCL reduce-scatter + sharded Adam + all-gather, or "
-                         "NCCL all-reduce + replicated Adam")
+                         "symmetric memory is unavailable), NCCL reduce-scatter + sharded Adam + all-gather, "
+                         "NCCL all-reduce + replicated Adam, or the visibility-sparse exchange (all-reduce of the "
+                         "union-visible gradient columns only) + replicated Adam")
     ap.add_argument("--no-naive", action="store_true", help="skip the K13 per-pixel-port comparison arm")
     ap.add_argument("--schedule", action="store_true",
                     help="keyframe-scheduled online + global optimisation run (PAPER.md:149; SURVEY §8(f) NEXT-1)")
@@ -498,6 +499,8 @@ def main():
             model.params = model.params.clone()
             model.grad = model.grad.clone()
             optimizer, optim_used = None, "sharded (peer unavailable on another rank)"
+    if dist_on and batched and args.optim == "sparse":
+        optimizer, optim_used = pipeline.SparseExchangeAdam(lib, model), "visibility-sparse exchange, replicated"
     if dist_on and batched and optimizer is None and args.optim in ("peer", "sharded"):
         optimizer = pipeline.ShardedAdam(lib, model)
         optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
@@ -771,6 +774,10 @@ def main():
                          "measured on up to 8 of this rank's views after the timed region"},
         "roofline": roof, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "naive_port": naive, "eager": eager,
     }
+    if getattr(tr.optimizer, "last_M", None) is not None:  # visibility-sparse exchange: columns on the wire
+        line["exchange"] = {"union_visible_columns": tr.optimizer.last_M, "P": model.P,
+                            "bytes_per_rank": 4 * model.F * tr.optimizer.last_M,
+                            "dense_bytes_per_rank": 4 * model.F * model.P}
     print(json.dumps(line), flush=True)
     if dist_on:
         dist.destroy_process_group()

@@ -301,6 +301,34 @@ gs_status gs_adam_step_peers(const gs_scene* scene /*HOST*/, int world, int rank
                              float* m, float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps,
                              int64_t step, int64_t begin, int64_t end, void* stream);
 
+/* ---------------------------------------------------------------- visibility-sparse exchange
+ * (SURVEY.md §8(f) NEXT-2 "visibility-sparse gradient exchange: union of visible masks,
+ * then compaction").  A Gaussian culled in every view of every rank has
+ * an exactly zero gradient on every rank, so only the columns of the union of the
+ * ranks' visible sets need to cross the wire:
+ *   gs_visibility_union: visible[i] = 1 if flags[v][i] lacks GS_FLAG_CULLED for some
+ *     v < n_views, else 0; accumulate != 0 ORs into the existing visible[i] instead
+ *     (flags: HOST array of n_views DEVICE uint8[P], gs_project's flags; visible:
+ *     DEVICE uint8[P]).  The ranks then combine their masks (an all-reduce MAX of P
+ *     bytes).
+ *   gs_compact_index: idx[0..M) = the i with visible[i] != 0, ascending (so every rank
+ *     derives the same list from the same mask); *count_dev (DEVICE int64) = M.
+ *     ws: scratch of gs_compact_workspace(P) bytes.  idx: DEVICE int32[P] (capacity).
+ *   gs_gather_columns: packed[r][j] = full[r][idx[j]] for r < F, j < M (full: [F][S],
+ *     packed: [F][M], both DEVICE float).
+ *   gs_scatter_columns: full[r][idx[j]] = packed[r][j] (other columns untouched).
+ * M is read by the host between the calls (the collective's size); P, F >= 0, S >= P,
+ * else GS_ERR_ARG; NULL pointers with a nonzero size, GS_ERR_ARG. */
+gs_status gs_visibility_union(int n_views, const uint8_t* const* flags /*HOST[n_views]*/, int64_t P, int accumulate,
+                              uint8_t* visible, void* stream);
+size_t gs_compact_workspace(int64_t P);
+gs_status gs_compact_index(const uint8_t* visible, int64_t P, void* ws, size_t ws_bytes, int32_t* idx,
+                           int64_t* count_dev, void* stream);
+gs_status gs_gather_columns(const float* full, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* packed,
+                            void* stream);
+gs_status gs_scatter_columns(const float* packed, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* full,
+                             void* stream);
+
 /* ---------------------------------------------------------------- layout (setup)
  * gs_spatial_order: params_out = params_in with the Gaussians (columns) permuted into
  * Morton (Z-curve) order of their means, 10 bits per axis inside the means'

@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-SOURCES = ["api.cu", "project.cu", "project_bwd.cu", "binning.cu", "render.cu", "optim.cu", "naive.cu", "schedule.cpp", "tsdf.cu", "seed.cu", "frame.cu"]
+SOURCES = ["api.cu", "project.cu", "project_bwd.cu", "binning.cu", "render.cu", "optim.cu", "naive.cu", "schedule.cpp", "tsdf.cu", "seed.cu", "frame.cu", "exchange.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIBS = {"libgsr.so": [], "libgsr_exact.so": ["-DGSR_EXACT_EXP"]}
 

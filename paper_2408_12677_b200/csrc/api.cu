@@ -481,6 +481,63 @@ gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, co
   return check_launch("gs_l1_loss_grad");
 }
 
+gs_status gs_visibility_union(int n_views, const uint8_t* const* flags, int64_t P, int accumulate, uint8_t* visible,
+                              void* stream) {
+  g_err[0] = 0;
+  if (n_views < 0 || P < 0 || (P > 0 && !visible) || (n_views > 0 && !flags)) {
+    set_error("gs_visibility_union: n_views=%d P=%lld", n_views, (long long)P);
+    return GS_ERR_ARG;
+  }
+  for (int v = 0; v < n_views; ++v)
+    if (P > 0 && !flags[v]) {
+      set_error("gs_visibility_union: flags[%d] is NULL", v);
+      return GS_ERR_ARG;
+    }
+  if (P == 0) return GS_OK;
+  if (n_views == 0 && accumulate) return GS_OK;
+  launch_vis_union(n_views, flags, P, accumulate != 0, visible, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_visibility_union");
+}
+
+size_t gs_compact_workspace(int64_t P) { return P < 0 ? 0 : compact_workspace(P); }
+
+gs_status gs_compact_index(const uint8_t* visible, int64_t P, void* ws, size_t ws_bytes, int32_t* idx,
+                           int64_t* count_dev, void* stream) {
+  g_err[0] = 0;
+  if (P < 0 || !count_dev || !ws || (P > 0 && (!visible || !idx))) {
+    set_error("gs_compact_index: P=%lld (NULL pointer)", (long long)P);
+    return GS_ERR_ARG;
+  }
+  if (ws_bytes < compact_workspace(P)) {
+    set_error("gs_compact_index: workspace %zu B < required %zu B", ws_bytes, compact_workspace(P));
+    return GS_ERR_ARG;
+  }
+  launch_compact_index(visible, P, static_cast<uint32_t*>(ws), idx, count_dev, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_compact_index");
+}
+
+gs_status gs_gather_columns(const float* full, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* packed,
+                            void* stream) {
+  g_err[0] = 0;
+  if (F < 0 || S < 0 || M < 0 || M > S || (F > 0 && M > 0 && (!full || !idx || !packed))) {
+    set_error("gs_gather_columns: F=%lld S=%lld M=%lld", (long long)F, (long long)S, (long long)M);
+    return GS_ERR_ARG;
+  }
+  launch_gather_cols(full, F, S, idx, M, packed, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_gather_columns");
+}
+
+gs_status gs_scatter_columns(const float* packed, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* full,
+                             void* stream) {
+  g_err[0] = 0;
+  if (F < 0 || S < 0 || M < 0 || M > S || (F > 0 && M > 0 && (!full || !idx || !packed))) {
+    set_error("gs_scatter_columns: F=%lld S=%lld M=%lld", (long long)F, (long long)S, (long long)M);
+    return GS_ERR_ARG;
+  }
+  launch_scatter_cols(packed, F, S, idx, M, full, static_cast<cudaStream_t>(stream));
+  return check_launch("gs_scatter_columns");
+}
+
 gs_status gs_decode_rgbd(int32_t width, int32_t height, const uint8_t* rgb, const uint16_t* depth, float depth_scale,
                          float* out_rgb, float* out_depth, void* stream) {
   g_err[0] = 0;

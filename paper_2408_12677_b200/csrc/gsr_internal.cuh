@@ -109,6 +109,17 @@ gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const flo
 void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
                float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s);
 
+// exchange.cu
+size_t compact_workspace(int64_t P);
+void launch_vis_union(int n_views, const uint8_t* const* flags, int64_t P, bool accumulate, uint8_t* visible,
+                      cudaStream_t s);
+void launch_compact_index(const uint8_t* visible, int64_t P, uint32_t* tile_cnt, int32_t* idx, int64_t* count,
+                          cudaStream_t s);
+void launch_gather_cols(const float* full, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* packed,
+                        cudaStream_t s);
+void launch_scatter_cols(const float* packed, int64_t F, int64_t S, const int32_t* idx, int64_t M, float* full,
+                         cudaStream_t s);
+
 // frame.cu
 void launch_decode_rgbd(int64_t npix, const uint8_t* rgb, const uint16_t* depth, float scale, float* out_rgb,
                         float* out_d, cudaStream_t s);

@@ -140,10 +140,17 @@ class Library:
         lib.gs_seed_gaussians.argtypes = [vp, vp, GsTsdfVolume, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         lib.gs_decode_rgbd.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_float, vp, vp, vp]
+        lib.gs_visibility_union.argtypes = [C.c_int, vp, i64, C.c_int, vp, vp]
+        lib.gs_compact_workspace.argtypes = [i64]
+        lib.gs_compact_workspace.restype = C.c_size_t
+        lib.gs_compact_index.argtypes = [vp, i64, vp, C.c_size_t, vp, vp, vp]
+        lib.gs_gather_columns.argtypes = [vp, i64, i64, vp, i64, vp, vp]
+        lib.gs_scatter_columns.argtypes = [vp, i64, i64, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",  # noqa: E501
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
                    "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
-                   "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd"):
+                   "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd", "gs_visibility_union", "gs_compact_index",
+                   "gs_gather_columns", "gs_scatter_columns"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -234,6 +241,29 @@ class Library:
         sg = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in sgrads])
         return self._check("gs_project_bwd_views", self.lib.gs_project_bwd_views(
             n, cam_arr, C.byref(sc), _ptr(params), fl, sg, _ptr(grad), 1 if accumulate else 0, _stream(stream)))
+
+    # -- visibility-sparse exchange (NEXT-2) -------------------------------
+    def visibility_union(self, flags, P, visible, accumulate=False, stream=None):
+        """flags: list of device uint8 tensors (gs_project flags); visible: uint8[P]."""
+        n = len(flags)
+        fl = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in flags])
+        return self._check("gs_visibility_union", self.lib.gs_visibility_union(
+            n, fl, int(P), 1 if accumulate else 0, _ptr(visible), _stream(stream)))
+
+    def compact_workspace(self, P) -> int:
+        return int(self.lib.gs_compact_workspace(int(P)))
+
+    def compact_index(self, visible, P, ws, idx, count, stream=None):
+        return self._check("gs_compact_index", self.lib.gs_compact_index(
+            _ptr(visible), int(P), _ptr(ws), ws.numel() * ws.element_size(), _ptr(idx), _ptr(count), _stream(stream)))
+
+    def gather_columns(self, full, F, S, idx, M, packed, stream=None):
+        return self._check("gs_gather_columns", self.lib.gs_gather_columns(
+            _ptr(full), int(F), int(S), _ptr(idx), int(M), _ptr(packed), _stream(stream)))
+
+    def scatter_columns(self, packed, F, S, idx, M, full, stream=None):
+        return self._check("gs_scatter_columns", self.lib.gs_scatter_columns(
+            _ptr(packed), int(F), int(S), _ptr(idx), int(M), _ptr(full), _stream(stream)))
 
     def spatial_order(self, sc, params_in, params_out, perm=None, stream=None):
         ws = torch.empty(max(int(self.lib.gs_spatial_order_workspace(C.byref(sc))), 16), dtype=torch.uint8,

@@ -431,6 +431,8 @@ class Trainer:
         self._hook("project_bwd", "begin")
         self.lib.project_bwd_views(gcams, self.model.desc, self.model.params, self.flags[base:base + n],
                                    self.sgrad[base:base + n], self.model.grad, accumulate=accumulate)
+        if n and hasattr(self.optimizer, "note_views"):  # visibility-sparse exchange: this chunk's views
+            self.optimizer.note_views(self.flags[base:base + n])
         self._hook("project_bwd", "end")
 
     def check_capacity(self) -> int:
@@ -540,6 +542,72 @@ class ShardedAdam:
         else:
             parts = list(self.ppad.view(self.world, self.shard).unbind(0))
             d.all_gather(parts, self.pshard, group=self.group)
+
+
+class SparseExchangeAdam:
+    """Visibility-sparse gradient exchange + replicated Adam (SURVEY.md §8(f) NEXT-2,
+    "union of visible masks, then compaction").  A Gaussian culled in
+    every view of every rank has an exactly zero gradient on every rank (the first
+    projection-backward chain of a step writes those columns as zeros), so only the
+    columns of the union of the ranks' visible sets are summed across ranks:
+
+      note_views(flags): visible |= the views' visible sets (gs_visibility_union; the
+                         Trainer calls it after each projection-backward chain)
+      step():            all-reduce MAX of the P-byte mask -> ordered compaction
+                         (gs_compact_index; M = the union's size, read by the host) ->
+                         gather the M gradient columns (gs_gather_columns) -> all-reduce
+                         SUM of F x M floats -> scatter them back (gs_scatter_columns)
+                         -> replicated Adam over every column (gs_adam_step; the
+                         moments of unseen Gaussians decay as in the dense step).
+
+    Every rank reduces the same packed array and runs the same Adam, so the parameters
+    stay bit-identical across ranks.  ``ops`` replaces the device calls with the same
+    signatures (the CPU gloo tests pass torch implementations)."""
+
+    def __init__(self, lib, model: GaussianModel, group=None, ops=None):
+        import torch.distributed as dist
+        self.dist, self.group, self.lib, self.model = dist, group, lib, model
+        dev = model.params.device
+        S = model.P_stride
+        self.visible = torch.zeros(S, dtype=torch.uint8, device=dev)
+        self.idx = torch.zeros(S, dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.packed = torch.empty(model.F * S, dtype=torch.float32, device=dev)
+        self.ops = ops if ops is not None else self._device_ops(lib)
+        self.ws = torch.empty(max(1, self.ops["compact_workspace"](S)), dtype=torch.uint8, device=dev)
+        self.last_M = None
+        self._fresh = True  # the next note_views starts a new step's union
+
+    def _device_ops(self, lib):
+        m = self.model
+        return {
+            "union": lambda flags, P, vis, acc: lib.visibility_union(flags, P, vis, accumulate=acc),
+            "compact_workspace": lib.compact_workspace,
+            "compact": lambda vis, P, ws, idx, cnt: lib.compact_index(vis, P, ws, idx, cnt),
+            "gather": lambda full, F, S, idx, M, packed: lib.gather_columns(full, F, S, idx, M, packed),
+            "scatter": lambda packed, F, S, idx, M, full: lib.scatter_columns(packed, F, S, idx, M, full),
+            "adam": lambda: lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False),
+        }
+
+    def note_views(self, flags):
+        self.ops["union"](list(flags), self.model.P, self.visible, not self._fresh)
+        self._fresh = False
+
+    def step(self):
+        d, m, o = self.dist, self.model, self.ops
+        P, F, S = m.P, m.F, m.P_stride
+        if self._fresh:  # no view this step: nothing is visible
+            self.visible.zero_()
+        d.all_reduce(self.visible[:P], op=d.ReduceOp.MAX, group=self.group)
+        o["compact"](self.visible, P, self.ws, self.idx, self.count)
+        M = int(self.count.item())  # the collective's size
+        packed = self.packed[:F * M].view(F, M)
+        o["gather"](m.grad, F, S, self.idx, M, packed)
+        d.all_reduce(packed, op=d.ReduceOp.SUM, group=self.group)
+        o["scatter"](packed, F, S, self.idx, M, m.grad)
+        o["adam"]()
+        self.last_M = M
+        self._fresh = True
 
 
 class PeerShardedAdam:

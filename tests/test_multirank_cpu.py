@@ -154,3 +154,92 @@ def test_gloo_two_ranks_sharded_adam_matches_replicated():
                                 np.array(pipeline.lr_per_row(0), np.float32), 1, P=S)
     np.testing.assert_array_equal(out["params"][0], out["params"][1])  # bit-identical across ranks
     np.testing.assert_allclose(out["params"][0].reshape(F, S), ref, rtol=1e-6, atol=1e-7)
+
+
+def _torch_sparse_ops(model):
+    """CPU stand-ins with the device calls' signatures (test only)."""
+    from oracle import gsref
+
+    def union(flags, P, vis, acc):
+        u = torch.zeros(P, dtype=torch.bool)
+        for f in flags:
+            u |= (f[:P] & 128) == 0
+        vis[:P] = (vis[:P].bool() | u).to(torch.uint8) if acc else u.to(torch.uint8)
+
+    def compact(vis, P, ws, idx, cnt):
+        nz = torch.nonzero(vis[:P]).flatten().to(torch.int32)
+        idx[:len(nz)] = nz
+        cnt[0] = len(nz)
+
+    def gather(full, F, S, idx, M, packed):
+        packed.copy_(full[:, idx[:M].long()])
+
+    def scatter(packed, F, S, idx, M, full):
+        full[:, idx[:M].long()] = packed
+
+    def adam():
+        S = model.P_stride
+        p1, m1, v1 = gsref.adam_step(model.params.numpy().astype(np.float64), model.grad.numpy().astype(np.float64),
+                                     model.m.numpy().astype(np.float64), model.v.numpy().astype(np.float64),
+                                     np.array(model.lr, np.float32), model.step_count, P=S)
+        model.params.copy_(torch.from_numpy(p1.astype(np.float32)))
+        model.m.copy_(torch.from_numpy(m1.astype(np.float32)))
+        model.v.copy_(torch.from_numpy(v1.astype(np.float32)))
+
+    return {"union": union, "compact_workspace": lambda P: 16, "compact": compact, "gather": gather,
+            "scatter": scatter, "adam": adam}
+
+
+def _sparse_worker(rank, world, port, out):
+    """pipeline.SparseExchangeAdam on gloo: each rank's gradient is zero outside the
+    columns its views see; only the union's columns are all-reduced."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_12677_b200 import pipeline
+    w, _ = _views()
+    model = pipeline.GaussianModel(w.scene, torch.device("cpu"))
+    P = model.P
+    rng = np.random.default_rng(200 + rank)
+    flags = [torch.from_numpy(np.where(rng.random(P + 16) < 0.3, 0, 128).astype(np.uint8)) for _ in range(2)]
+    seen = np.zeros(model.P_stride, bool)
+    for f in flags:
+        seen[:P] |= (f.numpy()[:P] & 128) == 0
+    g = rng.normal(size=model.grad.shape).astype(np.float32) * seen[None, :]
+    model.grad.copy_(torch.from_numpy(g))
+    opt = pipeline.SparseExchangeAdam(None, model, ops=_torch_sparse_ops(model))
+    opt.note_views(flags[:1])
+    opt.note_views(flags[1:])
+    g_local = model.grad.clone()
+    model.step_count += 1
+    opt.step()
+    gathered = [torch.zeros(model.params.numel()) for _ in range(world)]
+    dist.all_gather(gathered, model.params.reshape(-1).contiguous())
+    glist = [torch.zeros(g_local.numel()) for _ in range(world)]
+    dist.all_gather(glist, g_local.reshape(-1).contiguous())
+    seen_all = [torch.zeros(model.P_stride, dtype=torch.uint8) for _ in range(world)]
+    dist.all_gather(seen_all, torch.from_numpy(seen.astype(np.uint8)))
+    if rank == 0:
+        out["params"] = [x.numpy().copy() for x in gathered]
+        out["grads"] = [x.numpy().copy() for x in glist]
+        out["seen"] = [x.numpy().copy() for x in seen_all]
+        out["M"] = opt.last_M
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_sparse_exchange_matches_dense():
+    from oracle import gsref
+    from paper_2408_12677_b200 import pipeline
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sparse_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    w, _ = _views()
+    F, S = w.scene.params.shape
+    union = (out["seen"][0] | out["seen"][1]).astype(bool)
+    assert out["M"] == int(union.sum()) and 0 < out["M"] < w.scene.P
+    gsum = (out["grads"][0].astype(np.float32) + out["grads"][1].astype(np.float32)).astype(np.float64)
+    z = np.zeros((F, S))
+    ref, _, _ = gsref.adam_step(w.scene.params.astype(np.float64), gsum.reshape(F, S), z, z,
+                                np.array(pipeline.lr_per_row(0), np.float32), 1, P=S)
+    np.testing.assert_array_equal(out["params"][0], out["params"][1])  # bit-identical across ranks
+    np.testing.assert_array_equal(out["params"][0].reshape(F, S), ref.astype(np.float32))
