@@ -144,12 +144,15 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(int64_t P, const int32
   const int64_t base = (int64_t)part * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t flag = 0;
   unsigned long long cnt = 0;
+  uint32_t zk[kScanItems];  // depth keys of the visible items, gathered before the scan so
+                            // their latency overlaps the scan and the look-back
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     const int64_t i = base + k;
     const bool vis = i < P && tiles[i] > 0;
     flag |= (vis ? 1u : 0u) << k;
     cnt += vis;
+    zk[k] = vis ? __float_as_uint(rec[12 * i + 2]) : 0u;  // z > z_near > 0: bits order = value order
   }
   unsigned long long total;
   const unsigned long long excl = block_excl_scan256<unsigned long long>(cnt, s_warp, total);
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(kScanThreads) k_compact(int64_t P, const int32
   for (int k = 0; k < kScanItems; ++k) {
     if (flag >> k & 1) {
       const int64_t i = base + k;
-      const uint32_t key = __float_as_uint(rec[12 * i + 2]);  // z > z_near > 0: bits order = value order
+      const uint32_t key = zk[k];
       dkeys[pos] = key;
       dvals[pos] = (uint32_t)i;
       atomicAdd(&s_hist[0][key & 255], 1u);
