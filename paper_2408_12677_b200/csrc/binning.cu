@@ -258,6 +258,8 @@ __device__ __forceinline__ int64_t warp_search(const uint32_t* __restrict__ offs
   return lo;
 }
 
+// kHist: also the 2 x 256-bin tile-key histograms (needed by the radix tile passes only)
+template <bool kHist>
 __global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict__ sorted_gid,
                                                      const uint32_t* __restrict__ offs, const float* __restrict__ rec,
                                                      int TX, const Counters* __restrict__ ctr, int64_t cap,
@@ -322,17 +324,19 @@ __global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict_
           const uint32_t tile = (uint32_t)((y0 + row) * TX + x0 + col);
           kk[q] = (uint16_t)tile;
           vv[q] = gid;
-          atomicAdd(&s_hist[0][tile & 255], 1u);
-          const uint32_t hb = tile >> 8;
-          if (hb != hb_run) {
-            if (hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
-            hb_run = hb, hb_cnt = 0;
+          if (kHist) {
+            atomicAdd(&s_hist[0][tile & 255], 1u);
+            const uint32_t hb = tile >> 8;
+            if (hb != hb_run) {
+              if (kHist && hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
+              hb_run = hb, hb_cnt = 0;
+            }
+            ++hb_cnt;
           }
-          ++hb_cnt;
           if (++col == w) col = 0, ++row;
         }
       }
-      if (hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
+      if (kHist && hb_cnt) atomicAdd(&s_hist[1][hb_run], hb_cnt);
       if (nk == kEmItems) {
         uint4 k4;
         k4.x = kk[0] | ((uint32_t)kk[1] << 16);
@@ -350,10 +354,12 @@ __global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict_
     }
     __syncthreads();
   }
-  __syncthreads();
-  for (int i = t; i < 512; i += kEmThreads) {
-    const uint32_t c = (&s_hist[0][0])[i];
-    if (c) atomicAdd(&ghist[i], c);
+  if (kHist) {
+    __syncthreads();
+    for (int i = t; i < 512; i += kEmThreads) {
+      const uint32_t c = (&s_hist[0][0])[i];
+      if (c) atomicAdd(&ghist[i], c);
+    }
   }
 }
 
@@ -893,9 +899,15 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
                                                reinterpret_cast<long long*>(num_keys_dev));
   count_launch();
   const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * 4);
-  k_emit<<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0, ghist + 4 * 256);
+  const bool bucket = use_bucket(NT);
+  if (bucket)
+    k_emit<false><<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0,
+                                                                ghist + 4 * 256);
+  else
+    k_emit<true><<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0,
+                                                               ghist + 4 * 256);
   count_launch();
-  if (use_bucket(NT)) {
+  if (bucket) {
     // chunks: a multiple of the SMs (CTAs resident per SM by shared memory), each < 2^16 keys
     const int W = tscatter_warps(NT);
     const size_t smem = tscatter_smem(NT, W);
