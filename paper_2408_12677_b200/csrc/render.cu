@@ -58,6 +58,9 @@ namespace {
 #ifndef GSR_BWD_PAIR
 #define GSR_BWD_PAIR 1
 #endif
+#ifndef GSR_DEAD_EVERY
+#define GSR_DEAD_EVERY 8  // forward: keys between re-checks of the blocks whose pixels all terminated
+#endif
 #ifndef GSR_DENSE_FWD
 #define GSR_DENSE_FWD 3
 #endif
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       }
 #endif
       kb_mine = (lane == j) ? cm : kb_mine;
-      if (++since == 8) {
+      if (++since == GSR_DEAD_EVERY) {
         since = 0;
         bdone = dead_blocks(px);
         if (bdone == 0xffu) break;
