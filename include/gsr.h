@@ -125,6 +125,14 @@ int gs_exact_exp(void);           /* 1 in the GSR_EXACT_EXP debug build (libgsr_
 gs_status gs_project(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
                      gs_proj out, void* stream);
 
+/* gs_project for n_views cameras in one pass over the parameters (the projection of a
+ * batch of views, R21): outs[v] receives exactly what gs_project(&cams[v], ...) would
+ * write (bit-identical: the per-view arithmetic is the same), but the parameter rows
+ * are read once per batch of up to 8 views instead of once per view.  cams, outs:
+ * HOST arrays of n_views.  Errors as gs_project (per camera and output). */
+gs_status gs_project_views(int n_views, const gs_camera* cams /*HOST[n_views]*/, const gs_scene* scene /*HOST*/,
+                           const float* params, const gs_proj* outs /*HOST[n_views]*/, void* stream);
+
 /* ---------------------------------------------------------------- gs_bin_tiles
  * Duplicates every visible Gaussian into one key per touched tile and orders the
  * keys by (tile id = ty * tiles_x + tx, depth z, Gaussian index) (R12):

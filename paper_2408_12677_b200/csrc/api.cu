@@ -155,6 +155,29 @@ gs_status gs_project(const gs_camera* cam, const gs_scene* scene, const float* p
   return check_launch("gs_project");
 }
 
+gs_status gs_project_views(int n_views, const gs_camera* cams, const gs_scene* scene, const float* params,
+                           const gs_proj* outs, void* stream) {
+  g_err[0] = 0;
+  if (n_views < 0 || (n_views > 0 && (!cams || !outs))) {
+    set_error("gs_project_views: n_views=%d (NULL cams/outs)", n_views);
+    return GS_ERR_ARG;
+  }
+  GS_TRY(check_scene(scene, "gs_project_views"));
+  std::vector<DevCam> dc((size_t)n_views);
+  for (int v = 0; v < n_views; ++v) {
+    GS_TRY(check_camera(&cams[v], "gs_project_views"));
+    if (scene->P > 0)
+      GS_TRY(check_ptrs("gs_project_views", {{outs[v].rec, "outs.rec"}, {outs[v].radius, "outs.radius"},
+                                             {outs[v].tiles, "outs.tiles"}, {outs[v].flags, "outs.flags"}}));
+    dc[(size_t)v] = make_devcam(cams[v]);
+  }
+  if (scene->P == 0 || n_views == 0) return GS_OK;
+  GS_TRY(check_ptrs("gs_project_views", {{params, "params"}}));
+  launch_project_views(n_views, dc.data(), scene->P, scene->P_stride, scene->sh_degree, params, outs,
+                       static_cast<cudaStream_t>(stream));
+  return check_launch("gs_project_views");
+}
+
 size_t gs_bin_tiles_workspace(const gs_camera* cam, int64_t P, int64_t key_capacity) {
   if (!cam || P < 0 || key_capacity < 0) return 0;
   const int nt = ((cam->width + kTile - 1) / kTile) * ((cam->height + kTile - 1) / kTile);

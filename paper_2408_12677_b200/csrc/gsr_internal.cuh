@@ -64,6 +64,8 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 void launch_project(const DevCam& cam, int64_t P, int64_t P_stride, int deg, const float* params, gs_proj out,
                     cudaStream_t s);
 constexpr int kMaxViews = 8;  // views chained per pass of the projection backward
+void launch_project_views(int n_views, const DevCam* cams, int64_t P, int64_t S, int deg, const float* params,
+                          const gs_proj* outs, cudaStream_t s);
 void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* const* flags, float* const* sgrads,
                               int64_t P, int64_t S, int deg, const float* params, float* grad, int accumulate,
                               cudaStream_t s);

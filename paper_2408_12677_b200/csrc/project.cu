@@ -284,6 +284,103 @@ __global__ void __launch_bounds__(kPjThreads) k_project(DevCam cam, int64_t P, i
   }
 }
 
+// K1 over a batch of <= 8 views (gs_project_views): the 11 geometry rows (and, if a
+// Gaussian of the CTA is visible in any view, the SH rows) are staged ONCE for all the
+// views, instead of once per view.  Pass 1 computes O1-O7 for every view and writes
+// each view's record geometry, radius and tiles; pass 2 computes the colour (O8) of
+// every view's visible Gaussians and writes the colour and the flags.  The per-view
+// arithmetic is k_project's, so every output is bit-identical to gs_project's.
+struct ViewOuts {
+  DevCam cam[kMaxViews];
+  float4* rec[kMaxViews];
+  int32_t* radius[kMaxViews];
+  int32_t* tiles[kMaxViews];
+  uint8_t* flags[kMaxViews];
+  int n;
+};
+
+template <int DEG>
+__global__ void __launch_bounds__(kPjThreads) k_project_views(const __grid_constant__ ViewOuts vo, int64_t P, int64_t S,
+                                                              const float* __restrict__ prm) {
+  constexpr int NK = (DEG + 1) * (DEG + 1), NSH = 3 * NK;
+  __shared__ __align__(16) float s_geo[11][kPjThreads];
+  __shared__ __align__(16) float s_sh[NSH][kPjThreads];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPjThreads;
+  const int64_t ncol = S - i0 < kPjThreads ? S - i0 : (int64_t)kPjThreads;
+  const uint32_t bytes = (uint32_t)ncol * 4u;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar, 11u * bytes);
+#pragma unroll 1
+    for (int r = 0; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar);
+  }
+  mbar_wait(&bar, 0);
+  const int64_t i = i0 + tid;
+  uint64_t fl8 = 0;  // view v's flags in byte v
+  bool any = false;
+#pragma unroll 1
+  for (int v = 0; v < vo.n; ++v) {
+    Geom g;
+    g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
+    if (i < P)
+      g = project_geom_one(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
+                           [&](int row) { return s_geo[row][tid]; });
+    fl8 |= (uint64_t)g.flags << (8 * v);
+    if (g.rad > 0) {
+      any = true;
+      float4* r4 = vo.rec[v] + 3 * i;
+      r4[0] = g.q0;
+      r4[1] = make_float4(g.q1.x, g.q1.y, g.q1.z, 0.f);
+      r4[2] = make_float4(0.f, 0.f, __uint_as_float(g.rx), __uint_as_float(g.ry));
+    }
+    if (i < P) {
+      vo.radius[v][i] = g.rad;
+      vo.tiles[v][i] = g.ntiles;
+    }
+  }
+  if (__syncthreads_or(any)) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar, (uint32_t)NSH * bytes);
+#pragma unroll 1
+      for (int r = 0; r < NSH; ++r) bulk_g2s(s_sh[r], prm + (11 + r) * S + i0, bytes, &bar);
+    }
+    mbar_wait(&bar, 1);
+#pragma unroll 1
+    for (int v = 0; v < vo.n; ++v) {
+      uint8_t f = (uint8_t)(fl8 >> (8 * v));
+      if (f & GS_FLAG_CULLED) continue;
+      // O8: SH colour at the mean's viewing direction (R13); k_project's arithmetic
+      const DevCam& cam = vo.cam[v];
+      const float vx = s_geo[0][tid] - cam.ocam[0], vy = s_geo[1][tid] - cam.ocam[1], vz = s_geo[2][tid] - cam.ocam[2];
+      const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+      const float x = vx * inv, y = vy * inv, z = vz * inv;
+      float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        float Y, gx, gy, gz;
+        sh_term(k, x, y, z, Y, gx, gy, gz);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) acc[ch] = fmaf(s_sh[3 * k + ch][tid], Y, acc[ch]);
+      }
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        acc[ch] += 0.5f;
+        if (acc[ch] < 0.f) f |= (uint8_t)(1u << ch);
+        acc[ch] = fmaxf(acc[ch], 0.f);
+      }
+      float* r = reinterpret_cast<float*>(vo.rec[v] + 3 * i);
+      r[7] = acc[0];
+      *reinterpret_cast<float2*>(r + 8) = make_float2(acc[1], acc[2]);
+      fl8 = (fl8 & ~((uint64_t)0xff << (8 * v))) | ((uint64_t)f << (8 * v));
+    }
+  }
+  if (i < P)
+    for (int v = 0; v < vo.n; ++v) vo.flags[v][i] = (uint8_t)(fl8 >> (8 * v));
+}
+
 // Persistent, software-pipelined variant (GSR_PROJECT=pipe; slower, kept for A/B): grid = a few CTAs per SM, each
 // walking tiles blockIdx.x, blockIdx.x + gridDim.x, ...  The geometry rows of the NEXT
 // tile are bulk-copied (double buffer, one mbarrier per buffer) while the current
@@ -398,6 +495,29 @@ int project_mode() {
 }
 
 }  // namespace
+
+void launch_project_views(int n_views, const DevCam* cams, int64_t P, int64_t S, int deg, const float* params,
+                          const gs_proj* outs, cudaStream_t s) {
+  const int grid = (int)((P + kPjThreads - 1) / kPjThreads);
+  for (int v0 = 0; v0 < n_views; v0 += kMaxViews) {
+    ViewOuts vo{};
+    vo.n = std::min(kMaxViews, n_views - v0);
+    for (int v = 0; v < vo.n; ++v) {
+      vo.cam[v] = cams[v0 + v];
+      vo.rec[v] = reinterpret_cast<float4*>(outs[v0 + v].rec);
+      vo.radius[v] = outs[v0 + v].radius;
+      vo.tiles[v] = outs[v0 + v].tiles;
+      vo.flags[v] = outs[v0 + v].flags;
+    }
+    switch (deg) {
+      case 0: k_project_views<0><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+      case 1: k_project_views<1><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+      case 2: k_project_views<2><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+      default: k_project_views<3><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+    }
+    count_launch();
+  }
+}
 
 void launch_project(const DevCam& cam, int64_t P, int64_t S, int deg, const float* params, gs_proj out,
                     cudaStream_t s) {

@@ -140,6 +140,7 @@ class Library:
         lib.gs_seed_gaussians.argtypes = [vp, vp, GsTsdfVolume, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_keyframe_schedule.argtypes = [vp, i64, vp, vp, vp, i64, vp, vp]
         lib.gs_decode_rgbd.argtypes = [C.c_int32, C.c_int32, vp, vp, C.c_float, vp, vp, vp]
+        lib.gs_project_views.argtypes = [C.c_int, vp, vp, vp, vp, vp]
         lib.gs_visibility_union.argtypes = [C.c_int, vp, i64, C.c_int, vp, vp]
         lib.gs_compact_workspace.argtypes = [i64]
         lib.gs_compact_workspace.restype = C.c_size_t
@@ -150,7 +151,7 @@ class Library:
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
                    "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
                    "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd", "gs_visibility_union", "gs_compact_index",
-                   "gs_gather_columns", "gs_scatter_columns"):
+                   "gs_gather_columns", "gs_scatter_columns", "gs_project_views"):
             getattr(lib, fn).restype = i32
         self.lib = lib
         self.exact = bool(lib.gs_exact_exp())
@@ -171,6 +172,14 @@ class Library:
     def project(self, cam: GsCamera, sc: GsScene, params, proj: GsProj, stream=None):
         return self._check("gs_project", self.lib.gs_project(C.byref(cam), C.byref(sc), _ptr(params), proj,
                                                              _stream(stream)))
+
+    def project_views(self, cams, sc: GsScene, params, projs, stream=None):
+        """cams: list of GsCamera; projs: list of GsProj (one per view)."""
+        n = len(cams)
+        cam_arr = (GsCamera * max(n, 1))(*cams)
+        out_arr = (GsProj * max(n, 1))(*projs)
+        return self._check("gs_project_views", self.lib.gs_project_views(n, cam_arr, C.byref(sc), _ptr(params),
+                                                                         out_arr, _stream(stream)))
 
     def bin_tiles_workspace(self, cam: GsCamera, P: int, key_capacity: int) -> int:
         return int(self.lib.gs_bin_tiles_workspace(C.byref(cam), int(P), int(key_capacity)))

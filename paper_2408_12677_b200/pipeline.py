@@ -204,14 +204,16 @@ class Trainer:
         self._render_view(v, slot, b, gcam, proj, order, t_rgb, t_depth, targets_ready, targets_consumed)
         return gcam
 
-    def _bin_view(self, v: int, slot: int, b):
-        """gs_project -> gs_bin_tiles (-> gs_tile_order) of view v into buffer b."""
+    def _bin_view(self, v: int, slot: int, b, projected=False):
+        """gs_project (unless ``projected``: done by a batched gs_project_views) ->
+        gs_bin_tiles (-> gs_tile_order) of view v into buffer b."""
         lib, m, cam = self.lib, self.model, self.cameras[v]
         gcam = gsr.camera(cam)
         proj = gsr.GsProj(b.proj.rec, b.proj.radius, b.proj.tiles, self.flags[slot].data_ptr())
-        self._hook("project", "begin")
-        lib.project(gcam, m.desc, m.params, proj)
-        self._hook("project", "end")
+        if not projected:
+            self._hook("project", "begin")
+            lib.project(gcam, m.desc, m.params, proj)
+            self._hook("project", "end")
         self._hook("bin", "begin")
         lib.bin_tiles(gcam, m.desc, proj, b.bin_ws, b.key_capacity, b.sorted_ids, b.ranges,
                       num_keys_dev=self.num_keys[v:v + 1])
@@ -221,6 +223,29 @@ class Trainer:
             order = b.tile_order
         self._hook("bin", "end")
         return gcam, proj, order
+
+    def _project_chunk(self, views, k0, base, buf_ev, chain_ev):
+        """Bin-ahead mode, at the first view of a chunk: gs_project_views of the chunk's
+        views (the parameters read once instead of once per view) on the first bin
+        stream, when none of their buffers or slots is still in use this step (else
+        None: each view projects itself).  Returns the event the bins wait for."""
+        n = min(self.chunk, len(views) - k0)
+        bis = [(k0 + j) % len(self.bufs) for j in range(n)]
+        if (os.environ.get("GSR_PROJECT_VIEWS", "1") == "0" or chain_ev is not None or len(set(bis)) < n
+                or any(buf_ev[bi] is not None for bi in bis)):
+            return None
+        m = self.model
+        cams = [gsr.camera(self.cameras[views[k0 + j]]) for j in range(n)]
+        projs = [gsr.GsProj(self.bufs[bi].proj.rec, self.bufs[bi].proj.radius, self.bufs[bi].proj.tiles,
+                            self.flags[base + j].data_ptr()) for j, bi in enumerate(bis)]
+        bs = self._bin_streams[0]
+        with torch.cuda.stream(bs):
+            self._hook("project", "begin")
+            self.lib.project_views(cams, m.desc, m.params, projs)
+            self._hook("project", "end")
+            ev = torch.cuda.Event()
+            ev.record(bs)
+        return ev
 
     def _render_view(self, v, slot, b, gcam, proj, order, t_rgb, t_depth, targets_ready, targets_consumed):
         """gs_render_fwd -> (L1) -> gs_render_bwd_screen of view v from buffer b."""
@@ -332,6 +357,7 @@ class Trainer:
                 s.wait_event(start)
         pending, done = [], []
         buf_ev = [None] * len(self.bufs)  # per view buffer: the render that last read it (this step)
+        proj_ev = None  # bin-ahead: the batched projection of the current chunk (or None)
         n_sets = self._n_sets if S > 1 else 1
         chain_ev = [None] * n_sets  # per slot set: the chain that last consumed it
         first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
@@ -344,12 +370,16 @@ class Trainer:
             elif self.n_bin:  # bin-ahead: project + bin on a bin stream, render on a render stream
                 slot, bi = base + len(pending), k % len(self.bufs)
                 b, bs, s = self.bufs[bi], self._bin_streams[k % self.n_bin], self._streams[k % S]
+                if not pending:  # a new chunk: project its views in one pass if nothing waits
+                    proj_ev = self._project_chunk(views, k, base, buf_ev, chain_ev[n_chain % n_sets])
                 if chain_ev[n_chain % n_sets] is not None:  # this slot was consumed by that chain
                     bs.wait_event(chain_ev[n_chain % n_sets])
                 if buf_ev[bi] is not None:  # the buffer's previous view has been rendered
                     bs.wait_event(buf_ev[bi])
+                if proj_ev is not None:
+                    bs.wait_event(proj_ev)
                 with torch.cuda.stream(bs):
-                    gcam, proj, order = self._bin_view(v, slot, b)
+                    gcam, proj, order = self._bin_view(v, slot, b, projected=proj_ev is not None)
                     binned = torch.cuda.Event()
                     binned.record(bs)
                 s.wait_event(binned)

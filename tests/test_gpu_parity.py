@@ -791,3 +791,33 @@ def test_fused_l1_backward_matches_separate(lib):
     a, c = sa.cpu().numpy().astype(np.float64), sb.cpu().numpy().astype(np.float64)
     assert np.abs(a).max() > 0
     assert grad_mismatch(c, a, rtol=1e-5, atol=1e-9).mean() <= 1e-4
+
+
+def test_project_views_bitexact_vs_project(lib):
+    """gs_project_views (one pass over the parameters for a batch of views) writes, for
+    every view, exactly gs_project's outputs: records of visible Gaussians, radius,
+    tiles, flags -- 11 views (two batches of <= 8), the Morton-ordered scannetpp scene."""
+    w = workload("scannetpp")
+    scene = w.scene
+    params = torch.from_numpy(scene.params).to(DEV)
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    cams = [w.cameras[k % len(w.cameras)] for k in range(11)]
+    cams[9] = scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(2.0), [0.0, 0.0, 0.0])  # other size
+    outs, refs = [], []
+    for cam in cams:
+        pa, ta = gsr.make_proj(scene.P, DEV)
+        pb, tb = gsr.make_proj(scene.P, DEV)
+        lib.project(gsr.camera(cam), sc, params, pb)
+        outs.append((pa, ta))
+        refs.append(tb)
+    lib.project_views([gsr.camera(c) for c in cams], sc, params, [o[0] for o in outs])
+    torch.cuda.synchronize()
+    for (pa, ta), tb in zip(outs, refs):
+        P = scene.P
+        for key in ("radius", "tiles", "flags"):
+            assert torch.equal(ta[key][:P], tb[key][:P]), key
+        vis = tb["radius"][:P] > 0
+        assert int(vis.sum()) > 0
+        ra = ta["rec"][:P][vis].view(torch.int32)
+        rb = tb["rec"][:P][vis].view(torch.int32)
+        assert torch.equal(ra[:, :10], rb[:, :10]) and torch.equal(ra[:, 10:12], rb[:, 10:12])
