@@ -52,8 +52,49 @@ struct Geom {
   uint8_t flags;
 };
 
+// O1-O2 (view independent): activations and Sigma.  ok = false for a degenerate
+// quaternion (culled in every view).
+struct Act {
+  float Sig[3][3];
+  float opa;
+  bool ok;
+};
+
 template <class Fetch>
-__device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, float py, float pz, Fetch fetch) {
+__device__ __forceinline__ Act project_act(Fetch fetch) {
+  Act a;
+  a.ok = false;
+  // O1: activations (R3-R5, R9)
+  const float l0 = fetch(3), l1 = fetch(4), l2 = fetch(5);
+  const float qw = fetch(6), qx = fetch(7), qy = fetch(8), qz = fetch(9);
+  const float logit = fetch(10);
+  float s[3];
+  s[0] = act_exp(l0);
+  s[1] = act_exp(l1);
+  s[2] = act_exp(l2);
+  const float qn = __fsqrt_rn(FA(FA(FA(FM(qw, qw), FM(qx, qx)), FM(qy, qy)), FM(qz, qz)));
+  if (!(qn > 0.f) || !finitef(qn)) return a;
+  a.opa = act_sigmoid(logit);
+  float R[3][3];
+  quat_to_rot(FD(qw, qn), FD(qx, qn), FD(qy, qn), FD(qz, qn), R);
+  // O2: Sigma = (R S)(R S)^T  (Eq. 2)
+  float M[3][3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) M[r][c] = FM(R[r][c], s[c]);
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) a.Sig[r][c] = FA(FA(FM(M[r][0], M[c][0]), FM(M[r][1], M[c][1])), FM(M[r][2], M[c][2]));
+  a.ok = true;
+  return a;
+}
+
+// O3 and O4-O7 of one view.  act(): the Gaussian's Act, called only if z_c > z_near
+// (so a Gaussian behind every camera never evaluates its activations).
+template <class ActFn>
+__device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float py, float pz, ActFn act) {
   Geom g;
   // O3: p_c = W p + t  (Eq. 4)
   const float* W = cam.R;
@@ -64,29 +105,9 @@ __device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, fl
   g.flags = GS_FLAG_CULLED;
   do {
     if (!(zc > cam.z_near)) break;  // R6, R23
-    // O1: activations (R3-R5, R9)
-    const float l0 = fetch(3), l1 = fetch(4), l2 = fetch(5);
-    const float qw = fetch(6), qx = fetch(7), qy = fetch(8), qz = fetch(9);
-    const float logit = fetch(10);
-    float s[3];
-    s[0] = act_exp(l0);
-    s[1] = act_exp(l1);
-    s[2] = act_exp(l2);
-    const float qn = __fsqrt_rn(FA(FA(FA(FM(qw, qw), FM(qx, qx)), FM(qy, qy)), FM(qz, qz)));
-    if (!(qn > 0.f) || !finitef(qn)) break;
-    const float opa = act_sigmoid(logit);
-    float R[3][3];
-    quat_to_rot(FD(qw, qn), FD(qx, qn), FD(qy, qn), FD(qz, qn), R);
-    // O2: Sigma = (R S)(R S)^T  (Eq. 2)
-    float M[3][3], Sig[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) M[r][c] = FM(R[r][c], s[c]);
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) Sig[r][c] = FA(FA(FM(M[r][0], M[c][0]), FM(M[r][1], M[c][1])), FM(M[r][2], M[c][2]));
+    const Act& A = act();
+    if (!A.ok) break;
+    const float (&Sig)[3][3] = A.Sig;
     // O4: mean projection (Eq. 4), R1
     const float ux = FD(xc, zc), uy = FD(yc, zc);
     const float mux = FA(FM(cam.fx, ux), cam.cx);
@@ -136,11 +157,20 @@ __device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, fl
     g.flags = ((uxc != ux) ? GS_FLAG_JCLAMP_X : 0) | ((uyc != uy) ? GS_FLAG_JCLAMP_Y : 0);
     const uint32_t rx = (uint32_t)x0 | ((uint32_t)x1 << 16);
     const uint32_t ry = (uint32_t)y0 | ((uint32_t)y1 << 16);
-    g.q0 = make_float4(mux, muy, zc, opa);
+    g.q0 = make_float4(mux, muy, zc, A.opa);
     g.q1 = make_float4(cA, cB, cC, 0.f);
     g.rx = rx, g.ry = ry;
   } while (0);
   return g;
+}
+
+template <class Fetch>
+__device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, float py, float pz, Fetch fetch) {
+  Act a;
+  return project_view(cam, px, py, pz, [&]() -> const Act& {
+    a = project_act(fetch);
+    return a;
+  });
 }
 
 // ---------------------------------------------------------------------------
@@ -286,7 +316,8 @@ __global__ void __launch_bounds__(kPjThreads) k_project(DevCam cam, int64_t P, i
 
 // K1 over a batch of <= 8 views (gs_project_views): the 11 geometry rows (and, if a
 // Gaussian of the CTA is visible in any view, the SH rows) are staged ONCE for all the
-// views, instead of once per view.  Pass 1 computes O1-O7 for every view and writes
+// views, instead of once per view, and the activations / Sigma (O1-O2) are evaluated
+// once per Gaussian.  Pass 1 computes O1-O7 for every view and writes
 // each view's record geometry, radius and tiles; pass 2 computes the colour (O8) of
 // every view's visible Gaussians and writes the colour and the flags.  The per-view
 // arithmetic is k_project's, so every output is bit-identical to gs_project's.
@@ -321,13 +352,20 @@ __global__ void __launch_bounds__(kPjThreads) k_project_views(const __grid_const
   const int64_t i = i0 + tid;
   uint64_t fl8 = 0;  // view v's flags in byte v
   bool any = false;
+  Act act;  // O1-O2, computed once (at the first view that needs them) for all views
+  bool have_act = false;
 #pragma unroll 1
   for (int v = 0; v < vo.n; ++v) {
     Geom g;
     g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
     if (i < P)
-      g = project_geom_one(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
-                           [&](int row) { return s_geo[row][tid]; });
+      g = project_view(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&]() -> const Act& {
+        if (!have_act) {
+          act = project_act([&](int row) { return s_geo[row][tid]; });
+          have_act = true;
+        }
+        return act;
+      });
     fl8 |= (uint64_t)g.flags << (8 * v);
     if (g.rad > 0) {
       any = true;
