@@ -33,6 +33,9 @@ namespace {
 #endif
 constexpr int kScanThreads = 256, kScanItems = GSR_SCAN_ITEMS, kScanTile = kScanThreads * kScanItems;
 constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32;
+#ifndef GSR_EMIT_PER_SM
+#define GSR_EMIT_PER_SM 4  // k_emit CTAs per SM (persistent, 2048 keys per iteration)
+#endif
 #ifndef GSR_DEPTH_ITEMS
 #define GSR_DEPTH_ITEMS 16  // 4096 depth keys per onesweep partition (4: 6.01, 8: 5.98, 16: 5.96 ms/step)
 #endif
@@ -901,7 +904,7 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
                                                reinterpret_cast<unsigned long long*>(w + L.lb_scan1), offs,
                                                reinterpret_cast<long long*>(num_keys_dev));
   count_launch();
-  const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * 4);
+  const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * GSR_EMIT_PER_SM);
   const bool bucket = use_bucket(NT);
   if (bucket)
     k_emit<false><<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0,
