@@ -36,10 +36,11 @@ constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32;
 #ifndef GSR_EMIT_PER_SM
 #define GSR_EMIT_PER_SM 4  // k_emit CTAs per SM (persistent, 2048 keys per iteration)
 #endif
-#ifndef GSR_DEPTH_ITEMS
-#define GSR_DEPTH_ITEMS 16  // 4096 depth keys per onesweep partition (4: 6.01, 8: 5.98, 16: 5.96 ms/step)
-#endif
-constexpr int kRsItemsKeys = 16, kRsItemsDepth = GSR_DEPTH_ITEMS;  // items per thread: tile-key / depth passes
+// Depth passes: 4 keys per thread (1024 per partition) for scenes below 512K
+// Gaussians (one view per step, latency-bound: more partitions finish sooner), 16 (4096)
+// above (views in flight: fewer, longer CTAs churn fewer SM slots against the render
+// kernels; scannetpp 6.01 -> 5.96 ms/step).  GSR_DEPTH_ITEMS=4|16 forces one.
+constexpr int kRsItemsKeys = 16, kRsItemsDepth = 4, kRsItemsDepthBig = 16;  // items per thread
 constexpr int kRsTileKeys = kRsThreads * kRsItemsKeys, kRsTileDepth = kRsThreads * kRsItemsDepth;
 constexpr uint32_t kLbAgg = 1u << 30, kLbInc = 2u << 30, kLbMask = (1u << 30) - 1;
 constexpr unsigned long long kScAgg = 1ull << 62, kScInc = 2ull << 62, kScMask = (1ull << 62) - 1;
@@ -885,11 +886,19 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   uint32_t* kout = dk1;
   uint32_t* vout = dv1;
   const bool rts_mode = use_rts();
+  const char* di = std::getenv("GSR_DEPTH_ITEMS");
+  const bool big = di ? std::atoi(di) == 16 : P >= (int64_t)1 << 19;
+  const int rs_grid_big =
+      (int)std::min<int64_t>((P + kRsThreads * kRsItemsDepthBig - 1) / (kRsThreads * kRsItemsDepthBig), (int64_t)nsm * 3);
   for (int pass = 0; pass < 4; ++pass) {
-    uint32_t* lb = lbd + (int64_t)pass * L.depth_parts * 256;
+    uint32_t* lb = lbd + (int64_t)pass * L.depth_parts * 256;  // sized for the smaller partitions
     if (rts_mode) {
       rts::radix_pass<uint32_t, kRsItemsDepth>(kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256, lb, L.depth_parts,
                                                8 * pass, s);
+    } else if (big) {
+      k_onesweep<uint32_t, kRsItemsDepthBig><<<std::max(rs_grid_big, 1), kRsThreads, 0, s>>>(
+          kin, vin, kout, vout, &ctr->V, P, ghist + pass * 256, lb, &ctr->part[2 + pass], 8 * pass);
+      count_launch();
     } else {
       k_onesweep<uint32_t, kRsItemsDepth><<<rs_grid_d, kRsThreads, 0, s>>>(kin, vin, kout, vout, &ctr->V, P,
                                                                            ghist + pass * 256, lb,
