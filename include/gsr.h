@@ -253,7 +253,8 @@ gs_status gs_naive_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_sce
  * of every pixel is computed inside the backward from the rendered rgb / depth (as
  * written by gs_render_fwd) and the target images, with exactly the values
  * gs_l1_loss_grad writes (sign(residual) / (3 npix) per colour channel, w_depth
- * sign / npix for depth, sign(0) = 0), and the loss (nullable DEVICE float) += L.
+ * sign / npix for depth, sign(0) = 0, invalid target samples masked as there, R43),
+ * and the loss (nullable DEVICE float) += L.
  * One kernel instead of gs_l1_loss_grad + gs_render_bwd_screen; no dL/d-image buffers.
  * P == 0 is valid (background-only images; the loss is still accumulated). */
 gs_status gs_render_bwd_screen_l1(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
@@ -466,6 +467,9 @@ gs_status gs_seed_gaussians(const gs_camera* cam /*HOST*/, const gs_tsdf_params*
 
 /* ---------------------------------------------------------------- harness: Eq. 12
  * L = mean_{pixel,ch} |C - C*| + w_depth mean_pixel |D - D*| (R19), sign(0) = 0.
+ * A target sample that is not a measurement -- a non-finite colour, or a depth <= 0
+ * (the sensor's "invalid", R41) or non-finite -- contributes neither loss nor
+ * gradient (R43; the means still divide by npix).
  * Writes dL/drgb [3][npix], dL/ddepth [npix]; loss (nullable DEVICE float) += L. */
 gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
                           const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 namespace {
@@ -49,6 +50,73 @@ inline float act_sigmoid(float x) { return (float)(1.0 / (1.0 + std::exp(-(doubl
 inline double act_sigmoid(double x) { return 1.0 / (1.0 + std::exp(-x)); }
 
 template <class T> inline bool finite(T v) { return std::isfinite(v); }
+
+// ---------------------------------------------------------------------------
+// Rn: a value carried in double together with a first-order RUNNING ERROR BOUND
+// (Wilkinson's running error analysis; Higham, "Accuracy and Stability of
+// Numerical Algorithms", §3.3).  Test infrastructure for the parity tolerance of
+// the GPU gradients, not a precision mode of the method: v is computed exactly as
+// in the MIXED mode's value track (same double operations, bit-identical), and m
+// bounds |fl32(x) - x| / u for an fp32 evaluation of the same expression, u = 2^-24,
+// to first order:
+//   a +- b : m_a + m_b + |a +- b|
+//   acc += t: m_acc + m_t + |t|          (accumulation, e.g. over pixels or views:
+//                                          each term charged once, so a sum costs
+//                                          sum |terms| whatever the order)
+//   a * b  : m_a |b| + |a| m_b + |ab|
+//   a / b  : m_a / |b| + |a/b| m_b / |b| + |a/b|
+//   sqrt a : m_a / (2 sqrt a) + sqrt a
+//   exp a  : e^a (m_a + |a| + 2)          (covers ex2.approx(a log2 e): the scaled
+//                                          argument's rounding and 2 ulp)
+// Inputs (fp32 parameters, camera, upstream fields) are exact (m = 0).  Decisions
+// are never taken on Rn values (the decision track is fp32, as in MIXED).
+// ---------------------------------------------------------------------------
+struct Rn {
+  double v = 0.0, m = 0.0;
+  Rn() = default;
+  Rn(double x) : v(x), m(0.0) {}  // NOLINT: implicit, exact constant / input
+  Rn(double x, double e) : v(x), m(e) {}
+  explicit operator double() const { return v; }
+  explicit operator int32_t() const { return (int32_t)v; }
+  Rn& operator+=(const Rn& t) {
+    v += t.v;
+    m = std::hypot(m, std::hypot(t.m, v));
+    return *this;
+  }
+};
+inline double q3(double a, double b, double c) { return std::sqrt(a * a + b * b + c * c); }
+inline Rn operator+(const Rn& a, const Rn& b) { return {a.v + b.v, q3(a.m, b.m, a.v + b.v)}; }
+inline Rn operator-(const Rn& a, const Rn& b) { return {a.v - b.v, q3(a.m, b.m, a.v - b.v)}; }
+inline Rn operator-(const Rn& a) { return {-a.v, a.m}; }
+inline Rn operator*(const Rn& a, const Rn& b) {
+  const double p = a.v * b.v;
+  return {p, q3(a.m * b.v, a.v * b.m, p)};
+}
+inline Rn operator/(const Rn& a, const Rn& b) {
+  const double q = a.v / b.v;
+  return {q, q3(a.m / b.v, q * b.m / b.v, q)};
+}
+inline bool operator<(const Rn& a, const Rn& b) { return a.v < b.v; }
+inline bool operator>(const Rn& a, const Rn& b) { return a.v > b.v; }
+inline bool operator<=(const Rn& a, const Rn& b) { return a.v <= b.v; }
+inline bool operator>=(const Rn& a, const Rn& b) { return a.v >= b.v; }
+inline bool operator==(const Rn& a, const Rn& b) { return a.v == b.v; }
+inline Rn sqrt(const Rn& a) {
+  const double r = std::sqrt(a.v);
+  return {r, std::hypot(r > 0.0 ? a.m / (2.0 * r) : 0.0, r)};
+}
+inline Rn ceil(const Rn& a) { return {std::ceil(a.v), 0.0}; }
+inline Rn floor(const Rn& a) { return {std::floor(a.v), 0.0}; }
+inline Rn act_exp(const Rn& a) {
+  const double e = std::exp(a.v);
+  return {e, e * std::hypot(a.m, std::hypot(a.v, 2.0))};
+}
+inline Rn act_sigmoid(const Rn& a) {
+  const double o = 1.0 / (1.0 + std::exp(-a.v));
+  return {o, std::hypot(o * (1.0 - o) * std::hypot(a.m, std::hypot(a.v, 2.0)), 2.0 * o)};
+}
+inline bool finite(const Rn& a) { return std::isfinite(a.v); }
+template <class T> constexpr bool kIsRn = std::is_same_v<T, Rn>;
 
 // ---------------------------------------------------------------------------
 // Real spherical harmonics, textbook definition (Condon-Shortley phase), in
@@ -193,6 +261,9 @@ template <class S> struct Fwd {
 
 template <class S>
 Fwd<S> project_one(const RefCamera& cam, int deg, const ParamView<S>& g) {
+  using std::ceil;
+  using std::floor;
+  using std::sqrt;
   Fwd<S> f{};
   f.culled = true;
   S W[3][3], t[3];
@@ -208,7 +279,7 @@ Fwd<S> project_one(const RefCamera& cam, int deg, const ParamView<S>& g) {
 
   // O1: activations (R3, R4, R5)
   for (int j = 0; j < 3; ++j) f.s[j] = act_exp(g.l[j]);
-  f.qn = std::sqrt(((g.q[0] * g.q[0] + g.q[1] * g.q[1]) + g.q[2] * g.q[2]) + g.q[3] * g.q[3]);
+  f.qn = sqrt(((g.q[0] * g.q[0] + g.q[1] * g.q[1]) + g.q[2] * g.q[2]) + g.q[3] * g.q[3]);
   if (!(f.qn > S(0)) || !finite(f.qn)) return f;
   for (int j = 0; j < 4; ++j) f.qh[j] = g.q[j] / f.qn;
   f.o = act_sigmoid(g.logit);
@@ -271,10 +342,10 @@ Fwd<S> project_one(const RefCamera& cam, int deg, const ParamView<S>& g) {
   // O7: 3-sigma radius and tile rectangle (R10, R11)
   const S mid = S(0.5) * (f.a + f.c);
   const S disc = mid * mid - f.det;
-  const S lam = mid + std::sqrt(std::max(disc, S(0)));
-  f.radius_f = std::ceil(S(3) * std::sqrt(lam));
-  S xlo = std::ceil(f.mux - f.radius_f), xhi = std::floor(f.mux + f.radius_f);
-  S ylo = std::ceil(f.muy - f.radius_f), yhi = std::floor(f.muy + f.radius_f);
+  const S lam = mid + sqrt(std::max(disc, S(0)));
+  f.radius_f = ceil(S(3) * sqrt(lam));
+  S xlo = ceil(f.mux - f.radius_f), xhi = floor(f.mux + f.radius_f);
+  S ylo = ceil(f.muy - f.radius_f), yhi = floor(f.muy + f.radius_f);
   xlo = std::max(xlo, S(0));
   ylo = std::max(ylo, S(0));
   xhi = std::min(xhi, S(cam.width - 1));
@@ -289,7 +360,7 @@ Fwd<S> project_one(const RefCamera& cam, int deg, const ParamView<S>& g) {
   S o_cam[3];
   for (int c = 0; c < 3; ++c) o_cam[c] = -((W[0][c] * t[0] + W[1][c] * t[1]) + W[2][c] * t[2]);
   for (int c = 0; c < 3; ++c) f.v[c] = g.p[c] - o_cam[c];
-  f.vn = std::sqrt((f.v[0] * f.v[0] + f.v[1] * f.v[1]) + f.v[2] * f.v[2]);
+  f.vn = sqrt((f.v[0] * f.v[0] + f.v[1] * f.v[1]) + f.v[2] * f.v[2]);
   for (int c = 0; c < 3; ++c) f.d[c] = f.v[c] / f.vn;
   sh_eval<S>(deg, f.d, f.Y, nullptr);
   const int nk = (deg + 1) * (deg + 1);
@@ -334,6 +405,33 @@ Proj<S> project_all(const RefCamera& cam, int64_t P, int64_t P_stride, int deg, 
                   (f.jcly ? FLAG_JCLAMP_Y : 0);
   }
   return pr;
+}
+
+// The fp32 projection (O1-O8) as the raster step's inputs in precision S: the
+// stage-wise gradient parity reference (mode 3, STAGE; R42) composites
+// exactly the fp32 records the GPU's raster consumes (bit-exact by R9) and carries
+// every later value in fp64 (or Rn, with the records as exact inputs).
+template <class S> Proj<S> promote(const Proj<float>& pf) {
+  const int64_t P = (int64_t)pf.tiles.size();
+  Proj<S> p(P);
+  for (int64_t i = 0; i < P; ++i) {
+    p.mux[i] = S((double)pf.mux[i]);
+    p.muy[i] = S((double)pf.muy[i]);
+    p.z[i] = S((double)pf.z[i]);
+    p.A[i] = S((double)pf.A[i]);
+    p.B[i] = S((double)pf.B[i]);
+    p.C[i] = S((double)pf.C[i]);
+    p.o[i] = S((double)pf.o[i]);
+    for (int ch = 0; ch < 3; ++ch) p.col[ch][i] = S((double)pf.col[ch][i]);
+  }
+  p.radius = pf.radius;
+  p.x0 = pf.x0;
+  p.x1 = pf.x1;
+  p.y0 = pf.y0;
+  p.y1 = pf.y1;
+  p.tiles = pf.tiles;
+  p.flags = pf.flags;
+  return p;
 }
 
 // ---------------------------------------------------------------------------
@@ -384,9 +482,20 @@ template <class D, class S> struct PixelResult {
   S C[3], Dep, T;
   int32_t n;
   int64_t blended, evaluated;
-  double margin;
+  double margin;    // min relative distance of a decision quantity to its threshold
+  double margin_u;  // S == Rn only: min |q - threshold| / (u m_q), m_q q's running error bound
   std::vector<Entry<S>> entries;
 };
+
+constexpr double kU32 = 5.9604644775390625e-08;  // u = 2^-24, fp32 unit roundoff
+
+// |diff| in units of u m (how many first-order fp32 error bounds separate a decision
+// quantity from its threshold); m == 0 means the quantity is exact.
+inline double bound_units(double diff, double m) {
+  diff = std::fabs(diff);
+  if (m > 0.0) return diff / (kU32 * m);
+  return diff > 0.0 ? 1e300 : 0.0;
+}
 
 template <class T> inline T pixel_power(T A, T B, T C, T dx, T dy) {
   return T(-0.5) * ((A * dx) * dx + (C * dy) * dy) - (B * dx) * dy;
@@ -401,6 +510,7 @@ PixelResult<D, S> composite_pixel(int px, int py, const std::vector<int32_t>& li
   r.n = 0;
   r.blended = r.evaluated = 0;
   r.margin = 1e300;
+  r.margin_u = 1e300;
   D Td = D(1);
   S Ts = S(1);
   const D inv255 = D(1) / D(255), t_stop = D(1e-4), cap = D(0.99);
@@ -414,6 +524,24 @@ PixelResult<D, S> composite_pixel(int px, int py, const std::vector<int32_t>& li
       const double scale = 0.5 * (std::fabs((double)pd.A[i] * dxd * dxd) + std::fabs((double)pd.C[i] * dyd * dyd)) +
                            std::fabs((double)pd.B[i] * dxd * dyd);
       if (scale > 0) r.margin = std::min(r.margin, std::fabs((double)powd) / scale);
+    }
+    if constexpr (kIsRn<S>) {
+      // the same decisions, in units of the value track's running error bounds
+      const S pw = pixel_power(ps.A[i], ps.B[i], ps.C[i], ps.mux[i] - S(px), ps.muy[i] - S(py));
+      r.margin_u = std::min(r.margin_u, bound_units((double)powd, pw.m));
+      if (!(powd > D(0))) {
+        const D rawd = pd.o[i] * act_exp(powd);
+        const S raw = ps.o[i] * act_exp(pw);
+        const bool cp = rawd > cap;
+        r.margin_u = std::min(r.margin_u, bound_units((double)rawd - (double)cap, raw.m));
+        const S al = cp ? S(cap) : raw;
+        const D ald = std::min(cap, rawd);
+        if (!cp) r.margin_u = std::min(r.margin_u, bound_units((double)ald - (double)inv255, al.m));
+        if (!(ald < inv255)) {
+          const S Tn = Ts * (S(1) - al);
+          r.margin_u = std::min(r.margin_u, bound_units((double)(Td * (D(1) - ald)) - (double)t_stop, Tn.m));
+        }
+      }
     }
     if (powd > D(0)) continue;
     const D Gd = act_exp(powd);
@@ -572,6 +700,93 @@ void chain_to_params(const RefCamera& cam, int deg, const ParamView<S>& g, const
   // opacity: o = sigmoid(logit)
   out[10] = sg.o * f.o * (S(1) - f.o);
 }
+
+template <class DT, class ST>
+void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, const float* params,
+                    const float* g_rgb, const float* g_depth, const Proj<DT>& pd, const Proj<ST>& ps,
+                    const std::vector<std::vector<int32_t>>& lists, double* grad_out, double* bound_out,
+                    double* screen_out, double* screen_bound_out) {
+  const int W = cam->width, H = cam->height, TX = (W + kTile - 1) / kTile;
+  const int F = 11 + 3 * (deg + 1) * (deg + 1);
+    std::vector<ScreenGrad<ST>> sg((size_t)P);
+    for (int py = 0; py < H; ++py)
+      for (int px = 0; px < W; ++px) {
+        const int64_t pix = (int64_t)py * W + px;
+        if (g_rgb[pix] == 0.f && g_rgb[(int64_t)W * H + pix] == 0.f && g_rgb[2 * (int64_t)W * H + pix] == 0.f &&
+            (!g_depth || g_depth[pix] == 0.f))
+          continue;  // zero upstream: this pixel contributes exactly zero (linearity)
+        const auto& list = lists[(py / kTile) * TX + px / kTile];
+        PixelResult<DT, ST> r = composite_pixel<DT, ST>(px, py, list, pd, ps, *cam, true);
+        if constexpr (kIsRn<ST>) {
+          // Bound of T_k for ANY evaluation route through this pixel's factors
+          // (forward products, or T_final divided back by (1 - alpha_j), j >= k):
+          // twice the relative bound of the complete product T_final.
+          const double rho = r.T.v != 0.0 ? r.T.m / std::fabs(r.T.v) : 0.0;
+          for (auto& e : r.entries) e.T.m = std::max(e.T.m, 2.0 * rho * std::fabs(e.T.v));
+        }
+        ST gC[3];
+        for (int ch = 0; ch < 3; ++ch) gC[ch] = ST(g_rgb[ch * (int64_t)W * H + pix]);
+        const ST gD = g_depth ? ST(g_depth[pix]) : ST(0);
+        // suffix sums S^C_k = sum_{j>k} c_j a_j T_j + T_final bg,  S^D_k = sum_{j>k} z_j a_j T_j
+        const size_t n = r.entries.size();
+        std::vector<ST> SC(3 * (n + 1)), SD(n + 1);
+        for (int ch = 0; ch < 3; ++ch) SC[3 * n + ch] = r.T * ST(cam->bg[ch]);
+        SD[n] = ST(0);
+        for (size_t k = n; k-- > 0;) {
+          const auto& e = r.entries[k];
+          for (int ch = 0; ch < 3; ++ch) SC[3 * k + ch] = SC[3 * (k + 1) + ch] + ps.col[ch][e.id] * e.alpha * e.T;
+          SD[k] = SD[k + 1] + ps.z[e.id] * e.alpha * e.T;
+        }
+        for (size_t k = 0; k < n; ++k) {
+          const auto& e = r.entries[k];
+          const int32_t i = e.id;
+          ScreenGrad<ST>& s = sg[i];
+          const ST aT = e.alpha * e.T;
+          for (int ch = 0; ch < 3; ++ch) s.col[ch] += gC[ch] * aT;
+          s.z += gD * aT;
+          ST dalpha = ST(0);
+          for (int ch = 0; ch < 3; ++ch)
+            dalpha += gC[ch] * (ps.col[ch][i] * e.T - SC[3 * (k + 1) + ch] / (ST(1) - e.alpha));
+          dalpha += gD * (ps.z[i] * e.T - SD[k + 1] / (ST(1) - e.alpha));
+          if (e.capped) continue;  // alpha = 0.99: no derivative w.r.t. o, mu, conic (R18)
+          s.o += e.G * dalpha;
+          const ST dpow = ps.o[i] * e.G * dalpha;  // d(o exp(power))/d power = o G
+          s.mux += dpow * (-(ps.A[i] * e.dx + ps.B[i] * e.dy));
+          s.muy += dpow * (-(ps.B[i] * e.dx + ps.C[i] * e.dy));
+          s.A += dpow * (ST(-0.5) * e.dx * e.dx);
+          s.B += dpow * (-e.dx * e.dy);
+          s.C += dpow * (ST(-0.5) * e.dy * e.dy);
+        }
+      }
+    std::vector<ST> out(F);
+    for (int64_t i = 0; i < P; ++i) {
+      for (int r = 0; r < F; ++r) grad_out[r * P + i] = 0.0;
+      if (bound_out)
+        for (int r = 0; r < F; ++r) bound_out[r * P + i] = 0.0;
+      if (screen_out) {
+        const ScreenGrad<ST>& s = sg[i];
+        const ST v[10] = {s.mux, s.muy, s.A, s.B, s.C, s.o, s.col[0], s.col[1], s.col[2], s.z};
+        for (int r = 0; r < 10; ++r) screen_out[r * P + i] = (double)v[r];
+        if constexpr (kIsRn<ST>)
+          if (screen_bound_out)
+            for (int r = 0; r < 10; ++r) screen_bound_out[r * P + i] = v[r].m;
+      }
+      if (pd.flags[i] & 128) continue;  // culled: exactly zero gradient
+      const ParamView<ST> g = load_params<ST>(params, P_stride, deg, i);
+      Fwd<ST> f = project_one<ST>(*cam, deg, g);
+      if (f.culled) continue;  // value track disagrees with the decision track (flip)
+      // decisions (clamps) follow the decision track
+      f.jclx = pd.flags[i] & FLAG_JCLAMP_X;
+      f.jcly = pd.flags[i] & FLAG_JCLAMP_Y;
+      for (int ch = 0; ch < 3; ++ch) f.clamp[ch] = pd.flags[i] & (1 << ch);
+      chain_to_params<ST>(*cam, deg, g, f, sg[i], out.data());
+      for (int r = 0; r < F; ++r) grad_out[r * P + i] = (double)out[r];
+      if constexpr (kIsRn<ST>)
+        if (bound_out)
+          for (int r = 0; r < F; ++r) bound_out[r * P + i] = out[r].m;
+    }
+}
+
 
 }  // namespace
 
@@ -748,85 +963,62 @@ int gsref_render_pixels(const RefCamera* cam, int64_t P, int64_t P_stride, int d
 // dL/d(mu_x, mu_y, A, B, C, opacity, r, g, b, z).  g_depth may be NULL.
 int gsref_render_bwd(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, const float* params, int mode,
                      const float* g_rgb, const float* g_depth, double* grad_out, double* screen_out) {
-  if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || mode < 0 || mode > 2 || !g_rgb) return -1;
-  const int W = cam->width, H = cam->height, TX = (W + kTile - 1) / kTile;
-  const int F = 11 + 3 * (deg + 1) * (deg + 1);
-  auto run = [&](const auto& pd, const auto& ps, const auto& lists, auto sprec) {
-    using ST = decltype(sprec);
-    using DT = std::decay_t<decltype(pd.mux[0])>;
-    std::vector<ScreenGrad<ST>> sg((size_t)P);
-    for (int py = 0; py < H; ++py)
-      for (int px = 0; px < W; ++px) {
-        const int64_t pix = (int64_t)py * W + px;
-        if (g_rgb[pix] == 0.f && g_rgb[(int64_t)W * H + pix] == 0.f && g_rgb[2 * (int64_t)W * H + pix] == 0.f &&
-            (!g_depth || g_depth[pix] == 0.f))
-          continue;  // zero upstream: this pixel contributes exactly zero (linearity)
-        const auto& list = lists[(py / kTile) * TX + px / kTile];
-        const PixelResult<DT, ST> r = composite_pixel<DT, ST>(px, py, list, pd, ps, *cam, true);
-        ST gC[3];
-        for (int ch = 0; ch < 3; ++ch) gC[ch] = ST(g_rgb[ch * (int64_t)W * H + pix]);
-        const ST gD = g_depth ? ST(g_depth[pix]) : ST(0);
-        // suffix sums S^C_k = sum_{j>k} c_j a_j T_j + T_final bg,  S^D_k = sum_{j>k} z_j a_j T_j
-        const size_t n = r.entries.size();
-        std::vector<ST> SC(3 * (n + 1)), SD(n + 1);
-        for (int ch = 0; ch < 3; ++ch) SC[3 * n + ch] = r.T * ST(cam->bg[ch]);
-        SD[n] = ST(0);
-        for (size_t k = n; k-- > 0;) {
-          const auto& e = r.entries[k];
-          for (int ch = 0; ch < 3; ++ch) SC[3 * k + ch] = SC[3 * (k + 1) + ch] + ps.col[ch][e.id] * e.alpha * e.T;
-          SD[k] = SD[k + 1] + ps.z[e.id] * e.alpha * e.T;
-        }
-        for (size_t k = 0; k < n; ++k) {
-          const auto& e = r.entries[k];
-          const int32_t i = e.id;
-          ScreenGrad<ST>& s = sg[i];
-          const ST aT = e.alpha * e.T;
-          for (int ch = 0; ch < 3; ++ch) s.col[ch] += gC[ch] * aT;
-          s.z += gD * aT;
-          ST dalpha = ST(0);
-          for (int ch = 0; ch < 3; ++ch)
-            dalpha += gC[ch] * (ps.col[ch][i] * e.T - SC[3 * (k + 1) + ch] / (ST(1) - e.alpha));
-          dalpha += gD * (ps.z[i] * e.T - SD[k + 1] / (ST(1) - e.alpha));
-          if (e.capped) continue;  // alpha = 0.99: no derivative w.r.t. o, mu, conic (R18)
-          s.o += e.G * dalpha;
-          const ST dpow = ps.o[i] * e.G * dalpha;  // d(o exp(power))/d power = o G
-          s.mux += dpow * (-(ps.A[i] * e.dx + ps.B[i] * e.dy));
-          s.muy += dpow * (-(ps.B[i] * e.dx + ps.C[i] * e.dy));
-          s.A += dpow * (ST(-0.5) * e.dx * e.dx);
-          s.B += dpow * (-e.dx * e.dy);
-          s.C += dpow * (ST(-0.5) * e.dy * e.dy);
-        }
-      }
-    std::vector<ST> out(F);
-    for (int64_t i = 0; i < P; ++i) {
-      for (int r = 0; r < F; ++r) grad_out[r * P + i] = 0.0;
-      if (screen_out) {
-        const ScreenGrad<ST>& s = sg[i];
-        const ST v[10] = {s.mux, s.muy, s.A, s.B, s.C, s.o, s.col[0], s.col[1], s.col[2], s.z};
-        for (int r = 0; r < 10; ++r) screen_out[r * P + i] = (double)v[r];
-      }
-      if (pd.flags[i] & 128) continue;  // culled: exactly zero gradient
-      const ParamView<ST> g = load_params<ST>(params, P_stride, deg, i);
-      Fwd<ST> f = project_one<ST>(*cam, deg, g);
-      if (f.culled) continue;  // value track disagrees with the decision track (flip)
-      // decisions (clamps) follow the decision track
-      f.jclx = pd.flags[i] & FLAG_JCLAMP_X;
-      f.jcly = pd.flags[i] & FLAG_JCLAMP_Y;
-      for (int ch = 0; ch < 3; ++ch) f.clamp[ch] = pd.flags[i] & (1 << ch);
-      chain_to_params<ST>(*cam, deg, g, f, sg[i], out.data());
-      for (int r = 0; r < F; ++r) grad_out[r * P + i] = (double)out[r];
-    }
-  };
+  if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || mode < 0 || mode > 3 || !g_rgb) return -1;
   if (mode == 0) {
     const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
-    run(pf, pf, tile_lists(*cam, pf), float(0));
+    render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pf, pf, tile_lists(*cam, pf), grad_out,
+                   nullptr, screen_out, nullptr);
+  } else if (mode == 3) {
+    const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
+    render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pf, promote<double>(pf), tile_lists(*cam, pf),
+                   grad_out, nullptr, screen_out, nullptr);
   } else if (mode == 2) {
     const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
     const Proj<double> pd = project_all<double>(*cam, P, P_stride, deg, params);
-    run(pf, pd, tile_lists(*cam, pf), double(0));
+    render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pf, pd, tile_lists(*cam, pf), grad_out,
+                   nullptr, screen_out, nullptr);
   } else {
     const Proj<double> pd = project_all<double>(*cam, P, P_stride, deg, params);
-    run(pd, pd, tile_lists(*cam, pd), double(0));
+    render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pd, pd, tile_lists(*cam, pd), grad_out,
+                   nullptr, screen_out, nullptr);
+  }
+  return 0;
+}
+
+// MIXED-mode O10 + O11 with running error bounds (struct Rn): grad_out equals
+// gsref_render_bwd(mode = MIXED) bit for bit; bound_out [F][P] (double) is the
+// first-order bound M of each gradient element in units of u = 2^-24, so an fp32
+// evaluation of the same maths is expected within c u M of grad_out (the parity
+// tolerance).  screen_out / screen_bound_out (nullable): the same for
+// the [10][P] screen-space gradients.
+int gsref_render_bwd_bound(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, const float* params,
+                           int stage, const float* g_rgb, const float* g_depth, double* grad_out, double* bound_out,
+                           double* screen_out, double* screen_bound_out) {
+  if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || !g_rgb || !grad_out || !bound_out) return -1;
+  const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
+  const Proj<Rn> pr = stage ? promote<Rn>(pf) : project_all<Rn>(*cam, P, P_stride, deg, params);
+  render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pf, pr, tile_lists(*cam, pf), grad_out, bound_out,
+                 screen_out, screen_bound_out);
+  return 0;
+}
+
+// Decision margins in units of the running error bound, at n pixels (px[j], py[j]):
+// margin_u[j] = min over the pixel's decisions (power > 0, the 0.99 cap, alpha <
+// 1/255, T' < 1e-4) of |q_fp32 - threshold| / (u m_q), m_q the bound of q.  A GPU
+// decision can differ from the oracle's only where this is below the parity
+// constant c (a threshold flip); DESIGN.md §6.
+int gsref_margin_bound(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, const float* params, int stage,
+                       int64_t n,
+                       const int32_t* px, const int32_t* py, double* margin_u) {
+  if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || n < 0 || !margin_u) return -1;
+  const int TX = (cam->width + kTile - 1) / kTile;
+  const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
+  const Proj<Rn> pr = stage ? promote<Rn>(pf) : project_all<Rn>(*cam, P, P_stride, deg, params);
+  const auto lists = tile_lists(*cam, pf);
+  for (int64_t j = 0; j < n; ++j) {
+    if (px[j] < 0 || py[j] < 0 || px[j] >= cam->width || py[j] >= cam->height) return -1;
+    const auto& list = lists[(py[j] / kTile) * TX + px[j] / kTile];
+    margin_u[j] = composite_pixel<float, Rn>(px[j], py[j], list, pf, pr, *cam, false).margin_u;
   }
   return 0;
 }
@@ -853,7 +1045,9 @@ int gsref_adam_step(int64_t F, int64_t P, int64_t P_stride, const float* params,
   return 0;
 }
 
-// Eq. 12 harness (R19): L = mean_{px,ch}|C - C*| + w_d mean_px |D - D*|, sign(0) = 0.
+// Eq. 12 harness (R19): L = mean_{px,ch}|C - C*| + w_d mean_px |D - D*|, sign(0) = 0;
+// target samples that are not measurements (non-finite colour, depth <= 0 or
+// non-finite: R41, R43) contribute neither loss nor gradient (the means keep npix).
 // grads (double) dL/dC [3][H][W], dL/dD [H][W]; returns L via *loss.
 int gsref_l1_loss_grad(int64_t npix, const double* rgb, const double* depth, const float* t_rgb,
                        const float* t_depth, double w_depth, double* g_rgb, double* g_depth, double* loss) {
@@ -861,11 +1055,19 @@ int gsref_l1_loss_grad(int64_t npix, const double* rgb, const double* depth, con
   double L = 0.0;
   const double sc = 1.0 / (3.0 * (double)npix), sd = w_depth / (double)npix;
   for (int64_t j = 0; j < 3 * npix; ++j) {
+    if (!std::isfinite(t_rgb[j])) {  // not a measurement (R43): no loss, no gradient
+      g_rgb[j] = 0.0;
+      continue;
+    }
     const double r = rgb[j] - (double)t_rgb[j];
     L += std::fabs(r) * sc;
     g_rgb[j] = (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0)) * sc;
   }
   for (int64_t j = 0; j < npix; ++j) {
+    if (!(t_depth[j] > 0.f) || !std::isfinite(t_depth[j])) {  // invalid depth (R41, R43)
+      g_depth[j] = 0.0;
+      continue;
+    }
     const double r = depth[j] - (double)t_depth[j];
     L += std::fabs(r) * sd;
     g_depth[j] = (r > 0 ? 1.0 : (r < 0 ? -1.0 : 0.0)) * sd;

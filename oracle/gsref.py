@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "gsref.cpp")
 LIB = os.path.join(HERE, "libgsref.so")
 
-F32, F64, MIXED = 0, 1, 2
+F32, F64, MIXED, STAGE = 0, 1, 2, 3
 FLAG_CULLED = 128
 
 
@@ -68,6 +68,8 @@ def lib():
         _lib.gsref_render_fwd.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P, P, P, P]
         _lib.gsref_render_pixels.argtypes = [P, i64, i64, C.c_int, P, C.c_int, i64, P, P, P, P, P, P, P]
         _lib.gsref_render_bwd.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P]
+        _lib.gsref_render_bwd_bound.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P, P]
+        _lib.gsref_margin_bound.argtypes = [P, i64, i64, C.c_int, P, C.c_int, i64, P, P, P]
         _lib.gsref_adam_step.argtypes = [i64, i64, i64, P, P, P, P, P, C.c_double, C.c_double, C.c_double,
                                          i64, P, P, P]
         _lib.gsref_l1_loss_grad.argtypes = [i64, P, P, P, P, C.c_double, P, P, P]
@@ -185,6 +187,48 @@ def render_bwd(cam, scene, g_rgb, g_depth=None, mode=MIXED):
     _check(lib().gsref_render_bwd(C.byref(rc), P, scene.P_stride, scene.sh_degree, _p(prm), mode,
                                   _p(g_rgb), _p(g_d), _p(grad), _p(screen)), "render_bwd")
     return grad, screen
+
+
+U32 = 2.0 ** -24  # fp32 unit roundoff
+
+
+def render_bwd_bound(cam, scene, g_rgb, g_depth=None, stage=True):
+    """MIXED-mode gradients [F][P] (bit-identical to render_bwd(mode=MIXED)) with their
+    first-order running error bounds M [F][P] in units of U32 (see gsref.cpp, struct
+    Rn): an fp32 evaluation of the same maths is expected within c * U32 * M.  Also the
+    screen-space gradients [10][P] and their bounds."""
+    F, P = scene.F, scene.P
+    grad = np.zeros((F, P))
+    bound = np.zeros((F, P))
+    screen = np.zeros((10, P))
+    sbound = np.zeros((10, P))
+    g_rgb = np.ascontiguousarray(g_rgb, dtype=np.float32)
+    g_d = None if g_depth is None else np.ascontiguousarray(g_depth, dtype=np.float32)
+    rc = ref_camera(cam)
+    prm = _params(scene)
+    _check(lib().gsref_render_bwd_bound(C.byref(rc), P, scene.P_stride, scene.sh_degree, _p(prm), int(stage),
+                                        _p(g_rgb), _p(g_d),
+                                        _p(grad), _p(bound), _p(screen), _p(sbound)), "render_bwd_bound")
+    return {"grad": grad, "bound": bound, "screen": screen, "screen_bound": sbound}
+
+
+def margin_bound(cam, scene, px=None, py=None, stage=True):
+    """Per-pixel decision margin in units of the running error bound (min over the
+    pixel's skip / cap / stop decisions of |q - threshold| / (U32 m_q)).  px, py: pixel
+    coordinates (default: every pixel, returned as [H][W])."""
+    full = px is None
+    if full:
+        yy, xx = np.mgrid[0:cam.height, 0:cam.width]
+        px, py = xx.ravel(), yy.ravel()
+    px = np.ascontiguousarray(px, dtype=np.int32)
+    py = np.ascontiguousarray(py, dtype=np.int32)
+    out = np.zeros(px.size)
+    rc = ref_camera(cam)
+    prm = _params(scene)
+    _check(lib().gsref_margin_bound(C.byref(rc), scene.P, scene.P_stride, scene.sh_degree, _p(prm), int(stage), px.size,
+                                    _p(px),
+                                    _p(py), _p(out)), "margin_bound")
+    return out.reshape(cam.height, cam.width) if full else out
 
 
 def adam_step(params, grad, m, v, lr_per_row, step, beta1=0.9, beta2=0.999, eps=1e-15, P=None):

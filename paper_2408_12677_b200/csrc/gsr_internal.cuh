@@ -56,6 +56,15 @@ __device__ __forceinline__ void adam_update(float& p, float& m, float& v, float 
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(step, m), __fmaf_rn(__fsqrt_rn(v), rs_bc2, eps)));
 }
 
+// Eq. 12 residual of one target sample (reading R43): a target that is not a
+// measurement -- a non-finite colour, or a depth that is <= 0 (the sensor's
+// "invalid", R41) or non-finite -- gives residual 0: no loss term and no gradient
+// (sign(0) = 0, R19).  Shared by k_l1 and the fused backward so both are identical.
+__device__ __forceinline__ float l1_res_rgb(float x, float t) { return fabsf(t) <= 3.402823466e+38f ? x - t : 0.f; }
+__device__ __forceinline__ float l1_res_depth(float x, float t) {
+  return (t > 0.f && t <= 3.402823466e+38f) ? x - t : 0.f;
+}
+
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 

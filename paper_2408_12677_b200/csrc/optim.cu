@@ -121,11 +121,11 @@ __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restric
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
       const int64_t j = ch * npix + i;
-      const float r = rgb[j] - trgb[j];
+      const float r = l1_res_rgb(rgb[j], trgb[j]);
       L += fabsf(r) * sc;
       grgb[j] = r > 0.f ? sc : (r < 0.f ? -sc : 0.f);
     }
-    const float r = dep[i] - tdep[i];
+    const float r = l1_res_depth(dep[i], tdep[i]);
     L += fabsf(r) * sd;
     gdep[i] = r > 0.f ? sd : (r < 0.f ? -sd : 0.f);
   }

@@ -249,7 +249,8 @@ __device__ __forceinline__ void gather_rec_async(const float4* __restrict__ rec,
 // Upstream gradient of one pixel: dL/drgb, dL/ddepth read from the caller's buffers, or,
 // with the fused Eq. 12 loss (gs_render_bwd_screen_l1), computed here from the rendered
 // and target images exactly as gs_l1_loss_grad does (sign(residual) x 1/(3 npix), x
-// w_depth/npix for depth, sign(0) = 0), the pixel's loss terms added to `lsum`.
+// w_depth/npix for depth, sign(0) = 0, invalid targets masked per R43), the pixel's
+// loss terms added to `lsum`.
 struct L1Fuse {
   const float *rgb, *depth, *trgb, *tdep;
   float sc, sd;
@@ -260,8 +261,9 @@ __device__ __forceinline__ void upstream(const L1Fuse& l1, const float* __restri
                                          const float* __restrict__ g_dep, int64_t npix, int64_t p, float& gr,
                                          float& gg, float& gb, float& gd, float& lsum) {
   if (l1.trgb) {
-    const float r0 = l1.rgb[p] - l1.trgb[p], r1 = l1.rgb[npix + p] - l1.trgb[npix + p];
-    const float r2 = l1.rgb[2 * npix + p] - l1.trgb[2 * npix + p], rd = l1.depth[p] - l1.tdep[p];
+    const float r0 = l1_res_rgb(l1.rgb[p], l1.trgb[p]), r1 = l1_res_rgb(l1.rgb[npix + p], l1.trgb[npix + p]);
+    const float r2 = l1_res_rgb(l1.rgb[2 * npix + p], l1.trgb[2 * npix + p]);
+    const float rd = l1_res_depth(l1.depth[p], l1.tdep[p]);
     gr = l1_sign(r0, l1.sc), gg = l1_sign(r1, l1.sc), gb = l1_sign(r2, l1.sc), gd = l1_sign(rd, l1.sd);
     lsum += fabsf(r0) * l1.sc + fabsf(r1) * l1.sc + fabsf(r2) * l1.sc + fabsf(rd) * l1.sd;
   } else {
