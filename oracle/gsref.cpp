@@ -411,6 +411,20 @@ Proj<S> project_all(const RefCamera& cam, int64_t P, int64_t P_stride, int deg, 
 // stage-wise gradient parity reference (mode 3, STAGE; R42) composites
 // exactly the fp32 records the GPU's raster consumes (bit-exact by R9) and carries
 // every later value in fp64 (or Rn, with the records as exact inputs).
+template <class S> Proj<S> promote(const Proj<float>& pf);
+
+// Rn records for the stage-wise bound: the fp32 values, exact (m = 0) except the SH
+// colour, whose bound comes from its own evaluation (the GPU's colour is an
+// independent fp32 evaluation of O8, within 1e-6, not bit-exact; R9 covers O1-O7).
+Proj<Rn> stage_records(const RefCamera& cam, int64_t P, int64_t P_stride, int deg, const float* params,
+                       const Proj<float>& pf) {
+  Proj<Rn> p = promote<Rn>(pf);
+  const Proj<Rn> full = project_all<Rn>(cam, P, P_stride, deg, params);
+  for (int ch = 0; ch < 3; ++ch)
+    for (int64_t i = 0; i < P; ++i) p.col[ch][i].m = full.col[ch][i].m;
+  return p;
+}
+
 template <class S> Proj<S> promote(const Proj<float>& pf) {
   const int64_t P = (int64_t)pf.tiles.size();
   Proj<S> p(P);
@@ -772,6 +786,13 @@ void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, 
             for (int r = 0; r < 10; ++r) screen_bound_out[r * P + i] = v[r].m;
       }
       if (pd.flags[i] & 128) continue;  // culled: exactly zero gradient
+      {  // no pixel contributed: the (linear) chain gives exactly zero
+        const ScreenGrad<ST>& s = sg[i];
+        const ST v[10] = {s.mux, s.muy, s.A, s.B, s.C, s.o, s.col[0], s.col[1], s.col[2], s.z};
+        bool any = false;
+        for (int r = 0; r < 10; ++r) any = any || (double)v[r] != 0.0;
+        if (!any) continue;
+      }
       const ParamView<ST> g = load_params<ST>(params, P_stride, deg, i);
       Fwd<ST> f = project_one<ST>(*cam, deg, g);
       if (f.culled) continue;  // value track disagrees with the decision track (flip)
@@ -996,7 +1017,8 @@ int gsref_render_bwd_bound(const RefCamera* cam, int64_t P, int64_t P_stride, in
                            double* screen_out, double* screen_bound_out) {
   if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || !g_rgb || !grad_out || !bound_out) return -1;
   const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
-  const Proj<Rn> pr = stage ? promote<Rn>(pf) : project_all<Rn>(*cam, P, P_stride, deg, params);
+  const Proj<Rn> pr = stage ? stage_records(*cam, P, P_stride, deg, params, pf)
+                             : project_all<Rn>(*cam, P, P_stride, deg, params);
   render_bwd_run(cam, P, P_stride, deg, params, g_rgb, g_depth, pf, pr, tile_lists(*cam, pf), grad_out, bound_out,
                  screen_out, screen_bound_out);
   return 0;
@@ -1013,7 +1035,8 @@ int gsref_margin_bound(const RefCamera* cam, int64_t P, int64_t P_stride, int de
   if (!cam || P < 0 || P_stride < P || deg < 0 || deg > 3 || n < 0 || !margin_u) return -1;
   const int TX = (cam->width + kTile - 1) / kTile;
   const Proj<float> pf = project_all<float>(*cam, P, P_stride, deg, params);
-  const Proj<Rn> pr = stage ? promote<Rn>(pf) : project_all<Rn>(*cam, P, P_stride, deg, params);
+  const Proj<Rn> pr = stage ? stage_records(*cam, P, P_stride, deg, params, pf)
+                             : project_all<Rn>(*cam, P, P_stride, deg, params);
   const auto lists = tile_lists(*cam, pf);
   for (int64_t j = 0; j < n; ++j) {
     if (px[j] < 0 || py[j] < 0 || px[j] >= cam->width || py[j] >= cam->height) return -1;

@@ -5,11 +5,13 @@ fed the ORACLE's outputs of the previous stage on identical seeded inputs.
   gs_project    bit-exact radius, tiles, rect, mu, z, conic, opacity; colour 1e-6
   gs_bin_tiles  bit-exact sorted ids, tile ranges, K
   gs_render_fwd 1e-5 absolute rgb/depth, exact n_contrib, except proven threshold
-                flips (oracle decision margin < 1e-5 relative); the GSR_EXACT_EXP
-                build is bit-identical
-  gs_render_bwd rel < 1e-3 or abs < 1e-6 per gradient element against the MIXED
-                oracle (fp32 decisions, fp64 values); pixels with a proven flip
-                have their upstream gradient zeroed on both sides
+                flips (the pixel's decision margin is below C_FLIP running error
+                bounds, gpu_helpers.flip_pixels); the GSR_EXACT_EXP build is
+                bit-identical
+  gs_render_bwd EVERY gradient element within max(1e-6, 1e-3 |ref|, C_TOL u M)
+                of the stage-wise oracle (STAGE: fp32 decisions and records, fp64
+                values; M its running error bound), no fraction allowance; pixels
+                with a proven flip have their upstream gradient zeroed on both sides
   gs_adam_step  1e-6 relative
 Full-size configs are checked on sampled pixels / sampled upstream gradients.
 """
@@ -24,9 +26,9 @@ pytestmark = pytest.mark.gpu
 
 if torch.cuda.is_available():
     from paper_2408_12677_b200 import gsr, pipeline
-    from gpu_helpers import (DEV, gpu_bin, gpu_bwd, gpu_project, gpu_render, grad_mismatch, proj_from_oracle)
-
-FLIP_MARGIN = 1e-5
+    from gpu_helpers import (DEV, assert_grad_parity, flip_pixels, gpu_bin, gpu_bwd, gpu_project, gpu_render,
+                             grad_mismatch, proj_from_oracle)
+    from threshold_scenes import near_skip_scene
 
 
 @pytest.fixture(scope="module")
@@ -161,16 +163,16 @@ def test_render_fwd_exact_build_bitexact(lib_exact, name):
 def test_render_fwd_parity_with_flip_accounting(lib, name):
     w = workload(name)
     cam, scene = w.cameras[0], w.scene
-    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    ref = gsref.render_fwd(cam, scene, gsref.F32)
     _, _, _, out = _fwd_stagewise(lib, cam, scene)
     rgb = out["rgb"].cpu().numpy()
     dep = out["depth"].cpu().numpy()
     n = out["n_contrib"].cpu().numpy()
     bad = (np.abs(rgb - ref["rgb"]).max(0) > 1e-5) | (np.abs(dep - ref["depth"]) > 1e-5) | (n != ref["n_contrib"])
-    flips = bad & (ref["margin"] < FLIP_MARGIN)
-    unexplained = bad & ~flips
+    flagged = flip_pixels(cam, scene)
+    unexplained = bad & ~flagged
     assert unexplained.sum() == 0, f"{int(unexplained.sum())} pixels off without a threshold flip"
-    assert flips.sum() <= max(2, 1e-4 * bad.size)
+    assert flagged.sum() <= max(2, 1e-3 * bad.size)
     T = out["T_final"].cpu().numpy()
     assert T.min() >= 1e-4 and T.max() <= 1.0  # R16 invariant on the GPU path
 
@@ -201,18 +203,24 @@ def test_render_fwd_sampled_full_size(lib, name):
     n = out["n_contrib"].cpu().numpy()[py, px]
     # depth is unnormalised (z * alpha * T sums up to ~10 m): 1e-5 absolute on rgb, 1e-5 relative on depth
     bad = (np.abs(rgb - ref["rgb"]).max(0) > 1e-5) | (np.abs(dep - ref["depth"]) > 1e-5 * np.maximum(1.0, np.abs(ref["depth"]))) | (n != ref["n_contrib"])
-    unexplained = bad & ~(ref["margin"] < FLIP_MARGIN)
+    unexplained = bad & ~flip_pixels(cam, scene, px, py)
     assert unexplained.sum() == 0, f"{int(unexplained.sum())} sampled pixels off without a flip"
 
 
 # ----------------------------------------------------------------------------- gs_render_bwd
-def _bwd_stagewise(lib, cam, scene, seed=1, sample_mask=None):
+def _bwd_stagewise(lib, cam, scene, seed=1, sample_mask=None, screen=False):
+    """gs_render_bwd fed the oracle's fp32 projection, lists, T_final and n_contrib;
+    reference: the STAGE oracle with running error bounds.  Flip pixels (and pixels
+    outside sample_mask) get zero upstream on both sides."""
     pr = gsref.project(cam, scene, gsref.F32)
     b = gsref.bin_tiles(cam, scene)
-    f = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    f = gsref.render_fwd(cam, scene, gsref.F32)
     g_rgb, g_d = scenegen.upstream_fields(seed, cam.width, cam.height)
-    flips = f["margin"] < FLIP_MARGIN
-    keep = ~flips if sample_mask is None else (~flips & sample_mask)
+    keep = np.ones((cam.height, cam.width), bool) if sample_mask is None else sample_mask.copy()
+    ys, xs = np.nonzero(keep)
+    flips = np.zeros_like(keep)
+    flips[ys, xs] = flip_pixels(cam, scene, xs, ys)
+    keep &= ~flips
     g_rgb = (g_rgb * keep[None]).astype(np.float32)
     g_d = (g_d * keep).astype(np.float32)
     proj, _ = proj_from_oracle(pr)
@@ -222,23 +230,31 @@ def _bwd_stagewise(lib, cam, scene, seed=1, sample_mask=None):
     n = torch.from_numpy(f["n_contrib"]).to(DEV)
     params = torch.from_numpy(scene.params).to(DEV)
     g, ws = gpu_bwd(lib, cam, scene, params, proj, ids, ranges, T, n, g_rgb, g_d)
-    ref, screen = gsref.render_bwd(cam, scene, g_rgb, g_d, mode=gsref.MIXED)
-    return g, ref, ws, screen
+    if screen:
+        sg = torch.zeros((scene.P, 12), dtype=torch.float32, device=DEV)
+        lib.render_bwd_screen(gsr.camera(cam), gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree), proj, ids,
+                              ranges, T, n, torch.from_numpy(g_rgb).to(DEV), torch.from_numpy(g_d).to(DEV), sg)
+        torch.cuda.synchronize()
+        ws = sg.cpu().numpy().astype(np.float64)
+    ref = gsref.render_bwd_bound(cam, scene, g_rgb, g_d)
+    return g, ref, ws, int(flips.sum())
 
 
 @pytest.mark.parametrize("name", ["tiny", "small"])
 def test_render_bwd_parity_stagewise(lib, name):
+    """Every gradient element (all F rows of all P Gaussians) within tolerance."""
     w = workload(name)
-    g, ref, ws, screen = _bwd_stagewise(lib, w.cameras[0], w.scene)
-    bad = grad_mismatch(g, ref)
-    frac = bad.mean()
-    worst = np.argsort(-(np.abs(g - ref) / (np.abs(ref) + 1e-6)).ravel())[:5]
-    assert frac <= 1e-3, f"{int(bad.sum())}/{bad.size} gradient elements outside tolerance; worst {[(g.ravel()[k], ref.ravel()[k]) for k in worst]}"
+    g, ref, ws, _ = _bwd_stagewise(lib, w.cameras[0], w.scene, screen=True)
+    assert_grad_parity(g, ref["grad"], ref["bound"])
+    # the raster half alone (gs_render_bwd_screen), element by element: sgrad [P][12]
+    # = (dmu_x, dmu_y, dA, dB, dC, dopacity, dr, dg, db, dz, pad, pad), the oracle's order
+    assert_grad_parity(ws[:, :10].T, ref["screen"], ref["screen_bound"], what="screen-space gradient")
 
 
 @pytest.mark.parametrize("name", ["replica", "scannetpp", "large"])
 def test_render_bwd_sampled_full_size(lib, name):
-    """Full-size view with upstream gradient on a sampled set of 64 tiles."""
+    """Full-size view with upstream gradient on a sampled set of 64 tiles: every
+    gradient element of every Gaussian within tolerance."""
     w = workload(name)
     cam, scene = w.cameras[0], w.scene
     rng = np.random.default_rng(3)
@@ -247,8 +263,26 @@ def test_render_bwd_sampled_full_size(lib, name):
         ty, tx = divmod(int(t), cam.tiles_x)
         mask[ty * 16:(ty + 1) * 16, tx * 16:(tx + 1) * 16] = True
     g, ref, _, _ = _bwd_stagewise(lib, cam, scene, sample_mask=mask)
-    bad = grad_mismatch(g, ref)
-    assert bad.mean() <= 1e-3, f"{int(bad.sum())}/{bad.size} gradient elements outside tolerance"
+    assert np.count_nonzero(ref["grad"]) > 1000
+    assert_grad_parity(g, ref["grad"], ref["bound"])
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_threshold_scene_flips_explained(lib, seed):
+    """Decisions placed ON the 1/255 threshold (tests/threshold_scenes.py): the GPU's
+    forward may differ from the oracle only at flagged pixels, and with those pixels'
+    upstream zeroed every gradient element matches."""
+    scene, cam, pix = near_skip_scene(seed)
+    ref = gsref.render_fwd(cam, scene, gsref.F32)
+    _, _, _, out = _fwd_stagewise(lib, cam, scene)
+    bad = (np.abs(out["rgb"].cpu().numpy() - ref["rgb"]).max(0) > 1e-5) | \
+          (out["n_contrib"].cpu().numpy() != ref["n_contrib"])
+    flagged = flip_pixels(cam, scene)
+    assert (bad & ~flagged).sum() == 0
+    assert all(flagged[py, px] for px, py in pix)
+    g, refb, _, nflip = _bwd_stagewise(lib, cam, scene)
+    assert nflip >= len(pix)
+    assert_grad_parity(g, refb["grad"], refb["bound"])
 
 
 # ----------------------------------------------------------------------------- end-to-end chain
@@ -259,19 +293,20 @@ def test_chain_end_to_end(lib, name):
     proj, t, params = gpu_project(lib, cam, scene)
     b = gpu_bin(lib, cam, scene, proj)
     out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
-    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    ref = gsref.render_fwd(cam, scene, gsref.F32)
+    flagged = flip_pixels(cam, scene)
     rgb = out["rgb"].cpu().numpy()
     bad = np.abs(rgb - ref["rgb"]).max(0) > 1e-5
-    assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
-    assert abs(out["blended"] - ref["blended"]) <= 4 * (ref["margin"] < FLIP_MARGIN).sum()
+    assert (bad & ~flagged).sum() == 0
+    assert abs(out["blended"] - ref["blended"]) <= 4 * flagged.sum()
     g_rgb, g_d = scenegen.upstream_fields(2, cam.width, cam.height)
-    keep = ~(ref["margin"] < FLIP_MARGIN)
+    keep = ~flagged
     g_rgb = (g_rgb * keep[None]).astype(np.float32)
     g_d = (g_d * keep).astype(np.float32)
     g, _ = gpu_bwd(lib, cam, scene, params, proj, b["sorted_ids"], b["ranges"], out["T_final"], out["n_contrib"],
                    g_rgb, g_d)
-    gref, _ = gsref.render_bwd(cam, scene, g_rgb, g_d, mode=gsref.MIXED)
-    assert grad_mismatch(g, gref).mean() <= 1e-3
+    r = gsref.render_bwd_bound(cam, scene, g_rgb, g_d)
+    assert_grad_parity(g, r["grad"], r["bound"])
 
 
 # ----------------------------------------------------------------------------- Adam / L1
@@ -310,6 +345,9 @@ def test_l1_parity(lib):
     rgb, trgb = rng.uniform(size=(2, 3, H, W)).astype(np.float32)
     d, td = rng.uniform(1, 5, size=(2, H, W)).astype(np.float32)
     trgb[0, 0, 0] = rgb[0, 0, 0]
+    # targets that are not measurements (R43): no loss, zero gradient
+    trgb[1, 3, 4], trgb[2, 5, 6], trgb[0, 7, 8] = np.nan, np.inf, -np.inf
+    td[2, 2], td[4, 4], td[6, 6], td[8, 8] = 0.0, -1.0, np.nan, np.inf
     t = [torch.from_numpy(a).to(DEV) for a in (rgb, d, trgb, td)]
     g1 = torch.empty_like(t[0])
     g2 = torch.empty_like(t[1])
@@ -319,6 +357,90 @@ def test_l1_parity(lib):
     assert loss.item() == pytest.approx(L, rel=1e-5)
     np.testing.assert_allclose(g1.cpu().numpy(), r1, rtol=1e-6)
     np.testing.assert_allclose(g2.cpu().numpy(), r2, rtol=1e-6)
+    assert g1[1, 3, 4] == 0 and g1[2, 5, 6] == 0 and g1[0, 7, 8] == 0
+    assert g2[2, 2] == 0 and g2[4, 4] == 0 and g2[6, 6] == 0 and g2[8, 8] == 0
+    assert np.isfinite(loss.item())
+
+
+@pytest.mark.parametrize("name", ["replica", "scannetpp", "large"])
+def test_product_chain_full_size_sampled(lib, name):
+    """The product backward at full size, element by element: the GPU chain project ->
+    bin -> render_fwd with key masks -> gs_render_bwd_screen_l1 (fused Eq. 12, the
+    Trainer's kernel) -> gs_project_bwd_views, against the STAGE oracle with running
+    error bounds.  The loss is restricted to 64 sampled tiles by the R43 masking: every
+    other target sample (and every flagged flip pixel) is NaN, so it has no loss and
+    no gradient.  In the sampled tiles the targets are the ORACLE's fp32 render offset by
+    +-0.02 (colour) and +-(0.01 + 1%) (depth) with random signs, so the residual signs
+    -- hence the upstream gradient -- are fixed by oracle-side data alone (the GPU
+    render is within 1e-5 of the oracle's)."""
+    w = workload(name)
+    cam, scene = w.cameras[0], w.scene
+    H, W, npix = cam.height, cam.width, cam.height * cam.width
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    gcam = gsr.camera(cam)
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    K = b["K"]
+    rgb = torch.empty((3, H, W), device=DEV)
+    dep = torch.empty((H, W), device=DEV)
+    T = torch.empty((H, W), device=DEV)
+    n = torch.empty((H, W), dtype=torch.int32, device=DEV)
+    kb = torch.zeros(K + 16, dtype=torch.uint8, device=DEV)
+    lib.render_fwd(gcam, sc, proj, b["sorted_ids"], b["ranges"], rgb, dep, T, n, key_blocks=kb)
+    # sampled tiles -> target images
+    rng = np.random.default_rng(21)
+    ys, xs = [], []
+    for tt in rng.choice(cam.num_tiles, 64, replace=False):
+        ty, tx = divmod(int(tt), cam.tiles_x)
+        yy, xx = np.mgrid[ty * 16:min(ty * 16 + 16, H), tx * 16:min(tx * 16 + 16, W)]
+        ys.append(yy.ravel())
+        xs.append(xx.ravel())
+    ys, xs = np.concatenate(ys), np.concatenate(xs)
+    ok = ~flip_pixels(cam, scene, xs, ys)
+    ys, xs = ys[ok], xs[ok]
+    ref_px = gsref.render_pixels(cam, scene, xs, ys, gsref.F32)
+    sgn = rng.choice([-1.0, 1.0], size=(4, xs.size))
+    t_rgb = np.full((3, H, W), np.nan, np.float32)
+    t_dep = np.full((H, W), np.nan, np.float32)
+    t_rgb[:, ys, xs] = (ref_px["rgb"] + 0.02 * sgn[:3]).astype(np.float32)
+    t_dep[ys, xs] = (ref_px["depth"] + sgn[3] * (0.01 + 0.01 * np.abs(ref_px["depth"]))).astype(np.float32)
+    # oracle upstream: sign(oracle render - target) x the fp32 scales the GPU uses, R43 mask
+    s_c = np.float32(1.0 / (3.0 * npix))
+    s_d = np.float32(1.0 / npix)
+    g_rgb = np.zeros((3, H, W), np.float32)
+    g_d = np.zeros((H, W), np.float32)
+    g_rgb[:, ys, xs] = (np.sign(ref_px["rgb"] - t_rgb[:, ys, xs]) * s_c).astype(np.float32)
+    dv = t_dep[ys, xs] > 0
+    g_d[ys[dv], xs[dv]] = (np.sign(ref_px["depth"][dv] - t_dep[ys[dv], xs[dv]]) * s_d).astype(np.float32)
+    # the GPU render agrees with the oracle well inside the offsets (signs are shared)
+    assert np.abs(rgb.cpu().numpy()[:, ys, xs] - ref_px["rgb"]).max() < 1e-4
+    sg = torch.zeros((scene.P, 12), device=DEV)
+    loss = torch.zeros(1, device=DEV)
+    lib.render_bwd_screen_l1(gcam, sc, proj, b["sorted_ids"], b["ranges"], T, n, rgb, dep,
+                             torch.from_numpy(t_rgb).to(DEV), torch.from_numpy(t_dep).to(DEV), 1.0, sg, loss=loss,
+                             key_blocks=kb)
+    grad = torch.full((scene.F, scene.P_stride), np.nan, device=DEV)
+    lib.project_bwd_views([gcam], sc, params, [t["flags"]], [sg], grad, accumulate=False)
+    torch.cuda.synchronize()
+    L_ref = (np.abs(ref_px["rgb"] - t_rgb[:, ys, xs]).sum() * float(s_c) +
+             np.abs(ref_px["depth"][dv] - t_dep[ys[dv], xs[dv]]).sum() * float(s_d))
+    assert loss.item() == pytest.approx(L_ref, rel=1e-4)
+    ref = gsref.render_bwd_bound(cam, scene, g_rgb, g_d)
+    g = grad[:, :scene.P].cpu().numpy().astype(np.float64)
+    # colour-clamp decisions (R13) are the only projection decisions not bit-exact (the
+    # GPU colour is within 1e-6, not bit-identical): a differing flag must be a proven
+    # flip (both colours within 1e-6 of 0); such a Gaussian's SH and mean rows are excused
+    pr = gsref.project(cam, scene, gsref.F32)
+    fl_gpu = t["flags"][:scene.P].cpu().numpy()
+    excl = np.zeros_like(g, bool)
+    for ch in range(3):
+        differ = ((fl_gpu >> ch) & 1) != ((pr["flags"] >> ch) & 1)
+        if differ.any():
+            col = t["rec"][:scene.P, 7 + ch].cpu().numpy()[differ]
+            assert np.all(np.abs(col) <= 1e-6) and np.all(np.abs(pr[("r", "g", "b")[ch]][differ]) <= 1e-6)
+            excl[:, differ] = True
+    assert np.count_nonzero(ref["grad"]) > 1000
+    assert_grad_parity(g, ref["grad"], ref["bound"], scale=float(s_c), exclude=excl)
 
 
 # ----------------------------------------------------------------------------- edge cases
@@ -357,12 +479,12 @@ def test_all_culled(lib):
 def test_ragged_images(lib, wh):
     W, H = wh
     scene, cam = scenegen.random_small_scene(7, 60, 1, width=W, height=H, f=0.8 * max(W, H))
-    ref = gsref.render_fwd(cam, scene, gsref.F32, want_margin=True)
+    ref = gsref.render_fwd(cam, scene, gsref.F32)
     proj, _, params = gpu_project(lib, cam, scene)
     b = gpu_bin(lib, cam, scene, proj)
     out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
     bad = np.abs(out["rgb"].cpu().numpy() - ref["rgb"]).max(0) > 1e-5
-    assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
+    assert (bad & ~flip_pixels(cam, scene)).sum() == 0
 
 
 def test_single_gaussian_peak_closed_form(lib):
@@ -759,7 +881,7 @@ def test_bench_launch_configuration_full_size_sampled(lib):
         ref = gsref.render_pixels(cam, scene, px, py, gsref.F32)
         rgb = tr.bufs[v % nb].rgb.cpu().numpy()[:, py, px]
         bad = np.abs(rgb - ref["rgb"]).max(0) > 1e-5
-        assert (bad & ~(ref["margin"] < FLIP_MARGIN)).sum() == 0
+        assert (bad & ~flip_pixels(cam, scene, px, py)).sum() == 0
         K_ref = int(gsref.project(cam, scene, gsref.F32)["tiles"].sum())
         assert int(tr.num_keys[v].item()) == K_ref
 

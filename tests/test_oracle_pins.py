@@ -471,11 +471,12 @@ def test_mixed_mode_matches_f64_on_smooth_scene(oracle):
     g_rgb, g_d = scenegen.upstream_fields(1, cam.width, cam.height)
     a, _ = oracle.render_bwd(cam, w.scene, g_rgb, g_d, mode=oracle.MIXED)
     b, _ = oracle.render_bwd(cam, w.scene, g_rgb, g_d, mode=oracle.F64)
-    # identical decisions on this scene (checked by signature) => same values up to fp64 rounding
+    # identical decisions on this scene (asserted by signature) => same values up to the
+    # fp32 rounding of the decision-track-only inputs (none here) and fp64 rounding
     s32 = oracle.render_fwd(cam, w.scene, oracle.F32, want_signature=True)["signature"]
     s64 = oracle.render_fwd(cam, w.scene, oracle.F64, want_signature=True)["signature"]
-    if s32 == s64:
-        np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-9)
+    assert s32 == s64
+    np.testing.assert_allclose(a, b, rtol=1e-6, atol=1e-9)
 
 
 # --------------------------------------------------------------------------- O12 (Adam)
