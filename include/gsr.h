@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define GSR_VERSION 1
+#define GSR_VERSION 2
 #define GS_TILE 16         /* 16x16-pixel tiles (north_star) */
 #define GS_MAX_SH_DEGREE 3
 #define GS_MAX_TILES 65536 /* tile ids are sorted as 16-bit keys */
@@ -56,7 +56,7 @@ typedef enum {
   GS_ERR_ARG = -1,      /* invalid argument (NULL, negative size, bad degree, ...) */
   GS_ERR_ALIGN = -2,    /* pointer not 16-byte aligned or P_stride % 4 != 0 */
   GS_ERR_CAPACITY = -3, /* gs_bin_tiles: K > key_capacity (required K reported) */
-  GS_ERR_STATE = -4,    /* inconsistent sizes between calls (SPEC StateMismatch) */
+  GS_ERR_STATE = -4,    /* backward given buffers / sizes of another forward (SPEC StateMismatch) */
   GS_ERR_EMPTY = -5,    /* gs_adam_step with P == 0 (SPEC NoGaussians) */
   GS_ERR_CUDA = -6      /* a CUDA launch or runtime call failed; see gs_last_error() */
 } gs_status;
@@ -162,6 +162,49 @@ gs_status gs_bin_tiles(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HO
  *  tile_order:  int32[num_tiles] output permutation.  num_tiles <= 65536. */
 gs_status gs_tile_order(const gs_camera* cam /*HOST*/, const int32_t* tile_ranges, int32_t* tile_order, void* stream);
 
+/* ---------------------------------------------------------------- forward state
+ * What a backward consumes from its forward (SPEC.md:345-353 render_backward ->
+ * StateMismatch): gs_render_fwd fills a caller-owned HOST gs_fwd_state (fwd_out) with a
+ * process-unique id and the buffers and image size it used, and records, in a small
+ * process-wide table keyed by the n_contrib buffer, which forward call wrote that
+ * buffer last.  A backward given that state (gs_bwd_opts.fwd) returns GS_ERR_STATE,
+ * launching nothing, if
+ *   - its camera's width / height differ from the forward's,
+ *   - any of proj.rec, sorted_ids, tile_ranges, T_final, n_contrib (and key_blocks,
+ *     when the backward uses masks; rgb and depth for the fused-loss backward) is not
+ *     the buffer that forward used (e.g. the key masks or n_contrib of another view), or
+ *   - a later gs_render_fwd has rewritten n_contrib (the state is stale).
+ * Checks run on the host at call (or graph-capture) time; NULL skips them. */
+typedef struct {
+  uint64_t id; /* never 0 once written */
+  int32_t width, height;
+  const float* rec;
+  const int32_t* sorted_ids;
+  const int32_t* tile_ranges;
+  const float* rgb;
+  const float* depth;
+  const float* T_final;
+  const int32_t* n_contrib;
+  const uint8_t* key_blocks;
+} gs_fwd_state;
+
+/* Options of the backward calls (nullable pointer = all defaults):
+ *  fwd:      the forward's state (above): consistency check -> GS_ERR_STATE.
+ *  det_ws:   non-NULL selects the DETERMINISTIC reduction mode: every
+ *            (tile, Gaussian) pair's warp-reduced 10 screen-gradient components are
+ *            stored to det_ws[key][12] (no atomics), then one thread per Gaussian sums
+ *            its pairs in a fixed order (the tiles of its rectangle, row-major) into
+ *            sgrad.  Results are then bit-reproducible: independent of scheduling,
+ *            streams, graph replay and tile_order.  det_ws: DEVICE float[det_keys][12],
+ *            16-B aligned; det_keys >= the key_capacity given to gs_bin_tiles.  Costs
+ *            48 B per key of traffic and one binary search per key (a test mode).
+ *            The K13 port (gs_naive_render_bwd_screen) rejects it (GS_ERR_ARG). */
+typedef struct {
+  const gs_fwd_state* fwd;
+  float* det_ws;
+  int64_t det_keys;
+} gs_bwd_opts;
+
 /* ---------------------------------------------------------------- gs_render_fwd
  * Eq. 11 per pixel over its tile's depth-sorted list, front to back: alpha =
  * min(0.99, o exp(power)), skip alpha < 1/255 (and power > 0), stop before a
@@ -181,7 +224,7 @@ gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
                         const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order /*nullable*/,
                         float* rgb, float* depth,
                         float* T_final, int32_t* n_contrib, unsigned long long* blended, uint8_t* key_blocks,
-                        void* stream);
+                        gs_fwd_state* fwd_out /*HOST, nullable*/, void* stream);
 
 /* ---------------------------------------------------------------- gs_render_bwd
  * Exact derivative of gs_project + gs_render_fwd (R18) for upstream
@@ -196,14 +239,15 @@ gs_status gs_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *      gs_render_fwd); NULL = derive the pixel blocks geometrically.
  *  tile_order: nullable, as in gs_render_fwd.
  *  grad: float[F][P_stride], ACCUMULATED (+=) so that views sum (R21).
- * Float atomics make grad order-dependent in the last bits. */
+ *  opts: nullable gs_bwd_opts (forward-state check -> GS_ERR_STATE; deterministic mode).
+ * Float atomics make grad order-dependent in the last bits unless opts->det_ws is set. */
 size_t gs_render_bwd_workspace(const gs_scene* scene /*HOST*/);
 gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, const float* params,
                         gs_proj proj, const int32_t* sorted_ids, const int32_t* tile_ranges,
                         const int32_t* tile_order /*nullable*/, const float* T_final,
                         const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
                         const uint8_t* key_blocks /*nullable*/, void* ws, size_t ws_bytes, float* grad,
-                        void* stream);
+                        const gs_bwd_opts* opts /*HOST, nullable*/, void* stream);
 
 /* ---------------------------------------------------------------- batched backward
  * gs_render_bwd split in its two halves so that a batch of views (R21) chains the
@@ -227,7 +271,8 @@ gs_status gs_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* sc
                                const int32_t* sorted_ids, const int32_t* tile_ranges,
                                const int32_t* tile_order /*nullable*/, const float* T_final,
                                const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
-                               const uint8_t* key_blocks /*nullable*/, float* sgrad, void* stream);
+                               const uint8_t* key_blocks /*nullable*/, float* sgrad,
+                               const gs_bwd_opts* opts /*HOST, nullable*/, void* stream);
 gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views]*/, const gs_scene* scene /*HOST*/,
                                const float* params, const uint8_t* const* flags /*HOST[n_views] of DEVICE*/,
                                float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
@@ -243,11 +288,12 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views
  * (pixel, Gaussian) pair.  Results equal the product calls up to fp32 rounding. */
 gs_status gs_naive_render_fwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
                               const int32_t* sorted_ids, const int32_t* tile_ranges, float* rgb, float* depth,
-                              float* T_final, int32_t* n_contrib, unsigned long long* blended, void* stream);
+                              float* T_final, int32_t* n_contrib, unsigned long long* blended,
+                              gs_fwd_state* fwd_out /*HOST, nullable*/, void* stream);
 gs_status gs_naive_render_bwd_screen(const gs_camera* cam /*HOST*/, const gs_scene* scene /*HOST*/, gs_proj proj,
                                      const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
                                      const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
-                                     float* sgrad, void* stream);
+                                     float* sgrad, const gs_bwd_opts* opts /*HOST, nullable*/, void* stream);
 
 /* gs_render_bwd_screen with the harness loss of Eq. 12 fused in: the upstream gradient
  * of every pixel is computed inside the backward from the rendered rgb / depth (as
@@ -263,7 +309,7 @@ gs_status gs_render_bwd_screen_l1(const gs_camera* cam /*HOST*/, const gs_scene*
                                   const int32_t* n_contrib, const float* rgb, const float* depth,
                                   const float* target_rgb, const float* target_depth, float w_depth,
                                   float* loss /*nullable*/, const uint8_t* key_blocks /*nullable*/, float* sgrad,
-                                  void* stream);
+                                  const gs_bwd_opts* opts /*HOST, nullable*/, void* stream);
 
 /* ---------------------------------------------------------------- gs_adam_step
  * Dense bias-corrected Adam over all F x P scalars of the live Gaussians [0, P) (R20;

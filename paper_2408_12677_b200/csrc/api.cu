@@ -5,6 +5,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "gsr_internal.cuh"
@@ -128,6 +130,70 @@ gs_status check_ptrs(const char* fn, std::initializer_list<std::pair<const void*
 
 int rows_of(const gs_scene* sc) { return 11 + 3 * (sc->sh_degree + 1) * (sc->sh_degree + 1); }
 
+// ---- forward state (gs_fwd_state, GS_ERR_STATE): which forward call last wrote each
+// n_contrib buffer.  Host-side, at call (or graph-capture) time.
+std::mutex g_reg_mu;
+std::unordered_map<const void*, uint64_t> g_last_fwd;
+std::atomic<uint64_t> g_fwd_ids{0};
+
+void record_forward(const gs_camera* cam, gs_proj proj, const int32_t* ids, const int32_t* ranges, const float* rgb,
+                    const float* depth, const float* T, const int32_t* n, const uint8_t* kb, gs_fwd_state* out) {
+  const uint64_t id = ++g_fwd_ids;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    g_last_fwd[n] = id;
+  }
+  if (out) {
+    out->id = id;
+    out->width = cam->width, out->height = cam->height;
+    out->rec = proj.rec, out->sorted_ids = ids, out->tile_ranges = ranges;
+    out->rgb = rgb, out->depth = depth, out->T_final = T, out->n_contrib = n, out->key_blocks = kb;
+  }
+}
+
+gs_status check_forward(const gs_bwd_opts* opts, const char* fn, const gs_camera* cam, gs_proj proj,
+                        const int32_t* ids, const int32_t* ranges, const float* T, const int32_t* n,
+                        const uint8_t* kb, const float* rgb = nullptr, const float* depth = nullptr) {
+  if (!opts || !opts->fwd) return GS_OK;
+  const gs_fwd_state& f = *opts->fwd;
+  const char* why = nullptr;
+  if (f.id == 0) why = "the forward state was never written";
+  else if (f.width != cam->width || f.height != cam->height) why = "image size differs from the forward's";
+  else if (f.rec != proj.rec) why = "proj.rec is not the forward's";
+  else if (f.sorted_ids != ids || f.tile_ranges != ranges) why = "sorted_ids / tile_ranges are not the forward's";
+  else if (f.T_final != T || f.n_contrib != n) why = "T_final / n_contrib are not the forward's";
+  else if (kb && kb != f.key_blocks) why = "key_blocks are not the forward's";
+  else if ((rgb && rgb != f.rgb) || (depth && depth != f.depth)) why = "rgb / depth are not the forward's";
+  else {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    const auto it = g_last_fwd.find(n);
+    if (it == g_last_fwd.end() || it->second != f.id) why = "n_contrib was rewritten by a later gs_render_fwd";
+  }
+  if (why) {
+    set_error("%s: state mismatch: %s (forward id %llu)", fn, why, (unsigned long long)f.id);
+    return GS_ERR_STATE;
+  }
+  return GS_OK;
+}
+
+// deterministic-mode workspace (gs_bwd_opts.det_ws)
+gs_status check_det(const gs_bwd_opts* opts, const char* fn, float** det, int64_t* det_keys) {
+  *det = nullptr;
+  *det_keys = 0;
+  if (!opts || !opts->det_ws) return GS_OK;
+  if (opts->det_keys < 0 || opts->det_keys >= (1ll << 30)) {
+    set_error("%s: det_keys=%lld out of range", fn, (long long)opts->det_keys);
+    return GS_ERR_ARG;
+  }
+  if (!aligned16(opts->det_ws)) {
+    set_error("%s: det_ws is not 16-byte aligned", fn);
+    return GS_ERR_ALIGN;
+  }
+  *det = opts->det_ws;
+  *det_keys = opts->det_keys;
+  return GS_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -209,7 +275,7 @@ gs_status gs_bin_tiles(const gs_camera* cam, const gs_scene* scene, gs_proj proj
 
 gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
                         const int32_t* tile_ranges, const int32_t* tile_order, float* rgb, float* depth, float* T_final, int32_t* n_contrib,
-                        unsigned long long* blended, uint8_t* key_blocks, void* stream) {
+                        unsigned long long* blended, uint8_t* key_blocks, gs_fwd_state* fwd_out, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_render_fwd"));
   GS_TRY(check_scene(scene, "gs_render_fwd"));
@@ -222,7 +288,9 @@ gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj pro
   }
   launch_render_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, rgb, depth, T_final, n_contrib, blended,
                     key_blocks, static_cast<cudaStream_t>(stream));
-  return check_launch("gs_render_fwd");
+  GS_TRY(check_launch("gs_render_fwd"));
+  record_forward(cam, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, key_blocks, fwd_out);
+  return GS_OK;
 }
 
 size_t gs_render_bwd_workspace(const gs_scene* scene) {
@@ -234,10 +302,15 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
                         const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                         const float* T_final,
                         const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
-                        const uint8_t* key_blocks, void* ws, size_t ws_bytes, float* grad, void* stream) {
+                        const uint8_t* key_blocks, void* ws, size_t ws_bytes, float* grad, const gs_bwd_opts* opts,
+                        void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_render_bwd"));
   GS_TRY(check_scene(scene, "gs_render_bwd"));
+  GS_TRY(check_forward(opts, "gs_render_bwd", cam, proj, sorted_ids, tile_ranges, T_final, n_contrib, key_blocks));
+  float* det;
+  int64_t det_keys;
+  GS_TRY(check_det(opts, "gs_render_bwd", &det, &det_keys));
   if (scene->P == 0) return GS_OK;
   GS_TRY(check_ptrs("gs_render_bwd", {{params, "params"}, {proj.rec, "proj.rec"}, {proj.radius, "proj.radius"},
                                       {proj.flags, "proj.flags"}, {tile_ranges, "tile_ranges"}, {T_final, "T_final"},
@@ -254,8 +327,8 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(ws, 0, need, s) != cudaSuccess) return check_launch("gs_render_bwd memset");
   const DevCam dc = make_devcam(*cam);
-  launch_render_bwd(dc, proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth, key_blocks,
-                    static_cast<float*>(ws), s);
+  launch_render_bwd(dc, proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth,
+                    key_blocks, static_cast<float*>(ws), s, nullptr, det, det_keys);
   const uint8_t* fl = proj.flags;
   float* sg = static_cast<float*>(ws);
   launch_project_bwd_views(1, &dc, &fl, &sg, scene->P, scene->P_stride, scene->sh_degree, params, grad, 1, s);
@@ -265,10 +338,15 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
 gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
                                const int32_t* tile_ranges, const int32_t* tile_order, const float* T_final, const int32_t* n_contrib,
                                const float* dL_drgb, const float* dL_ddepth, const uint8_t* key_blocks, float* sgrad,
-                               void* stream) {
+                               const gs_bwd_opts* opts, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_render_bwd_screen"));
   GS_TRY(check_scene(scene, "gs_render_bwd_screen"));
+  GS_TRY(check_forward(opts, "gs_render_bwd_screen", cam, proj, sorted_ids, tile_ranges, T_final, n_contrib,
+                       key_blocks));
+  float* det;
+  int64_t det_keys;
+  GS_TRY(check_det(opts, "gs_render_bwd_screen", &det, &det_keys));
   if (scene->P == 0) return GS_OK;
   GS_TRY(check_ptrs("gs_render_bwd_screen", {{proj.rec, "proj.rec"}, {tile_ranges, "tile_ranges"},
                                              {T_final, "T_final"}, {n_contrib, "n_contrib"}, {dL_drgb, "dL_drgb"},
@@ -277,8 +355,8 @@ gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_p
     set_error("gs_render_bwd_screen: dL_ddepth is not 16-byte aligned");
     return GS_ERR_ALIGN;
   }
-  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth,
-                    key_blocks, sgrad, static_cast<cudaStream_t>(stream));
+  launch_render_bwd(make_devcam(*cam), proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib,
+                    dL_drgb, dL_ddepth, key_blocks, sgrad, static_cast<cudaStream_t>(stream), nullptr, det, det_keys);
   return check_launch("gs_render_bwd_screen");
 }
 
@@ -286,18 +364,23 @@ gs_status gs_render_bwd_screen_l1(const gs_camera* cam, const gs_scene* scene, g
                                   const int32_t* sorted_ids, const int32_t* tile_ranges, const int32_t* tile_order,
                                   const float* T_final, const int32_t* n_contrib, const float* rgb, const float* depth,
                                   const float* target_rgb, const float* target_depth, float w_depth, float* loss,
-                                  const uint8_t* key_blocks, float* sgrad, void* stream) {
+                                  const uint8_t* key_blocks, float* sgrad, const gs_bwd_opts* opts, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_render_bwd_screen_l1"));
   GS_TRY(check_scene(scene, "gs_render_bwd_screen_l1"));
+  GS_TRY(check_forward(opts, "gs_render_bwd_screen_l1", cam, proj, sorted_ids, tile_ranges, T_final, n_contrib,
+                       key_blocks, rgb, depth));
+  float* det;
+  int64_t det_keys;
+  GS_TRY(check_det(opts, "gs_render_bwd_screen_l1", &det, &det_keys));
   GS_TRY(check_ptrs("gs_render_bwd_screen_l1", {{tile_ranges, "tile_ranges"}, {T_final, "T_final"},
                                                 {n_contrib, "n_contrib"}, {rgb, "rgb"}, {depth, "depth"},
                                                 {target_rgb, "target_rgb"}, {target_depth, "target_depth"},
                                                 {sgrad, "sgrad"}}));
   if (scene->P > 0) GS_TRY(check_ptrs("gs_render_bwd_screen_l1", {{proj.rec, "proj.rec"}}));
   const L1Targets l1{rgb, depth, target_rgb, target_depth, w_depth, loss};
-  launch_render_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, nullptr,
-                    nullptr, key_blocks, sgrad, static_cast<cudaStream_t>(stream), &l1);
+  launch_render_bwd(make_devcam(*cam), proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib,
+                    nullptr, nullptr, key_blocks, sgrad, static_cast<cudaStream_t>(stream), &l1, det, det_keys);
   return check_launch("gs_render_bwd_screen_l1");
 }
 
@@ -312,7 +395,7 @@ gs_status gs_tile_order(const gs_camera* cam, const int32_t* tile_ranges, int32_
 
 gs_status gs_naive_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj proj, const int32_t* sorted_ids,
                               const int32_t* tile_ranges, float* rgb, float* depth, float* T_final,
-                              int32_t* n_contrib, unsigned long long* blended, void* stream) {
+                              int32_t* n_contrib, unsigned long long* blended, gs_fwd_state* fwd_out, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_naive_render_fwd"));
   GS_TRY(check_scene(scene, "gs_naive_render_fwd"));
@@ -325,16 +408,24 @@ gs_status gs_naive_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_pr
   }
   launch_naive_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended,
                    static_cast<cudaStream_t>(stream));
-  return check_launch("gs_naive_render_fwd");
+  GS_TRY(check_launch("gs_naive_render_fwd"));
+  record_forward(cam, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, nullptr, fwd_out);
+  return GS_OK;
 }
 
 gs_status gs_naive_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_proj proj,
                                      const int32_t* sorted_ids, const int32_t* tile_ranges, const float* T_final,
                                      const int32_t* n_contrib, const float* dL_drgb, const float* dL_ddepth,
-                                     float* sgrad, void* stream) {
+                                     float* sgrad, const gs_bwd_opts* opts, void* stream) {
   g_err[0] = 0;
   GS_TRY(check_camera(cam, "gs_naive_render_bwd_screen"));
   GS_TRY(check_scene(scene, "gs_naive_render_bwd_screen"));
+  GS_TRY(check_forward(opts, "gs_naive_render_bwd_screen", cam, proj, sorted_ids, tile_ranges, T_final, n_contrib,
+                       nullptr));
+  if (opts && opts->det_ws) {
+    set_error("gs_naive_render_bwd_screen: the K13 port has no deterministic mode");
+    return GS_ERR_ARG;
+  }
   if (scene->P == 0) return GS_OK;
   GS_TRY(check_ptrs("gs_naive_render_bwd_screen", {{proj.rec, "proj.rec"}, {tile_ranges, "tile_ranges"},
                                                    {T_final, "T_final"}, {n_contrib, "n_contrib"},

@@ -99,9 +99,12 @@ struct L1Targets {
   float w_depth;
   float* loss;
 };
-void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
-                       const int32_t* order, const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Targets* l1 = nullptr);
+// det != nullptr: deterministic reduction (gs_bwd_opts.det_ws): per-key partials to
+// det[key][12] (zeroed here), then a fixed-order per-Gaussian sum into sgrad.
+void launch_render_bwd(const DevCam& cam, gs_proj proj, int64_t P, const int32_t* ids, const int32_t* ranges,
+                       const int32_t* order, const float* T_final, const int32_t* n_contrib, const float* g_rgb,
+                       const float* g_depth, const uint8_t* key_blocks, float* sgrad, cudaStream_t s,
+                       const L1Targets* l1 = nullptr, float* det = nullptr, int64_t det_keys = 0);
 // naive.cu (K13 comparison baseline, not the product path)
 void launch_naive_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, float* rgb,
                       float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended, cudaStream_t s);

@@ -640,7 +640,10 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
 
 // kMasks: the forward's per-key block masks are given (key_blocks != NULL; the
 // product path) -- a compile-time switch, so the key loop carries no test for it.
-template <int WPC, bool kMasks>
+// kDet: deterministic mode (gs_bwd_opts.det_ws): each (tile, key) pair's reduced 10
+// components are stored to det[key][12] instead of atomically added (k_det_reduce sums
+// them per Gaussian in a fixed order).
+template <int WPC, bool kMasks, bool kDet>
 __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
@@ -649,7 +652,8 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
                                                                    const uint8_t* __restrict__ key_blocks,
-                                                                   float* __restrict__ sgrad, L1Fuse l1) {
+                                                                   float* __restrict__ sgrad, L1Fuse l1,
+                                                                   float* __restrict__ det, int64_t det_keys) {
   __shared__ float4 s_rec[WPC][2][32][3];
   __shared__ int s_gid[WPC][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -780,24 +784,32 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
         v[7] = a.g;
         v[8] = a.b;
         v[9] = a.z;
-#if GSR_BWD_PAIR
-        float h[5];
-        reduce_half10(v, lane, h);
-        const int gid = s_gid[warp][buf][j];
-        if (gid_p >= 0) {
-          reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
-          gid_p = -1;
+        if constexpr (kDet) {
+          float out;
+          int slot;
+          warp_reduce10(v, lane, out, slot);
+          const int64_t kpos = (int64_t)lo + j;
+          if (slot >= 0 && kpos < det_keys) det[(int64_t)GS_SGRAD_FLOATS * kpos + slot] = out;
         } else {
+#if GSR_BWD_PAIR
+          float h[5];
+          reduce_half10(v, lane, h);
+          const int gid = s_gid[warp][buf][j];
+          if (gid_p >= 0) {
+            reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
+            gid_p = -1;
+          } else {
 #pragma unroll
-          for (int k = 0; k < 5; ++k) h_p[k] = h[k];
-          gid_p = gid;
-        }
+            for (int k = 0; k < 5; ++k) h_p[k] = h[k];
+            gid_p = gid;
+          }
 #else
-        float out;
-        int slot;
-        warp_reduce10(v, lane, out, slot);
-        if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
+          float out;
+          int slot;
+          warp_reduce10(v, lane, out, slot);
+          if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
 #endif
+        }
       }
     }
     __syncwarp();
@@ -959,7 +971,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
                                                                    const float* __restrict__ g_rgb,
                                                                    const float* __restrict__ g_dep,
                                                                    const uint8_t* __restrict__ key_blocks,
-                                                                   float* __restrict__ sgrad, L1Fuse l1) {
+                                                                   float* __restrict__ sgrad, L1Fuse l1,
+                                                                   float* __restrict__ det, int64_t det_keys) {
   __shared__ float4 s_rec[kWarpsPerCta][2][32][3];
   __shared__ int s_gid[kWarpsPerCta][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1097,7 +1110,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
         float out;
         int slot;
         warp_reduce10(v, lane, out, slot);
-        if (slot >= 0) atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
+        if (det) {
+          const int64_t kpos = (int64_t)lo + j;
+          if (slot >= 0 && kpos < det_keys) det[(int64_t)GS_SGRAD_FLOATS * kpos + slot] = out;
+        } else if (slot >= 0) {
+          atomicAdd(sgrad + (int64_t)GS_SGRAD_FLOATS * s_gid[warp][buf][j] + slot, out);
+        }
       }
     }
     __syncwarp();
@@ -1106,6 +1124,46 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) k_render_bwd(DevCam cam, co
   cp_async_wait<0>();
 }
 #endif  // GSR_EXACT_EXP
+
+// Deterministic mode, second pass: one thread per visible Gaussian sums its (tile, key)
+// partials in a fixed order -- the tiles of its rectangle, row-major -- and adds them to
+// its screen-gradient entry (no atomics: one writer per entry).  Its key in tile t is
+// found by a binary search of t's list on the sort key (depth bits, index) (R12).
+__global__ void __launch_bounds__(256) k_det_reduce(DevCam cam, const float4* __restrict__ rec,
+                                                    const int32_t* __restrict__ radius,
+                                                    const int32_t* __restrict__ ids, const int2* __restrict__ ranges,
+                                                    const float* __restrict__ det, int64_t det_keys, int64_t P,
+                                                    float* __restrict__ sgrad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P || radius[i] <= 0) return;
+  const float4 q0 = rec[3 * i], q2 = rec[3 * i + 2];
+  const uint32_t zb = __float_as_uint(q0.z);
+  const uint32_t rx = __float_as_uint(q2.z), ry = __float_as_uint(q2.w);
+  const int x0 = (int)(rx & 0xffffu), x1 = (int)(rx >> 16), y0 = (int)(ry & 0xffffu), y1 = (int)(ry >> 16);
+  float acc[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) acc[k] = 0.f;
+  for (int ty = y0; ty < y1; ++ty)
+    for (int tx = x0; tx < x1; ++tx) {
+      const int2 rg = ranges[ty * cam.TX + tx];
+      int lo = rg.x, hi = rg.y;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const int g = ids[mid];
+        const uint32_t zg = __float_as_uint(rec[3 * (int64_t)g].z);
+        if (zg < zb || (zg == zb && g < i)) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo < rg.y && ids[lo] == i && lo < det_keys) {
+        const float* d = det + (int64_t)GS_SGRAD_FLOATS * lo;
+#pragma unroll
+        for (int k = 0; k < 10; ++k) acc[k] += d[k];
+      }
+    }
+  float* o = sgrad + (int64_t)GS_SGRAD_FLOATS * i;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) o[k] += acc[k];
+}
 
 #ifndef GSR_EXACT_EXP
 // Warps (= tiles) per CTA of the fast kernels.  Tile work is very uneven (list lengths
@@ -1129,18 +1187,19 @@ void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, con
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, rgb, depth, T_final,
       n_contrib, blended, key_blocks);
 }
-template <int WPC>
+template <int WPC, bool kDet>
 void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                    const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1) {
+                    const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1, float* det,
+                    int64_t det_keys) {
   if (key_blocks)
-    k_render_bwd<WPC, true><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+    k_render_bwd<WPC, true, kDet><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
         cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-        g_rgb, g_depth, key_blocks, sgrad, l1);
+        g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys);
   else
-    k_render_bwd<WPC, false><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+    k_render_bwd<WPC, false, kDet><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
         cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-        g_rgb, g_depth, key_blocks, sgrad, l1);
+        g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys);
 }
 #endif
 
@@ -1163,9 +1222,12 @@ void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, 
   count_launch();
 }
 
-void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
-                       const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
-                       const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Targets* l1t) {
+void launch_render_bwd(const DevCam& cam, gs_proj proj, int64_t P, const int32_t* ids, const int32_t* ranges,
+                       const int32_t* order, const float* T_final, const int32_t* n_contrib, const float* g_rgb,
+                       const float* g_depth, const uint8_t* key_blocks, float* sgrad, cudaStream_t s,
+                       const L1Targets* l1t, float* det, int64_t det_keys) {
+  const float* rec = proj.rec;
+  if (det && det_keys > 0) cudaMemsetAsync(det, 0, (size_t)det_keys * GS_SGRAD_FLOATS * sizeof(float), s);
   L1Fuse l1{};
   if (l1t) {
     const int64_t npix = (int64_t)cam.W * cam.H;
@@ -1175,17 +1237,27 @@ void launch_render_bwd(const DevCam& cam, const float* rec, const int32_t* ids, 
     l1.loss = l1t->loss;
   }
 #ifndef GSR_EXACT_EXP
-  switch (render_wpc()) {
-    case 4: launch_bwd_wpc<4>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1); break;
-    case 2: launch_bwd_wpc<2>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1); break;
-    default: launch_bwd_wpc<1>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1);
+  if (det) {  // deterministic mode: one warp per CTA
+    launch_bwd_wpc<1, true>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1,
+                            det, det_keys);
+  } else {
+    switch (render_wpc()) {
+      case 4: launch_bwd_wpc<4, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0); break;
+      case 2: launch_bwd_wpc<2, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0); break;
+      default: launch_bwd_wpc<1, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0);
+    }
   }
 #else
   k_render_bwd<<<ceil_div(cam.TX * cam.TY, kWarpsPerCta), kWarpsPerCta * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-      g_rgb, g_depth, key_blocks, sgrad, l1);
+      g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys);
 #endif
   count_launch();
+  if (det && P > 0) {
+    k_det_reduce<<<ceil_div(P, 256), 256, 0, s>>>(cam, reinterpret_cast<const float4*>(rec), proj.radius, ids,
+                                                   reinterpret_cast<const int2*>(ranges), det, det_keys, P, sgrad);
+    count_launch();
+  }
 }
 
 }  // namespace gsr

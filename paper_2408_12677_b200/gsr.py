@@ -60,6 +60,35 @@ class GsProj(C.Structure):
     _fields_ = [("rec", C.c_void_p), ("radius", C.c_void_p), ("tiles", C.c_void_p), ("flags", C.c_void_p)]
 
 
+class GsFwdState(C.Structure):
+    """gs_fwd_state: written by gs_render_fwd, checked by the backward (GS_ERR_STATE)."""
+    _fields_ = [("id", C.c_uint64), ("width", C.c_int32), ("height", C.c_int32), ("rec", C.c_void_p),
+                ("sorted_ids", C.c_void_p), ("tile_ranges", C.c_void_p), ("rgb", C.c_void_p), ("depth", C.c_void_p),
+                ("T_final", C.c_void_p), ("n_contrib", C.c_void_p), ("key_blocks", C.c_void_p)]
+
+
+class GsBwdOpts(C.Structure):
+    _fields_ = [("fwd", C.POINTER(GsFwdState)), ("det_ws", C.c_void_p), ("det_keys", C.c_int64)]
+
+
+def bwd_opts(fwd=None, det=None):
+    """gs_bwd_opts for the backward calls: fwd = a GsFwdState the forward filled,
+    det = a float32 device tensor [keys][12] selecting the deterministic mode."""
+    if fwd is None and det is None:
+        return None
+    o = GsBwdOpts()
+    if fwd is not None:
+        o.fwd = C.pointer(fwd)
+    if det is not None:
+        o.det_ws = det.data_ptr()
+        o.det_keys = det.numel() // SGRAD_FLOATS
+    return o
+
+
+def _ref(x):
+    return None if x is None else C.byref(x)
+
+
 def camera(cam) -> GsCamera:
     """Marshal a scenegen.Camera (or any object with the same fields)."""
     g = GsCamera()
@@ -111,16 +140,16 @@ class Library:
         lib.gs_bin_tiles_workspace.argtypes = [vp, i64, i64]
         lib.gs_bin_tiles_workspace.restype = C.c_size_t
         lib.gs_bin_tiles.argtypes = [vp, vp, GsProj, vp, C.c_size_t, i64, vp, vp, vp, vp, vp]
-        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_render_bwd_workspace.argtypes = [vp]
         lib.gs_render_bwd_workspace.restype = C.c_size_t
-        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp]
-        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_render_bwd.argtypes = [vp, vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp, vp]
+        lib.gs_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_tile_order.argtypes = [vp, vp, vp, vp]
         lib.gs_render_bwd_screen_l1.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_float, vp,
-                                                vp, vp, vp]
-        lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
-        lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp]
+                                                vp, vp, vp, vp]
+        lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
         lib.gs_spatial_order_workspace.argtypes = [vp]
@@ -198,49 +227,52 @@ class Library:
                                                                    _stream(stream)))
 
     def render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
-                   key_blocks=None, stream=None, tile_order=None):
+                   key_blocks=None, stream=None, tile_order=None, fwd_state=None):
+        """fwd_state: optional GsFwdState (host) the call fills for the backward's check."""
         return self._check("gs_render_fwd", self.lib.gs_render_fwd(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(rgb),
             _ptr(depth),
-            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _ptr(key_blocks), _stream(stream)))
+            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _ptr(key_blocks), _ref(fwd_state), _stream(stream)))
 
     def render_bwd_workspace(self, sc: GsScene) -> int:
         return int(self.lib.gs_render_bwd_workspace(C.byref(sc)))
 
     def render_bwd(self, cam, sc, params, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, ws,
-                   grad, key_blocks=None, stream=None, tile_order=None):
+                   grad, key_blocks=None, stream=None, tile_order=None, fwd=None, det=None):
         return self._check("gs_render_bwd", self.lib.gs_render_bwd(
             C.byref(cam), C.byref(sc), _ptr(params), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order),
             _ptr(T_final),
             _ptr(n_contrib), _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(ws),
-            ws.numel() * ws.element_size(), _ptr(grad), _stream(stream)))
+            ws.numel() * ws.element_size(), _ptr(grad), _ref(bwd_opts(fwd, det)), _stream(stream)))
 
     def render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth, sgrad,
-                          key_blocks=None, stream=None, tile_order=None):
+                          key_blocks=None, stream=None, tile_order=None, fwd=None, det=None):
         return self._check("gs_render_bwd_screen", self.lib.gs_render_bwd_screen(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(T_final),
             _ptr(n_contrib),
-            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
+            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(key_blocks), _ptr(sgrad), _ref(bwd_opts(fwd, det)),
+            _stream(stream)))
 
     # -- K13 comparison baseline (per-pixel port; not the product path) ---
     def naive_render_fwd(self, cam, sc, proj, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended=None,
-                         stream=None):
+                         stream=None, fwd_state=None):
         return self._check("gs_naive_render_fwd", self.lib.gs_naive_render_fwd(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(rgb), _ptr(depth),
-            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _stream(stream)))
+            _ptr(T_final), _ptr(n_contrib), _ptr(blended), _ref(fwd_state), _stream(stream)))
 
     def naive_render_bwd_screen(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
-                                sgrad, stream=None):
+                                sgrad, stream=None, fwd=None, det=None):
         return self._check("gs_naive_render_bwd_screen", self.lib.gs_naive_render_bwd_screen(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(T_final), _ptr(n_contrib),
-            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _stream(stream)))
+            _ptr(dL_drgb), _ptr(dL_ddepth), _ptr(sgrad), _ref(bwd_opts(fwd, det)), _stream(stream)))
 
     def render_bwd_screen_l1(self, cam, sc, proj, sorted_ids, tile_ranges, T_final, n_contrib, rgb, depth, t_rgb,
-                             t_depth, w_depth, sgrad, loss=None, key_blocks=None, stream=None, tile_order=None):
+                             t_depth, w_depth, sgrad, loss=None, key_blocks=None, stream=None, tile_order=None,
+                             fwd=None, det=None):
         return self._check("gs_render_bwd_screen_l1", self.lib.gs_render_bwd_screen_l1(
             C.byref(cam), C.byref(sc), proj, _ptr(sorted_ids), _ptr(tile_ranges), _ptr(tile_order), _ptr(T_final),
             _ptr(n_contrib), _ptr(rgb), _ptr(depth), _ptr(t_rgb), _ptr(t_depth), float(w_depth), _ptr(loss),
-            _ptr(key_blocks), _ptr(sgrad), _stream(stream)))
+            _ptr(key_blocks), _ptr(sgrad), _ref(bwd_opts(fwd, det)), _stream(stream)))
 
     def project_bwd_views(self, cams, sc, params, flags, sgrads, grad, accumulate=True, stream=None):
         """cams: list of GsCamera; flags / sgrads: lists of device tensors (one per view)."""

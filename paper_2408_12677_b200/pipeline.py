@@ -58,7 +58,7 @@ def spatially_order(lib, model: GaussianModel):
 class ViewBuffers:
     """Device buffers for one view in flight (reused across views of equal size)."""
 
-    def __init__(self, lib: gsr.Library, cam, P: int, key_capacity: int, device):
+    def __init__(self, lib: gsr.Library, cam, P: int, key_capacity: int, device, deterministic: bool = False):
         self.lib = lib
         self.W, self.H = int(cam.width), int(cam.height)
         self.NT = ((self.W + 15) // 16) * ((self.H + 15) // 16)
@@ -80,6 +80,12 @@ class ViewBuffers:
         self.g_depth = torch.empty((self.H, self.W), dtype=torch.float32, device=device)
         sgrad_bytes = lib.render_bwd_workspace(gsr.scene_desc(P, P, 0))
         self.bwd_ws = torch.empty(max(sgrad_bytes // 4, 4), dtype=torch.float32, device=device)
+        # the forward's state (gs_fwd_state), filled by gs_render_fwd and checked by the
+        # backward (GS_ERR_STATE on buffers of another forward)
+        self.fwd_state = gsr.GsFwdState()
+        # deterministic reduction workspace (gs_bwd_opts.det_ws): float[key_capacity][12]
+        self.det = (torch.empty((max(key_capacity, 1), gsr.SGRAD_FLOATS), dtype=torch.float32, device=device)
+                    if deterministic else None)
         assert npx > 0
 
 
@@ -126,7 +132,7 @@ class Trainer:
 
     def __init__(self, lib, model: GaussianModel, cameras, targets, device, key_capacity: int,
                  w_depth: float = 1.0, allreduce=None, chunk: int = 8, streams: int = 1, optimizer=None,
-                 capacity: int = None):
+                 capacity: int = None, deterministic: bool = False):
         # capacity: the most Gaussians the per-view buffers must hold (a growing online
         # map passes its P_stride; default the model's current P)
         cap_p = int(capacity) if capacity is not None else model.P
@@ -153,7 +159,11 @@ class Trainer:
         nb = os.environ.get("GSR_BIN_STREAMS")
         self.n_bin = (int(nb) if nb is not None else 8) if n_streams > 1 else 0
         n_bufs = n_streams + self.n_bin
-        self.bufs = [ViewBuffers(lib, cameras[0], cap_p, key_capacity, device) for _ in range(n_bufs)]
+        # deterministic: the backward's reduction in a fixed order (gs_bwd_opts.det_ws), so
+        # an iteration's parameters are bit-reproducible whatever the streams / graphs
+        self.deterministic = bool(deterministic)
+        self.bufs = [ViewBuffers(lib, cameras[0], cap_p, key_capacity, device, deterministic=self.deterministic)
+                     for _ in range(n_bufs)]
         self.buf = self.bufs[0]
         # (equal priorities: staggering the streams' priorities measured 4% slower)
         self._streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)] if n_streams > 1 else None
@@ -253,10 +263,10 @@ class Trainer:
         self._hook("render_fwd", "begin")
         if self.naive:
             lib.naive_render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n,
-                                 blended=self.blended)
+                                 blended=self.blended, fwd_state=b.fwd_state)
         else:
             lib.render_fwd(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.rgb, b.depth, b.T, b.n,
-                           blended=self.blended, key_blocks=b.key_blocks, tile_order=order)
+                           blended=self.blended, key_blocks=b.key_blocks, tile_order=order, fwd_state=b.fwd_state)
         self._hook("render_fwd", "end")
         if targets_ready is not None:
             torch.cuda.current_stream().wait_event(targets_ready)
@@ -267,16 +277,17 @@ class Trainer:
         self._hook("render_bwd", "begin")
         if self.naive:
             lib.naive_render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
-                                        self.sgrad[slot])
+                                        self.sgrad[slot], fwd=b.fwd_state)
         elif self.fuse_l1:  # Eq. 12's upstream computed inside the backward (one kernel)
             lib.render_bwd_screen_l1(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.rgb, b.depth, t_rgb,
                                      t_depth, self.w_depth, self.sgrad[slot], loss=self.loss, key_blocks=b.key_blocks,
-                                     tile_order=order)
+                                     tile_order=order, fwd=b.fwd_state, det=b.det)
             if targets_consumed is not None:
                 targets_consumed.record()
         else:
             lib.render_bwd_screen(gcam, m.desc, proj, b.sorted_ids, b.ranges, b.T, b.n, b.g_rgb, b.g_depth,
-                                  self.sgrad[slot], key_blocks=b.key_blocks, tile_order=order)
+                                  self.sgrad[slot], key_blocks=b.key_blocks, tile_order=order, fwd=b.fwd_state,
+                                  det=b.det)
         self._hook("render_bwd", "end")
 
     def step(self, views, targets_override=None):

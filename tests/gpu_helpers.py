@@ -154,10 +154,3 @@ def assert_grad_parity(g, ref, bound, scale=1.0, what="gradient", exclude=None):
 def flip_pixels(cam, scene, px=None, py=None):
     """Pixels whose decisions are within C_FLIP error bounds of a threshold."""
     return gsref.margin_bound(cam, scene, px, py) < C_FLIP
-
-
-def grad_mismatch(g, ref, rtol=1e-3, atol=1e-6):
-    """GPU-vs-GPU comparisons of runs that differ only in float-atomic summation order
-    (replaced by bit-equality under the deterministic build where one exists)."""
-    d = np.abs(g - ref)
-    return ~((d <= atol) | (d <= rtol * np.abs(ref)))

@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(libs):
 
 def test_versions_and_flags(libs):
     fast, exact = libs
-    assert fast.lib.gs_version() == 1 and exact.lib.gs_version() == 1
+    assert fast.lib.gs_version() == 2 and exact.lib.gs_version() == 2
     assert fast.lib.gs_exact_exp() == 0 and exact.lib.gs_exact_exp() == 1
     assert fast.launch_count() >= 0
 
@@ -89,3 +89,37 @@ def test_product_package_does_not_import_oracle():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "paper_2408_12677_b200", f)).read()
             assert "oracle" not in re.sub(r'""".*?"""|#.*', "", src, flags=re.S), f
+
+
+def test_state_mismatch_detected_on_host(libs):
+    """GS_ERR_STATE (SPEC.md:349 StateMismatch) is decided on the host before any launch:
+    a never-written state, another image size, or buffers that are not the forward's."""
+    from paper_2408_12677_b200 import gsr
+    import scenegen
+    lib = libs[0]
+    cam = gsr.camera(scenegen.identity_camera(64, 48, 60.0, 32.0, 24.0))
+    sc = gsr.scene_desc(4, 4, 0)
+    A = [C.c_void_p(0x10000 * (k + 1)) for k in range(8)]  # fake, aligned, never dereferenced
+    proj = gsr.GsProj(A[0], A[1], A[2], A[3])
+    st = gsr.GsFwdState()  # id 0: never written by a forward
+    opts = gsr.bwd_opts(fwd=st)
+
+    def call(o):
+        return lib.lib.gs_render_bwd_screen(C.byref(cam), C.byref(sc), proj, A[4], A[5], None, A[6], A[7], A[4],
+                                            None, None, A[5], C.byref(o), None)
+    assert call(opts) == gsr.GS_ERR_STATE and "never written" in lib.last_error()
+    st.id, st.width, st.height = 12345, 64, 40
+    assert call(opts) == gsr.GS_ERR_STATE and "size" in lib.last_error()
+    st.height = 48
+    st.rec, st.sorted_ids, st.tile_ranges, st.T_final, st.n_contrib = 0x10000, 0x50000, 0x60000, 0x70000, 0x80000
+    assert call(opts) == gsr.GS_ERR_STATE and "n_contrib" in lib.last_error()  # no forward wrote A[7]: stale
+    st.sorted_ids = 0x90000
+    assert call(opts) == gsr.GS_ERR_STATE and "sorted_ids" in lib.last_error()
+    # the deterministic workspace is validated too; the K13 port rejects the mode
+    o2 = gsr.GsBwdOpts()
+    o2.det_ws, o2.det_keys = 0x10004, 16
+    assert call(o2) == gsr.GS_ERR_ALIGN
+    o2.det_ws = 0x10000
+    st2 = lib.lib.gs_naive_render_bwd_screen(C.byref(cam), C.byref(sc), proj, A[4], A[5], A[6], A[7], A[4], None,
+                                             A[5], C.byref(o2), None)
+    assert st2 == gsr.GS_ERR_ARG and "deterministic" in lib.last_error()

@@ -7,7 +7,7 @@ import pytest
 import torch
 
 import scenegen
-from gpu_helpers import DEV, grad_mismatch
+from gpu_helpers import DEV
 from paper_2408_12677_b200 import gsr, pipeline
 
 pytestmark = pytest.mark.gpu
@@ -87,8 +87,8 @@ def test_sparse_exchange_adam_single_rank_nccl(lib):
         cap = pipeline.default_capacity(pipeline.measure_keys(lib, models[0], cams, DEV))
         targets = pipeline.render_targets(lib, tgt, cams, DEV, cap)
         opt = pipeline.SparseExchangeAdam(lib, models[1])
-        trs = [pipeline.Trainer(lib, models[0], cams, targets, DEV, cap, streams=2),
-               pipeline.Trainer(lib, models[1], cams, targets, DEV, cap, streams=2, optimizer=opt)]
+        trs = [pipeline.Trainer(lib, models[0], cams, targets, DEV, cap, streams=2, deterministic=True),
+               pipeline.Trainer(lib, models[1], cams, targets, DEV, cap, streams=2, optimizer=opt, deterministic=True)]
         for it in range(3):
             snap = models[1].params.cpu().numpy().copy()
             for tr in trs:
@@ -102,7 +102,7 @@ def test_sparse_exchange_adam_single_rank_nccl(lib):
                 for c in cams:
                     vis |= (gsref.project(c, scene, gsref.F32)["flags"] & 128) == 0
                 assert opt.last_M == int(vis.sum()) and 0 < opt.last_M < w.scene.P
-        p0, p1 = (m.params.cpu().numpy().astype(np.float64) for m in models)
-        assert grad_mismatch(p1, p0, rtol=1e-4, atol=1e-6).mean() <= 1e-3
+        # deterministic reduction: the sparse exchange updates exactly what the dense step does
+        assert torch.equal(models[0].params, models[1].params)
     finally:
         dist.destroy_process_group()

@@ -5,7 +5,7 @@ import pytest
 import torch
 
 import scenegen
-from gpu_helpers import DEV, grad_mismatch
+from gpu_helpers import DEV
 from oracle import frame
 from paper_2408_12677_b200 import gsr, pipeline
 
@@ -93,7 +93,7 @@ def test_step_host_sensor_frames_match_decoded_targets(lib, streams):
         host[v] = (torch.from_numpy(c8).pin_memory(), torch.from_numpy(d16.view(np.int16)).pin_memory())
         o_rgb, o_d = frame.decode_rgbd(c8, d16, scenegen.DEPTH_SCALE)
         targets.append((torch.from_numpy(o_rgb).to(DEV), torch.from_numpy(o_d).to(DEV)))
-    trs = [pipeline.Trainer(lib, m, cams, targets, DEV, cap, streams=streams) for m in models]
+    trs = [pipeline.Trainer(lib, m, cams, targets, DEV, cap, streams=streams, deterministic=True) for m in models]
     for it in range(3):
         for tr in trs:
             tr.loss.zero_()
@@ -104,7 +104,6 @@ def test_step_host_sensor_frames_match_decoded_targets(lib, streams):
         assert trs[1].loss.item() == pytest.approx(trs[0].loss.item(), rel=1e-5)
         if it == 0:
             assert trs[1].blended.item() == trs[0].blended.item()
-    p0, p1 = (m.params.cpu().numpy().astype(np.float64) for m in models)
-    assert grad_mismatch(p1, p0, rtol=1e-4, atol=1e-6).mean() <= 1e-3
+    assert torch.equal(models[0].params, models[1].params)  # deterministic reduction: bit-identical
     with pytest.raises(ValueError):
         trs[1].step_host([0], host)  # sensor frames need depth_scale
