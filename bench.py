@@ -412,12 +412,39 @@ def run_online(args):
     print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- launcher
+def self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) run without torchrun: re-launch this command under
+    torch.distributed.run with N ranks, one per GPU (the contract's launch line).  Fails
+    loudly when fewer than N GPUs are visible (no silent 1-GPU number)."""
+    import socket
+    if args.impl != "reference":
+        import torch
+        n_vis = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if n_vis < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {n_vis} GPU(s) visible; refusing to report a "
+                  f"{n_vis}-GPU number as {args.gpus}", file=sys.stderr, flush=True)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------------------- GPU arm
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != max(args.gpus, 1) and "WORLD_SIZE" in os.environ and os.environ.get("GSR_FORCE_DIST") != "1":
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -545,10 +572,14 @@ def main():
         else:
             stage_ev[stage].append((open_ev.pop(stage), ev))
 
-    # CUDA-graph mode (single rank): each distinct view set of the timed steps is
-    # captured once as a whole iteration and replayed; launches per step are counted
-    # while capturing (a replay does not pass through the library's counter)
-    use_graph = args.graph and world == 1 and not args.profile and tr.optimizer is None
+    # CUDA-graph mode: each distinct view set of the timed steps is captured once as a
+    # whole iteration -- at N > 1 including the exchange (NCCL collectives, or the
+    # peer-memory kernel and its barriers) and Adam with the device step counter -- and
+    # replayed, so N = 1 and N = 8 are timed alike; launches per step are counted while
+    # capturing (a replay does not pass through the library's counter).  The
+    # visibility-sparse exchange reads its size on the host and stays eager.
+    use_graph = (args.graph and not args.profile and
+                 (tr.optimizer is None or hasattr(tr.optimizer, "device_step")))
     graphs, graph_launches = {}, {}
     if use_graph:
         for i in range(args.steps):

@@ -341,6 +341,13 @@ gs_status gs_adam_step_range(const gs_scene* scene /*HOST*/, float* params, cons
                              const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps, int64_t step,
                              int64_t begin, int64_t end, void* stream);
 
+/* gs_adam_step_range with the 1-based step counter in DEVICE memory (as gs_adam_step_dev:
+ * *step_dev is incremented on the stream first; graph-capturable).  Every rank calls it,
+ * also one whose range is empty (it then only advances its counter). */
+gs_status gs_adam_step_range_dev(const gs_scene* scene /*HOST*/, float* params, const float* grad_range, float* m,
+                                 float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps,
+                                 int64_t* step_dev, int64_t begin, int64_t end, void* stream);
+
 /* Reduce-scatter + Adam + all-gather fused in ONE kernel over peer memory (SURVEY.md
  * §8(f) NEXT-2): for the scalars [begin, end) this rank owns, sum every rank's
  * gradient (P2P loads over NVLink from grad_peers[0..world-1], in rank order), apply
@@ -355,6 +362,12 @@ gs_status gs_adam_step_peers(const gs_scene* scene /*HOST*/, int world, int rank
                              const float* const* grad_peers /*HOST[world]*/, float* const* param_peers /*HOST[world]*/,
                              float* m, float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2, float eps,
                              int64_t step, int64_t begin, int64_t end, void* stream);
+/* gs_adam_step_peers with the step counter in DEVICE memory (*step_dev incremented first;
+ * graph-capturable, so the multi-GPU iteration replays as one CUDA graph per rank). */
+gs_status gs_adam_step_peers_dev(const gs_scene* scene /*HOST*/, int world, int rank,
+                                 const float* const* grad_peers /*HOST[world]*/, float* const* param_peers /*HOST[world]*/,
+                                 float* m, float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2,
+                                 float eps, int64_t* step_dev, int64_t begin, int64_t end, void* stream);
 
 /* ---------------------------------------------------------------- visibility-sparse exchange
  * (SURVEY.md §8(f) NEXT-2 "visibility-sparse gradient exchange: union of visible masks,

@@ -530,53 +530,100 @@ gs_status gs_adam_step_dev(const gs_scene* scene, float* params, float* grad, fl
   return check_launch("gs_adam_step_dev");
 }
 
-gs_status gs_adam_step_range(const gs_scene* scene, float* params, const float* grad_range, float* m, float* v,
-                             const float* lr_per_row, float beta1, float beta2, float eps, int64_t step, int64_t begin,
-                             int64_t end, void* stream) {
+namespace {
+// gs_adam_step_range / gs_adam_step_peers with the step on the host (step_dev NULL) or on
+// the device (the *_dev calls: *step_dev is incremented first, graph-capturable).
+gs_status adam_range_impl(const char* fn, const gs_scene* scene, float* params, const float* grad_range, float* m,
+                          float* v, const float* lr_per_row, float beta1, float beta2, float eps, int64_t step,
+                          int64_t* step_dev, int64_t begin, int64_t end, void* stream) {
   g_err[0] = 0;
-  GS_TRY(check_scene(scene, "gs_adam_step_range"));
+  GS_TRY(check_scene(scene, fn));
   const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
-  if (!lr_per_row || step < 1 || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f) ||
-      begin < 0 || end < begin || end > n) {
-    set_error("gs_adam_step_range: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", (long long)step,
-              (long long)begin, (long long)end, (long long)n);
+  if (!lr_per_row || (!step_dev && step < 1) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) ||
+      !(eps >= 0.f) || begin < 0 || end < begin || end > n) {
+    set_error("%s: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", fn, (long long)step, (long long)begin,
+              (long long)end, (long long)n);
     return GS_ERR_ARG;
   }
   if ((begin & 3) || (end & 3)) {
-    set_error("gs_adam_step_range: begin/end must be multiples of 4");
+    set_error("%s: begin/end must be multiples of 4", fn);
     return GS_ERR_ALIGN;
   }
-  if (end == begin) return GS_OK;
-  GS_TRY(check_ptrs("gs_adam_step_range", {{params, "params"}, {grad_range, "grad_range"}, {m, "m"}, {v, "v"}}));
-  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
-  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (end == begin) {
+    if (step_dev) launch_adam(rows_of(scene), scene->P_stride, nullptr, nullptr, nullptr, nullptr, lr_per_row, beta1,
+                              beta2, eps, 1.f, 1.f, 0, s, 0, 0, -1, step_dev);  // only advances the counter
+    return step_dev ? check_launch(fn) : GS_OK;
+  }
+  GS_TRY(check_ptrs(fn, {{params, "params"}, {grad_range, "grad_range"}, {m, "m"}, {v, "v"}}));
+  const double bc1 = step_dev ? 1.0 : 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = step_dev ? 1.0 : 1.0 - std::pow((double)beta2, (double)step);
   launch_adam(rows_of(scene), scene->P_stride, params, const_cast<float*>(grad_range), m, v, lr_per_row, beta1, beta2,
-              eps, (float)bc1, (float)bc2, 0, static_cast<cudaStream_t>(stream), begin, end);
-  return check_launch("gs_adam_step_range");
+              eps, (float)bc1, (float)bc2, 0, s, begin, end, -1, step_dev);
+  return check_launch(fn);
+}
+
+gs_status adam_peers_impl(const char* fn, const gs_scene* scene, int world, int rank, const float* const* grad_peers,
+                          float* const* param_peers, float* m, float* v, const float* lr_per_row, float beta1,
+                          float beta2, float eps, int64_t step, int64_t* step_dev, int64_t begin, int64_t end,
+                          void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, fn));
+  const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
+  if (!grad_peers || !param_peers || !lr_per_row || (!step_dev && step < 1) || !(beta1 >= 0.f && beta1 < 1.f) ||
+      !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f) || begin < 0 || end < begin || end > n) {
+    set_error("%s: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", fn, (long long)step, (long long)begin,
+              (long long)end, (long long)n);
+    return GS_ERR_ARG;
+  }
+  if ((begin & 3) || (end & 3)) {
+    set_error("%s: begin/end must be multiples of 4", fn);
+    return GS_ERR_ALIGN;
+  }
+  if (end > begin) GS_TRY(check_ptrs(fn, {{m, "m"}, {v, "v"}}));
+  const double bc1 = step_dev ? 1.0 : 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = step_dev ? 1.0 : 1.0 - std::pow((double)beta2, (double)step);
+  GS_TRY(launch_adam_peers(rows_of(scene), scene->P_stride, world, rank, grad_peers, param_peers, m, v, lr_per_row,
+                           beta1, beta2, eps, (float)bc1, (float)bc2, begin, end, static_cast<cudaStream_t>(stream),
+                           step_dev));
+  return check_launch(fn);
+}
+}  // namespace
+
+gs_status gs_adam_step_range(const gs_scene* scene, float* params, const float* grad_range, float* m, float* v,
+                             const float* lr_per_row, float beta1, float beta2, float eps, int64_t step, int64_t begin,
+                             int64_t end, void* stream) {
+  return adam_range_impl("gs_adam_step_range", scene, params, grad_range, m, v, lr_per_row, beta1, beta2, eps, step,
+                         nullptr, begin, end, stream);
+}
+
+gs_status gs_adam_step_range_dev(const gs_scene* scene, float* params, const float* grad_range, float* m, float* v,
+                                 const float* lr_per_row, float beta1, float beta2, float eps, int64_t* step_dev,
+                                 int64_t begin, int64_t end, void* stream) {
+  if (!step_dev) {
+    set_error("gs_adam_step_range_dev: step_dev is NULL");
+    return GS_ERR_ARG;
+  }
+  return adam_range_impl("gs_adam_step_range_dev", scene, params, grad_range, m, v, lr_per_row, beta1, beta2, eps, 0,
+                         step_dev, begin, end, stream);
 }
 
 gs_status gs_adam_step_peers(const gs_scene* scene, int world, int rank, const float* const* grad_peers,
                              float* const* param_peers, float* m, float* v, const float* lr_per_row, float beta1,
                              float beta2, float eps, int64_t step, int64_t begin, int64_t end, void* stream) {
-  g_err[0] = 0;
-  GS_TRY(check_scene(scene, "gs_adam_step_peers"));
-  const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
-  if (!grad_peers || !param_peers || !lr_per_row || step < 1 || !(beta1 >= 0.f && beta1 < 1.f) ||
-      !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f) || begin < 0 || end < begin || end > n) {
-    set_error("gs_adam_step_peers: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", (long long)step,
-              (long long)begin, (long long)end, (long long)n);
+  return adam_peers_impl("gs_adam_step_peers", scene, world, rank, grad_peers, param_peers, m, v, lr_per_row, beta1,
+                         beta2, eps, step, nullptr, begin, end, stream);
+}
+
+gs_status gs_adam_step_peers_dev(const gs_scene* scene, int world, int rank, const float* const* grad_peers,
+                                 float* const* param_peers, float* m, float* v, const float* lr_per_row, float beta1,
+                                 float beta2, float eps, int64_t* step_dev, int64_t begin, int64_t end, void* stream) {
+  if (!step_dev) {
+    set_error("gs_adam_step_peers_dev: step_dev is NULL");
     return GS_ERR_ARG;
   }
-  if ((begin & 3) || (end & 3)) {
-    set_error("gs_adam_step_peers: begin/end must be multiples of 4");
-    return GS_ERR_ALIGN;
-  }
-  if (end > begin) GS_TRY(check_ptrs("gs_adam_step_peers", {{m, "m"}, {v, "v"}}));
-  const double bc1 = 1.0 - std::pow((double)beta1, (double)step);
-  const double bc2 = 1.0 - std::pow((double)beta2, (double)step);
-  GS_TRY(launch_adam_peers(rows_of(scene), scene->P_stride, world, rank, grad_peers, param_peers, m, v, lr_per_row,
-                           beta1, beta2, eps, (float)bc1, (float)bc2, begin, end, static_cast<cudaStream_t>(stream)));
-  return check_launch("gs_adam_step_peers");
+  return adam_peers_impl("gs_adam_step_peers_dev", scene, world, rank, grad_peers, param_peers, m, v, lr_per_row,
+                         beta1, beta2, eps, 0, step_dev, begin, end, stream);
 }
 
 gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,

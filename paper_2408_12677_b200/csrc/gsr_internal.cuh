@@ -114,12 +114,13 @@ void launch_naive_bwd(const DevCam& cam, const float* rec, const int32_t* ids, c
 // optim.cu
 void launch_adam(int64_t F, int64_t P_stride, float* params, float* grad, float* m, float* v, const float* lr,
                  float beta1, float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s,
-                 int64_t begin = 0, int64_t end = -1, int64_t live = -1);
+                 int64_t begin = 0, int64_t end = -1, int64_t live = -1, int64_t* step_dev = nullptr);
 void launch_adam_dev(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
                      float beta2, float eps, int64_t* step_dev, int zero_grad, cudaStream_t s, int64_t live = -1);
 gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const float* const* grad_peers,
                             float* const* param_peers, float* m, float* v, const float* lr, float beta1, float beta2,
-                            float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s);
+                            float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s,
+                            int64_t* step_dev = nullptr);
 void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
                float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s);
 

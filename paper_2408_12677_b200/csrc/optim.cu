@@ -7,8 +7,31 @@ namespace gsr {
 namespace {
 
 struct LrTable {
-  float step[64];  // lr_row / (1 - beta1^t)
+  float step[64];  // lr_row / (1 - beta1^t)   (raw lr_row when the step is on the device)
 };
+
+// Per-row step sizes and 1/sqrt(1 - beta2^t) of one Adam step, in shared memory.  With
+// step_dev == nullptr they come from the host (lr already divided by bc1, rs_bc2
+// given); otherwise every block derives them from the device step counter t = *step_dev
+// (CUDA-graph replays, gs_adam_step*_dev), with the same arithmetic as the host (t in
+// double, bias corrections rounded to fp32), so both give bit-identical updates.
+__device__ __forceinline__ void adam_steps(const LrTable& lr, int F, float b1, float b2, float rs_host,
+                                           const int64_t* __restrict__ step_dev, float* s_step, float& s_rs) {
+  __shared__ float rs;
+  if (threadIdx.x < 64) {
+    if (step_dev) {
+      const double t = (double)*step_dev;
+      const float bc1 = (float)(1.0 - pow((double)b1, t));
+      s_step[threadIdx.x] = threadIdx.x < F ? lr.step[threadIdx.x] / bc1 : 0.f;
+      if (threadIdx.x == 0) rs = 1.f / sqrtf((float)(1.0 - pow((double)b2, t)));
+    } else {
+      s_step[threadIdx.x] = lr.step[threadIdx.x];
+      if (threadIdx.x == 0) rs = rs_host;
+    }
+  }
+  __syncthreads();
+  s_rs = rs;
+}
 
 // Scalars [4 b4, 4 e4) of the flattened [F][P_stride] arrays; g holds the gradient of
 // that range (g[i - b4]), so a rank of the sharded optimiser passes its reduce-scattered
@@ -17,12 +40,16 @@ struct LrTable {
 // Gaussians [0, P) of a map that grows into its capacity P_stride.
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
                                               float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4, int64_t cl4,
-                                              LrTable lr, float b1, float b2, float eps, float rs_bc2, int zero_grad) {
+                                              LrTable lr_in, int F, float b1, float b2, float eps, float rs_host,
+                                              const int64_t* __restrict__ step_dev, int zero_grad) {
+  __shared__ float s_step[64];
+  float rs_bc2;
+  adam_steps(lr_in, F, b1, b2, rs_host, step_dev, s_step, rs_bc2);
   const float c1 = 1.f - b1, c2 = 1.f - b2;
   const int64_t count = cl4 < S4 ? (e4 / S4) * cl4 : e4 - b4;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = cl4 < S4 ? (j / cl4) * S4 + j % cl4 : b4 + j;
-    const float step = lr.step[i / S4];
+    const float step = s_step[i / S4];
     const float4 gg = g[i - b4];
     float4 mm = m[i], vv = v[i], pp = p[i];
     adam_update(pp.x, mm.x, vv.x, gg.x, b1, b2, c1, c2, step, rs_bc2, eps);
@@ -87,10 +114,14 @@ struct Peers {
 
 __global__ void __launch_bounds__(256) k_adam_peers(const __grid_constant__ Peers pr, float4* __restrict__ m,
                                                     float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4,
-                                                    LrTable lr, float b1, float b2, float eps, float rs_bc2) {
+                                                    LrTable lr_in, int F, float b1, float b2, float eps, float rs_host,
+                                                    const int64_t* __restrict__ step_dev) {
+  __shared__ float s_step[64];
+  float rs_bc2;
+  adam_steps(lr_in, F, b1, b2, rs_host, step_dev, s_step, rs_bc2);
   const float c1 = 1.f - b1, c2 = 1.f - b2;
   for (int64_t i = b4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e4; i += (int64_t)gridDim.x * blockDim.x) {
-    const float step = lr.step[i / S4];
+    const float step = s_step[i / S4];
     float4 gs[kMaxPeers];
 #pragma unroll
     for (int r = 0; r < kMaxPeers; ++r)
@@ -139,9 +170,13 @@ __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restric
 
 void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
                  float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s, int64_t begin,
-                 int64_t end, int64_t live) {
+                 int64_t end, int64_t live, int64_t* step_dev) {
   LrTable t{};
-  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = step_dev ? lr[r] : lr[r] / bc1;
+  if (step_dev) {
+    k_step_inc<<<1, 1, 0, s>>>(step_dev);
+    count_launch();
+  }
   int64_t cl4 = S / 4;
   if (end < 0) {
     end = F * S;
@@ -151,7 +186,8 @@ void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, flo
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
   k_adam<<<std::max(grid, 1), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grad),
                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
-                                           end / 4, S / 4, cl4, t, beta1, beta2, eps, 1.f / sqrtf(bc2), zero_grad);
+                                           end / 4, S / 4, cl4, t, (int)F, beta1, beta2, eps,
+                                           step_dev ? 0.f : 1.f / sqrtf(bc2), step_dev, zero_grad);
   count_launch();
 }
 
@@ -171,7 +207,8 @@ void launch_adam_dev(int64_t F, int64_t S, float* params, float* grad, float* m,
 
 gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const float* const* grad_peers,
                             float* const* param_peers, float* m, float* v, const float* lr, float beta1, float beta2,
-                            float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s) {
+                            float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s,
+                            int64_t* step_dev) {
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world) {
     set_error("gs_adam_step_peers: world %d / rank %d outside [1, %d]", world, rank, kMaxPeers);
     return GS_ERR_ARG;
@@ -187,12 +224,17 @@ gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const flo
     pr.param[r] = reinterpret_cast<float4*>(param_peers[r]);
   }
   LrTable t{};
-  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = lr[r] / bc1;
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = step_dev ? lr[r] : lr[r] / bc1;
+  if (step_dev) {  // every rank advances its own counter, whether or not it owns scalars
+    k_step_inc<<<1, 1, 0, s>>>(step_dev);
+    count_launch();
+  }
   const int64_t n4 = (end - begin) / 4;
   const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
   if (n4 > 0) {
     k_adam_peers<<<std::max(grid, 1), 256, 0, s>>>(pr, reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
-                                                    begin / 4, end / 4, S / 4, t, beta1, beta2, eps, 1.f / sqrtf(bc2));
+                                                    begin / 4, end / 4, S / 4, t, (int)F, beta1, beta2, eps,
+                                                    step_dev ? 0.f : 1.f / sqrtf(bc2), step_dev);
     count_launch();
   }
   return GS_OK;

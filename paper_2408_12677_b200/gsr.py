@@ -160,6 +160,10 @@ class Library:
         lib.gs_adam_step_peers.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float,
                                            i64, i64, i64, vp]
         lib.gs_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp]
+        lib.gs_adam_step_range_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, i64, i64,
+                                               vp]
+        lib.gs_adam_step_peers_dev.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float,
+                                               C.c_float, vp, i64, i64, vp]
         lib.gs_tsdf_reset.argtypes = [GsTsdfVolume, vp]
         lib.gs_tsdf_allocate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
         lib.gs_tsdf_integrate.argtypes = [vp, GsTsdfVolume, vp, vp, vp, vp]
@@ -178,7 +182,7 @@ class Library:
         lib.gs_scatter_columns.argtypes = [vp, i64, i64, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",  # noqa: E501
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_adam_step_range_dev", "gs_adam_step_peers_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
                    "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd", "gs_visibility_union", "gs_compact_index",
                    "gs_gather_columns", "gs_scatter_columns", "gs_project_views"):
             getattr(lib, fn).restype = i32
@@ -328,17 +332,27 @@ class Library:
 
     def adam_step_range(self, sc, params, grad_range, m, v, lr_per_row, step, begin, end, beta1=0.9, beta2=0.999,
                         eps=1e-15, stream=None):
+        """step: an int (host step counter) or an int64 device tensor (gs_adam_step_range_dev)."""
         lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        if isinstance(step, torch.Tensor):
+            return self._check("gs_adam_step_range_dev", self.lib.gs_adam_step_range_dev(
+                C.byref(sc), _ptr(params), _ptr(grad_range), _ptr(m), _ptr(v), lr, beta1, beta2, eps, _ptr(step),
+                int(begin), int(end), _stream(stream)))
         return self._check("gs_adam_step_range", self.lib.gs_adam_step_range(
             C.byref(sc), _ptr(params), _ptr(grad_range), _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step),
             int(begin), int(end), _stream(stream)))
 
     def adam_step_peers(self, sc, world, rank, grad_ptrs, param_ptrs, m, v, lr_per_row, step, begin, end, beta1=0.9,
                         beta2=0.999, eps=1e-15, stream=None):
-        """grad_ptrs / param_ptrs: lists of `world` device addresses (ints)."""
+        """grad_ptrs / param_ptrs: lists of `world` device addresses (ints); step: an int or
+        an int64 device tensor (gs_adam_step_peers_dev)."""
         lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
         gp = (C.c_void_p * max(world, 1))(*grad_ptrs)
         pp = (C.c_void_p * max(world, 1))(*param_ptrs)
+        if isinstance(step, torch.Tensor):
+            return self._check("gs_adam_step_peers_dev", self.lib.gs_adam_step_peers_dev(
+                C.byref(sc), int(world), int(rank), gp, pp, _ptr(m), _ptr(v), lr, beta1, beta2, eps, _ptr(step),
+                int(begin), int(end), _stream(stream)))
         return self._check("gs_adam_step_peers", self.lib.gs_adam_step_peers(
             C.byref(sc), int(world), int(rank), gp, pp, _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step), int(begin),
             int(end), _stream(stream)))

@@ -445,11 +445,13 @@ class Trainer:
         (the launch-bound configs run as one graph per iteration).
         Binning runs in capacity mode (K stays on the device), Adam takes the step
         counter from the device.  Returns the graph; replay it with replay()."""
-        if self.optimizer is not None:
-            raise ValueError("graph capture supports the single-rank / all-reduce optimiser path only")
+        if self.optimizer is not None and not hasattr(self.optimizer, "device_step"):
+            raise ValueError("this optimiser cannot be graph-captured (its exchange size is read on the host)")
         m = self.model
         m.step_dev.fill_(m.step_count)
         self.device_step = True
+        if self.optimizer is not None:
+            self.optimizer.device_step = True
         hooks, self.hooks = self.hooks, None
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
@@ -563,9 +565,12 @@ class ShardedAdam:
         self.begin = min(self.rank * self.shard, self.n)
         self.end = min(self.begin + self.shard, self.n)
         self.nccl = dist.get_backend(group) == "nccl"
+        # device_step: Adam reads / advances model.step_dev (CUDA-graph capture, Trainer.capture)
+        self.device_step = False
         if adam_range is None:
             def adam_range(b, e, g):
-                lib.adam_step_range(model.desc, model.params, g, model.m, model.v, model.lr, model.step_count, b, e)
+                step = model.step_dev if self.device_step else model.step_count
+                lib.adam_step_range(model.desc, model.params, g, model.m, model.v, model.lr, step, b, e)
         self.adam_range = adam_range
 
     def step(self):
@@ -575,7 +580,7 @@ class ShardedAdam:
         else:  # gloo (CPU tests): no reduce-scatter; all-reduce and keep this rank's shard
             d.all_reduce(self.gpad, op=d.ReduceOp.SUM, group=self.group)
             self.gshard.copy_(self.gpad[self.rank * self.shard:(self.rank + 1) * self.shard])
-        if self.end > self.begin:
+        if self.end > self.begin or self.device_step:  # (an empty range still advances step_dev)
             self.adam_range(self.begin, self.end, self.gshard)
         self.pshard.copy_(self.ppad[self.rank * self.shard:(self.rank + 1) * self.shard])
         if self.nccl:
@@ -686,12 +691,13 @@ class PeerShardedAdam:
         self.end = min(self.begin + self.shard, self.n)
         torch.cuda.synchronize(dev)
         self.hg.barrier(channel=0)
+        self.device_step = False  # True: the step counter is model.step_dev (graph capture)
 
     def step(self):
         m = self.model
         self.hg.barrier(channel=0)  # every rank's gradient is final
-        self.lib.adam_step_peers(m.desc, self.world, self.rank, self.gptrs, self.pptrs, m.m, m.v, m.lr, m.step_count,
-                                 self.begin, self.end)
+        self.lib.adam_step_peers(m.desc, self.world, self.rank, self.gptrs, self.pptrs, m.m, m.v, m.lr,
+                                 m.step_dev if self.device_step else m.step_count, self.begin, self.end)
         self.hp.barrier(channel=1)  # every rank's parameter stores have landed
 
 

@@ -962,3 +962,54 @@ def test_project_views_bitexact_vs_project(lib):
         ra = ta["rec"][:P][vis].view(torch.int32)
         rb = tb["rec"][:P][vis].view(torch.int32)
         assert torch.equal(ra[:, :10], rb[:, :10]) and torch.equal(ra[:, 10:12], rb[:, 10:12])
+
+
+@pytest.mark.parametrize("kind", ["sharded", "peer", "allreduce"])
+def test_graph_capture_with_exchange(lib, kind):
+    """The N > 1 iteration as one CUDA graph (bench.py at N > 1): the exchange (NCCL
+    reduce-scatter / all-gather, the peer-memory kernel and its symmetric-memory
+    barriers, or an NCCL all-reduce) and Adam with the device step counter captured with
+    the views; replays are bit-identical to eager steps (deterministic mode; world size 1
+    on this GPU, so the collectives run with one rank)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = workload("small")
+        cams = [scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.03 * (k - 2)),
+                                   [0.05 * k, 0.0, 0.0]) for k in range(4)]
+        models = [pipeline.GaussianModel(w.scene, DEV) for _ in range(2)]
+        tgt = pipeline.GaussianModel(w.target_scene, DEV)
+        cap = pipeline.default_capacity(pipeline.measure_keys(lib, models[0], cams, DEV))
+        targets = pipeline.render_targets(lib, tgt, cams, DEV, cap)
+        trs = []
+        for m in models:
+            opt, ar = None, None
+            if kind == "sharded":
+                opt = pipeline.ShardedAdam(lib, m)
+            elif kind == "peer":
+                opt = pipeline.PeerShardedAdam(lib, m)
+            else:
+                ar = lambda g: dist.all_reduce(g, op=dist.ReduceOp.SUM)  # noqa: E731
+            trs.append(pipeline.Trainer(lib, m, cams, targets, DEV, cap, streams=2, optimizer=opt, allreduce=ar,
+                                        deterministic=True))
+        views = list(range(len(cams)))
+        trs[0].step(views)
+        trs[1].step(views)
+        g = trs[1].capture(views)  # one more eager step while capturing
+        trs[0].step(views)
+        for it in range(3):
+            trs[0].step(views)
+            trs[1].replay(g)
+        torch.cuda.synchronize()
+        assert models[0].step_count == models[1].step_count == int(models[1].step_dev.item()) == 5
+        assert torch.equal(models[0].params, models[1].params)
+        assert torch.equal(models[0].m, models[1].m) and torch.equal(models[0].v, models[1].v)
+    finally:
+        dist.destroy_process_group()
