@@ -154,45 +154,119 @@ def cpu_window_camera(cam, size=584):
     return c
 
 
-def oracle_step_sample(w, view=0, size=584, tgt=None):
-    """One view's fwd (F32) + L1 + bwd (MIXED) + Adam on the oracle, on a window.
-    The target image (setup, untimed) is rendered once and can be passed back in."""
+def oracle_step_sample(w, view=0, size=584, tgt=None, views=None):
+    """fwd (F32) + L1 + bwd (MIXED) per view, the views' gradients summed (R21), then one
+    Adam step, on the oracle: views (default [view]) on a size x size central window (or
+    the full image when size covers it).  The target images (setup, untimed) are rendered
+    once and can be passed back in (a list, one per view)."""
     import numpy as np
     from oracle import gsref
     from paper_2408_12677_b200.pipeline import lr_per_row
-    cam = cpu_window_camera(w.cameras[view], size)
+    views = [view] if views is None else list(views)
+    cams = [cpu_window_camera(w.cameras[v], size) for v in views]
     t0 = time.perf_counter()
     if tgt is None:  # the target scene's render as a sensor frame (R41), decoded
         import scenegen
         from oracle import frame
-        tgt = gsref.render_fwd(cam, w.target_scene, gsref.F32)
-        c8, d16 = scenegen.quantize_frame(tgt["rgb"], tgt["depth"])
-        tgt["rgb"], tgt["depth"] = frame.decode_rgbd(c8, d16, scenegen.DEPTH_SCALE)
+        tgt = []
+        for cam in cams:
+            t = gsref.render_fwd(cam, w.target_scene, gsref.F32)
+            c8, d16 = scenegen.quantize_frame(t["rgb"], t["depth"])
+            t["rgb"], t["depth"] = frame.decode_rgbd(c8, d16, scenegen.DEPTH_SCALE)
+            tgt.append(t)
     t1 = time.perf_counter()
-    f = gsref.render_fwd(cam, w.scene, gsref.F32)
-    L, g_rgb, g_d = gsref.l1_loss_grad(f["rgb"], f["depth"], tgt["rgb"].astype(np.float32),
-                                       tgt["depth"].astype(np.float32), 1.0)
-    grad, _ = gsref.render_bwd(cam, w.scene, g_rgb.astype(np.float32), g_d.astype(np.float32), mode=gsref.MIXED)
+    gfull = np.zeros(w.scene.params.shape, np.float64)
+    blended = 0
+    for cam, t in zip(cams, tgt):
+        f = gsref.render_fwd(cam, w.scene, gsref.F32)
+        L, g_rgb, g_d = gsref.l1_loss_grad(f["rgb"], f["depth"], t["rgb"].astype(np.float32),
+                                           t["depth"].astype(np.float32), 1.0)
+        grad, _ = gsref.render_bwd(cam, w.scene, g_rgb.astype(np.float32), g_d.astype(np.float32), mode=gsref.MIXED)
+        gfull[:, :w.scene.P] += grad
+        blended += f["blended"]
     S = w.scene.params.shape[1]
-    gfull = np.zeros_like(w.scene.params)
-    gfull[:, :w.scene.P] = grad
     z = np.zeros_like(w.scene.params)
-    gsref.adam_step(w.scene.params, gfull, z, z, np.array(lr_per_row(w.scene.sh_degree), np.float32), 1, P=S)
+    gsref.adam_step(w.scene.params, gfull.astype(np.float32), z, z,
+                    np.array(lr_per_row(w.scene.sh_degree), np.float32), 1, P=S)
     t2 = time.perf_counter()
-    return {"seconds": t2 - t1, "blended": f["blended"], "window": f"{cam.width}x{cam.height}",
-            "target_seconds": t1 - t0, "target": tgt}
+    return {"seconds": t2 - t1, "blended": blended, "window": f"{cams[0].width}x{cams[0].height}",
+            "views": len(cams), "target_seconds": t1 - t0, "target": tgt}
+
+
+def host_cpu():
+    """nproc and the CPU model of this host (recorded with every CPU number)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def cpu_oracle_legs(w, config, budget_s=60.0):
+    """The CPU oracle as it stands (never tuned), timed on this host:
+    (a) on ALL host cores (OpenMP over tiles; results independent of the thread count)
+        on the §8(d) workload -- scannetpp one full iteration of its 8 views, large one
+        full view (the rate is per blended pixel, so x64 views is the same rate), the
+        single-view configs one full view -- or, if a pilot predicts more than budget_s,
+        the same views on a central window sized to fit the budget;
+    (b) on ONE core, a bounded sample (one view, 584x584 central window).
+    Returns the cpu_baseline object: value = (a)'s rate, with (b) under single_core."""
+    from oracle import gsref
+    gsref.build()
+    n_all = gsref.set_threads(0)
+    batched = config in ("scannetpp", "large")
+    views = list(range(len(w.cameras))) if config == "scannetpp" else [0]
+    cam0 = w.cameras[0]
+    full_px = cam0.width * cam0.height
+    pilot = oracle_step_sample(w, 0, 256)  # all cores: rate of the workload on this host
+    # seconds for the full workload at the pilot's time per pixel
+    est = len(views) * full_px * (pilot["seconds"] / (min(256, cam0.width) * min(256, cam0.height)))
+    if est <= budget_s:
+        size = max(cam0.width, cam0.height)
+    else:  # a central window with about budget_s of work
+        side = int((budget_s / est) ** 0.5 * (full_px ** 0.5)) // 16 * 16
+        size = max(64, min(side, max(cam0.width, cam0.height)))
+    r = oracle_step_sample(w, 0, size, views=views)
+    full = size >= max(cam0.width, cam0.height)
+    what = (f"{'one full iteration of ' if batched and len(views) > 1 else ''}{len(views)} view(s) of "
+            f"'{config}' at {r['window']}" + ("" if full else " (central window: the full workload was predicted "
+                                                              f"at {est:.0f} s)") +
+            (" (large: 1 of its 64 views; per-pixel rate, so the 64-view iteration has the same rate)"
+             if config == "large" else ""))
+    gsref.set_threads(1)
+    one = oracle_step_sample(w, 0, 584)
+    gsref.set_threads(n_all)
+    return {"value": r["blended"] / r["seconds"], "unit": UNIT, "cores": n_all, "kind": "oracle",
+            "sample": f"{what}: fwd(F32)+L1+bwd(MIXED) per view, summed gradient, Adam; {r['seconds']:.1f} s",
+            "iters_per_s": (1.0 / r["seconds"]) if full and (len(views) == len(w.cameras) or not batched) else None,
+            "single_core": {"value": one["blended"] / one["seconds"], "unit": UNIT, "cores": 1,
+                            "sample": f"1 view, {one['window']} central window of '{config}' view 0, "
+                                      f"{one['seconds']:.1f} s"},
+            **host_cpu()}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands, timed on this box's host cores."""
+    """--impl reference: the CPU oracle as it stands, timed on this box's host cores (all
+    of them, OpenMP over tiles), on the same config, metric and unit.  Each step is a
+    bounded sample of the workload (one view on a central window sized from a pilot so
+    that warm-up + steps take about two minutes); under torchrun only rank 0 runs."""
     if rank != 0:
         return
     import scenegen
     from oracle import gsref
     gsref.build()
+    n_all = gsref.set_threads(0)
     kw = {"num_views": 1} if args.config in ("replica", "scannetpp", "large") else {}
     w = scenegen.make(args.config, args.seed, **kw)
-    size = 584 if args.config in ("replica", "scannetpp", "large") else 10 ** 6
+    cam0 = w.cameras[0]
+    pilot = oracle_step_sample(w, 0, 256)
+    t_px = pilot["seconds"] / (min(256, cam0.width) * min(256, cam0.height))
+    per_step = min(10.0, 120.0 / max(1, args.steps + min(args.warmup, 1)))
+    size = max(64, min(int((per_step / t_px) ** 0.5) // 16 * 16, max(cam0.width, cam0.height)))
     tgt = None
     for _ in range(min(args.warmup, 1)):
         tgt = oracle_step_sample(w, 0, size)["target"]
@@ -203,12 +277,14 @@ def run_reference(args, rank, world):
         tot_s += r["seconds"]
         tot_b += r["blended"]
     value = tot_b / tot_s
-    sample = f"1 view, {r['window']} central window of config '{args.config}', fwd(F32)+L1+bwd(MIXED)+Adam per step"
+    sample = (f"1 view, {r['window']} " + ("full image" if size >= max(cam0.width, cam0.height) else "central window")
+              + f" of config '{args.config}', fwd(F32)+L1+bwd(MIXED)+Adam per step, {n_all} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "config": {"workload": args.config, "seed": args.seed},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_all, "kind": "oracle", "sample": sample,
+                             **host_cpu()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -771,15 +847,9 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         try:
-            from oracle import gsref
-            gsref.build()
-            size = 584 if args.config in ("replica", "scannetpp", "large") else 10 ** 6
-            r = oracle_step_sample(w, 0, size)
-            cpu = {"value": r["blended"] / r["seconds"], "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": f"1 view, {r['window']} central window of '{args.config}' view 0, "
-                             f"fwd(F32)+L1+bwd(MIXED)+Adam, {r['seconds']:.1f} s"}
+            cpu = cpu_oracle_legs(w, args.config)
         except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {ex}"}
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

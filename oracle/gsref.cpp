@@ -6,8 +6,10 @@
 // (paper_2408_12677_b200/, libgsr.so) never links, imports or calls it, and this
 // file shares no code, header, table or constant generator with it.
 //
-// Build: g++ -O2 -std=c++17 -ffp-contract=off -fPIC -shared (no fast-math), so the
-// float ("parity") mode rounds every operation in the order written here.
+// Build: g++ -O2 -std=c++17 -ffp-contract=off -fopenmp -fPIC -shared (no fast-math), so
+// the float ("parity") mode rounds every operation in the order written here.  OpenMP
+// only distributes independent loop iterations (tiles, rows, samples, Gaussians); every
+// sum is taken in one fixed order, so results do not depend on the thread count.
 //
 // Every step cites the passage it follows.  Readings R1-R27 are listed in
 // DESIGN.md §"Readings"; the ones used here are named inline.
@@ -27,6 +29,9 @@
 #include <cstring>
 #include <type_traits>
 #include <vector>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 namespace {
 
@@ -377,6 +382,7 @@ Fwd<S> project_one(const RefCamera& cam, int deg, const ParamView<S>& g) {
 template <class S>
 Proj<S> project_all(const RefCamera& cam, int64_t P, int64_t P_stride, int deg, const float* params) {
   Proj<S> pr(P);
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t i = 0; i < P; ++i) {
     const Fwd<S> f = project_one<S>(cam, deg, load_params<S>(params, P_stride, deg, i));
     if (f.culled) {
@@ -487,7 +493,7 @@ template <class S> std::vector<std::vector<int32_t>> tile_lists(const RefCamera&
 // R27), depth channel D = sum z alpha T (R17), background T*bg (R26).
 // ---------------------------------------------------------------------------
 template <class S> struct Entry {
-  int32_t id;
+  int32_t id, pos;  // Gaussian index, position in the tile list
   S alpha, G, T, dx, dy;
   bool capped;
 };
@@ -576,7 +582,7 @@ PixelResult<D, S> composite_pixel(int px, int py, const std::vector<int32_t>& li
     const S w = as * Ts;
     for (int ch = 0; ch < 3; ++ch) r.C[ch] = r.C[ch] + ps.col[ch][i] * w;
     r.Dep = r.Dep + ps.z[i] * w;
-    if (keep_entries) r.entries.push_back({i, as, Gs, Ts, dxs, dys, capped});
+    if (keep_entries) r.entries.push_back({i, (int32_t)pos, as, Gs, Ts, dxs, dys, capped});
     Ts = Ts * (S(1) - as);
     Td = Tnd;
     r.n = (int32_t)pos + 1;
@@ -598,6 +604,10 @@ uint64_t mix64(uint64_t h, uint64_t v) {
 // ---------------------------------------------------------------------------
 template <class S> struct ScreenGrad {
   S mux = 0, muy = 0, A = 0, B = 0, C = 0, o = 0, col[3] = {0, 0, 0}, z = 0;
+  void add(const ScreenGrad& t) {
+    mux += t.mux, muy += t.muy, A += t.A, B += t.B, C += t.C, o += t.o, z += t.z;
+    for (int ch = 0; ch < 3; ++ch) col[ch] += t.col[ch];
+  }
 };
 
 template <class S>
@@ -720,16 +730,26 @@ void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, 
                     const float* g_rgb, const float* g_depth, const Proj<DT>& pd, const Proj<ST>& ps,
                     const std::vector<std::vector<int32_t>>& lists, double* grad_out, double* bound_out,
                     double* screen_out, double* screen_bound_out) {
-  const int W = cam->width, H = cam->height, TX = (W + kTile - 1) / kTile;
+  const int W = cam->width, H = cam->height, TX = (W + kTile - 1) / kTile, TY = (H + kTile - 1) / kTile;
   const int F = 11 + 3 * (deg + 1) * (deg + 1);
-    std::vector<ScreenGrad<ST>> sg((size_t)P);
-    for (int py = 0; py < H; ++py)
-      for (int px = 0; px < W; ++px) {
+  const int NT = TX * TY;
+  // Pixels are visited tile by tile (row-major inside the tile); a tile's contributions
+  // are summed per position of its list, and the tiles' sums are then added to the
+  // Gaussians in tile order: ONE summation order whatever the number of threads
+  // (OpenMP over tiles: the CPU baseline on all host cores).
+  std::vector<std::vector<ScreenGrad<ST>>> tile_acc((size_t)NT);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int t = 0; t < NT; ++t) {
+    const auto& list = lists[t];
+    std::vector<ScreenGrad<ST>>& acc = tile_acc[(size_t)t];
+    const int ox = (t % TX) * kTile, oy = (t / TX) * kTile;
+    for (int py = oy; py < std::min(oy + kTile, H); ++py)
+      for (int px = ox; px < std::min(ox + kTile, W); ++px) {
         const int64_t pix = (int64_t)py * W + px;
         if (g_rgb[pix] == 0.f && g_rgb[(int64_t)W * H + pix] == 0.f && g_rgb[2 * (int64_t)W * H + pix] == 0.f &&
             (!g_depth || g_depth[pix] == 0.f))
           continue;  // zero upstream: this pixel contributes exactly zero (linearity)
-        const auto& list = lists[(py / kTile) * TX + px / kTile];
+        if (acc.empty()) acc.resize(list.size());
         PixelResult<DT, ST> r = composite_pixel<DT, ST>(px, py, list, pd, ps, *cam, true);
         if constexpr (kIsRn<ST>) {
           // Bound of T_k for ANY evaluation route through this pixel's factors
@@ -754,7 +774,7 @@ void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, 
         for (size_t k = 0; k < n; ++k) {
           const auto& e = r.entries[k];
           const int32_t i = e.id;
-          ScreenGrad<ST>& s = sg[i];
+          ScreenGrad<ST>& s = acc[(size_t)e.pos];
           const ST aT = e.alpha * e.T;
           for (int ch = 0; ch < 3; ++ch) s.col[ch] += gC[ch] * aT;
           s.z += gD * aT;
@@ -772,8 +792,14 @@ void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, 
           s.C += dpow * (ST(-0.5) * e.dy * e.dy);
         }
       }
-    std::vector<ST> out(F);
+  }
+  std::vector<ScreenGrad<ST>> sg((size_t)P);
+  for (int t = 0; t < NT; ++t)
+    for (size_t k = 0; k < tile_acc[(size_t)t].size(); ++k) sg[(size_t)lists[t][k]].add(tile_acc[(size_t)t][k]);
+  tile_acc.clear();
+#pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < P; ++i) {
+      std::vector<ST> out(F);
       for (int r = 0; r < F; ++r) grad_out[r * P + i] = 0.0;
       if (bound_out)
         for (int r = 0; r < F; ++r) bound_out[r * P + i] = 0.0;
@@ -817,6 +843,19 @@ void render_bwd_run(const RefCamera* cam, int64_t P, int64_t P_stride, int deg, 
 extern "C" {
 
 int gsref_version(void) { return 1; }
+
+// OpenMP threads of the oracle's parallel loops (over tiles, rows, samples and
+// Gaussians); every result is independent of the count.  n <= 0: the runtime default
+// (OMP_NUM_THREADS or all host cores).  Returns the count now in effect.
+int gsref_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}
 
 // Real SH values Y_k(d) for k < (deg+1)^2 at n directions d[3n] (double); test hook.
 int gsref_sh_basis(int deg, int64_t n, const double* dirs, double* Y, double* dY) {
@@ -907,6 +946,10 @@ int gsref_render_fwd(const RefCamera* cam, int64_t P, int64_t P_stride, int deg,
       sig = mix64(sig, ((uint64_t)pd.x0[i] << 48) ^ ((uint64_t)pd.x1[i] << 32) ^ ((uint64_t)pd.y0[i] << 16) ^
                            (uint64_t)pd.y1[i]);
     }
+    // every pixel is independent (OpenMP over rows); the signature folds the pixels'
+    // decision hashes in pixel order afterwards
+    std::vector<uint64_t> pix_sig(signature ? (size_t)W * H : 0);
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : nb, ne)
     for (int py = 0; py < H; ++py)
       for (int px = 0; px < W; ++px) {
         const auto& list = lists[(py / kTile) * TX + px / kTile];
@@ -920,10 +963,12 @@ int gsref_render_fwd(const RefCamera* cam, int64_t P, int64_t P_stride, int deg,
         nb += r.blended;
         ne += r.evaluated;
         if (signature) {
-          sig = mix64(sig, (uint64_t)r.n);
-          for (const auto& e : r.entries) sig = mix64(sig, ((uint64_t)e.id << 1) | (e.capped ? 1 : 0));
+          uint64_t h = mix64(0, (uint64_t)r.n);
+          for (const auto& e : r.entries) h = mix64(h, ((uint64_t)e.id << 1) | (e.capped ? 1 : 0));
+          pix_sig[(size_t)pix] = h;
         }
       }
+    for (const uint64_t h : pix_sig) sig = mix64(sig, h);
     if (blended) *blended = nb;
     if (evaluated) *evaluated = ne;
     if (signature) *signature = sig;
@@ -954,8 +999,10 @@ int gsref_render_pixels(const RefCamera* cam, int64_t P, int64_t P_stride, int d
     using DT = std::decay_t<decltype(pd.mux[0])>;
     using ST = std::decay_t<decltype(ps.mux[0])>;
     const auto lists = tile_lists(*cam, pd);
-    for (int64_t j = 0; j < n; ++j) {
+    for (int64_t j = 0; j < n; ++j)
       if (px[j] < 0 || py[j] < 0 || px[j] >= cam->width || py[j] >= cam->height) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t j = 0; j < n; ++j) {
       const auto& list = lists[(py[j] / kTile) * TX + px[j] / kTile];
       const PixelResult<DT, ST> r = composite_pixel<DT, ST>(px[j], py[j], list, pd, ps, *cam, false);
       for (int ch = 0; ch < 3; ++ch) rgb[ch * n + j] = (double)r.C[ch];
@@ -1038,8 +1085,10 @@ int gsref_margin_bound(const RefCamera* cam, int64_t P, int64_t P_stride, int de
   const Proj<Rn> pr = stage ? stage_records(*cam, P, P_stride, deg, params, pf)
                              : project_all<Rn>(*cam, P, P_stride, deg, params);
   const auto lists = tile_lists(*cam, pf);
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = 0; j < n; ++j)
     if (px[j] < 0 || py[j] < 0 || px[j] >= cam->width || py[j] >= cam->height) return -1;
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t j = 0; j < n; ++j) {
     const auto& list = lists[(py[j] / kTile) * TX + px[j] / kTile];
     margin_u[j] = composite_pixel<float, Rn>(px[j], py[j], list, pf, pr, *cam, false).margin_u;
   }

@@ -24,7 +24,7 @@ FLAG_CULLED = 128
 def build(force: bool = False) -> str:
     """Compile the oracle (g++ -O2 -ffp-contract=off, no fast-math)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                "-o", LIB + ".tmp", SRC]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
@@ -63,6 +63,7 @@ def lib():
         P = C.c_void_p
         i64 = C.c_int64
         _lib.gsref_sh_basis.argtypes = [C.c_int, i64, P, P, P]
+        _lib.gsref_set_threads.argtypes = [C.c_int]
         _lib.gsref_project.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P]
         _lib.gsref_bin_tiles.argtypes = [P, i64, i64, C.c_int, P, i64, P, P, P, P]
         _lib.gsref_render_fwd.argtypes = [P, i64, i64, C.c_int, P, C.c_int, P, P, P, P, P, P, P, P]
@@ -74,6 +75,12 @@ def lib():
                                          i64, P, P, P]
         _lib.gsref_l1_loss_grad.argtypes = [i64, P, P, P, P, C.c_double, P, P, P]
     return _lib
+
+
+def set_threads(n: int = 0) -> int:
+    """OpenMP threads of the oracle (0 = all host cores / OMP_NUM_THREADS); results are
+    independent of the count.  Returns the count in effect."""
+    return int(lib().gsref_set_threads(int(n)))
 
 
 def _p(a):

@@ -181,3 +181,25 @@ def test_render_pixels_equals_render_fwd(oracle, mode):
     np.testing.assert_array_equal(s["margin"], full["margin"][py, px])
     mu_full = oracle.margin_bound(cam, scene)
     np.testing.assert_array_equal(oracle.margin_bound(cam, scene, px, py), mu_full[py, px])
+
+
+def test_oracle_results_independent_of_thread_count(oracle):
+    """The oracle's OpenMP loops distribute independent iterations only and take every
+    sum in one fixed order: 1 thread and all host threads give bit-identical outputs
+    (forward, MIXED / STAGE gradients, bounds, margins)."""
+    w = scenegen.make("small")
+    cam, scene = w.cameras[0], w.scene
+    g_rgb, g_d = scenegen.upstream_fields(2, cam.width, cam.height)
+    outs = []
+    n_all = oracle.set_threads(0)
+    for n in (1, max(n_all, 2)):
+        oracle.set_threads(n)
+        f = oracle.render_fwd(cam, scene, oracle.F32, want_margin=True, want_signature=True)
+        gm, sm = oracle.render_bwd(cam, scene, g_rgb, g_d, mode=oracle.MIXED)
+        b = oracle.render_bwd_bound(cam, scene, g_rgb, g_d)
+        mu = oracle.margin_bound(cam, scene)
+        outs.append([f["rgb"], f["depth"], f["margin"], np.array([f["signature"], f["blended"]]), gm, sm, b["grad"],
+                     b["bound"], mu])
+    oracle.set_threads(n_all)
+    for a, c in zip(*outs):
+        np.testing.assert_array_equal(a, c)
