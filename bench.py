@@ -206,6 +206,20 @@ def host_cpu():
     return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
+def pilot_cost(w):
+    """Two windows (128^2, 256^2) of view 0 through oracle_step_sample: the per-view
+    fixed cost a (projection of all P Gaussians, list building, Adam) and the cost b per
+    pixel, so that a workload can be sized to a time budget on this host."""
+    cam0 = w.cameras[0]
+    t = []
+    for size in (128, 256):
+        r = oracle_step_sample(w, 0, size)
+        t.append((min(size, cam0.width) * min(size, cam0.height), r["seconds"]))
+    (p1, t1), (p2, t2) = t
+    b = max((t2 - t1) / max(p2 - p1, 1), 1e-12)
+    return max(t1 - b * p1, 0.0), b
+
+
 def cpu_oracle_legs(w, config, budget_s=60.0):
     """The CPU oracle as it stands (never tuned), timed on this host:
     (a) on ALL host cores (OpenMP over tiles; results independent of the thread count)
@@ -222,14 +236,13 @@ def cpu_oracle_legs(w, config, budget_s=60.0):
     views = list(range(len(w.cameras))) if config == "scannetpp" else [0]
     cam0 = w.cameras[0]
     full_px = cam0.width * cam0.height
-    pilot = oracle_step_sample(w, 0, 256)  # all cores: rate of the workload on this host
-    # seconds for the full workload at the pilot's time per pixel
-    est = len(views) * full_px * (pilot["seconds"] / (min(256, cam0.width) * min(256, cam0.height)))
+    a, b = pilot_cost(w)  # all cores: seconds per view = a + b * pixels on this host
+    est = len(views) * (a + b * full_px)
     if est <= budget_s:
         size = max(cam0.width, cam0.height)
     else:  # a central window with about budget_s of work
-        side = int((budget_s / est) ** 0.5 * (full_px ** 0.5)) // 16 * 16
-        size = max(64, min(side, max(cam0.width, cam0.height)))
+        side = int(max(budget_s / len(views) - a, 0.0) / b) ** 0.5 // 16 * 16
+        size = int(max(64, min(side, max(cam0.width, cam0.height))))
     r = oracle_step_sample(w, 0, size, views=views)
     full = size >= max(cam0.width, cam0.height)
     what = (f"{'one full iteration of ' if batched and len(views) > 1 else ''}{len(views)} view(s) of "
@@ -263,10 +276,9 @@ def run_reference(args, rank, world):
     kw = {"num_views": 1} if args.config in ("replica", "scannetpp", "large") else {}
     w = scenegen.make(args.config, args.seed, **kw)
     cam0 = w.cameras[0]
-    pilot = oracle_step_sample(w, 0, 256)
-    t_px = pilot["seconds"] / (min(256, cam0.width) * min(256, cam0.height))
+    a, b = pilot_cost(w)
     per_step = min(10.0, 120.0 / max(1, args.steps + min(args.warmup, 1)))
-    size = max(64, min(int((per_step / t_px) ** 0.5) // 16 * 16, max(cam0.width, cam0.height)))
+    size = int(max(64, min(int(max(per_step - a, 0.0) / b) ** 0.5 // 16 * 16, max(cam0.width, cam0.height))))
     tgt = None
     for _ in range(min(args.warmup, 1)):
         tgt = oracle_step_sample(w, 0, size)["target"]

@@ -86,7 +86,7 @@ def test_shard_views_partition():
 def test_gloo_two_ranks_allreduce_matches_sum():
     from oracle import gsref
     gsref.build()
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     w, cams = _views()
@@ -142,7 +142,7 @@ def _sharded_worker(rank, world, port, out):
 def test_gloo_two_ranks_sharded_adam_matches_replicated():
     from oracle import gsref
     from paper_2408_12677_b200 import pipeline
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_sharded_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     w, _ = _views()
@@ -230,7 +230,7 @@ def _sparse_worker(rank, world, port, out):
 def test_gloo_two_ranks_sparse_exchange_matches_dense():
     from oracle import gsref
     from paper_2408_12677_b200 import pipeline
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_sparse_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     w, _ = _views()
