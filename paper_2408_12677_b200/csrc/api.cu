@@ -57,6 +57,14 @@ DevCam make_devcam(const gs_camera& c) {
   for (int i = 0; i < 9; ++i) d.R[i] = c.R_cw[i];
   for (int i = 0; i < 3; ++i) d.t[i] = c.t_cw[i], d.bg[i] = c.bg[i];
   d.z_near = c.z_near;
+  // R7's tangent clamps, per camera instead of per Gaussian: the fixed fp32 order of
+  // O5 (1.3 * (W / (2 fx))), each operation rounded (host SSE float arithmetic)
+  {
+    volatile float two_fx = 2.f * c.fx, two_fy = 2.f * c.fy;
+    volatile float qx = (float)c.width / two_fx, qy = (float)c.height / two_fy;
+    d.limx = 1.3f * qx;
+    d.limy = 1.3f * qy;
+  }
   for (int j = 0; j < 3; ++j) {  // camera centre -R^T t
     double acc = 0.0;
     for (int i = 0; i < 3; ++i) acc += (double)c.R_cw[3 * i + j] * (double)c.t_cw[i];

@@ -780,10 +780,163 @@ int tscatter_warps(int NT) {
   return tscatter_own_bits(NT, 8) ? 8 : 0;
 }
 
+// ---------------------------------------------------------------------------
+// K4'' (GSR_TILE_SORT=lsd; measured slower, kept for A/B): the stable tile placement as two LSD passes over the bytes of the
+// 16-bit tile id (low byte, then high byte; one pass if NT <= 256), each pass three
+// short, light kernels with no look-back chain and no persistent CTAs, so that they
+// interleave with the render kernels of the views in flight instead of holding whole
+// SMs (k_tscatter's 218 KB of shared memory, the onesweep passes' register file):
+//   k_dcount:   per chunk of kDcTile keys, the 256-bin histogram of the pass's byte,
+//               stored bin-major: dch[b][c]
+//   k_dscan:    one CTA per bin: exclusive scan of dch[b][.] over the chunks (in
+//               place) and the bin's total -> dtot[b]
+//   k_dscatter: per chunk: stable warp-multisplit ranks (the chunk's keys in order),
+//               block-sorted staging in shared memory, and coalesced per-bin runs to
+//               start(b) + dch[b][c] + (rank within the chunk), start(b) = exclusive
+//               scan of dtot, recomputed by every CTA (256 values).
+// Keys enter in depth order; each pass is stable, so the output is the (tile, depth,
+// index) order (R12), bit-identical to the other placements.
+// ---------------------------------------------------------------------------
+constexpr int kDcItems = 8, kDcTile = kRsThreads * kDcItems;  // 2048 keys per chunk
+
+__global__ void __launch_bounds__(kRsThreads) k_dcount(const uint16_t* __restrict__ keys,
+                                                       const Counters* __restrict__ ctr, int64_t cap, int shift,
+                                                       int64_t cstride, uint32_t* __restrict__ dch) {
+  __shared__ uint32_t s_h[256];
+  int64_t K = (int64_t)ctr->K;
+  if (K > cap) K = 0;
+  const int64_t k0 = (int64_t)blockIdx.x * kDcTile;
+  if (k0 >= K) return;
+  const int t = threadIdx.x;
+  s_h[t] = 0;
+  __syncthreads();
+  const int64_t kb = k0 + 8 * (int64_t)t;  // 8 keys (16 B) per thread
+  if (kb < K) {
+    if (kb + 8 <= K) {
+      const uint4 q = *reinterpret_cast<const uint4*>(keys + kb);
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) atomicAdd(&s_h[(((w[e >> 1] >> (16 * (e & 1))) & 0xffffu) >> shift) & 255u], 1u);
+    } else {
+      for (int64_t k = kb; k < K; ++k) atomicAdd(&s_h[(keys[k] >> shift) & 255u], 1u);
+    }
+  }
+  __syncthreads();
+  dch[(int64_t)t * cstride + blockIdx.x] = s_h[t];
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_dscan(const Counters* __restrict__ ctr, int64_t cap, int64_t cstride,
+                                                      uint32_t* __restrict__ dch, uint32_t* __restrict__ dtot) {
+  __shared__ uint32_t s_scan[8];
+  int64_t K = (int64_t)ctr->K;
+  if (K > cap) K = 0;
+  const int64_t C = (K + kDcTile - 1) / kDcTile;
+  uint32_t* row = dch + (int64_t)blockIdx.x * cstride;
+  uint32_t carry = 0;
+  for (int64_t c0 = 0; c0 < C; c0 += kRsThreads * 4) {
+    uint32_t v[4], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t c = c0 + 4 * (int64_t)threadIdx.x + i;
+      v[i] = c < C ? row[c] : 0u;
+      sum += v[i];
+    }
+    uint32_t tot;
+    uint32_t run = carry + block_excl_scan256<uint32_t>(sum, s_scan, tot);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t c = c0 + 4 * (int64_t)threadIdx.x + i;
+      if (c < C) row[c] = run;
+      run += v[i];
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) dtot[blockIdx.x] = carry;
+}
+
+template <typename KeyOutT>
+__global__ void __launch_bounds__(kRsThreads) k_dscatter(const uint16_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin,
+                                                         KeyOutT* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                         const Counters* __restrict__ ctr, int64_t cap, int shift,
+                                                         int64_t cstride, const uint32_t* __restrict__ dch,
+                                                         const uint32_t* __restrict__ dtot) {
+  __shared__ uint16_t s_keys[kDcTile];
+  __shared__ uint32_t s_vals[kDcTile];
+  __shared__ uint32_t s_whist[kRsWarps][256];
+  __shared__ uint32_t s_gbase[256], s_bexcl[256];
+  __shared__ uint32_t s_scan[8];
+  int64_t K = (int64_t)ctr->K;
+  if (K > cap) K = 0;
+  const int64_t k0 = (int64_t)blockIdx.x * kDcTile;
+  if (k0 >= K) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+#pragma unroll
+  for (int w = 0; w < kRsWarps; ++w) s_whist[w][t] = 0;
+  {
+    uint32_t tot;  // bin starts: exclusive scan of the bin totals, plus this chunk's offset
+    s_gbase[t] = block_excl_scan256<uint32_t>(dtot[t], s_scan, tot) + dch[(int64_t)t * cstride + blockIdx.x];
+  }
+  const int64_t base = k0 + warp * (kDcItems * 32);  // this warp's sub-chunk, keys in order
+  uint32_t key[kDcItems], rank[kDcItems];
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < kDcItems; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    key[i] = idx < K ? (uint32_t)kin[idx] : 0u;
+  }
+  __syncthreads();  // s_whist zeroed
+#pragma unroll
+  for (int i = 0; i < kDcItems; ++i) {
+    const bool valid = base + i * 32 + lane < K;
+    const uint32_t d = (key[i] >> shift) & 255u;
+    const uint32_t peers = digit_peers(d, valid);
+    const uint32_t r = __popc(peers & lt);
+    uint32_t b = 0;
+    if (valid) b = s_whist[warp][d];
+    __syncwarp();
+    if (valid && r == 0) s_whist[warp][d] = b + __popc(peers);
+    __syncwarp();
+    rank[i] = valid ? (b + r) : 0xffffffffu;
+  }
+  __syncthreads();
+  uint32_t cnt = 0;  // per digit t: exclusive over the warps, then over the digits
+#pragma unroll
+  for (int w = 0; w < kRsWarps; ++w) {
+    const uint32_t c = s_whist[w][t];
+    s_whist[w][t] = cnt;
+    cnt += c;
+  }
+  {
+    uint32_t tot;
+    s_bexcl[t] = block_excl_scan256<uint32_t>(cnt, s_scan, tot);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kDcItems; ++i) {
+    if (rank[i] != 0xffffffffu) {
+      const uint32_t d = (key[i] >> shift) & 255u;
+      const uint32_t pos = s_bexcl[d] + s_whist[warp][d] + rank[i];
+      s_keys[pos] = (uint16_t)key[i];
+      s_vals[pos] = vin[base + i * 32 + lane];
+    }
+  }
+  __syncthreads();
+  const int64_t rem = K - k0;
+  const int nv = (int)(rem < kDcTile ? rem : kDcTile);
+  for (int j = t; j < nv; j += kRsThreads) {
+    const uint32_t k = s_keys[j];
+    const uint32_t d = (k >> shift) & 255u;
+    const uint32_t dst = s_gbase[d] + (uint32_t)j - s_bexcl[d];
+    if (kout) kout[dst] = (KeyOutT)k;
+    vout[dst] = s_vals[j];
+  }
+}
+
 struct Layout {
   size_t ctr, ghist, lb_scan0, lb_scan1, lb_depth, lb_tile, zero_end;
-  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, chist, total;
-  int64_t depth_parts, tile_parts;
+  size_t dk0, dk1, dv0, dv1, offs, tk0, tk1, tv0, tv1, chist, dch, dtot, total;
+  int64_t depth_parts, tile_parts, dc_stride;
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -817,17 +970,27 @@ Layout make_layout(int64_t P, int64_t cap, int NT) {
   L.tv0 = take(cap * 4);
   L.tv1 = take(cap * 4);
   L.chist = take((size_t)kBkMaxChunks * ((NT + 3) & ~3) * 4);
+  L.dc_stride = (cap + kDcTile - 1) / kDcTile + 1;
+  L.dch = take((size_t)256 * L.dc_stride * 4);
+  L.dtot = take(256 * 4);
   L.total = o;
   return L;
 }
 
-// Tile placement: "bucket" (K4', default when its shared memory fits) or "radix"
-// (two onesweep / reduce-then-scan 8-bit passes; GSR_TILE_SORT=radix forces it).
-bool use_bucket(int NT) {
-  const char* e = std::getenv("GSR_TILE_SORT");
-  if (e && std::strcmp(e, "radix") == 0) return false;
-  return tscatter_warps(NT) > 0;
+// Tile placement: "bucket" (K4', default when its shared memory fits), "radix" (two
+// onesweep / reduce-then-scan 8-bit passes, GSR_TILE_SORT=radix) or "lsd" (K4'',
+// GSR_TILE_SORT=lsd).  scannetpp step (r02 A/B): bucket 6.02, lsd 6.35, radix 6.41 ms
+// (lsd: 2 x (dcount 8 + dscan 5 + dscatter 37) + ranges 12 us per view serialised).
+int tile_sort_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("GSR_TILE_SORT");
+    if (e && std::strcmp(e, "radix") == 0) return 0;
+    if (e && std::strcmp(e, "lsd") == 0) return 2;
+    return 1;
+  }();
+  return mode;
 }
+bool use_bucket(int NT) { return tile_sort_mode() == 1 && tscatter_warps(NT) > 0; }
 
 }  // namespace
 
@@ -915,13 +1078,38 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   count_launch();
   const int emit_grid = (int)std::min<int64_t>((cap + kEmTile - 1) / kEmTile, (int64_t)nsm * GSR_EMIT_PER_SM);
   const bool bucket = use_bucket(NT);
-  if (bucket)
+  if (bucket || tile_sort_mode() == 2)
     k_emit<false><<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0,
                                                                 ghist + 4 * 256);
   else
     k_emit<true><<<std::max(emit_grid, 1), kEmThreads, 0, s>>>(vin, offs, proj.rec, cam.TX, ctr, cap, tk0, tv0,
                                                                ghist + 4 * 256);
   count_launch();
+  if (tile_sort_mode() == 2) {
+    uint32_t* dch = reinterpret_cast<uint32_t*>(w + L.dch);
+    uint32_t* dtot = reinterpret_cast<uint32_t*>(w + L.dtot);
+    const int cgrid = (int)std::max<int64_t>(1, (cap + kDcTile - 1) / kDcTile);
+    auto lsd_pass = [&](const uint16_t* ki, const uint32_t* vi, uint16_t* ko, uint32_t* vo, int shift) {
+      k_dcount<<<cgrid, kRsThreads, 0, s>>>(ki, ctr, cap, shift, L.dc_stride, dch);
+      k_dscan<<<256, kRsThreads, 0, s>>>(ctr, cap, L.dc_stride, dch, dtot);
+      k_dscatter<uint16_t><<<cgrid, kRsThreads, 0, s>>>(ki, vi, ko, vo, ctr, cap, shift, L.dc_stride, dch, dtot);
+      count_launch(3);
+    };
+    const uint16_t* final_keys;
+    uint32_t* ids_out = reinterpret_cast<uint32_t*>(sorted_ids);
+    if (NT <= 256) {
+      lsd_pass(tk0, tv0, tk1, ids_out, 0);
+      final_keys = tk1;
+    } else {
+      lsd_pass(tk0, tv0, tk1, tv1, 0);
+      lsd_pass(tk1, tv1, tk0, ids_out, 8);
+      final_keys = tk0;
+    }
+    const int rg_grid = (int)std::min<int64_t>((cap + 255) / 256, (int64_t)nsm * 8);
+    k_ranges<<<std::max(rg_grid, 1), 256, 0, s>>>(final_keys, ctr, cap, reinterpret_cast<int2*>(tile_ranges));
+    count_launch();
+    return finish_bin(ctr, cap, num_keys_host, s);
+  }
   if (bucket) {
     // chunks: a multiple of the SMs (CTAs resident per SM by shared memory), each < 2^16 keys
     const int W = tscatter_warps(NT);

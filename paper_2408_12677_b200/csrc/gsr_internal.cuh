@@ -22,6 +22,7 @@ struct DevCam {
   float z_near;
   float bg[3];
   float ocam[3];  // camera centre in world coordinates, -R^T t (SH view direction)
+  float limx, limy;  // R7 tangent clamps 1.3 W / (2 fx), 1.3 H / (2 fy), fp32 in that order
 };
 
 DevCam make_devcam(const gs_camera& c);

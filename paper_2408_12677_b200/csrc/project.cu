@@ -113,8 +113,7 @@ __device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float 
     const float mux = FA(FM(cam.fx, ux), cam.cx);
     const float muy = FA(FM(cam.fy, uy), cam.cy);
     // O5: EWA (Eq. 5) with the 1.3x tangent clamp (R7) and the 0.3 low-pass (R8)
-    const float limx = FM(1.3f, FD((float)cam.W, FM(2.f, cam.fx)));
-    const float limy = FM(1.3f, FD((float)cam.H, FM(2.f, cam.fy)));
+    const float limx = cam.limx, limy = cam.limy;  // 1.3 W / (2 fx), 1.3 H / (2 fy) (make_devcam)
     const float uxc = fminf(fmaxf(ux, -limx), limx);
     const float uyc = fminf(fmaxf(uy, -limy), limy);
     const float J00 = FD(cam.fx, zc), J02 = FD(-FM(cam.fx, uxc), zc);
@@ -419,6 +418,171 @@ __global__ void __launch_bounds__(kPjThreads) k_project_views(const __grid_const
     for (int v = 0; v < vo.n; ++v) vo.flags[v][i] = (uint8_t)(fl8 >> (8 * v));
 }
 
+// O8 of one visible Gaussian: SH colour at the mean's viewing direction (R13),
+// coefficients fetched by sh(row) (row = 3k + ch); +0.5, clamp at 0, clamp flags.
+// The arithmetic of every projection kernel (gs_project and gs_project_views agree).
+template <int DEG, class ShFetch>
+__device__ __forceinline__ void sh_colour(const DevCam& cam, float px, float py, float pz, ShFetch sh, float (&acc)[3],
+                                          uint8_t& flags) {
+  constexpr int NK = (DEG + 1) * (DEG + 1);
+  const float vx = px - cam.ocam[0], vy = py - cam.ocam[1], vz = pz - cam.ocam[2];
+  const float inv = rsqrtf(vx * vx + vy * vy + vz * vz);
+  const float x = vx * inv, y = vy * inv, z = vz * inv;
+  acc[0] = acc[1] = acc[2] = 0.f;
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    float Y, gx, gy, gz;
+    sh_term(k, x, y, z, Y, gx, gy, gz);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) acc[ch] = fmaf(sh(3 * k + ch), Y, acc[ch]);
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    acc[ch] += 0.5f;
+    if (acc[ch] < 0.f) flags |= (uint8_t)(1u << ch);
+    acc[ch] = fmaxf(acc[ch], 0.f);
+  }
+}
+
+// O3's camera z of a mean (the fixed-order chain of project_view).
+__device__ __forceinline__ float cam_z(const DevCam& cam, float px, float py, float pz) {
+  const float* W = cam.R;
+  return FA(FA(FA(FM(W[6], px), FM(W[7], py)), FM(W[8], pz)), cam.t[2]);
+}
+
+// ---------------------------------------------------------------------------
+// K1 v2 (default): as K1, with the bytes a view does not need left in HBM and twice
+// the Gaussians in flight per SM.
+//  * The 3 mean rows are staged first (TMA bulk, 1.5 KB); only if a Gaussian of the
+//    CTA lies in front of the near plane (R6) are the other 8 geometry rows staged:
+//    with the Morton layout whole CTAs lie behind the camera, and they move 12 B per
+//    Gaussian instead of 44.
+//  * The SH coefficients are read straight from the parameter rows by the visible
+//    threads only (coalesced 128-B rows per warp, no shared staging): no 24 KB of
+//    shared memory per CTA, so 16 instead of 7 CTAs fit on an SM, and a partly
+//    visible CTA reads no coefficient of its culled Gaussians.
+// Same arithmetic as K1 (outputs bit-identical).
+// ---------------------------------------------------------------------------
+template <int DEG>
+__global__ void __launch_bounds__(kPjThreads, 10) k_project2(DevCam cam, int64_t P, int64_t S,
+                                                             const float* __restrict__ prm, float4* __restrict__ rec,
+                                                             int32_t* __restrict__ radius_out,
+                                                             int32_t* __restrict__ tiles_out,
+                                                             uint8_t* __restrict__ flags_out) {
+  __shared__ __align__(16) float s_geo[11][kPjThreads];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPjThreads;
+  const int64_t ncol = S - i0 < kPjThreads ? S - i0 : (int64_t)kPjThreads;
+  const uint32_t bytes = (uint32_t)ncol * 4u;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar[0], 3u * bytes);
+#pragma unroll 1
+    for (int r = 0; r < 3; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[0]);
+  }
+  mbar_wait(&bar[0], 0);
+  const int64_t i = i0 + tid;
+  const bool front = i < P && cam_z(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid]) > cam.z_near;
+  Geom g;
+  g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
+  if (__syncthreads_or(front)) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar[1], 8u * bytes);
+#pragma unroll 1
+      for (int r = 3; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[1]);
+    }
+    mbar_wait(&bar[1], 0);
+    if (front) g = project_geom_one(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&](int row) { return s_geo[row][tid]; });
+    if (g.rad > 0) {
+      float acc[3];
+      sh_colour<DEG>(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
+                     [&](int row) { return __ldg(prm + (int64_t)(11 + row) * S + i); }, acc, g.flags);
+      float4* r4 = rec + 3 * i;
+      r4[0] = g.q0;
+      r4[1] = make_float4(g.q1.x, g.q1.y, g.q1.z, acc[0]);
+      r4[2] = make_float4(acc[1], acc[2], __uint_as_float(g.rx), __uint_as_float(g.ry));
+    }
+  }
+  if (i < P) {
+    radius_out[i] = g.rad;
+    tiles_out[i] = g.ntiles;
+    flags_out[i] = g.flags;
+  }
+}
+
+// gs_project_views, v2: the same two changes for a batch of <= 8 views (the 8 other
+// geometry rows staged if a Gaussian of the CTA is in front of ANY view's near plane;
+// the SH coefficients read per visible (Gaussian, view) straight from the rows -- the
+// second and later views hit L1 / L2).  Bit-identical to gs_project.
+template <int DEG>
+__global__ void __launch_bounds__(kPjThreads, 8) k_project_views2(const __grid_constant__ ViewOuts vo, int64_t P,
+                                                                   int64_t S, const float* __restrict__ prm) {
+  __shared__ __align__(16) float s_geo[11][kPjThreads];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int64_t i0 = (int64_t)blockIdx.x * kPjThreads;
+  const int64_t ncol = S - i0 < kPjThreads ? S - i0 : (int64_t)kPjThreads;
+  const uint32_t bytes = (uint32_t)ncol * 4u;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&bar[0], 3u * bytes);
+#pragma unroll 1
+    for (int r = 0; r < 3; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[0]);
+  }
+  mbar_wait(&bar[0], 0);
+  const int64_t i = i0 + tid;
+  bool front = false;
+  if (i < P)
+    for (int v = 0; v < vo.n; ++v) front = front || cam_z(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid]) > vo.cam[v].z_near;
+  const bool any_front = __syncthreads_or(front);
+  if (any_front) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(&bar[1], 8u * bytes);
+#pragma unroll 1
+      for (int r = 3; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[1]);
+    }
+    mbar_wait(&bar[1], 0);
+  }
+  Act act;
+  bool have_act = false;
+#pragma unroll 1
+  for (int v = 0; v < vo.n; ++v) {
+    Geom g;
+    g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
+    if (front)
+      g = project_view(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&]() -> const Act& {
+        if (!have_act) {
+          act = project_act([&](int row) { return s_geo[row][tid]; });
+          have_act = true;
+        }
+        return act;
+      });
+    if (g.rad > 0) {
+      float acc[3];
+      sh_colour<DEG>(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
+                     [&](int row) { return __ldg(prm + (int64_t)(11 + row) * S + i); }, acc, g.flags);
+      float4* r4 = vo.rec[v] + 3 * i;
+      r4[0] = g.q0;
+      r4[1] = make_float4(g.q1.x, g.q1.y, g.q1.z, acc[0]);
+      r4[2] = make_float4(acc[1], acc[2], __uint_as_float(g.rx), __uint_as_float(g.ry));
+    }
+    if (i < P) {
+      vo.radius[v][i] = g.rad;
+      vo.tiles[v][i] = g.ntiles;
+      vo.flags[v][i] = g.flags;
+    }
+  }
+}
+
 // Persistent, software-pipelined variant (GSR_PROJECT=pipe; slower, kept for A/B): grid = a few CTAs per SM, each
 // walking tiles blockIdx.x, blockIdx.x + gridDim.x, ...  The geometry rows of the NEXT
 // tile are bulk-copied (double buffer, one mbarrier per buffer) while the current
@@ -527,7 +691,8 @@ int project_mode() {
     const char* e = getenv("GSR_PROJECT");
     if (e && e[0] == 'l') return 0;
     if (e && e[0] == 'p') return 2;
-    return 1;
+    if (e && e[0] == 't') return 1;
+    return 3;
   }();
   return mode;
 }
@@ -547,11 +712,20 @@ void launch_project_views(int n_views, const DevCam* cams, int64_t P, int64_t S,
       vo.tiles[v] = outs[v0 + v].tiles;
       vo.flags[v] = outs[v0 + v].flags;
     }
-    switch (deg) {
-      case 0: k_project_views<0><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
-      case 1: k_project_views<1><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
-      case 2: k_project_views<2><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
-      default: k_project_views<3><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+    if (project_mode() == 3) {
+      switch (deg) {
+        case 0: k_project_views2<0><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        case 1: k_project_views2<1><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        case 2: k_project_views2<2><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        default: k_project_views2<3><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+      }
+    } else {
+      switch (deg) {
+        case 0: k_project_views<0><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        case 1: k_project_views<1><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        case 2: k_project_views<2><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+        default: k_project_views<3><<<grid, kPjThreads, 0, s>>>(vo, P, S, params); break;
+      }
     }
     count_launch();
   }
@@ -568,6 +742,18 @@ void launch_project(const DevCam& cam, int64_t P, int64_t S, int deg, const floa
       case 1: k_project_pipe<1><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
       case 2: k_project_pipe<2><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
       default: k_project_pipe<3><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags);
+    }
+    count_launch();
+    return;
+  }
+  if (project_mode() == 3) {
+    const int grid = (int)((P + kPjThreads - 1) / kPjThreads);
+    float4* rec = reinterpret_cast<float4*>(out.rec);
+    switch (deg) {
+      case 0: k_project2<0><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      case 1: k_project2<1><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      case 2: k_project2<2><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags); break;
+      default: k_project2<3><<<grid, kPjThreads, 0, s>>>(cam, P, S, params, rec, out.radius, out.tiles, out.flags);
     }
     count_launch();
     return;

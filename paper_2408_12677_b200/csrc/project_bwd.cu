@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(256, 2) k_project_bwd_geom(const __grid_consta
       const float zc = W[6] * px + W[7] * py + W[8] * pz + cam.t[2];
       const float iz = 1.f / zc, iz2 = iz * iz;
       const float ux = xc * iz, uy = yc * iz;
-      const float limx = 1.3f * ((float)cam.W / (2.f * cam.fx)), limy = 1.3f * ((float)cam.H / (2.f * cam.fy));
+      const float limx = cam.limx, limy = cam.limy;
       const bool jx = fl[v] & GS_FLAG_JCLAMP_X, jy = fl[v] & GS_FLAG_JCLAMP_Y;
       const float uxc = jx ? fminf(fmaxf(ux, -limx), limx) : ux;
       const float uyc = jy ? fminf(fmaxf(uy, -limy), limy) : uy;
