@@ -39,8 +39,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
                     help="views in flight (one CUDA stream + buffer set each)")
     ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of whole iterations (N = 1)")
-    ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "8")),
-                    help="views chained per projection-backward pass (<= 8)")
+    ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "0")),
+                    help="views chained per projection-backward pass (<= 64; 0 = all views of a step)")
     ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated", "sparse"],
                     help="N > 1: fused peer-memory reduce-scatter+Adam+all-gather kernel (falls back to 'sharded' if "
                          "symmetric memory is unavailable), NCCL reduce-scatter + sharded Adam + all-gather, "
@@ -621,8 +621,9 @@ def main():
         optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
     if optimizer is not None:
         allreduce = None
+    chunk = args.chunk if args.chunk > 0 else min(64, max(1, len(my_views) if batched else 1))
     tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, allreduce=allreduce,
-                          streams=args.streams if batched else 1, optimizer=optimizer, chunk=args.chunk)
+                          streams=args.streams if batched else 1, optimizer=optimizer, chunk=chunk)
     stream = torch.cuda.current_stream()
 
     # --- warm-up
@@ -870,7 +871,7 @@ def main():
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": args.config, "views_per_step": B if batched else 1, "views": B, "P": w.scene.P, "sh_degree": w.scene.sh_degree,
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if dist_on else "")) if batched else f"replicas x{world}",
-                   "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": args.chunk, "max_keys_per_view": kmax,
+                   "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
                    "targets": "renders of the target scene quantised to RGB-D sensor frames (8-bit colour, 16-bit mm "
                               "depth) and decoded on the GPU",

@@ -263,7 +263,9 @@ gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *    flags: HOST array of n_views DEVICE pointers to each view's gs_proj.flags (uint8[P],
  *    as written by gs_project for that view); sgrads: HOST array of n_views DEVICE
  *    pointers to float[P][12].  Each params row is read and each grad row updated once
- *    per 8 views; every consumed sgrad entry is reset to zero.  accumulate != 0:
+ *    per call for up to 64 views (<= 8 views: unrolled per-view registers; more: the
+ *    views in the inner loop of each Gaussian); every consumed sgrad entry is reset to
+ *    zero.  accumulate != 0:
  *    grad += the batch's gradient; accumulate == 0: grad := the batch's gradient
  *    (every row of every Gaussian written, none read -- the first batch of an
  *    iteration, so that the optimiser need not zero grad). */

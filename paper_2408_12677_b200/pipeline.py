@@ -142,7 +142,9 @@ class Trainer:
         # step() combines the gradient across ranks and updates the parameters
         # (ShardedAdam); it is called after the step counter is incremented
         self.optimizer = optimizer
-        self.chunk = max(1, min(8, int(chunk)))
+        # views chained per gs_project_bwd_views pass: up to 64 (above 8 the wide kernels
+        # chain them all in one pass: every parameter / gradient row touched once)
+        self.chunk = max(1, min(64, int(chunk)))
         # views in flight: view k of a step runs on stream k % streams with its own
         # buffers, so that one view's latency-bound projection / binning kernels overlap
         # another view's rendering (the views of a batch are independent until the

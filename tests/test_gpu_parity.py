@@ -564,14 +564,17 @@ def test_trainer_step_host_matches_step(lib):
     assert torch.equal(models[0].m, models[1].m) and torch.equal(models[0].v, models[1].v)
 
 
-def test_batched_views_backward_matches_per_view(lib):
+@pytest.mark.parametrize("n_views", [3, 11])
+def test_batched_views_backward_matches_per_view(lib, n_views):
     """gs_render_bwd_screen x n + gs_project_bwd_views == sum of per-view gs_render_bwd
-    (and the sgrad buffers are left zero)."""
+    (and the sgrad buffers are left zero); n = 11 > 8 takes the wide kernels (views in
+    the inner loop, one pass for all views)."""
     w = workload("small")
     scene = w.scene
     cams = []
-    for k in range(3):
-        c = scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.05 * (k - 1)), [0.1 * k, -0.05 * k, 0.0])
+    for k in range(n_views):
+        c = scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.05 * (k - 1)),
+                               [0.1 * (k % 4), -0.05 * (k % 3), 0.02 * k])
         cams.append(c)
     params = torch.from_numpy(scene.params).to(DEV)
     sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
@@ -587,7 +590,7 @@ def test_batched_views_backward_matches_per_view(lib):
         ur, ud = (ur * keep_px[None]).astype(np.float32), (ud * keep_px).astype(np.float32)
         upstream.append((ur, ud))
         g_rgb, g_d = torch.from_numpy(ur).to(DEV), torch.from_numpy(ud).to(DEV)
-        ws = torch.zeros(scene.P * 12, dtype=torch.float32, device=DEV)
+        ws = torch.zeros(scene.P * 12, dtype=torch.float32, device=DEV)  # gs_render_bwd clears it
         lib.render_bwd(gsr.camera(cam), sc, params, proj, b["sorted_ids"], b["ranges"], out["T_final"],
                        out["n_contrib"], g_rgb, g_d, ws, grad_sum)
         sg = torch.zeros((scene.P, 12), dtype=torch.float32, device=DEV)

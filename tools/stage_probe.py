@@ -20,6 +20,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="scannetpp")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--views", type=int, default=8)
+    ap.add_argument("--chunk", type=int, default=8)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     lib = gsr.load()
@@ -28,18 +30,18 @@ def main():
     pipeline.spatially_order(lib, model)
     tgt = pipeline.GaussianModel(w.target_scene, dev)
     pipeline.spatially_order(lib, tgt)
-    cams = w.cameras[:8]
+    cams = w.cameras[:a.views]
     cap = pipeline.default_capacity(pipeline.measure_keys(lib, model, cams, dev))
     targets = pipeline.render_targets(lib, tgt, cams, dev, cap)
-    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, streams=1)
+    tr = pipeline.Trainer(lib, model, cams, targets, dev, cap, streams=1, chunk=a.chunk)
     tr.tile_order = False
     views = list(range(len(cams)))
     for _ in range(a.reps):
         tr.step(views)
     # isolated projections of a batch (gs_project_views) for the capture
-    projs = [gsr.make_proj(model.P, dev) for _ in cams]
+    projs = [gsr.make_proj(model.P, dev) for _ in cams[:8]]
     for _ in range(a.reps):
-        lib.project_views([gsr.camera(c) for c in cams], model.desc, model.params, [p[0] for p in projs])
+        lib.project_views([gsr.camera(c) for c in cams[:8]], model.desc, model.params, [p[0] for p in projs])
     torch.cuda.synchronize()
     print("ok", model.P, len(cams))
 
