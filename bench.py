@@ -41,8 +41,9 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of whole iterations (N = 1)")
     ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "0")),
                     help="views chained per projection-backward pass (<= 64; 0 = all views of a step)")
-    ap.add_argument("--optim", default="peer", choices=["peer", "sharded", "replicated", "sparse"],
-                    help="N > 1: fused peer-memory reduce-scatter+Adam+all-gather kernel (falls back to 'sharded' if "
+    ap.add_argument("--optim", default="nvls", choices=["nvls", "peer", "sharded", "replicated", "sparse"],
+                    help="N > 1: 'nvls' in-switch reduce (multimem) + Adam + multicast store kernel (falls back to "
+                         "'peer' without multicast), fused peer-memory reduce-scatter+Adam+all-gather kernel (falls back to 'sharded' if "
                          "symmetric memory is unavailable), NCCL reduce-scatter + sharded Adam + all-gather, "
                          "NCCL all-reduce + replicated Adam, or the visibility-sparse exchange (all-reduce of the "
                          "union-visible gradient columns only) + replicated Adam")
@@ -601,11 +602,19 @@ def main():
     def step_views(i):
         return my_views if batched else [my_views[i % len(my_views)]]
     optimizer, optim_used = None, ("replicated" if dist_on and batched else "local")
-    if dist_on and batched and args.optim == "peer":
-        try:
-            optimizer, optim_used = pipeline.PeerShardedAdam(lib, model), "peer"
-        except Exception as ex:  # noqa: BLE001  (no symmetric memory / P2P: NCCL path)
-            optim_used = f"sharded (peer unavailable: {type(ex).__name__})"
+    if dist_on and batched and args.optim in ("nvls", "peer"):
+        if args.optim == "nvls":
+            try:
+                optimizer, optim_used = pipeline.NvlsShardedAdam(lib, model), "nvls"
+            except Exception as ex:  # noqa: BLE001  (no multicast: the P2P kernel)
+                model.params, model.grad = model.params.clone(), model.grad.clone()
+                optim_used = f"peer (nvls unavailable: {ex})"
+        if optimizer is None:
+            try:
+                optimizer = pipeline.PeerShardedAdam(lib, model)
+                optim_used = optim_used if optim_used.startswith("peer") else "peer"
+            except Exception as ex:  # noqa: BLE001  (no symmetric memory / P2P: NCCL path)
+                optim_used = f"sharded (peer unavailable: {type(ex).__name__})"
         ok = torch.tensor([1 if optimizer is not None else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)  # every rank takes the same path
         if int(ok.item()) == 0 and optimizer is not None:
@@ -616,7 +625,7 @@ def main():
             optimizer, optim_used = None, "sharded (peer unavailable on another rank)"
     if dist_on and batched and args.optim == "sparse":
         optimizer, optim_used = pipeline.SparseExchangeAdam(lib, model), "visibility-sparse exchange, replicated"
-    if dist_on and batched and optimizer is None and args.optim in ("peer", "sharded"):
+    if dist_on and batched and optimizer is None and args.optim in ("nvls", "peer", "sharded"):
         optimizer = pipeline.ShardedAdam(lib, model)
         optim_used = optim_used if optim_used.startswith("sharded") else "sharded"
     if optimizer is not None:
@@ -631,7 +640,7 @@ def main():
         tr.step(step_views(i))
     torch.cuda.synchronize()
     if dist_on and not pipeline.params_agree_across_ranks(model):
-        if optim_used != "peer":
+        if not optim_used.startswith(("peer", "nvls")):
             raise RuntimeError(f"parameters differ across ranks after warm-up (optimiser: {optim_used})")
         # the peer-memory path misbehaved on this machine: resynchronise from rank 0
         # and continue on the NCCL reduce-scatter path (m, v shards keep their owners)

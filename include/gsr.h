@@ -371,7 +371,25 @@ gs_status gs_adam_step_peers_dev(const gs_scene* scene /*HOST*/, int world, int 
                                  float* m, float* v, const float* lr_per_row /*HOST*/, float beta1, float beta2,
                                  float eps, int64_t* step_dev, int64_t begin, int64_t end, void* stream);
 
-/* ---------------------------------------------------------------- visibility-sparse exchange
+/* The same step with the reduction and the broadcast done by the NVSwitch (NVLS,
+ * SURVEY.md §8(f) NEXT-2): for the scalars [begin, end) this rank owns, one
+ * multimem.ld_reduce (add, fp32) on the MULTICAST address of the symmetric gradient
+ * buffer returns the sum over all ranks, Adam updates the local m, v and this rank's
+ * parameter copy `param` (read only), and one multimem.st on the MULTICAST address of
+ * the symmetric parameter buffer writes the new values into every rank's copy.
+ *  mc_grad, mc_param: DEVICE multicast addresses (e.g. torch symmetric memory's
+ *  multicast_ptr, which exists only on NVSwitch systems with multicast support);
+ *  param: this rank's unicast view of the parameter buffer.
+ *  step_dev: nullable DEVICE int64; non-NULL: the step counter on the device
+ *  (incremented first, as gs_adam_step_dev), else `step` (>= 1).
+ * The caller orders the ranks around the call as for gs_adam_step_peers.  begin, end
+ * multiples of 4 (GS_ERR_ALIGN). */
+gs_status gs_adam_step_multimem(const gs_scene* scene /*HOST*/, const float* mc_grad, float* mc_param,
+                                const float* param, float* m, float* v, const float* lr_per_row /*HOST*/, float beta1,
+                                float beta2, float eps, int64_t step, int64_t* step_dev, int64_t begin, int64_t end,
+                                void* stream);
+
+/* ---------------------------------------------------------------- visibility-sparse exchange/* ---------------------------------------------------------------- visibility-sparse exchange
  * (SURVEY.md §8(f) NEXT-2 "visibility-sparse gradient exchange: union of visible masks,
  * then compaction").  A Gaussian culled in every view of every rank has
  * an exactly zero gradient on every rank, so only the columns of the union of the

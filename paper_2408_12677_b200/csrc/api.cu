@@ -634,6 +634,33 @@ gs_status gs_adam_step_peers_dev(const gs_scene* scene, int world, int rank, con
                          beta1, beta2, eps, 0, step_dev, begin, end, stream);
 }
 
+gs_status gs_adam_step_multimem(const gs_scene* scene, const float* mc_grad, float* mc_param, const float* param,
+                                float* m, float* v, const float* lr_per_row, float beta1, float beta2, float eps,
+                                int64_t step, int64_t* step_dev, int64_t begin, int64_t end, void* stream) {
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, "gs_adam_step_multimem"));
+  const int64_t n = (int64_t)rows_of(scene) * scene->P_stride;
+  if (!lr_per_row || (!step_dev && step < 1) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) ||
+      !(eps >= 0.f) || begin < 0 || end < begin || end > n) {
+    set_error("gs_adam_step_multimem: invalid arguments (step=%lld begin=%lld end=%lld n=%lld)", (long long)step,
+              (long long)begin, (long long)end, (long long)n);
+    return GS_ERR_ARG;
+  }
+  if ((begin & 3) || (end & 3)) {
+    set_error("gs_adam_step_multimem: begin/end must be multiples of 4");
+    return GS_ERR_ALIGN;
+  }
+  if (end > begin)
+    GS_TRY(check_ptrs("gs_adam_step_multimem",
+                      {{mc_grad, "mc_grad"}, {mc_param, "mc_param"}, {param, "param"}, {m, "m"}, {v, "v"}}));
+  const double bc1 = step_dev ? 1.0 : 1.0 - std::pow((double)beta1, (double)step);
+  const double bc2 = step_dev ? 1.0 : 1.0 - std::pow((double)beta2, (double)step);
+  GS_TRY(launch_adam_multimem(rows_of(scene), scene->P_stride, mc_grad, mc_param, param, m, v, lr_per_row, beta1,
+                              beta2, eps, (float)bc1, (float)bc2, begin, end, static_cast<cudaStream_t>(stream),
+                              step_dev));
+  return check_launch("gs_adam_step_multimem");
+}
+
 gs_status gs_l1_loss_grad(int64_t npix, const float* rgb, const float* depth, const float* target_rgb,
                           const float* target_depth, float w_depth, float* dL_drgb, float* dL_ddepth, float* loss,
                           void* stream) {

@@ -122,6 +122,9 @@ gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const flo
                             float* const* param_peers, float* m, float* v, const float* lr, float beta1, float beta2,
                             float eps, float bc1, float bc2, int64_t begin, int64_t end, cudaStream_t s,
                             int64_t* step_dev = nullptr);
+gs_status launch_adam_multimem(int64_t F, int64_t S, const float* mc_grad, float* mc_param, const float* param,
+                               float* m, float* v, const float* lr, float beta1, float beta2, float eps, float bc1,
+                               float bc2, int64_t begin, int64_t end, cudaStream_t s, int64_t* step_dev = nullptr);
 void launch_l1(int64_t npix, const float* rgb, const float* depth, const float* t_rgb, const float* t_depth,
                float w_depth, float* g_rgb, float* g_depth, float* loss, cudaStream_t s);
 

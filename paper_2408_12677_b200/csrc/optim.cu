@@ -143,6 +143,50 @@ __global__ void __launch_bounds__(256) k_adam_peers(const __grid_constant__ Peer
   }
 }
 
+// NVLS (in-switch) variant of k_adam_peers (SURVEY.md §8(f) NEXT-2 remainder): this
+// rank's shard of the SUM of every rank's gradient arrives in ONE multicast load-reduce
+// (multimem.ld_reduce: the NVSwitch adds the ranks' values, fp32), Adam runs on the
+// local m, v and parameters, and ONE multicast store (multimem.st) writes the new
+// parameters into every rank's copy.  mc_grad / mc_param: multicast addresses of the
+// symmetric gradient / parameter buffers; param: this rank's own copy (unicast).  Each
+// scalar is reduced and stored once, by its owner: the ranks stay bit-identical.
+__device__ __forceinline__ float4 mc_ld_reduce_add(const float4* mc) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(mc)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void mc_st(float4* mc, const float4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_adam_multimem(const float4* __restrict__ mc_grad, float4* __restrict__ mc_param,
+                                                       const float4* __restrict__ param, float4* __restrict__ m,
+                                                       float4* __restrict__ v, int64_t b4, int64_t e4, int64_t S4,
+                                                       LrTable lr_in, int F, float b1, float b2, float eps,
+                                                       float rs_host, const int64_t* __restrict__ step_dev) {
+  __shared__ float s_step[64];
+  float rs_bc2;
+  adam_steps(lr_in, F, b1, b2, rs_host, step_dev, s_step, rs_bc2);
+  const float c1 = 1.f - b1, c2 = 1.f - b2;
+  for (int64_t i = b4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float step = s_step[i / S4];
+    const float4 gg = mc_ld_reduce_add(mc_grad + i);
+    float4 mm = m[i], vv = v[i], pp = param[i];
+    adam_update(pp.x, mm.x, vv.x, gg.x, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.y, mm.y, vv.y, gg.y, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.z, mm.z, vv.z, gg.z, b1, b2, c1, c2, step, rs_bc2, eps);
+    adam_update(pp.w, mm.w, vv.w, gg.w, b1, b2, c1, c2, step, rs_bc2, eps);
+    m[i] = mm;
+    v[i] = vv;
+    mc_st(mc_param + i, pp);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restrict__ rgb, const float* __restrict__ dep,
                                             const float* __restrict__ trgb, const float* __restrict__ tdep, float sc,
                                             float sd, float* __restrict__ grgb, float* __restrict__ gdep,
@@ -235,6 +279,27 @@ gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const flo
     k_adam_peers<<<std::max(grid, 1), 256, 0, s>>>(pr, reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v),
                                                     begin / 4, end / 4, S / 4, t, (int)F, beta1, beta2, eps,
                                                     step_dev ? 0.f : 1.f / sqrtf(bc2), step_dev);
+    count_launch();
+  }
+  return GS_OK;
+}
+
+gs_status launch_adam_multimem(int64_t F, int64_t S, const float* mc_grad, float* mc_param, const float* param,
+                               float* m, float* v, const float* lr, float beta1, float beta2, float eps, float bc1,
+                               float bc2, int64_t begin, int64_t end, cudaStream_t s, int64_t* step_dev) {
+  LrTable t{};
+  for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = step_dev ? lr[r] : lr[r] / bc1;
+  if (step_dev) {
+    k_step_inc<<<1, 1, 0, s>>>(step_dev);
+    count_launch();
+  }
+  const int64_t n4 = (end - begin) / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, (int64_t)sm_count() * 8);
+  if (n4 > 0) {
+    k_adam_multimem<<<std::max(grid, 1), 256, 0, s>>>(
+        reinterpret_cast<const float4*>(mc_grad), reinterpret_cast<float4*>(mc_param),
+        reinterpret_cast<const float4*>(param), reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
+        end / 4, S / 4, t, (int)F, beta1, beta2, eps, step_dev ? 0.f : 1.f / sqrtf(bc2), step_dev);
     count_launch();
   }
   return GS_OK;

@@ -160,6 +160,8 @@ class Library:
         lib.gs_adam_step_peers.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float,
                                            i64, i64, i64, vp]
         lib.gs_adam_step_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, C.c_int, vp]
+        lib.gs_adam_step_multimem.argtypes = [vp, vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, vp,
+                                              i64, i64, vp]
         lib.gs_adam_step_range_dev.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, vp, i64, i64,
                                                vp]
         lib.gs_adam_step_peers_dev.argtypes = [vp, C.c_int, C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_float,
@@ -182,7 +184,7 @@ class Library:
         lib.gs_scatter_columns.argtypes = [vp, i64, i64, vp, i64, vp, vp]
         for fn in ("gs_project", "gs_bin_tiles", "gs_render_fwd", "gs_render_bwd", "gs_render_bwd_screen",  # noqa: E501
                    "gs_project_bwd_views", "gs_spatial_order", "gs_adam_step", "gs_l1_loss_grad",
-                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_adam_step_range_dev", "gs_adam_step_peers_dev", "gs_tsdf_reset", "gs_tsdf_allocate",
+                   "gs_naive_render_fwd", "gs_naive_render_bwd_screen", "gs_tile_order", "gs_render_bwd_screen_l1", "gs_keyframe_schedule", "gs_adam_step_range", "gs_adam_step_peers", "gs_adam_step_dev", "gs_adam_step_range_dev", "gs_adam_step_peers_dev", "gs_adam_step_multimem", "gs_tsdf_reset", "gs_tsdf_allocate",
                    "gs_tsdf_integrate", "gs_quadtree", "gs_seed_gaussians", "gs_decode_rgbd", "gs_visibility_union", "gs_compact_index",
                    "gs_gather_columns", "gs_scatter_columns", "gs_project_views"):
             getattr(lib, fn).restype = i32
@@ -356,6 +358,17 @@ class Library:
         return self._check("gs_adam_step_peers", self.lib.gs_adam_step_peers(
             C.byref(sc), int(world), int(rank), gp, pp, _ptr(m), _ptr(v), lr, beta1, beta2, eps, int(step), int(begin),
             int(end), _stream(stream)))
+
+    def adam_step_multimem(self, sc, mc_grad, mc_param, param, m, v, lr_per_row, step, begin, end, beta1=0.9,
+                           beta2=0.999, eps=1e-15, stream=None):
+        """NVLS variant: mc_grad / mc_param multicast device addresses (ints); step: int or
+        int64 device tensor."""
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        dev_step = isinstance(step, torch.Tensor)
+        return self._check("gs_adam_step_multimem", self.lib.gs_adam_step_multimem(
+            C.byref(sc), C.c_void_p(int(mc_grad)), C.c_void_p(int(mc_param)), _ptr(param), _ptr(m), _ptr(v), lr, beta1,
+            beta2, eps, 0 if dev_step else int(step), _ptr(step) if dev_step else None, int(begin), int(end),
+            _stream(stream)))
 
     # -- NEXT-3: TSDF fusion ---------------------------------------------
     def tsdf_reset(self, vol, stream=None):

@@ -703,6 +703,31 @@ class PeerShardedAdam:
         self.hp.barrier(channel=1)  # every rank's parameter stores have landed
 
 
+class NvlsShardedAdam(PeerShardedAdam):
+    """PeerShardedAdam with the NVSwitch doing the reduction and the broadcast
+    (gs_adam_step_multimem): the gradient and parameter
+    buffers' MULTICAST addresses come from torch symmetric memory; rank r's kernel
+    load-reduces its shard of the summed gradient in the switch (one multimem.ld_reduce
+    per 16 B instead of world P2P loads), updates it, and multicast-stores the new
+    parameters to every rank (one multimem.st instead of world P2P stores).  Raises
+    RuntimeError where multicast is unavailable (no NVSwitch multicast support, e.g.
+    a single-GPU box) so that callers fall back to the peer / NCCL paths."""
+
+    def __init__(self, lib, model: GaussianModel, group=None):
+        super().__init__(lib, model, group)
+        mcg, mcp = int(self.hg.multicast_ptr), int(self.hp.multicast_ptr)
+        if not mcg or not mcp:
+            raise RuntimeError("symmetric memory has no multicast address (NVLS unavailable)")
+        self.mc_grad, self.mc_param = mcg, mcp
+
+    def step(self):
+        m = self.model
+        self.hg.barrier(channel=0)  # every rank's gradient is final
+        self.lib.adam_step_multimem(m.desc, self.mc_grad, self.mc_param, self.pbuf, m.m, m.v, m.lr,
+                                    m.step_dev if self.device_step else m.step_count, self.begin, self.end)
+        self.hp.barrier(channel=1)  # every rank's parameter stores have landed
+
+
 def params_agree_across_ranks(model: GaussianModel, group=None) -> bool:
     """Runtime check of the data-parallel invariant: parameters bit-identical on every
     rank (a float64 checksum and a sampled-bits hash compared across ranks)."""

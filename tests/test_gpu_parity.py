@@ -809,6 +809,97 @@ def test_peer_sharded_adam_single_rank(lib):
         dist.destroy_process_group()
 
 
+def test_nvls_sharded_adam_single_rank(lib):
+    """NvlsShardedAdam (gs_adam_step_multimem: multimem.ld_reduce of the gradient shard
+    through the NVSwitch, Adam, multimem.st of the parameters; world size 1 on this GPU,
+    so the in-switch sum has one term) equals gs_adam_step bit for bit, with the host and
+    the device step counter.  Where the box has no multicast the optimizer must refuse
+    cleanly (RuntimeError) and the test says so by skipping."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = workload("small")
+        rng = np.random.default_rng(10)
+        g = torch.from_numpy(rng.normal(size=w.scene.params.shape).astype(np.float32)).to(DEV)
+        ma, mb = pipeline.GaussianModel(w.scene, DEV), pipeline.GaussianModel(w.scene, DEV)
+        try:
+            opt = pipeline.NvlsShardedAdam(lib, mb)
+        except RuntimeError as ex:
+            assert "multicast" in str(ex)
+            pytest.skip("torch symmetric memory has no multicast address on this box (the kernel itself is "
+                        "covered by test_adam_multimem_one_device_multicast)")
+        for it in range(4):
+            ma.grad.copy_(g * (it + 1))
+            mb.grad.copy_(g * (it + 1))
+            ma.step_count += 1
+            lib.adam_step(ma.desc, ma.params, ma.grad, ma.m, ma.v, ma.lr, ma.step_count, zero_grad=False)
+            opt.device_step = it >= 2
+            mb.step_count += 1
+            if it == 2:
+                mb.step_dev.fill_(mb.step_count - 1)
+            opt.step()
+        torch.cuda.synchronize()
+        assert int(mb.step_dev.item()) == 4
+        assert torch.equal(ma.params, mb.params)
+        assert torch.equal(ma.m, mb.m) and torch.equal(ma.v, mb.v)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("device_step", [False, True])
+def test_adam_multimem_one_device_multicast(lib, device_step):
+    """gs_adam_step_multimem on a real NVLS multicast object of this one device
+    (tests/mc_helpers.py): multimem.ld_reduce of the gradient, Adam, multimem.st of the
+    parameters through the multicast address, over a sharded range with a ragged end;
+    equals gs_adam_step (unicast) bit for bit inside the range and leaves the rest alone."""
+    import mc_helpers
+    w = workload("small")
+    rng = np.random.default_rng(12)
+    F, S = w.scene.params.shape
+    n = F * S
+    try:
+        gb, pb = mc_helpers.MulticastBuffer(n), mc_helpers.MulticastBuffer(n)
+    except RuntimeError as ex:
+        pytest.skip(f"no multicast object on this box: {ex}")
+    try:
+        ma = pipeline.GaussianModel(w.scene, DEV)
+        g = torch.from_numpy(rng.normal(size=(F, S)).astype(np.float32)).to(DEV)
+        pb.tensor.copy_(ma.params.reshape(-1))
+        m2, v2 = torch.zeros_like(ma.m), torch.zeros_like(ma.v)
+        begin, end = 4 * 37, n - 4 * 5  # a sharded range: neither end at the array's
+        ref_p = ma.params.clone()
+        ref_m, ref_v = ma.m.clone(), ma.v.clone()
+        step_dev = torch.zeros(1, dtype=torch.int64, device=DEV)
+        for it in range(1, 4):
+            gb.tensor.copy_((g * it).reshape(-1))
+            ma.grad.copy_(g * it)
+            lib.adam_step(ma.desc, ma.params, ma.grad, ma.m, ma.v, ma.lr, it, zero_grad=False)
+            lib.adam_step_multimem(ma.desc, gb.mc, pb.mc, pb.tensor, m2, v2, ma.lr, step_dev if device_step else it,
+                                   begin, end)
+        torch.cuda.synchronize()
+        if device_step:
+            assert int(step_dev.item()) == 3
+        got = pb.tensor.reshape(F, S)
+        inside = torch.zeros(n, dtype=torch.bool, device=DEV)
+        inside[begin:end] = True
+        inside = inside.reshape(F, S)
+        assert torch.equal(got[inside], ma.params[inside])
+        assert torch.equal(m2[inside], ma.m[inside]) and torch.equal(v2[inside], ma.v[inside])
+        assert torch.equal(got[~inside], ref_p[~inside])  # outside the shard: untouched
+        assert torch.count_nonzero(m2[~inside]) == 0
+        assert not torch.equal(got, ref_p)
+    finally:
+        gb.close()
+        pb.close()
+
+
 @pytest.mark.parametrize("streams", [1, 3])
 def test_graph_replay_matches_eager(lib, streams):
     """Trainer.capture: a whole iteration (project/bin/fwd/L1/bwd per view on its
