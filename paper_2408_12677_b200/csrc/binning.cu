@@ -19,6 +19,7 @@
 // per-digit counts, resolves its global offsets by decoupled look-back over the
 // preceding partitions, stages keys in shared memory in block-sorted order and
 // writes them out as per-digit coalesced runs.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -39,7 +40,7 @@ constexpr int kRsThreads = 256, kRsWarps = kRsThreads / 32;
 // Depth passes: 4 keys per thread (1024 per partition) for scenes below 512K
 // Gaussians (one view per step, latency-bound: more partitions finish sooner), 16 (4096)
 // above (views in flight: fewer, longer CTAs churn fewer SM slots against the render
-// kernels; scannetpp 6.01 -> 5.96 ms/step).  GSR_DEPTH_ITEMS=4|16 forces one.
+// kernels; scannetpp 6.01 -> 5.96 ms/step): a P heuristic, depth_items_big().
 constexpr int kRsItemsKeys = 16, kRsItemsDepth = 4, kRsItemsDepthBig = 16;  // items per thread
 constexpr int kRsTileKeys = kRsThreads * kRsItemsKeys, kRsTileDepth = kRsThreads * kRsItemsDepth;
 constexpr uint32_t kLbAgg = 1u << 30, kLbInc = 2u << 30, kLbMask = (1u << 30) - 1;
@@ -1002,6 +1003,21 @@ bool use_rts() {
   return e && std::strcmp(e, "rts") == 0;
 }
 
+// Depth-pass partition size (see kRsItemsDepthBig): a P heuristic (P >= 512K stands in
+// for "several views in flight", true of every workload that large in bench.py);
+// GSR_DEPTH_ITEMS=4|16 overrides it, any other value is reported once and ignored.
+bool depth_items_big(int64_t P) {
+  static const int forced = [] {
+    const char* e = std::getenv("GSR_DEPTH_ITEMS");
+    if (!e) return 0;
+    if (std::strcmp(e, "4") == 0) return 4;
+    if (std::strcmp(e, "16") == 0) return 16;
+    std::fprintf(stderr, "gsr: GSR_DEPTH_ITEMS=%s ignored (accepted: 4, 16)\n", e);
+    return 0;
+  }();
+  return forced ? forced == 16 : P >= ((int64_t)1 << 19);
+}
+
 size_t bin_workspace_bytes(int64_t P, int64_t cap, int num_tiles) { return make_layout(P, cap, num_tiles).total; }
 
 gs_status finish_bin(const void* ctr, int64_t cap, int64_t* num_keys_host, cudaStream_t s);
@@ -1049,8 +1065,7 @@ gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws,
   uint32_t* kout = dk1;
   uint32_t* vout = dv1;
   const bool rts_mode = use_rts();
-  const char* di = std::getenv("GSR_DEPTH_ITEMS");
-  const bool big = di ? std::atoi(di) == 16 : P >= (int64_t)1 << 19;
+  const bool big = depth_items_big(P);
   const int rs_grid_big =
       (int)std::min<int64_t>((P + kRsThreads * kRsItemsDepthBig - 1) / (kRsThreads * kRsItemsDepthBig), (int64_t)nsm * 3);
   for (int pass = 0; pass < 4; ++pass) {

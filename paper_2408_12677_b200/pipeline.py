@@ -610,7 +610,10 @@ class SparseExchangeAdam:
 
     Every rank reduces the same packed array and runs the same Adam, so the parameters
     stay bit-identical across ranks.  ``ops`` replaces the device calls with the same
-    signatures (the CPU gloo tests pass torch implementations)."""
+    signatures (the CPU gloo tests pass torch implementations).  Reading M costs one host
+    sync per step (an NCCL collective's size is a host argument), so this optimiser runs
+    eagerly and is never graph-captured; the default N > 1 exchanges (nvls, peer) are
+    fixed-size and captured."""
 
     def __init__(self, lib, model: GaussianModel, group=None, ops=None):
         import torch.distributed as dist
