@@ -15,7 +15,11 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "gsref.cpp")
-LIB = os.path.join(HERE, "libgsref.so")
+# GSREF_SANITIZE=1: an ASan + UBSan build (libgsref_san.so; tests/test_oracle_sanitize.py
+# runs the pins against it in a subprocess with libasan preloaded)
+SANITIZE = os.environ.get("GSREF_SANITIZE") == "1"
+SAN_FLAGS = ["-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined", "-fno-sanitize-recover=all"]
+LIB = os.path.join(HERE, "libgsref_san.so" if SANITIZE else "libgsref.so")
 
 F32, F64, MIXED, STAGE = 0, 1, 2, 3
 FLAG_CULLED = 128
@@ -24,7 +28,7 @@ FLAG_CULLED = 128
 def build(force: bool = False) -> str:
     """Compile the oracle (g++ -O2 -ffp-contract=off, no fast-math)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        cmd = ["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
+        cmd = ["g++", *(SAN_FLAGS if SANITIZE else ["-O2"]), "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
                "-o", LIB + ".tmp", SRC]
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)

@@ -11,12 +11,14 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "tsdf_ref.cpp")
-LIB = os.path.join(HERE, "libtsdfref.so")
+SANITIZE = os.environ.get("GSREF_SANITIZE") == "1"  # see oracle/gsref.py
+SAN_FLAGS = ["-O1", "-g", "-fno-omit-frame-pointer", "-fsanitize=address,undefined", "-fno-sanitize-recover=all"]
+LIB = os.path.join(HERE, "libtsdfref_san.so" if SANITIZE else "libtsdfref.so")
 
 
 def build(force: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+        subprocess.check_call(["g++", *(SAN_FLAGS if SANITIZE else ["-O2"]), "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
                                "-o", LIB + ".tmp", SRC])
         os.replace(LIB + ".tmp", LIB)
     return LIB

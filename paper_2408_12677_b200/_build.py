@@ -16,7 +16,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 SOURCES = ["api.cu", "project.cu", "project_bwd.cu", "binning.cu", "render.cu", "optim.cu", "naive.cu", "schedule.cpp", "tsdf.cu", "seed.cu", "frame.cu", "exchange.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-LIBS = {"libgsr.so": [], "libgsr_exact.so": ["-DGSR_EXACT_EXP"]}
+LIBS = {"libgsr.so": [], "libgsr_exact.so": ["-DGSR_EXACT_EXP"], "libgsr_check.so": ["-DGSR_BOUNDS_CHECK"]}
 
 
 def nvcc() -> str:

@@ -204,6 +204,17 @@ gs_status check_det(const gs_bwd_opts* opts, const char* fn, float** det, int64_
 
 }  // namespace
 
+// libgsr_check.so only (GSR_BOUNDS_CHECK): validate the lists a render call is given
+static void check_lists(const gs_camera* cam, const gs_scene* scene, const int32_t* ids, const int32_t* ranges,
+                        void* stream) {
+#ifdef GSR_BOUNDS_CHECK
+  const DevCam dc = make_devcam(*cam);
+  launch_check_lists(dc.TX * dc.TY, scene->P, ids, ranges, static_cast<cudaStream_t>(stream));
+#else
+  (void)cam, (void)scene, (void)ids, (void)ranges, (void)stream;
+#endif
+}
+
 extern "C" {
 
 int gs_version(void) { return GSR_VERSION; }
@@ -294,6 +305,7 @@ gs_status gs_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_proj pro
     set_error("gs_render_fwd: blended is not 8-byte aligned");
     return GS_ERR_ALIGN;
   }
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_render_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, tile_order, rgb, depth, T_final, n_contrib, blended,
                     key_blocks, static_cast<cudaStream_t>(stream));
   GS_TRY(check_launch("gs_render_fwd"));
@@ -335,6 +347,7 @@ gs_status gs_render_bwd(const gs_camera* cam, const gs_scene* scene, const float
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (cudaMemsetAsync(ws, 0, need, s) != cudaSuccess) return check_launch("gs_render_bwd memset");
   const DevCam dc = make_devcam(*cam);
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_render_bwd(dc, proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib, dL_drgb, dL_ddepth,
                     key_blocks, static_cast<float*>(ws), s, nullptr, det, det_keys);
   const uint8_t* fl = proj.flags;
@@ -363,6 +376,7 @@ gs_status gs_render_bwd_screen(const gs_camera* cam, const gs_scene* scene, gs_p
     set_error("gs_render_bwd_screen: dL_ddepth is not 16-byte aligned");
     return GS_ERR_ALIGN;
   }
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_render_bwd(make_devcam(*cam), proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib,
                     dL_drgb, dL_ddepth, key_blocks, sgrad, static_cast<cudaStream_t>(stream), nullptr, det, det_keys);
   return check_launch("gs_render_bwd_screen");
@@ -387,6 +401,7 @@ gs_status gs_render_bwd_screen_l1(const gs_camera* cam, const gs_scene* scene, g
                                                 {sgrad, "sgrad"}}));
   if (scene->P > 0) GS_TRY(check_ptrs("gs_render_bwd_screen_l1", {{proj.rec, "proj.rec"}}));
   const L1Targets l1{rgb, depth, target_rgb, target_depth, w_depth, loss};
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_render_bwd(make_devcam(*cam), proj, scene->P, sorted_ids, tile_ranges, tile_order, T_final, n_contrib,
                     nullptr, nullptr, key_blocks, sgrad, static_cast<cudaStream_t>(stream), &l1, det, det_keys);
   return check_launch("gs_render_bwd_screen_l1");
@@ -414,6 +429,7 @@ gs_status gs_naive_render_fwd(const gs_camera* cam, const gs_scene* scene, gs_pr
     set_error("gs_naive_render_fwd: blended is not 8-byte aligned");
     return GS_ERR_ALIGN;
   }
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_naive_fwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, rgb, depth, T_final, n_contrib, blended,
                    static_cast<cudaStream_t>(stream));
   GS_TRY(check_launch("gs_naive_render_fwd"));
@@ -438,6 +454,7 @@ gs_status gs_naive_render_bwd_screen(const gs_camera* cam, const gs_scene* scene
   GS_TRY(check_ptrs("gs_naive_render_bwd_screen", {{proj.rec, "proj.rec"}, {tile_ranges, "tile_ranges"},
                                                    {T_final, "T_final"}, {n_contrib, "n_contrib"},
                                                    {dL_drgb, "dL_drgb"}, {sgrad, "sgrad"}}));
+  check_lists(cam, scene, sorted_ids, tile_ranges, stream);
   launch_naive_bwd(make_devcam(*cam), proj.rec, sorted_ids, tile_ranges, T_final, n_contrib, dL_drgb, dL_ddepth,
                    sgrad, static_cast<cudaStream_t>(stream));
   return check_launch("gs_naive_render_bwd_screen");

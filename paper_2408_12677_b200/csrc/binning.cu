@@ -324,12 +324,14 @@ __global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict_
         if (q < nk) {
           if ((uint32_t)(kb + q) >= next) {
             ++j;
+            GSR_CHECK(j < ns);
             next = s_off[j + 1];
             x0 = s_rx[j] & 0xffff, w = (int)(s_rx[j] >> 16) - x0, y0 = s_ry[j] & 0xffff;
             gid = s_gid[j];
             row = 0, col = 0;
           }
           const uint32_t tile = (uint32_t)((y0 + row) * TX + x0 + col);
+          GSR_CHECK(w > 0 && col < w && x0 + col < TX && tile < 65536u && (int64_t)(kb + q) < cap);
           kk[q] = (uint16_t)tile;
           vv[q] = gid;
           if (kHist) {
@@ -741,6 +743,7 @@ __global__ void __launch_bounds__(32 * kTsWarps) k_tscatter(const uint16_t* __re
       if (__all_sync(kFull, own[t & omask] == (uint8_t)lane)) {
         const uint32_t run = my[t];
         my[t] = (uint16_t)(run + 1u);
+        GSR_CHECK(!valid || (t < (uint32_t)NT && (int64_t)s_base[t] + run < K));
         if (valid) out[s_base[t] + run] = (int32_t)id;
         continue;
       }
@@ -751,6 +754,7 @@ __global__ void __launch_bounds__(32 * kTsWarps) k_tscatter(const uint16_t* __re
       __syncwarp();
       if (valid && r == 0) my[t] = (uint16_t)(run + __popc(peers));
       __syncwarp();
+      GSR_CHECK(!valid || (t < (uint32_t)NT && (int64_t)s_base[t] + run + r < K));
       if (valid) out[s_base[t] + run + r] = (int32_t)id;
     }
     __syncwarp();  // buffer sb is restaged two batches from now
@@ -1017,6 +1021,25 @@ bool depth_items_big(int64_t P) {
   }();
   return forced ? forced == 16 : P >= ((int64_t)1 << 19);
 }
+
+#ifdef GSR_BOUNDS_CHECK
+__global__ void k_check_lists(int NT, int64_t P, const int32_t* __restrict__ ids, const int2* __restrict__ ranges) {
+  int32_t kmax = 0;
+  for (int t = 0; t < NT; ++t) kmax = max(kmax, ranges[t].y);  // every thread: K = the largest end
+  const int lane = threadIdx.x & 31;
+  for (int t = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); t < NT; t += (int)((gridDim.x * blockDim.x) >> 5)) {
+    const int2 rg = ranges[t];
+    GSR_CHECK(rg.x >= 0 && rg.x <= rg.y && rg.y <= kmax);
+    for (int k = rg.x + lane; k < rg.y; k += 32) GSR_CHECK(ids[k] >= 0 && (int64_t)ids[k] < P);
+  }
+}
+void launch_check_lists(int NT, int64_t P, const int32_t* ids, const int32_t* ranges, cudaStream_t s) {
+  k_check_lists<<<std::max(1, std::min(NT / 8 + 1, 4 * sm_count())), 256, 0, s>>>(NT, P, ids,
+                                                                                 reinterpret_cast<const int2*>(ranges));
+}
+#else
+void launch_check_lists(int, int64_t, const int32_t*, const int32_t*, cudaStream_t) {}
+#endif
 
 size_t bin_workspace_bytes(int64_t P, int64_t cap, int num_tiles) { return make_layout(P, cap, num_tiles).total; }
 

@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(256) k_gather_cols(const float* __restrict__ f
                                                      float* __restrict__ packed) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx[j];
+    GSR_CHECK(c >= 0 && c < S);
     for (int64_t r = 0; r < F; ++r) packed[r * M + j] = full[r * S + c];
   }
 }
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(256) k_scatter_cols(const float* __restrict__ 
                                                       float* __restrict__ full) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = idx[j];
+    GSR_CHECK(c >= 0 && c < S);
     for (int64_t r = 0; r < F; ++r) full[r * S + c] = packed[r * M + j];
   }
 }

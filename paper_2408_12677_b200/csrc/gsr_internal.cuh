@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <utility>
 
 #include "gsr.h"
@@ -26,6 +27,28 @@ struct DevCam {
 };
 
 DevCam make_devcam(const gs_camera& c);
+
+// Bounds-checked build (libgsr_check.so, -DGSR_BOUNDS_CHECK; compute-sanitizer is
+// closed on the GPU pool): device-side index asserts in the kernels that scatter
+// through computed indices, plus validation of the caller's lists at the ABI
+// (launch_check_lists).  A failed check prints its condition and traps, which turns
+// into cudaErrorLaunchFailure at the next check_launch.  Compiled out otherwise.
+#ifdef GSR_BOUNDS_CHECK
+#define GSR_CHECK(cond)                                                                        \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("GSR_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #cond);                                                         \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define GSR_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+// every id of every tile's list in [0, P), 0 <= start <= end <= K (K = the largest end)
+void launch_check_lists(int NT, int64_t P, const int32_t* ids, const int32_t* ranges, cudaStream_t s);
 
 // error plumbing (api.cu)
 void set_error(const char* fmt, ...);

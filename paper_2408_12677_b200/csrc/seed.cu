@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(1024) k_seed(SeedCtx sc, gs_tsdf_volume vol, D
       const int4 lf = reinterpret_cast<const int4*>(leaves)[q];
       const int u = lf.x + lf.z / 2, v = lf.y + lf.w / 2;  // centre pixel (R38)
       const int64_t pp = (int64_t)v * cam.W + u;
+      GSR_CHECK(u >= 0 && u < cam.W && v >= 0 && v < cam.H);
       const float d = depth[pp];
       if (d > 0.f) {
         // Eq. 10: p_q = T_WC pi^-1(u_q, D[u_q])
