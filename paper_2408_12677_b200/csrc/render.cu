@@ -64,6 +64,16 @@ namespace {
 #ifndef GSR_DENSE_FWD
 #define GSR_DENSE_FWD 3
 #endif
+// Dense (branch-free) paths on packed FP32 pairs (FFMA2 / FMUL2, fma.rn.f32x2 etc.):
+// the two pixels of a lane in one block row (columns lx, lx + 8) share dy, so their
+// per-pixel arithmetic is issued as one paired instruction -- the same IEEE fp32
+// operations per element, half the issue slots (the render kernels are issue-bound).
+#ifndef GSR_FFMA2
+#define GSR_FFMA2 1
+#endif
+#ifndef GSR_FFMA2_FWD
+#define GSR_FFMA2_FWD GSR_FFMA2
+#endif
 #ifndef GSR_DENSE_BWD
 #define GSR_DENSE_BWD 6
 #endif
@@ -373,9 +383,17 @@ __device__ __forceinline__ float geo_p2(const Geo& g, float Ch, int b) {
   return __fmaf_rn(dy, __fmaf_rn(Ch, dy, g.b0[b & 1]), g.a0[b & 1]);
 }
 
+// Per-lane pixel state; pixels 2r and 2r + 1 (one block row, columns lx and lx + 8)
+// are the two halves of one float2 so that the dense paths can use packed FP32 ops.
 struct FwdPix {
-  float T[kPix], Cr[kPix], Cg[kPix], Cb[kPix], D[kPix];  // T < 0: terminated (|T| final)
+  float2 T2[kPix / 2], Cr2[kPix / 2], Cg2[kPix / 2], Cb2[kPix / 2], D2[kPix / 2];  // T < 0: terminated (|T| final)
   int n[kPix];
+  __device__ __forceinline__ float& T(int b) { return (b & 1) ? T2[b >> 1].y : T2[b >> 1].x; }
+  __device__ __forceinline__ float& Cr(int b) { return (b & 1) ? Cr2[b >> 1].y : Cr2[b >> 1].x; }
+  __device__ __forceinline__ float& Cg(int b) { return (b & 1) ? Cg2[b >> 1].y : Cg2[b >> 1].x; }
+  __device__ __forceinline__ float& Cb(int b) { return (b & 1) ? Cb2[b >> 1].y : Cb2[b >> 1].x; }
+  __device__ __forceinline__ float& D(int b) { return (b & 1) ? D2[b >> 1].y : D2[b >> 1].x; }
+  __device__ __forceinline__ float Tc(int b) const { return (b & 1) ? T2[b >> 1].y : T2[b >> 1].x; }
 };
 
 // alpha of pixel b and the composite test "alpha >= 1/255 (and power <= 0)".
@@ -414,19 +432,75 @@ __device__ __forceinline__ void fwd_blend(FwdPix& px, int b, bool cond, float al
       "neg.f32 ta, ta;\n\t"
       "@pc selp.f32 %0, tn, ta, pcomp;\n\t"
       "}"
-      : "+f"(px.T[b]), "+f"(px.Cr[b]), "+f"(px.Cg[b]), "+f"(px.Cb[b]), "+f"(px.D[b]), "+r"(px.n[b]), "+r"(lm)
+      : "+f"(px.T(b)), "+f"(px.Cr(b)), "+f"(px.Cg(b)), "+f"(px.Cb(b)), "+f"(px.D(b)), "+r"(px.n[b]), "+r"(lm)
       : "r"((uint32_t)cond), "f"(al), "f"(r), "f"(g), "f"(bl), "f"(q0.z), "r"(pos1), "r"(1u << b));
 }
+
+#if GSR_FFMA2_FWD
+// fwd_blend for the pixel pair (2r, 2r + 1) on packed FP32 ops: the composited pixels
+// get w = alpha T, the others w = 0 (C + col x 0 == C exactly), so the colour / depth
+// accumulations need no predicate; per element the same fp32 operations as fwd_blend.
+__device__ __forceinline__ void fwd_blend2(FwdPix& px, int r, bool c0, bool c1, float al0, float al1, float z,
+                                           float cr, float cg, float cb, int pos1, uint32_t& lm) {
+  const float2 T = px.T2[r];
+  const float2 tn = __ffma2_rn(make_float2(-al0, -al1), T, T);
+  const bool k0 = c0 && tn.x >= kTStop, k1 = c1 && tn.y >= kTStop;
+  float a0z, a1z, t0, t1;
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %2, 0;\n\tselp.f32 %0, %1, 0f00000000, pk;\n\t}"
+      : "=f"(a0z) : "f"(al0), "r"((uint32_t)k0));
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %2, 0;\n\tselp.f32 %0, %1, 0f00000000, pk;\n\t}"
+      : "=f"(a1z) : "f"(al1), "r"((uint32_t)k1));
+  const float2 w = __fmul2_rn(make_float2(a0z, a1z), T);
+  px.Cr2[r] = __ffma2_rn(make_float2(cr, cr), w, px.Cr2[r]);
+  px.Cg2[r] = __ffma2_rn(make_float2(cg, cg), w, px.Cg2[r]);
+  px.Cb2[r] = __ffma2_rn(make_float2(cb, cb), w, px.Cb2[r]);
+  px.D2[r] = __ffma2_rn(make_float2(z, z), w, px.D2[r]);
+  // T := composited ? tn : (tested ? -|T| : T)
+  asm("{\n\t.reg .pred pc, pk;\n\t.reg .f32 ta;\n\t"
+      "setp.ne.u32 pc, %2, 0;\n\tsetp.ne.u32 pk, %3, 0;\n\t"
+      "abs.f32 ta, %1;\n\tneg.f32 ta, ta;\n\t"
+      "selp.f32 ta, %4, ta, pk;\n\t"
+      "selp.f32 %0, ta, %1, pc;\n\t}"
+      : "=f"(t0) : "f"(T.x), "r"((uint32_t)c0), "r"((uint32_t)k0), "f"(tn.x));
+  asm("{\n\t.reg .pred pc, pk;\n\t.reg .f32 ta;\n\t"
+      "setp.ne.u32 pc, %2, 0;\n\tsetp.ne.u32 pk, %3, 0;\n\t"
+      "abs.f32 ta, %1;\n\tneg.f32 ta, ta;\n\t"
+      "selp.f32 ta, %4, ta, pk;\n\t"
+      "selp.f32 %0, ta, %1, pc;\n\t}"
+      : "=f"(t1) : "f"(T.y), "r"((uint32_t)c1), "r"((uint32_t)k1), "f"(tn.y));
+  px.T2[r] = make_float2(t0, t1);
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %2, 0;\n\t@pk mov.b32 %0, %3;\n\t@pk or.b32 %1, %1, %4;\n\t}"
+      : "+r"(px.n[2 * r]), "+r"(lm) : "r"((uint32_t)k0), "r"(pos1), "r"(1u << (2 * r)));
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %2, 0;\n\t@pk mov.b32 %0, %3;\n\t@pk or.b32 %1, %1, %4;\n\t}"
+      : "+r"(px.n[2 * r + 1]), "+r"(lm) : "r"((uint32_t)k1), "r"(pos1), "r"(1u << (2 * r + 1)));
+}
+#endif
 
 template <bool kCap>
 __device__ __forceinline__ void fwd_dense(FwdPix& px, const Geo& g, const float4& q0, const float4& q1,
                                           const float4& q2, int pos1, uint32_t& lm) {
   float al[kPix];
   bool c[kPix];
+#if GSR_FFMA2_FWD
+  // p2 of both columns of a block row at once: fma(dy, fma(Ch, dy, b0_e), a0_e)
+  const float2 a0 = make_float2(g.a0[0], g.a0[1]), b0 = make_float2(g.b0[0], g.b0[1]);
+  const float2 ch = make_float2(q1.z, q1.z);
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r) {
+    const float2 dy = make_float2(g.dy[r], g.dy[r]);
+    const float2 p2 = __ffma2_rn(dy, __ffma2_rn(ch, dy, b0), a0);
+    c[2 * r] = fwd_alpha<kCap, false>(p2.x, q0.w, al[2 * r]);
+    c[2 * r + 1] = fwd_alpha<kCap, false>(p2.y, q0.w, al[2 * r + 1]);
+  }
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r)
+    fwd_blend2(px, r, c[2 * r], c[2 * r + 1], al[2 * r], al[2 * r + 1], q0.z, q1.w, q2.x, q2.y, pos1, lm);
+#else
 #pragma unroll
   for (int b = 0; b < kPix; ++b) c[b] = fwd_alpha<kCap, false>(geo_p2(g, q1.z, b), q0.w, al[b]);
 #pragma unroll
   for (int b = 0; b < kPix; ++b) fwd_blend(px, b, c[b], al[b], q0, q1.w, q2.x, q2.y, pos1, lm);
+#endif
 }
 
 template <bool kGen>
@@ -446,7 +520,7 @@ __device__ __forceinline__ void fwd_sparse(FwdPix& px, uint32_t m, const Geo& g,
 __device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
   uint32_t d = 0;
 #pragma unroll
-  for (int b = 0; b < kPix; ++b) d |= (__float_as_uint(px.T[b]) >> 31) << b;
+  for (int b = 0; b < kPix; ++b) d |= (__float_as_uint(px.Tc(b)) >> 31) << b;
   return __reduce_and_sync(kFull, d);
 }
 
@@ -475,8 +549,8 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
 #pragma unroll
   for (int b = 0; b < kPix; ++b) {
     const bool inside = ox + lx + 8 * (b & 1) < cam.W && oy + ly + 4 * (b >> 1) < cam.H;
-    px.T[b] = inside ? 1.f : -1.f;  // pixels outside the image start terminated
-    px.Cr[b] = px.Cg[b] = px.Cb[b] = px.D[b] = 0.f;
+    px.T(b) = inside ? 1.f : -1.f;  // pixels outside the image start terminated
+    px.Cr(b) = px.Cg(b) = px.Cb(b) = px.D(b) = 0.f;
     px.n[b] = 0;
   }
   uint32_t nblend = 0;
@@ -548,11 +622,11 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
     const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
     if (x < cam.W && y < cam.H) {
       const int64_t p = (int64_t)y * cam.W + x;
-      const float T = fabsf(px.T[b]);
-      out_rgb[p] = fmaf(T, cam.bg[0], px.Cr[b]);
-      out_rgb[npix + p] = fmaf(T, cam.bg[1], px.Cg[b]);
-      out_rgb[2 * npix + p] = fmaf(T, cam.bg[2], px.Cb[b]);
-      out_d[p] = px.D[b];
+      const float T = fabsf(px.T(b));
+      out_rgb[p] = fmaf(T, cam.bg[0], px.Cr(b));
+      out_rgb[npix + p] = fmaf(T, cam.bg[1], px.Cg(b));
+      out_rgb[2 * npix + p] = fmaf(T, cam.bg[2], px.Cb(b));
+      out_d[p] = px.D(b);
       out_T[p] = T;
       out_n[p] = px.n[b];
     }
@@ -564,13 +638,24 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
 }
 
 // ---------------------------------------------------------------------------
+// Pixel pairs (2r, 2r + 1) in float2 halves, as FwdPix.
 struct BwdPix {
-  float T[kPix], Q[kPix], gr[kPix], gg[kPix], gb[kPix], gd[kPix];
+  float2 T2[kPix / 2], Q2[kPix / 2], gr2[kPix / 2], gg2[kPix / 2], gb2[kPix / 2], gd2[kPix / 2];
   int n[kPix];
+  __device__ __forceinline__ float& T(int b) { return (b & 1) ? T2[b >> 1].y : T2[b >> 1].x; }
+  __device__ __forceinline__ float& Q(int b) { return (b & 1) ? Q2[b >> 1].y : Q2[b >> 1].x; }
+  __device__ __forceinline__ float& gr(int b) { return (b & 1) ? gr2[b >> 1].y : gr2[b >> 1].x; }
+  __device__ __forceinline__ float& gg(int b) { return (b & 1) ? gg2[b >> 1].y : gg2[b >> 1].x; }
+  __device__ __forceinline__ float& gb(int b) { return (b & 1) ? gb2[b >> 1].y : gb2[b >> 1].x; }
+  __device__ __forceinline__ float& gd(int b) { return (b & 1) ? gd2[b >> 1].y : gd2[b >> 1].x; }
 };
+// Lane partial sums over the key's pixels, per pixel column (x: lx, y: lx + 8):
+// colour / depth  sum g_ch w;  s0 = sum dp, s1 = sum dp dy, s2 = sum dp dy^2
+// (dp = dL/dpower).  The two columns are added before the warp reduction.
 struct BwdAcc {
-  float r, g, b, z;       // sum_pixels g_ch w
-  float s0[2], s1[2], s2;  // per column: sum dp, sum dp dy; sum dp dy^2  (dp = dL/dpower)
+  float r, g, b, z, s2;
+  float2 s0, s1;
+  __device__ __forceinline__ float& c(float2& v, int b) { return (b & 1) ? v.y : v.x; }
 };
 
 // One pixel's reverse step (alpha_k, T_{k+1} = T, suffix Q): dL/dalpha =
@@ -581,10 +666,10 @@ __device__ __forceinline__ void bwd_pixel(BwdPix& px, int b, bool valid, float r
   const float al = kCap ? fminf(raw, kAlphaCap) : raw;
   const float inv = rcp_approx(1.f - al);
   const float ai = al * inv;
-  const float T = px.T[b];
+  const float T = px.T(b);
   const float Tk = T * inv;
-  const float u = fmaf(px.gr[b], q1.w, fmaf(px.gg[b], q2.x, fmaf(px.gb[b], q2.y, px.gd[b] * q0.z)));
-  const float x = fmaf(T, u, -px.Q[b]);
+  const float u = fmaf(px.gr(b), q1.w, fmaf(px.gg(b), q2.x, fmaf(px.gb(b), q2.y, px.gd(b) * q0.z)));
+  const float x = fmaf(T, u, -px.Q(b));
   float dp = ai * x;
   if (kCap) dp = (raw > kAlphaCap) ? 0.f : dp;
   const float w = ai * T;
@@ -602,21 +687,91 @@ __device__ __forceinline__ void bwd_pixel(BwdPix& px, int b, bool valid, float r
       "@p fma.rn.f32 %7, %17, %18, %7;\n\t"
       "@p fma.rn.f32 %8, %17, %19, %8;\n\t"
       "}"
-      : "+f"(px.Q[b]), "+f"(px.T[b]), "+f"(a.r), "+f"(a.g), "+f"(a.b), "+f"(a.z), "+f"(a.s0[b & 1]),
-        "+f"(a.s1[b & 1]), "+f"(a.s2)
-      : "r"((uint32_t)valid), "f"(w), "f"(u), "f"(Tk), "f"(px.gr[b]), "f"(px.gg[b]), "f"(px.gb[b]), "f"(px.gd[b]),
+      : "+f"(px.Q(b)), "+f"(px.T(b)), "+f"(a.r), "+f"(a.g), "+f"(a.b), "+f"(a.z), "+f"(a.c(a.s0, b)),
+        "+f"(a.c(a.s1, b)), "+f"(a.s2)
+      : "r"((uint32_t)valid), "f"(w), "f"(u), "f"(Tk), "f"(px.gr(b)), "f"(px.gg(b)), "f"(px.gb(b)), "f"(px.gd(b)),
         "f"(dp), "f"(dy), "f"(dy2));
 }
+
+#if GSR_FFMA2
+__device__ __forceinline__ float sel0(bool p, float v) {  // p ? v : +0
+  float r;
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %2, 0;\n\tselp.f32 %0, %1, 0f00000000, pk;\n\t}"
+      : "=f"(r) : "f"(v), "r"((uint32_t)p));
+  return r;
+}
+__device__ __forceinline__ float selv(bool p, float v, float w) {  // p ? v : w
+  float r;
+  asm("{\n\t.reg .pred pk;\n\tsetp.ne.u32 pk, %3, 0;\n\tselp.f32 %0, %1, %2, pk;\n\t}"
+      : "=f"(r) : "f"(v), "f"(w), "r"((uint32_t)p));
+  return r;
+}
+// bwd_pixel for the pixel pair (2r, 2r + 1) on packed FP32 ops: a pixel that does not
+// take part gets ai = 0, hence dp = w = 0, and adds exact zeros to every sum; T keeps
+// its value by a select.  Per element the same fp32 operations as bwd_pixel.
+template <bool kCap>
+__device__ __forceinline__ void bwd_pixel2(BwdPix& px, int r, bool v0, bool v1, float raw0, float raw1, float dy,
+                                           float dy2, const float4& q0, const float4& q1, const float4& q2,
+                                           BwdAcc& a) {
+  const float2 al = kCap ? make_float2(fminf(raw0, kAlphaCap), fminf(raw1, kAlphaCap)) : make_float2(raw0, raw1);
+  const float2 om = __fadd2_rn(make_float2(1.f, 1.f), make_float2(-al.x, -al.y));
+  const float2 inv = make_float2(rcp_approx(om.x), rcp_approx(om.y));
+  float2 ai = __fmul2_rn(al, inv);
+  ai = make_float2(sel0(v0, ai.x), sel0(v1, ai.y));
+  const float2 T = px.T2[r];
+  const float2 Tk = __fmul2_rn(T, inv);
+  const float2 u = __ffma2_rn(px.gr2[r], make_float2(q1.w, q1.w),
+                              __ffma2_rn(px.gg2[r], make_float2(q2.x, q2.x),
+                                         __ffma2_rn(px.gb2[r], make_float2(q2.y, q2.y),
+                                                    __fmul2_rn(px.gd2[r], make_float2(q0.z, q0.z)))));
+  const float2 x = __ffma2_rn(T, u, make_float2(-px.Q2[r].x, -px.Q2[r].y));
+  float2 dp = __fmul2_rn(ai, x);
+  if (kCap) dp = make_float2(sel0(!(raw0 > kAlphaCap), dp.x), sel0(!(raw1 > kAlphaCap), dp.y));
+  const float2 w = __fmul2_rn(ai, T);
+  px.Q2[r] = __ffma2_rn(w, u, px.Q2[r]);
+  px.T2[r] = make_float2(selv(v0, Tk.x, T.x), selv(v1, Tk.y, T.y));
+  // the column-independent sums stay scalar (pixel 2r, then 2r + 1, as bwd_pixel):
+  // paired accumulators would cost 5 more registers in the register-capped kernel
+  a.r = fmaf(px.gr2[r].x, w.x, a.r);
+  a.g = fmaf(px.gg2[r].x, w.x, a.g);
+  a.b = fmaf(px.gb2[r].x, w.x, a.b);
+  a.z = fmaf(px.gd2[r].x, w.x, a.z);
+  a.s2 = fmaf(dp.x, dy2, a.s2);
+  a.r = fmaf(px.gr2[r].y, w.y, a.r);
+  a.g = fmaf(px.gg2[r].y, w.y, a.g);
+  a.b = fmaf(px.gb2[r].y, w.y, a.b);
+  a.z = fmaf(px.gd2[r].y, w.y, a.z);
+  a.s2 = fmaf(dp.y, dy2, a.s2);
+  a.s0 = __fadd2_rn(a.s0, dp);
+  a.s1 = __ffma2_rn(dp, make_float2(dy, dy), a.s1);
+}
+#endif
 
 template <bool kCap>
 __device__ __forceinline__ bool bwd_dense(BwdPix& px, int pos, const Geo& g, const float (&dy2)[4], const float4& q0,
                                           const float4& q1, const float4& q2, BwdAcc& a) {
   float raw[kPix];
+#if GSR_FFMA2
+  const float2 a0 = make_float2(g.a0[0], g.a0[1]), b0 = make_float2(g.b0[0], g.b0[1]);
+  const float2 ch = make_float2(q1.z, q1.z);
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r) {
+    const float2 dy = make_float2(g.dy[r], g.dy[r]);
+    const float2 p2 = __ffma2_rn(dy, __ffma2_rn(ch, dy, b0), a0);
+    raw[2 * r] = ex2_approx(p2.x);
+    raw[2 * r + 1] = ex2_approx(p2.y);
+  }
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r)
+    bwd_pixel2<kCap>(px, r, pos < px.n[2 * r] && raw[2 * r] >= kAlphaMin, pos < px.n[2 * r + 1] && raw[2 * r + 1] >= kAlphaMin,
+                     raw[2 * r], raw[2 * r + 1], g.dy[r], dy2[r], q0, q1, q2, a);
+#else
 #pragma unroll
   for (int b = 0; b < kPix; ++b) raw[b] = ex2_approx(geo_p2(g, q1.z, b));
 #pragma unroll
   for (int b = 0; b < kPix; ++b)
     bwd_pixel<kCap>(px, b, pos < px.n[b] && raw[b] >= kAlphaMin, raw[b], g.dy[b >> 1], dy2[b >> 1], q0, q1, q2, a);
+#endif
   return true;  // dense keys (>= 6 blocks composited in the forward) practically always contribute
 }
 
@@ -676,13 +831,13 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
     const int x = ox + lx + 8 * (b & 1), y = oy + ly + 4 * (b >> 1);
     if (x < cam.W && y < cam.H) {
       const int64_t p = (int64_t)y * cam.W + x;
-      px.T[b] = T_final[p];
+      px.T(b) = T_final[p];
       px.n[b] = n_contrib[p];
-      upstream(l1, g_rgb, g_dep, npix, p, px.gr[b], px.gg[b], px.gb[b], px.gd[b], lsum);
+      upstream(l1, g_rgb, g_dep, npix, p, px.gr(b), px.gg(b), px.gb(b), px.gd(b), lsum);
     } else {
-      px.T[b] = 1.f, px.n[b] = 0, px.gr[b] = px.gg[b] = px.gb[b] = px.gd[b] = 0.f;
+      px.T(b) = 1.f, px.n[b] = 0, px.gr(b) = px.gg(b) = px.gb(b) = px.gd(b) = 0.f;
     }
-    px.Q[b] = px.T[b] * (px.gr[b] * cam.bg[0] + px.gg[b] * cam.bg[1] + px.gb[b] * cam.bg[2]);
+    px.Q(b) = px.T(b) * (px.gr(b) * cam.bg[0] + px.gg(b) * cam.bg[1] + px.gb(b) * cam.bg[2]);
     bmaxn[b] = __reduce_max_sync(kFull, px.n[b]);
     maxn = max(maxn, bmaxn[b]);
   }
@@ -754,7 +909,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       for (int r = 0; r < 4; ++r) dy2[r] = g.dy[r] * g.dy[r];
       BwdAcc a;
       a.r = a.g = a.b = a.z = a.s2 = 0.f;
-      a.s0[0] = a.s0[1] = a.s1[0] = a.s1[1] = 0.f;
+      a.s0 = a.s1 = make_float2(0.f, 0.f);
       bool any;
       if (fl & kFlagGeneral)
         any = bwd_sparse<true>(px, m, pos, g, dy2, q0, q1, q2, a);
@@ -769,17 +924,17 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
         // dpower/dmu = -(A dx + B dy, B dx + C dy)
         const float A = q1.x * (1.f / kHalfL2e), B = q1.y * (1.f / kNegL2e), C = q1.z * (1.f / kHalfL2e);
         const float dx0 = g.dx[0], dx1 = g.dx[1];
-        const float sx = dx0 * a.s0[0] + dx1 * a.s0[1];
-        const float sxx = dx0 * dx0 * a.s0[0] + dx1 * dx1 * a.s0[1];
-        const float sy = a.s1[0] + a.s1[1];
-        const float sxy = dx0 * a.s1[0] + dx1 * a.s1[1];
+        const float sx = dx0 * a.s0.x + dx1 * a.s0.y;
+        const float sxx = dx0 * dx0 * a.s0.x + dx1 * dx1 * a.s0.y;
+        const float sy = a.s1.x + a.s1.y;
+        const float sxy = dx0 * a.s1.x + dx1 * a.s1.y;
         float v[10];
         v[0] = -(A * sx + B * sy);
         v[1] = -(B * sx + C * sy);
         v[2] = -0.5f * sxx;
         v[3] = -sxy;
         v[4] = -0.5f * a.s2;
-        v[5] = __fdividef(a.s0[0] + a.s0[1], q2.z);  // dalpha/do = exp(power) = alpha / o
+        v[5] = __fdividef(a.s0.x + a.s0.y, q2.z);  // dalpha/do = exp(power) = alpha / o
         v[6] = a.r;
         v[7] = a.g;
         v[8] = a.b;
