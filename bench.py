@@ -928,20 +928,32 @@ def stage_hbm(peaks, stage_ms, P, deg, V, K, NT):
 
 
 def roofline(dev, peaks, clk, stage_ms, blended_per_view, evaluated_per_view, traffic):
-    """Issue-bound roofline of the dominant kernel, k_render_bwd:
-    algorithmic FP32 ops = 8 per evaluated pair + 21 per blended pair, against the
-    FP32 issue peak SMs x 128 lanes x SM clock measured during the run."""
+    """Issue-bound roofline of the dominant kernel, k_render_bwd, on
+    SURVEY.md §8(d) row a5's algorithmic count: 70 lane-instructions per blended pair
+    (the row's 60-80 range, bounds reported as frac_range) + 15 per evaluated-but-skipped
+    pair, against the FP32-lane issue peak SMs x 128 lanes x SM clock measured during the
+    run.  The builder's narrower count (8 FP32 ops per evaluated + 21 per blended pair:
+    the arithmetic alone) is reported alongside as "arith"."""
     import torch
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     mhz = (clk or {}).get("sm_mhz") or peaks.get("sm_max_mhz") or 1965.0
     peak = sms * 128 * mhz * 1e6 / 1e12
-    ops = 8.0 * evaluated_per_view + 21.0 * blended_per_view
+    skipped = max(0.0, evaluated_per_view - blended_per_view)
     ms = stage_ms["render_bwd"]
-    achieved = ops / (ms / 1e3) / 1e12
-    return {"kernel": "k_render_bwd (gs_render_bwd_screen)", "bound": "alu", "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-            "algorithmic_ops_per_launch": ops, "launch_ms": ms,
+
+    def rate(per_blended):
+        return (per_blended * blended_per_view + 15.0 * skipped) / (ms / 1e3) / 1e12
+    ops = 70.0 * blended_per_view + 15.0 * skipped
+    achieved = rate(70.0)
+    arith_ops = 8.0 * evaluated_per_view + 21.0 * blended_per_view
+    arith = arith_ops / (ms / 1e3) / 1e12
+    return {"kernel": "k_render_bwd (gs_render_bwd_screen_l1)", "bound": "alu", "achieved": achieved, "peak": peak,
+            "unit": "T lane-instr/s", "frac": achieved / peak, "frac_range": [rate(60.0) / peak, rate(80.0) / peak],
+            "count": "SURVEY 8(d) a5: 70 (60-80) lane-instr per blended pair + 15 per skipped pair",
+            "traffic": traffic, "algorithmic_ops_per_launch": ops, "launch_ms": ms,
+            "arith": {"ops_per_launch": arith_ops, "achieved": arith, "frac": arith / peak,
+                      "count": "8 FP32 ops per evaluated pair + 21 per blended pair"},
             "peak_source": f"derived: {sms} SMs x 128 FP32 lanes x {mhz:.0f} MHz (SM clock sampled during the run)"}
 
 

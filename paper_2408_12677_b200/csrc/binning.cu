@@ -377,6 +377,10 @@ __global__ void __launch_bounds__(kEmThreads) k_emit(const uint32_t* __restrict_
 // K4: one onesweep LSD pass (8-bit digit at `shift`) over n = *n_ptr items
 // (n := 0 if n > cap).  Persistent CTAs pull 4096-item partitions in order.
 // ---------------------------------------------------------------------------
+#ifndef GSR_LB_WIN
+#define GSR_LB_WIN 16
+#endif
+constexpr int kLbWin = GSR_LB_WIN;
 template <typename KeyT, int ITEMS>
 __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                             KeyT* __restrict__ kout, uint32_t* __restrict__ vout,
@@ -393,12 +397,13 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restri
   int64_t n = (int64_t)*n_ptr;
   if (n > cap) n = 0;
   const int64_t num_parts = (n + TILE - 1) / TILE;
-  if (num_parts == 0) return;
+  // CTAs past the partition count (the grid is sized from P, the pass sorts V <= P
+  // items) leave before touching anything: ids are claimed in order, so the first
+  // num_parts CTAs take them all
+  if ((int64_t)blockIdx.x >= num_parts) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  {
-    uint32_t tot;
-    s_gpref[t] = block_excl_scan256<uint32_t>(ghist[t], s_scan, tot);
-  }
+  const uint32_t g_t = ghist[t];  // in flight with the claim and the key loads
+  bool first = true;
   const uint32_t lt = lanemask_lt();
   for (;;) {
     if (t == 0) s_part = atomicAdd(part_ctr, 1u);
@@ -408,11 +413,17 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restri
     const uint32_t part = s_part;
     if ((int64_t)part >= num_parts) break;
     const int64_t base = (int64_t)part * TILE + warp * (ITEMS * 32);
-    uint32_t key[ITEMS], rank[ITEMS];
+    uint32_t key[ITEMS], rank[ITEMS], val[ITEMS];
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {  // values with the keys: no load after the look-back
       const int64_t idx = base + i * 32 + lane;
       key[i] = idx < n ? (uint32_t)kin[idx] : 0u;
+      val[i] = idx < n ? vin[idx] : 0u;
+    }
+    if (first) {  // global digit offsets (exclusive scan of the pass histogram)
+      uint32_t tot;
+      s_gpref[t] = block_excl_scan256<uint32_t>(g_t, s_scan, tot);
+      first = false;
     }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -440,16 +451,18 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restri
     st_vol(lb, (part == 0 ? kLbInc : kLbAgg) | cnt);
     uint32_t tot;
     s_bexcl[t] = block_excl_scan256<uint32_t>(cnt, s_scan, tot);
-    // decoupled look-back over a window of 4 predecessors per round trip
+    // decoupled look-back over a window of kLbWin predecessors per round trip (the
+    // partitions publish their aggregates at about the same time, so a wide window
+    // cuts the round trips of the last partition from ~parts/4 to ~parts/16)
     uint32_t excl = 0;
     for (int64_t p = (int64_t)part - 1; p >= 0;) {
-      uint32_t v[4];
+      uint32_t v[kLbWin];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = (p - k >= 0) ? ld_vol(lookback + (p - k) * 256 + t) : kLbInc;
+      for (int k = 0; k < kLbWin; ++k) v[k] = (p - k >= 0) ? ld_vol(lookback + (p - k) * 256 + t) : kLbInc;
       int k = 0;
       bool done = false;
 #pragma unroll
-      for (; k < 4; ++k) {
+      for (; k < kLbWin; ++k) {
         const uint32_t f = v[k] >> 30;
         if (f == 0) break;
         excl += v[k] & kLbMask;
@@ -470,7 +483,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) k_onesweep(const KeyT* __restri
         const uint32_t d = (key[i] >> shift) & 255u;
         const uint32_t pos = s_bexcl[d] + s_whist[warp][d] + rank[i];
         s_keys[pos] = key[i];
-        s_vals[pos] = vin[base + i * 32 + lane];
+        s_vals[pos] = val[i];
       }
     }
     __syncthreads();

@@ -338,7 +338,7 @@ __device__ __forceinline__ void reduce_pair_commit(const float (&a)[5], const fl
 }
 
 // Staged record (3 x float4 in shared memory), rewritten in place by its lane:
-//   (mx, my, z, lo2) (Ah, Bh, Ch, r) (g, b, o, mask | flags)
+//   (mx, my, z, lo2) (Ah, Bh, Ch, r) (g, b, 1/o, mask | flags)
 // lo2 = log2(o), Ah = -log2(e)/2 A, Bh = -log2(e) B, Ch = -log2(e)/2 C, so that
 // log2(alpha) = lo2 + Ah dx^2 + Bh dx dy + Ch dy^2 = lo2 + log2(e) power.  Every value
 // is computed by one fixed instruction sequence, so the forward and the backward
@@ -354,7 +354,7 @@ __device__ __forceinline__ void stage_fast(float4* dst, int ox, int oy) {
   dst[0].w = lg2_approx(o);
   dst[1] = make_float4(__fmul_rn(kHalfL2e, A), __fmul_rn(kNegL2e, B), __fmul_rn(kHalfL2e, C), q1.w);
   float* q2 = reinterpret_cast<float*>(dst + 2);
-  q2[2] = o;
+  q2[2] = rcp_approx(o);  // the backward's dalpha/do = alpha / o (keys with o < 1/255 are never visited)
   q2[3] = __uint_as_float(fl);
 }
 
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
         v[2] = -0.5f * sxx;
         v[3] = -sxy;
         v[4] = -0.5f * a.s2;
-        v[5] = __fdividef(a.s0.x + a.s0.y, q2.z);  // dalpha/do = exp(power) = alpha / o
+        v[5] = (a.s0.x + a.s0.y) * q2.z;  // dalpha/do = exp(power) = alpha / o; q2.z = 1/o
         v[6] = a.r;
         v[7] = a.g;
         v[8] = a.b;
