@@ -93,8 +93,28 @@ __device__ __forceinline__ Act project_act(Fetch fetch) {
 
 // O3 and O4-O7 of one view.  act(): the Gaussian's Act, called only if z_c > z_near
 // (so a Gaussian behind every camera never evaluates its activations).
-template <class ActFn>
-__device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float py, float pz, ActFn act) {
+// Conservative frustum pre-cull of a Gaussian in front of the near plane, BEFORE its
+// activations (R9's IEEE chain and the double-precision exp / sigmoid): true only if
+// the exact chain is certain to cull it at O7's rectangle test.  The O7 radius is
+// rf = ceil(3 sqrt(lam)), lam the larger eigenvalue of T Sigma T^T + 0.3 I, and
+// lam <= ||T||_F^2 max_k s_k^2 + 0.3 = ||J||_F^2 exp(2 lmax) + 0.3 (T = J W, W a
+// rotation; Sigma = R S^2 R^T).  The bound is inflated (1% on each factor, +2 px) so
+// that the fast fp32 evaluation here can only over-estimate; the mean's position is
+// approximated to well under the 1 px slack.  A NaN anywhere fails every comparison
+// and leaves the Gaussian to the exact chain.  Bit-identical outputs.
+__device__ __forceinline__ bool precull(const DevCam& cam, float xc, float yc, float zc, float lmax) {
+  const float iz = __frcp_rn(zc);
+  const float ux = xc * iz, uy = yc * iz;
+  const float uxc = fminf(fmaxf(ux, -cam.limx), cam.limx), uyc = fminf(fmaxf(uy, -cam.limy), cam.limy);
+  const float jn2 = (cam.fx * cam.fx * fmaf(uxc, uxc, 1.f) + cam.fy * cam.fy * fmaf(uyc, uyc, 1.f)) * (iz * iz);
+  const float smax = __expf(fminf(lmax, 80.f)) * 1.01f;
+  const float R = fmaf(3.03f, sqrtf(fmaf(jn2 * 1.01f, smax * smax, 0.31f)), 2.f);
+  const float mx = fmaf(cam.fx, ux, cam.cx), my = fmaf(cam.fy, uy, cam.cy);
+  return (mx + R < -1.f) || (mx - R > (float)cam.W) || (my + R < -1.f) || (my - R > (float)cam.H);
+}
+
+template <class ActFn, class LmaxFn>
+__device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float py, float pz, ActFn act, LmaxFn lmax) {
   Geom g;
   // O3: p_c = W p + t  (Eq. 4)
   const float* W = cam.R;
@@ -105,6 +125,7 @@ __device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float 
   g.flags = GS_FLAG_CULLED;
   do {
     if (!(zc > cam.z_near)) break;  // R6, R23
+    if (precull(cam, xc, yc, zc, lmax())) break;
     const Act& A = act();
     if (!A.ok) break;
     const float (&Sig)[3][3] = A.Sig;
@@ -166,10 +187,13 @@ __device__ __forceinline__ Geom project_view(const DevCam& cam, float px, float 
 template <class Fetch>
 __device__ __forceinline__ Geom project_geom_one(const DevCam& cam, float px, float py, float pz, Fetch fetch) {
   Act a;
-  return project_view(cam, px, py, pz, [&]() -> const Act& {
-    a = project_act(fetch);
-    return a;
-  });
+  return project_view(
+      cam, px, py, pz,
+      [&]() -> const Act& {
+        a = project_act(fetch);
+        return a;
+      },
+      [&]() { return fmaxf(fmaxf(fetch(3), fetch(4)), fetch(5)); });
 }
 
 // ---------------------------------------------------------------------------
@@ -358,13 +382,16 @@ __global__ void __launch_bounds__(kPjThreads) k_project_views(const __grid_const
     Geom g;
     g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
     if (i < P)
-      g = project_view(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&]() -> const Act& {
-        if (!have_act) {
-          act = project_act([&](int row) { return s_geo[row][tid]; });
-          have_act = true;
-        }
-        return act;
-      });
+      g = project_view(
+          vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
+          [&]() -> const Act& {
+            if (!have_act) {
+              act = project_act([&](int row) { return s_geo[row][tid]; });
+              have_act = true;
+            }
+            return act;
+          },
+          [&]() { return fmaxf(fmaxf(s_geo[3][tid], s_geo[4][tid]), s_geo[5][tid]); });
     fl8 |= (uint64_t)g.flags << (8 * v);
     if (g.rad > 0) {
       any = true;
@@ -559,13 +586,16 @@ __global__ void __launch_bounds__(kPjThreads, 8) k_project_views2(const __grid_c
     Geom g;
     g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
     if (front)
-      g = project_view(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&]() -> const Act& {
-        if (!have_act) {
-          act = project_act([&](int row) { return s_geo[row][tid]; });
-          have_act = true;
-        }
-        return act;
-      });
+      g = project_view(
+          vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
+          [&]() -> const Act& {
+            if (!have_act) {
+              act = project_act([&](int row) { return s_geo[row][tid]; });
+              have_act = true;
+            }
+            return act;
+          },
+          [&]() { return fmaxf(fmaxf(s_geo[3][tid], s_geo[4][tid]), s_geo[5][tid]); });
     if (g.rad > 0) {
       float acc[3];
       sh_colour<DEG>(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid],
