@@ -477,6 +477,9 @@ __device__ __forceinline__ float cam_z(const DevCam& cam, float px, float py, fl
   return FA(FA(FA(FM(W[6], px), FM(W[7], py)), FM(W[8], pz)), cam.t[2]);
 }
 
+#ifndef GSR_PROJ_SPEC
+#define GSR_PROJ_SPEC 1
+#endif
 // ---------------------------------------------------------------------------
 // K1 v2 (default): as K1, with the bytes a view does not need left in HBM and twice
 // the Gaussians in flight per SM.
@@ -511,19 +514,32 @@ __global__ void __launch_bounds__(kPjThreads, 10) k_project2(DevCam cam, int64_t
     mbar_arrive_expect_tx(&bar[0], 3u * bytes);
 #pragma unroll 1
     for (int r = 0; r < 3; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[0]);
+#if GSR_PROJ_SPEC
+    // the 8 other rows speculatively in the same round trip (a CTA behind the camera
+    // moves 32 B per Gaussian it does not need, every other CTA saves a round trip)
+    mbar_arrive_expect_tx(&bar[1], 8u * bytes);
+#pragma unroll 1
+    for (int r = 3; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[1]);
+#endif
   }
   mbar_wait(&bar[0], 0);
   const int64_t i = i0 + tid;
   const bool front = i < P && cam_z(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid]) > cam.z_near;
   Geom g;
   g.rad = 0, g.ntiles = 0, g.flags = GS_FLAG_CULLED;
-  if (__syncthreads_or(front)) {
+  const bool any_front = __syncthreads_or(front);
+#if GSR_PROJ_SPEC
+  mbar_wait(&bar[1], 0);  // also when nothing is in front: no copy may outlive the CTA
+#endif
+  if (any_front) {
+#if !GSR_PROJ_SPEC
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar[1], 8u * bytes);
 #pragma unroll 1
       for (int r = 3; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[1]);
     }
     mbar_wait(&bar[1], 0);
+#endif
     if (front) g = project_geom_one(cam, s_geo[0][tid], s_geo[1][tid], s_geo[2][tid], [&](int row) { return s_geo[row][tid]; });
     if (g.rad > 0) {
       float acc[3];
