@@ -62,7 +62,7 @@ namespace {
 #define GSR_DEAD_EVERY 8  // forward: keys between re-checks of the blocks whose pixels all terminated
 #endif
 #ifndef GSR_DENSE_FWD
-#define GSR_DENSE_FWD 3
+#define GSR_DENSE_FWD 2
 #endif
 // Dense (branch-free) paths on packed FP32 pairs (FFMA2 / FMUL2, fma.rn.f32x2 etc.):
 // the two pixels of a lane in one block row (columns lx, lx + 8) share dy, so their
@@ -75,7 +75,7 @@ namespace {
 #define GSR_FFMA2_FWD GSR_FFMA2
 #endif
 #ifndef GSR_DENSE_BWD
-#define GSR_DENSE_BWD 6
+#define GSR_DENSE_BWD 5
 #endif
 [[maybe_unused]] constexpr int kDenseBlocks = GSR_DENSE_FWD;     // fwd: masks with >= this many 8x4 blocks take the branch-free path
 [[maybe_unused]] constexpr int kDenseBlocksBwd = GSR_DENSE_BWD;  // bwd: same (its per-block body is ~2x longer)

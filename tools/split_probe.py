@@ -54,3 +54,9 @@ for t in range(rg.shape[0]):
 print("iterations: current", cur_it, "split", split_it, f"ratio {split_it / max(cur_it, 1):.3f}")
 print("block evaluations (warp): current", cur_blocks, "(1 px/lane each); split", split_blocks,
       f"(2 px/lane each) ratio {2 * split_blocks / max(cur_blocks, 1):.3f}")
+# Gaussians that composited anything (a nonzero key mask) vs the projected-visible set
+ids = buf.sorted_ids[:K].long()
+hit = torch.zeros(model.P, dtype=torch.bool, device=dev)
+hit[ids[buf.key_blocks[:K] != 0]] = True
+nvis = int((buf.proj_t["radius"][:model.P] > 0).sum())
+print("gaussians visible", nvis, "hit (composited >= 1 pixel)", int(hit.sum()), "of P", model.P)
