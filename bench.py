@@ -36,7 +36,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-morton", action="store_true", help="keep the generated Gaussian order")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "4")),
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("GSR_STREAMS", "8")),
                     help="views in flight (one CUDA stream + buffer set each)")
     ap.add_argument("--graph", type=int, default=1, help="1: time CUDA-graph replays of whole iterations (N = 1)")
     ap.add_argument("--chunk", type=int, default=int(os.environ.get("GSR_CHUNK", "0")),
