@@ -697,13 +697,53 @@ class PeerShardedAdam:
         torch.cuda.synchronize(dev)
         self.hg.barrier(channel=0)
         self.device_step = False  # True: the step counter is model.step_dev (graph capture)
+        self._self_test()
+
+    def _launch(self, lr, step):
+        m = self.model
+        self.lib.adam_step_peers(m.desc, self.world, self.rank, self.gptrs, self.pptrs, m.m, m.v, lr, step,
+                                 self.begin, self.end)
 
     def step(self):
         m = self.model
         self.hg.barrier(channel=0)  # every rank's gradient is final
-        self.lib.adam_step_peers(m.desc, self.world, self.rank, self.gptrs, self.pptrs, m.m, m.v, m.lr,
-                                 m.step_dev if self.device_step else m.step_count, self.begin, self.end)
+        self._launch(m.lr, m.step_dev if self.device_step else m.step_count)
         self.hp.barrier(channel=1)  # every rank's parameter stores have landed
+
+    def _self_test(self):
+        """One exchange of a known gradient before the first real step: rank r's whole
+        gradient buffer holds r + 1, every learning rate is 0 (parameters unchanged), m
+        starts at 0, so after the kernel m on this rank's shard must equal
+        fp32(1 - beta1) x world (world + 1) / 2 exactly.  Catches a path that sums the
+        wrong terms on a machine where it has never run (the cross-rank parameter check
+        cannot: the owner of a shard writes it to every rank).  Raises RuntimeError on
+        any rank's mismatch; state is restored either way."""
+        import torch.distributed as dist
+        m = self.model
+        saved = (self.gbuf.clone(), m.m.clone(), m.v.clone())
+        try:
+            self.gbuf.fill_(float(self.rank + 1))
+            m.m.zero_()
+            m.v.zero_()
+            torch.cuda.synchronize()
+            self.hg.barrier(channel=0)
+            self._launch([0.0] * len(m.lr), 1)
+            self.hp.barrier(channel=1)
+            torch.cuda.synchronize()
+            f32 = torch.float32  # the kernel's fp32 ops: (1 - beta1) x g, g an exact small integer
+            expect = ((torch.tensor(1.0, dtype=f32) - torch.tensor(0.9, dtype=f32)) *
+                      torch.tensor(float(self.world * (self.world + 1) // 2), dtype=f32)).to(m.m.device)
+            got = m.m.reshape(-1)[self.begin:self.end]
+            ok = torch.tensor([1 if bool(torch.all(got == expect)) else 0], dtype=torch.int32, device=got.device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        finally:
+            self.gbuf.copy_(saved[0])
+            m.m.copy_(saved[1])
+            m.v.copy_(saved[2])
+            torch.cuda.synchronize()
+            self.hg.barrier(channel=0)
+        if int(ok.item()) != 1:
+            raise RuntimeError(f"{type(self).__name__}: exchange self-test failed (the summed gradient is wrong)")
 
 
 class NvlsShardedAdam(PeerShardedAdam):
@@ -722,13 +762,14 @@ class NvlsShardedAdam(PeerShardedAdam):
         if not mcg or not mcp:
             raise RuntimeError("symmetric memory has no multicast address (NVLS unavailable)")
         self.mc_grad, self.mc_param = mcg, mcp
+        self._self_test()  # again, now through the multicast kernel
 
-    def step(self):
+    def _launch(self, lr, step):
         m = self.model
-        self.hg.barrier(channel=0)  # every rank's gradient is final
-        self.lib.adam_step_multimem(m.desc, self.mc_grad, self.mc_param, self.pbuf, m.m, m.v, m.lr,
-                                    m.step_dev if self.device_step else m.step_count, self.begin, self.end)
-        self.hp.barrier(channel=1)  # every rank's parameter stores have landed
+        if not hasattr(self, "mc_grad"):  # during the base class's construction: the P2P kernel
+            return super()._launch(lr, step)
+        self.lib.adam_step_multimem(m.desc, self.mc_grad, self.mc_param, self.pbuf, m.m, m.v, lr, step,
+                                    self.begin, self.end)
 
 
 def params_agree_across_ranks(model: GaussianModel, group=None) -> bool:

@@ -809,6 +809,40 @@ def test_peer_sharded_adam_single_rank(lib):
         dist.destroy_process_group()
 
 
+def test_exchange_self_test_catches_a_wrong_sum(lib):
+    """PeerShardedAdam's construction-time self-test (a known gradient exchanged with zero
+    learning rates) rejects a path that sums the wrong terms -- here the kernel pointed
+    at a zero gradient buffer -- and leaves the model's state as it was."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=DEV)
+    try:
+        w = workload("small")
+        zero = torch.zeros(w.scene.params.size + 64, device=DEV)
+
+        class Broken(pipeline.PeerShardedAdam):
+            def _launch(self, lr, step):
+                m = self.model
+                self.lib.adam_step_peers(m.desc, self.world, self.rank, [zero.data_ptr()], self.pptrs, m.m, m.v, lr,
+                                         step, self.begin, self.end)
+        mb = pipeline.GaussianModel(w.scene, DEV)
+        mb.m.fill_(0.25)
+        p0 = mb.params.clone()
+        with pytest.raises(RuntimeError, match="self-test"):
+            Broken(lib, mb)
+        torch.cuda.synchronize()
+        assert torch.equal(mb.params, p0) and bool(torch.all(mb.m == 0.25))
+        pipeline.PeerShardedAdam(lib, pipeline.GaussianModel(w.scene, DEV))  # the real path passes
+    finally:
+        dist.destroy_process_group()
+
+
 def test_nvls_sharded_adam_single_rank(lib):
     """NvlsShardedAdam (gs_adam_step_multimem: multimem.ld_reduce of the gradient shard
     through the NVSwitch, Adam, multimem.st of the parameters; world size 1 on this GPU,
