@@ -778,13 +778,34 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        hs = None
+        # the graph-replayed iteration fed from the host (pipeline.HostStreamedGraphs) where a
+        # step's frames are a small share of it (scannetpp: 82 MB, e2e 5.87 vs 6.18 ms eager);
+        # with config 4's 885 MB of frames per step the eager ring (Trainer.step_host, copies
+        # spread over the step) measured faster (82 vs 91-93 ms, tools/e2e_diag2.py)
+        if use_graph and batched and h2d <= (256 << 20):
+            hs = pipeline.HostStreamedGraphs(tr, step_views(0), [host_t, host_t], scenegen.DEPTH_SCALE)
+            for _ in range(2):  # first replay of each parity's graphs (upload) outside the timing
+                hs.step()
+            torch.cuda.synchronize()
+            tr.blended.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
         s0.record(stream)
         for i in range(args.steps):
             sv = step_views(i)
-            tr.loss.zero_()
-            tr.step_host(sv, host_t, scenegen.DEPTH_SCALE)  # every view's frame: host -> device + decode
-            loss_host.copy_(tr.loss, non_blocking=True)
+            if hs is not None:
+                # frames copied + decoded under the previous step; loss read back on a side stream
+                hs.step(prefetch=i + 2 < args.steps)
+            else:
+                tr.loss.zero_()
+                tr.step_host(sv, host_t, scenegen.DEPTH_SCALE)  # every view's frame: host -> device + decode
+                loss_host.copy_(tr.loss, non_blocking=True)
         s1.record(stream)
+        if hs is not None:
+            stream.wait_stream(hs.readback_stream)  # the last loss has reached the host
+            s1.record(stream)
         torch.cuda.synchronize()
         ems = s0.elapsed_time(s1)
         eb = int(tr.blended.item())
@@ -798,7 +819,9 @@ def main():
         e2e = {"value": eb / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4,
                "iters_per_s": args.steps / (ems / 1000.0),
                "inputs": "per view an RGB-D sensor frame (uint8 [H][W][3] + uint16 mm [H][W]) from pinned host "
-                         "memory, copied and decoded (gs_decode_rgbd) inside the step; loss read back"}
+                         "memory, copied and decoded (gs_decode_rgbd) inside the step; loss read back",
+               "mode": ("CUDA graphs: per step a copy+decode graph on a copy stream and the iteration graph "
+                        "(pipeline.HostStreamedGraphs)" if hs is not None else "eager (Trainer.step_host)")}
 
     # --- K13: the straightforward per-pixel GPU port (north_star's >= 10x target), same
     # steps with gs_naive_render_fwd / gs_naive_render_bwd_screen, device-timed the same way

@@ -441,7 +441,7 @@ class Trainer:
         else:
             self.lib.adam_step(m.desc, m.params, m.grad, m.m, m.v, m.lr, m.step_count, zero_grad=False)
 
-    def capture(self, views):
+    def capture(self, views, targets_override=None):
         """One whole iteration over ``views`` (every view's project -> bin -> fwd -> L1 ->
         bwd on its stream, the projection backward, Adam) captured in a CUDA graph
         (the launch-bound configs run as one graph per iteration).
@@ -458,11 +458,11 @@ class Trainer:
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            self.step(views)  # one eager iteration on a side stream (lazy allocations)
+            self.step(views, targets_override)  # one eager iteration on a side stream (lazy allocations)
         torch.cuda.current_stream().wait_stream(side)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            self.step(views)
+            self.step(views, targets_override)
         m.step_count -= 1  # the captured iteration has not run yet
         self.hooks = hooks
         return g
@@ -503,6 +503,110 @@ def render_targets(lib, target_model: GaussianModel, cameras, device, key_capaci
 
 def default_capacity(K: int) -> int:
     return int(math.ceil(K * 1.3)) + 4096
+
+
+
+class HostStreamedGraphs:
+    """Graph-replayed iterations over a fixed view set, fed sensor frames from pinned
+    host memory (the end-to-end path of bench.py for the batched configs).  Two slot
+    sets alternate by step parity; per parity one CUDA graph copies every view's frame
+    (uint8 rgb [H][W][3] + 16-bit depth [H][W], R41) host -> device and
+    decodes it (gs_decode_rgbd) on a copy stream, and one graph runs the whole
+    iteration (Trainer.capture) reading that slot set.  Step i's compute waits only for
+    its own copies; the copies of step i + 2 start as soon as step i has consumed its
+    slots, so the frames' DMA runs under the previous step's rendering instead of ahead
+    of it.  host_frames[p] = {view: (rgb_u8, depth_u16)} pinned CPU tensors for parity p."""
+
+    def __init__(self, trainer, views, host_frames, depth_scale, copy_priority=None, graph_copies=False):
+        lib, dev = trainer.lib, trainer.device
+        self.trainer, self.views = trainer, list(views)
+        r0, d0 = host_frames[0][self.views[0]]
+        H, W = int(d0.shape[0]), int(d0.shape[1])
+        # highest priority: the decode kernels between the copies must not queue behind the
+        # render CTAs of the step they run under
+        self.copy_stream = torch.cuda.Stream(device=dev, priority=(torch.cuda.Stream.priority_range()[1]
+                                                                   if copy_priority is None else copy_priority))
+        self.slots = [{v: (torch.empty((3, H, W), dtype=torch.float32, device=dev),
+                           torch.empty((H, W), dtype=torch.float32, device=dev)) for v in self.views}
+                      for _ in range(2)]
+        self.raw = [{v: (torch.empty((H, W, 3), dtype=torch.uint8, device=dev),
+                         torch.empty((H, W), dtype=d0.dtype, device=dev)) for v in self.views} for _ in range(2)]
+        self.h2d_bytes = sum(host_frames[0][v][0].numel() * host_frames[0][v][0].element_size() +
+                             host_frames[0][v][1].numel() * host_frames[0][v][1].element_size() for v in self.views)
+
+        def copies(p):
+            for v in self.views:
+                r, d = host_frames[p][v]
+                self.raw[p][v][0].copy_(r, non_blocking=True)
+                self.raw[p][v][1].copy_(d, non_blocking=True)
+                lib.decode_rgbd(self.raw[p][v][0], self.raw[p][v][1], depth_scale, self.slots[p][v][0],
+                                self.slots[p][v][1])
+        # the copies are issued eagerly by default (copy-engine DMA); graph_copies=True
+        # captures them (measured slower for large frame volumes: config 4 moves 885 MB
+        # per step)
+        self._copies = copies
+        self.copy_graphs = []
+        cs = self.copy_stream
+        cs.wait_stream(torch.cuda.current_stream())
+        for p in range(2):
+            with torch.cuda.stream(cs):
+                copies(p)  # eager once: the slots hold valid targets for the capture below
+            if graph_copies:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cs):
+                    copies(p)
+                self.copy_graphs.append(g)
+        torch.cuda.current_stream().wait_stream(cs)
+        # per parity its own loss accumulator (baked into that parity's graph) and pinned
+        # host copy: the loss readback runs on its own stream and never holds the
+        # compute stream behind the copy engine's frame transfers
+        self.losses = [torch.zeros(1, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.loss_host = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.readback_stream = torch.cuda.Stream(device=dev)
+        saved_loss = trainer.loss
+        self.compute_graphs = []
+        for p in range(2):
+            trainer.loss = self.losses[p]
+            self.compute_graphs.append(trainer.capture(self.views, targets_override=self.slots[p]))
+        trainer.loss = saved_loss
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.computed = [torch.cuda.Event() for _ in range(2)]
+        self.read = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        for p in range(2):
+            self._copy(p)
+
+    def _copy(self, p):
+        cs = self.copy_stream
+        cs.wait_event(self.computed[p])  # the compute that last read slot set p
+        with torch.cuda.stream(cs):
+            if self.copy_graphs:
+                self.copy_graphs[p].replay()
+            else:
+                self._copies(p)
+        self.copied[p].record(cs)
+
+    def step(self, prefetch=True):
+        """One iteration: waits for its frames, replays the iteration, reads its loss back
+        to the host (self.loss_host[parity], a separate stream), then (prefetch) launches
+        the frame copies of the iteration after next into the slots it has just consumed.
+        Returns the parity whose loss_host entry this step fills."""
+        p = self.i % 2
+        main = torch.cuda.current_stream()
+        main.wait_event(self.copied[p])
+        main.wait_event(self.read[p])  # the readback of two steps ago has taken this loss
+        self.losses[p].zero_()
+        self.trainer.replay(self.compute_graphs[p])
+        self.computed[p].record(main)
+        rb = self.readback_stream
+        rb.wait_event(self.computed[p])
+        with torch.cuda.stream(rb):
+            self.loss_host[p].copy_(self.losses[p], non_blocking=True)
+        self.read[p].record(rb)
+        self.i += 1
+        if prefetch:
+            self._copy(p)
+        return p
 
 
 class KeyframeOptimizer:

@@ -107,3 +107,39 @@ def test_step_host_sensor_frames_match_decoded_targets(lib, streams):
     assert torch.equal(models[0].params, models[1].params)  # deterministic reduction: bit-identical
     with pytest.raises(ValueError):
         trs[1].step_host([0], host)  # sensor frames need depth_scale
+
+
+@pytest.mark.parametrize("graph_copies", [False, True])
+def test_host_streamed_graphs_match_step_host(lib, graph_copies):
+    """pipeline.HostStreamedGraphs (bench.py's e2e path for the batched configs: per step
+    parity a frame copy + decode on a copy stream and a captured iteration reading those
+    slots, the loss read back on a side stream) gives the iterations of Trainer.step on
+    the oracle-decoded targets bit for bit (deterministic reduction)."""
+    w = scenegen.make("small")
+    models = [pipeline.GaussianModel(w.scene, DEV) for _ in range(2)]
+    tgt_model = pipeline.GaussianModel(w.target_scene, DEV)
+    cams = [scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.03 * (k - 2)), [0.05 * k, 0.0, 0.0])
+            for k in range(4)]
+    cap = pipeline.default_capacity(pipeline.measure_keys(lib, models[0], cams, DEV))
+    rendered = pipeline.render_targets(lib, tgt_model, cams, DEV, cap)
+    host, targets = {}, []
+    for v, (r, d) in enumerate(rendered):
+        c8, d16 = scenegen.quantize_frame(r.cpu().numpy(), d.cpu().numpy())
+        host[v] = (torch.from_numpy(c8).pin_memory(), torch.from_numpy(d16.view(np.int16)).pin_memory())
+        o_rgb, o_d = frame.decode_rgbd(c8, d16, scenegen.DEPTH_SCALE)
+        targets.append((torch.from_numpy(o_rgb).to(DEV), torch.from_numpy(o_d).to(DEV)))
+    trs = [pipeline.Trainer(lib, m, cams, targets, DEV, cap, streams=2, deterministic=True) for m in models]
+    views = list(range(len(cams)))
+    hs = pipeline.HostStreamedGraphs(trs[1], views, [host, host], scenegen.DEPTH_SCALE, graph_copies=graph_copies)
+    trs[0].step(views)  # HostStreamedGraphs' two captures ran one eager iteration each
+    trs[0].step(views)
+    for it in range(4):
+        trs[0].loss.zero_()
+        trs[0].step(views)
+        p = hs.step(prefetch=it + 2 < 4)
+        torch.cuda.synchronize()
+        # (the loss sums warp partials by atomics in any order: equal to fp32 rounding)
+        assert hs.loss_host[p].item() == pytest.approx(trs[0].loss.item(), rel=1e-5)
+    assert models[0].step_count == models[1].step_count == 6
+    assert torch.equal(models[0].params, models[1].params)
+    assert torch.equal(models[0].m, models[1].m) and torch.equal(models[0].v, models[1].v)
