@@ -60,3 +60,8 @@ hit = torch.zeros(model.P, dtype=torch.bool, device=dev)
 hit[ids[buf.key_blocks[:K] != 0]] = True
 nvis = int((buf.proj_t["radius"][:model.P] > 0).sum())
 print("gaussians visible", nvis, "hit (composited >= 1 pixel)", int(hit.sum()), "of P", model.P)
+# tile list lengths (for per-tile sorting designs)
+lens = (rg[:, 1] - rg[:, 0]).astype(np.int64)
+q = np.percentile(lens, [50, 90, 99, 99.9, 100])
+print("tile list lengths: tiles", len(lens), "mean", lens.mean(), "p50/p90/p99/p99.9/max", q.tolist(),
+      "keys in tiles > 2048:", int(lens[lens > 2048].sum()), "> 4096:", int(lens[lens > 4096].sum()))
