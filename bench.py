@@ -20,6 +20,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# before the CUDA context exists: 32 hardware work queues for the ~18 streams of a step
+# (see paper_2408_12677_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "fwd+bwd+Adam iters/s and blended Gaussian-pixels/s, 1/2/4/8 B200"
 UNIT = "blended Gaussian-pixels/s"
@@ -779,11 +782,11 @@ def main():
         torch.cuda.synchronize()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         hs = None
-        # the graph-replayed iteration fed from the host (pipeline.HostStreamedGraphs) where a
-        # step's frames are a small share of it (scannetpp: 82 MB, e2e 5.87 vs 6.18 ms eager);
-        # with config 4's 885 MB of frames per step the eager ring (Trainer.step_host, copies
-        # spread over the step) measured faster (82 vs 91-93 ms, tools/e2e_diag2.py)
-        if use_graph and batched and h2d <= (256 << 20):
+        # the graph-replayed iteration fed from the host (pipeline.HostStreamedGraphs):
+        # scannetpp 82 MB of frames per step (e2e 5.87 vs 6.18 ms eager), config 4 885 MB
+        # (80.4 ms vs 82-84 eager, once CUDA_DEVICE_MAX_CONNECTIONS lifts the false
+        # serialisation of the copy stream with the render streams, tools/e2e_diag4.py)
+        if use_graph and batched:
             hs = pipeline.HostStreamedGraphs(tr, step_views(0), [host_t, host_t], scenegen.DEPTH_SCALE)
             for _ in range(2):  # first replay of each parity's graphs (upload) outside the timing
                 hs.step()
@@ -820,8 +823,8 @@ def main():
                "iters_per_s": args.steps / (ems / 1000.0),
                "inputs": "per view an RGB-D sensor frame (uint8 [H][W][3] + uint16 mm [H][W]) from pinned host "
                          "memory, copied and decoded (gs_decode_rgbd) inside the step; loss read back",
-               "mode": ("CUDA graphs: per step a copy+decode graph on a copy stream and the iteration graph "
-                        "(pipeline.HostStreamedGraphs)" if hs is not None else "eager (Trainer.step_host)")}
+               "mode": ("per step the frames copied + decoded on a high-priority copy stream under the "
+                        "previous step, then the iteration graph (pipeline.HostStreamedGraphs)" if hs is not None else "eager (Trainer.step_host)")}
 
     # --- K13: the straightforward per-pixel GPU port (north_star's >= 10x target), same
     # steps with gs_naive_render_fwd / gs_naive_render_bwd_screen, device-timed the same way
