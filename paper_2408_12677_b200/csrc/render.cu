@@ -59,10 +59,10 @@ namespace {
 #define GSR_BWD_PAIR 1
 #endif
 #ifndef GSR_DEAD_EVERY
-#define GSR_DEAD_EVERY 8  // forward: keys between re-checks of the blocks whose pixels all terminated
+#define GSR_DEAD_EVERY 16  // forward: keys between re-checks of the blocks whose pixels all terminated
 #endif
 #ifndef GSR_DENSE_FWD
-#define GSR_DENSE_FWD 2
+#define GSR_DENSE_FWD 1  // r02: 1 (every non-general key branch-free) -> fwd -3.5% at config 4 and scannetpp vs 2
 #endif
 // Dense (branch-free) paths on packed FP32 pairs (FFMA2 / FMUL2, fma.rn.f32x2 etc.):
 // the two pixels of a lane in one block row (columns lx, lx + 8) share dy, so their
