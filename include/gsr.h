@@ -265,7 +265,9 @@ gs_status gs_render_bwd(const gs_camera* cam /*HOST*/, const gs_scene* scene /*H
  *    pointers to float[P][12].  Each params row is read and each grad row updated once
  *    per call for up to 64 views (<= 8 views: unrolled per-view registers; more: the
  *    views in the inner loop of each Gaussian); every consumed sgrad entry is reset to
- *    zero.  accumulate != 0:
+ *    zero (floats 10-11 of the first view's records, unused by the render backward,
+ *    carry the wide pass's per-Gaussian visibility mask between its two kernels and
+ *    are zero again on return; the n_views buffers must be distinct).  accumulate != 0:
  *    grad += the batch's gradient; accumulate == 0: grad := the batch's gradient
  *    (every row of every Gaussian written, none read -- the first batch of an
  *    iteration, so that the optimiser need not zero grad). */

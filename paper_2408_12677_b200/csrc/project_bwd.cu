@@ -330,11 +330,27 @@ __global__ void __launch_bounds__(256, 2) k_project_bwd_geom(const __grid_consta
 // iteration's views (config 4: 64) are chained in one pass -- every parameter row
 // read and every gradient row written once per iteration instead of once per 8 views.
 // A thread first loads the flag byte of every view (all loads in flight at once) into
-// a visibility mask, then walks only its visible views, kWideGroup at a time with the
+// a visibility mask, then walks only its visible views, kWideGroup (geometry:
+// kWideGroupGeom) at a time with the
 // group's screen-gradient loads issued together: a Gaussian is seen by few of the
 // views, and no dependent load chain runs over all of them.
 // ---------------------------------------------------------------------------
-constexpr int kMaxWide = 64, kWideGroup = 4;
+#ifndef GSR_WIDE_VIS_HANDOFF
+#define GSR_WIDE_VIS_HANDOFF 1
+#endif
+#ifndef GSR_WIDE_GROUP
+#define GSR_WIDE_GROUP 2  // r02: 2 (was 4; config 4 chain 3.10 -> 2.86 ms with GEOM min blocks 6)
+#endif
+#ifndef GSR_WIDE_GROUP_GEOM
+#define GSR_WIDE_GROUP_GEOM GSR_WIDE_GROUP
+#endif
+#ifndef GSR_WIDE_MINB_COLOR
+#define GSR_WIDE_MINB_COLOR 4
+#endif
+#ifndef GSR_WIDE_MINB_GEOM
+#define GSR_WIDE_MINB_GEOM 6
+#endif
+constexpr int kMaxWide = 64, kWideGroup = GSR_WIDE_GROUP, kWideGroupGeom = GSR_WIDE_GROUP_GEOM;
 struct WideBatch {
   DevCam cam[kMaxWide];
   const uint8_t* flags[kMaxWide];
@@ -352,23 +368,30 @@ __device__ __forceinline__ uint64_t wide_visible(const WideBatch& vb, int64_t i)
   return vis;
 }
 
-// the next up-to-kWideGroup views of the mask (removed from it); -1 = none
-__device__ __forceinline__ void wide_take(uint64_t& vis, int (&vv)[kWideGroup]) {
+// the next up-to-G views of the mask (removed from it); -1 = none
+template <int G>
+__device__ __forceinline__ void wide_take(uint64_t& vis, int (&vv)[G]) {
 #pragma unroll
-  for (int j = 0; j < kWideGroup; ++j) {
+  for (int j = 0; j < G; ++j) {
     vv[j] = vis ? __ffsll((long long)vis) - 1 : -1;
     vis &= vis - 1;
   }
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(128, 4) k_project_bwd_color_wide(const __grid_constant__ WideBatch vb, int64_t P,
+__global__ void __launch_bounds__(128, GSR_WIDE_MINB_COLOR) k_project_bwd_color_wide(const __grid_constant__ WideBatch vb, int64_t P,
                                                                     int64_t S, const float* __restrict__ prm,
                                                                     float* __restrict__ grad, int accumulate) {
   constexpr int NK = (DEG + 1) * (DEG + 1);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
     uint64_t vis = wide_visible(vb, i);
+#if GSR_WIDE_VIS_HANDOFF
+    // hand the mask to the geometry kernel in the two spare floats (10, 11) of view 0's
+    // screen-gradient record (the render backward writes floats 0-9 only); the geometry
+    // kernel reads one 8-B word instead of 64 flag bytes and zeroes it again
+    *reinterpret_cast<uint64_t*>(vb.sgrad[0] + 12 * i + 10) = vis;
+#endif
     float acc[NK][3];  // the SH gradient rows, in registers across the views
     bool loaded = false;
     float gp0 = 0.f, gp1 = 0.f, gp2 = 0.f, px = 0.f, py = 0.f, pz = 0.f;
@@ -450,12 +473,18 @@ __global__ void __launch_bounds__(128, 4) k_project_bwd_color_wide(const __grid_
   }
 }
 
-__global__ void __launch_bounds__(128, 4) k_project_bwd_geom_wide(const __grid_constant__ WideBatch vb, int64_t P,
+__global__ void __launch_bounds__(128, GSR_WIDE_MINB_GEOM) k_project_bwd_geom_wide(const __grid_constant__ WideBatch vb, int64_t P,
                                                                    int64_t S, const float* __restrict__ prm,
                                                                    float* __restrict__ grad, int accumulate) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P; i += stride) {
+#if GSR_WIDE_VIS_HANDOFF
+    uint64_t* vslot = reinterpret_cast<uint64_t*>(vb.sgrad[0] + 12 * i + 10);
+    const uint64_t vis_all = *vslot;
+    if (!(vis_all & 1ull)) *vslot = 0ull;  // (view 0 visible: its whole record is cleared below)
+#else
     const uint64_t vis_all = wide_visible(vb, i);
+#endif
     uint64_t vis = vis_all;
     bool loaded = false;
     float px = 0.f, py = 0.f, pz = 0.f, iqn = 0.f, w = 0.f, x = 0.f, y = 0.f, z = 0.f;
@@ -464,14 +493,14 @@ __global__ void __launch_bounds__(128, 4) k_project_bwd_geom_wide(const __grid_c
     float gp[3] = {0.f, 0.f, 0.f};
     float gop = 0.f;
     while (vis) {
-      int vv[kWideGroup];
+      int vv[kWideGroupGeom];
       wide_take(vis, vv);
-      float4 g0[kWideGroup];
-      float2 g1[kWideGroup];
-      float gzz[kWideGroup];
-      uint32_t flv[kWideGroup];
+      float4 g0[kWideGroupGeom];
+      float2 g1[kWideGroupGeom];
+      float gzz[kWideGroupGeom];
+      uint32_t flv[kWideGroupGeom];
 #pragma unroll
-      for (int j = 0; j < kWideGroup; ++j) {  // the group's loads in flight together (clears after the loop)
+      for (int j = 0; j < kWideGroupGeom; ++j) {  // the group's loads in flight together (clears after the loop)
         g0[j] = make_float4(0.f, 0.f, 0.f, 0.f), g1[j] = make_float2(0.f, 0.f), gzz[j] = 0.f, flv[j] = 0;
         if (vv[j] >= 0) {
           const float4* sg4 = reinterpret_cast<const float4*>(vb.sgrad[vv[j]] + 12 * i);
@@ -482,7 +511,7 @@ __global__ void __launch_bounds__(128, 4) k_project_bwd_geom_wide(const __grid_c
         }
       }
 #pragma unroll
-      for (int j = 0; j < kWideGroup; ++j) {
+      for (int j = 0; j < kWideGroupGeom; ++j) {
         if (vv[j] < 0) continue;
         gop += g1[j].y;
         const float gmx = g0[j].x, gmy = g0[j].y, gA = g0[j].z, gB = g0[j].w, gC = g1[j].x, gz = gzz[j];
