@@ -59,7 +59,10 @@ namespace {
 #define GSR_BWD_PAIR 1
 #endif
 #ifndef GSR_DEAD_EVERY
-#define GSR_DEAD_EVERY 16  // forward: keys between re-checks of the blocks whose pixels all terminated
+#define GSR_DEAD_EVERY 0  // forward: keys between mid-batch re-checks of the blocks whose pixels all terminated (0: batch ends only; r02: 8 -> 16 -> 0)
+#endif
+#ifndef GSR_FWD_KB_SMEM
+#define GSR_FWD_KB_SMEM 0  // 1: the per-key block masks collected in shared memory (one STS per key; measured slower)
 #endif
 #ifndef GSR_DENSE_FWD
 #define GSR_DENSE_FWD 1  // r02: 1 (every non-general key branch-free) -> fwd -3.5% at config 4 and scannetpp vs 2
@@ -534,6 +537,9 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
                                                                    unsigned long long* blended,
                                                                    uint8_t* __restrict__ key_blocks) {
   __shared__ float4 s_rec[WPC][2][32][3];
+#if GSR_FWD_KB_SMEM
+  __shared__ uint8_t s_kb[WPC][32];  // the batch's key masks (key j's byte written by the whole warp)
+#endif
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wslot = blockIdx.x * WPC + warp;
   if (wslot >= cam.TX * cam.TY) return;
@@ -571,10 +577,16 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       stage_fast<true>(s_rec[warp][buf][lane], ox, oy);
       my_fl = __float_as_uint(reinterpret_cast<const float*>(&s_rec[warp][buf][lane][2])[3]);
     }
+#if GSR_FWD_KB_SMEM
+    s_kb[warp][lane] = 0;
+#endif
     __syncwarp();
     uint32_t live = __ballot_sync(kFull, (my_fl & ~bdone & 0xffu) != 0u);
+#if !GSR_FWD_KB_SMEM
     uint32_t kb_mine = 0;  // lane j: 8x4 blocks in which key b0 + j composited >= 1 pixel
-    int since = 0;
+#endif
+    [[maybe_unused]] int since = 0;
+    const int pos0 = b0 - rg.x + 1;  // 1-based position of the batch's key 0 in the tile's list
     while (live) {
       const int j = __ffs(live) - 1;
       live &= live - 1;
@@ -582,7 +594,7 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       const uint32_t fl = __float_as_uint(q2.w);
       const uint32_t m = fl & ~bdone & 0xffu;
       if (m == 0) continue;
-      const int pos1 = b0 + j - rg.x + 1;
+      const int pos1 = pos0 + j;
       const Geo g = make_geo(q0, q1, pxf0, pyf0);
       uint32_t lm = 0;  // this lane's composited pixels (bit b = block b) for this key
       if (fl & kFlagGeneral) {
@@ -604,14 +616,23 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
         nblend += GSR_COUNT_EVAL == 1 ? (dense ? 8u : (uint32_t)__popc(m)) : GSR_COUNT_EVAL == 2 ? 1u : (uint32_t)__popc(cm);
       }
 #endif
+#if GSR_FWD_KB_SMEM
+      s_kb[warp][j] = (uint8_t)cm;  // every lane stores the same (warp-uniform) byte: one STS, no lane test
+#else
       kb_mine = (lane == j) ? cm : kb_mine;
-      if (++since == GSR_DEAD_EVERY) {
+#endif
+      if (GSR_DEAD_EVERY > 0 && ++since == GSR_DEAD_EVERY) {
         since = 0;
         bdone = dead_blocks(px);
         if (bdone == 0xffu) break;
       }
     }
+#if GSR_FWD_KB_SMEM
+    __syncwarp();
+    if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = s_kb[warp][lane];
+#else
     if (key_blocks && b0 + lane < rg.y) key_blocks[b0 + lane] = (uint8_t)kb_mine;
+#endif
     bdone = dead_blocks(px);
     __syncwarp();
   }
