@@ -89,6 +89,10 @@ namespace {
 [[maybe_unused]] constexpr float kUncappedO = 0.9f;         // o <= this: alpha = o exp(power) < 0.99 (no cap)
 [[maybe_unused]] constexpr uint32_t kFlagGeneral = 1u << 8;  // conic not positive definite: keep the power > 0 test
 [[maybe_unused]] constexpr uint32_t kFlagCap = 1u << 9;      // o > kUncappedO: the 0.99 cap may bind
+[[maybe_unused]] constexpr int kGidShift = 10;                // backward, kPack: Gaussian id in bits 10-31
+#ifndef GSR_BWD_PACK
+#define GSR_BWD_PACK 1
+#endif
 [[maybe_unused]] constexpr float kHalfL2e = -0.5f * kLog2e;  // Ah = kHalfL2e A, Ch = kHalfL2e C
 [[maybe_unused]] constexpr float kNegL2e = -kLog2e;          // Bh = kNegL2e B
 
@@ -819,7 +823,11 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
 // kDet: deterministic mode (gs_bwd_opts.det_ws): each (tile, key) pair's reduced 10
 // components are stored to det[key][12] instead of atomically added (k_det_reduce sums
 // them per Gaussian in a fixed order).
-template <int WPC, bool kMasks, bool kDet>
+// kPack (product path, P < 2^22): each staged record carries its Gaussian id in bits
+// 10-31 of its flag word (the block-mask bits are unused with the forward's key
+// masks), so a key's id is one shift of a value already loaded instead of a shared-memory
+// read per key.
+template <int WPC, bool kMasks, bool kDet, bool kPack = false>
 __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
@@ -905,6 +913,8 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
     __syncwarp();
     if (lo + lane < hi && kb_cur) {
       stage_fast<!kMasks>(s_rec[warp][buf][lane], ox, oy);
+      if constexpr (kPack)
+        reinterpret_cast<uint32_t*>(&s_rec[warp][buf][lane][2])[3] |= (uint32_t)s_gid[warp][buf][lane] << kGidShift;
     }
     __syncwarp();
     uint32_t live = __ballot_sync(kFull, kb_cur != 0);
@@ -970,7 +980,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
 #if GSR_BWD_PAIR
           float h[5];
           reduce_half10(v, lane, h);
-          const int gid = s_gid[warp][buf][j];
+          const int gid = kPack ? (int)(fl >> kGidShift) : s_gid[warp][buf][j];
           if (gid_p >= 0) {
             reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
             gid_p = -1;
@@ -1367,7 +1377,15 @@ template <int WPC, bool kDet>
 void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order,
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                     const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1, float* det,
-                    int64_t det_keys) {
+                    int64_t det_keys, int64_t P) {
+  if constexpr (!kDet) {
+    if (GSR_BWD_PACK && key_blocks && P < (int64_t(1) << (32 - kGidShift))) {
+      k_render_bwd<WPC, true, false, true><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
+          cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
+          g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys);
+      return;
+    }
+  }
   if (key_blocks)
     k_render_bwd<WPC, true, kDet><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
         cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
@@ -1415,12 +1433,12 @@ void launch_render_bwd(const DevCam& cam, gs_proj proj, int64_t P, const int32_t
 #ifndef GSR_EXACT_EXP
   if (det) {  // deterministic mode: one warp per CTA
     launch_bwd_wpc<1, true>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1,
-                            det, det_keys);
+                            det, det_keys, P);
   } else {
     switch (render_wpc()) {
-      case 4: launch_bwd_wpc<4, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0); break;
-      case 2: launch_bwd_wpc<2, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0); break;
-      default: launch_bwd_wpc<1, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0);
+      case 4: launch_bwd_wpc<4, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0, P); break;
+      case 2: launch_bwd_wpc<2, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0, P); break;
+      default: launch_bwd_wpc<1, false>(cam, rec, ids, ranges, order, T_final, n_contrib, g_rgb, g_depth, key_blocks, sgrad, s, l1, nullptr, 0, P);
     }
   }
 #else

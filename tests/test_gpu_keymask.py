@@ -91,3 +91,44 @@ def test_keymask_semantics_small():
             assert kbn[s + pos] == want, (t, pos, kbn[s + pos], want)
             checked += 1
     assert checked > 1000
+
+
+def test_packed_gaussian_ids_match_unpacked():
+    """The product backward packs each staged record's Gaussian id into its flag word
+    when P < 2^22 (render.cu kPack) and reads it from shared memory otherwise.  The
+    small scene alone (packed) and the same scene followed by 2^22 culled Gaussians
+    (P >= 2^22: unpacked) have identical key lists, so their screen gradients agree
+    (up to the atomics' summation order) and every culled Gaussian's stays zero."""
+    lib = gsr.load()
+    w = scenegen.make("small")
+    cam, small = w.cameras[0], w.scene
+    P_big = (1 << 22) + 64
+    S_big = (P_big + 3) // 4 * 4
+    pb = np.zeros((small.F, S_big), np.float32)
+    pb[:, :small.P] = small.params[:, :small.P]
+    pb[:, small.P:P_big] = small.params[:, :1]  # copies of Gaussian 0 ...
+    pb[2, small.P:P_big] = -5.0  # ... behind the camera: culled, no keys
+    big = scenegen.Scene(P_big, small.sh_degree, pb)
+    sg = {}
+    for nm, scene in (("packed", small), ("unpacked", big)):
+        proj, t, params = gpu_project(lib, cam, scene)
+        b = gpu_bin(lib, cam, scene, proj)
+        H, W = cam.height, cam.width
+        sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+        rgb, dep, T = (torch.empty((3, H, W), device=DEV), torch.empty((H, W), device=DEV),
+                       torch.empty((H, W), device=DEV))
+        n = torch.empty((H, W), dtype=torch.int32, device=DEV)
+        kb = torch.zeros((max(b["K"], 1) + 16,), dtype=torch.uint8, device=DEV)
+        lib.render_fwd(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], rgb, dep, T, n, key_blocks=kb)
+        g_rgb, g_d = (torch.from_numpy(np.ascontiguousarray(a).astype(np.float32)).to(DEV)
+                      for a in scenegen.upstream_fields(5, W, H))
+        s = torch.zeros((scene.P, 12), device=DEV)
+        lib.render_bwd_screen(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], T, n, g_rgb, g_d, s,
+                              key_blocks=kb)
+        torch.cuda.synchronize()
+        sg[nm] = s.cpu().numpy()
+    a, c = sg["packed"], sg["unpacked"]
+    assert np.abs(a).max() > 0
+    assert not np.any(c[small.P:])
+    # north_star's gradient tolerance (float atomics reorder the sums)
+    np.testing.assert_allclose(c[:small.P], a, rtol=1e-3, atol=1e-6)
