@@ -77,6 +77,12 @@ namespace {
 #ifndef GSR_FFMA2_FWD
 #define GSR_FFMA2_FWD GSR_FFMA2
 #endif
+#ifndef GSR_FFMA2_GEO
+#define GSR_FFMA2_GEO GSR_FFMA2  // forward: the per-key column / row terms (make_geo) as packed pairs
+#endif
+#ifndef GSR_FFMA2_GEO_BWD
+#define GSR_FFMA2_GEO_BWD 0  // backward: measured slower (+24 B of spills in the register-capped kernel)
+#endif
 #ifndef GSR_DENSE_BWD
 #define GSR_DENSE_BWD 5
 #endif
@@ -371,10 +377,22 @@ __device__ __forceinline__ void stage_fast(float4* dst, int ox, int oy) {
 struct Geo {
   float dx[2], a0[2], b0[2], dy[4];
 };
+template <bool kPair>
 __device__ __forceinline__ Geo make_geo(const float4& q0, const float4& q1, float pxf0, float pyf0) {
   Geo g;
   g.dx[0] = __fsub_rn(q0.x, pxf0);
   g.dx[1] = __fsub_rn(g.dx[0], 8.f);
+  if constexpr (kPair) {
+  // the two columns' terms as packed pairs (per element the same IEEE operations)
+  const float2 dx = make_float2(g.dx[0], g.dx[1]);
+  const float2 a0 = __ffma2_rn(__fmul2_rn(make_float2(q1.x, q1.x), dx), dx, make_float2(q0.w, q0.w));
+  const float2 b0 = __fmul2_rn(make_float2(q1.y, q1.y), dx);
+  g.a0[0] = a0.x, g.a0[1] = a0.y, g.b0[0] = b0.x, g.b0[1] = b0.y;
+  g.dy[0] = __fsub_rn(q0.y, pyf0);
+  const float2 d12 = __fadd2_rn(make_float2(g.dy[0], g.dy[0]), make_float2(-4.f, -8.f));
+  g.dy[1] = d12.x, g.dy[2] = d12.y;
+  g.dy[3] = __fsub_rn(g.dy[0], 12.f);
+  } else {
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     g.a0[e] = __fmaf_rn(__fmul_rn(q1.x, g.dx[e]), g.dx[e], q0.w);
@@ -383,6 +401,7 @@ __device__ __forceinline__ Geo make_geo(const float4& q0, const float4& q1, floa
   g.dy[0] = __fsub_rn(q0.y, pyf0);
 #pragma unroll
   for (int r = 1; r < 4; ++r) g.dy[r] = __fsub_rn(g.dy[0], 4.f * r);
+  }
   return g;
 }
 __device__ __forceinline__ float geo_p2(const Geo& g, float Ch, int b) {
@@ -599,7 +618,7 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       const uint32_t m = fl & ~bdone & 0xffu;
       if (m == 0) continue;
       const int pos1 = pos0 + j;
-      const Geo g = make_geo(q0, q1, pxf0, pyf0);
+      const Geo g = make_geo<GSR_FFMA2_GEO>(q0, q1, pxf0, pyf0);
       uint32_t lm = 0;  // this lane's composited pixels (bit b = block b) for this key
       if (fl & kFlagGeneral) {
         fwd_sparse<true>(px, m, g, q0, q1, q2, pos1, lm);
@@ -934,10 +953,18 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
           if (pos >= bmaxn[b]) m &= ~(1u << b);
         if (m == 0) continue;
       }
-      const Geo g = make_geo(q0, q1, pxf0, pyf0);
+      const Geo g = make_geo<GSR_FFMA2_GEO_BWD>(q0, q1, pxf0, pyf0);
       float dy2[4];
+#if GSR_FFMA2_GEO_BWD
+      {
+        const float2 d01 = make_float2(g.dy[0], g.dy[1]), d23 = make_float2(g.dy[2], g.dy[3]);
+        const float2 s01 = __fmul2_rn(d01, d01), s23 = __fmul2_rn(d23, d23);
+        dy2[0] = s01.x, dy2[1] = s01.y, dy2[2] = s23.x, dy2[3] = s23.y;
+      }
+#else
 #pragma unroll
       for (int r = 0; r < 4; ++r) dy2[r] = g.dy[r] * g.dy[r];
+#endif
       BwdAcc a;
       a.r = a.g = a.b = a.z = a.s2 = 0.f;
       a.s0 = a.s1 = make_float2(0.f, 0.f);
