@@ -96,6 +96,9 @@ namespace {
 [[maybe_unused]] constexpr uint32_t kFlagGeneral = 1u << 8;  // conic not positive definite: keep the power > 0 test
 [[maybe_unused]] constexpr uint32_t kFlagCap = 1u << 9;      // o > kUncappedO: the 0.99 cap may bind
 [[maybe_unused]] constexpr int kGidShift = 10;                // backward, kPack: Gaussian id in bits 10-31
+#ifndef GSR_BWD_PAIR_INPLACE
+#define GSR_BWD_PAIR_INPLACE 1
+#endif
 #ifndef GSR_BWD_PACK
 #define GSR_BWD_PACK 1
 #endif
@@ -1005,9 +1008,21 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
           if (slot >= 0 && kpos < det_keys) det[(int64_t)GS_SGRAD_FLOATS * kpos + slot] = out;
         } else {
 #if GSR_BWD_PAIR
+          const int gid = kPack ? (int)(fl >> kGidShift) : s_gid[warp][buf][j];
+#if GSR_BWD_PAIR_INPLACE
+          // the pending key's first stage is reduced straight into h_p (no register copies)
+          if (gid_p >= 0) {
+            float h[5];
+            reduce_half10(v, lane, h);
+            reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
+            gid_p = -1;
+          } else {
+            reduce_half10(v, lane, h_p);
+            gid_p = gid;
+          }
+#else
           float h[5];
           reduce_half10(v, lane, h);
-          const int gid = kPack ? (int)(fl >> kGidShift) : s_gid[warp][buf][j];
           if (gid_p >= 0) {
             reduce_pair_commit(h_p, h, gid_p, gid, lane, sgrad);
             gid_p = -1;
@@ -1016,6 +1031,7 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
             for (int k = 0; k < 5; ++k) h_p[k] = h[k];
             gid_p = gid;
           }
+#endif
 #else
           float out;
           int slot;
