@@ -120,6 +120,21 @@ namespace {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// one MUFU.SQRT (relative error ~2^-22); only for the conservative block masks, whose
+// 1% quadratic margin and 0.01 px slack dwarf it -- never for a value the oracle checks
+[[maybe_unused]] __device__ __forceinline__ float sqrt_approx(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+#ifndef GSR_MASK_SQRT_APPROX
+#define GSR_MASK_SQRT_APPROX 1
+#endif
+#if GSR_MASK_SQRT_APPROX
+#define GSR_MASK_SQRT sqrt_approx
+#else
+#define GSR_MASK_SQRT sqrtf
+#endif
 
 // Support box of alpha >= 1/255: {d : 0.5 d^T Sigma_hat^{-1} d <= ln(255 o)} has
 // half-extents sqrt(2 L Sigma_hat_xx), sqrt(2 L Sigma_hat_yy).  Returns the 8-bit mask
@@ -185,7 +200,7 @@ namespace {
   if (!(det > 0.f) || !(A > 0.f) || !(C > 0.f)) return 0xffu;
   const float qmax = 2.f * fmaxf(L, 0.f) * 1.0201f + 1e-3f;  // (1.01)^2 margin, as block_mask
   const float idet = __fdividef(1.f, det), iA = __fdividef(1.f, A);
-  const float hx = sqrtf(qmax * C * idet), hy = sqrtf(qmax * A * idet);
+  const float hx = GSR_MASK_SQRT(qmax * C * idet), hy = GSR_MASK_SQRT(qmax * A * idet);
   if (!(hx < 1e6f) || !(hy < 1e6f)) return 0xffu;
   const float yR = -B * hx * __fdividef(1.f, C);  // y of the rightmost point; leftmost at -yR
   const float fx0 = (float)ox - 0.5f - mx, fy0 = (float)oy - 0.5f - my;
@@ -194,7 +209,7 @@ namespace {
 #pragma unroll
   for (int k = 0; k < 5; ++k) {
     const float y = fy0 + 4.f * k;
-    const float s = sqrtf(fmaxf(fmaf(-det, y * y, A * qmax), 0.f));
+    const float s = GSR_MASK_SQRT(fmaxf(fmaf(-det, y * y, A * qmax), 0.f));
     const bool in = fabsf(y) <= hy + kSlack;
     xr[k] = in ? (s - B * y) * iA : -3.4e38f;
     xl[k] = in ? (-s - B * y) * iA : 3.4e38f;
