@@ -638,7 +638,14 @@ def main():
                           streams=args.streams if batched else 1, optimizer=optimizer, chunk=chunk)
     stream = torch.cuda.current_stream()
 
-    # --- warm-up
+    # --- warm-up (and the render kernels' block-row walk chosen for this scene by timing
+    # both forms of a few views' render passes: gs_set_render_rows, same results)
+    render_tune = None
+    if batched and not args.profile and os.environ.get("GSR_RENDER_ROWS") is None:
+        tr.autotune_render(step_views(0))
+        render_tune = tr.render_tune
+    elif os.environ.get("GSR_RENDER_ROWS") is not None:
+        lib.set_render_rows(os.environ["GSR_RENDER_ROWS"] != "0")
     for i in range(args.warmup):
         tr.step(step_views(i))
     torch.cuda.synchronize()
@@ -918,6 +925,7 @@ def main():
                    "resolution": f"{cams[0].width}x{cams[0].height}", "parallelism": (f"views/dp{world}" + (f" ({optim_used} Adam)" if dist_on else "")) if batched else f"replicas x{world}",
                    "key_capacity": cap, "streams": args.streams if batched else 1, "chunk": chunk, "max_keys_per_view": kmax,
                    "gaussian_order": "generated" if args.no_morton else "morton",
+                   "render_rows": lib.render_rows(), "render_tune": render_tune,
                    "targets": "renders of the target scene quantised to RGB-D sensor frames (8-bit colour, 16-bit mm "
                               "depth) and decoded on the GPU",
                    "launch": "CUDA graph per iteration" if use_graph else "eager",

@@ -112,6 +112,15 @@ typedef struct {
 int gs_version(void);
 const char* gs_last_error(void);  /* thread-local text of the last failure ("" if none) */
 int64_t gs_launch_count(void);    /* kernels launched by this library (process-wide) */
+/* Performance switch of gs_render_fwd / gs_render_bwd_screen(_l1) (process-wide, read at
+ * each launch; results are identical either way, tests/test_gpu_keymask.py):
+ * 0 (default) = each key evaluates all four 8x4-block rows of its tile, straight-line;
+ * 1 = each key visits only the block rows its block mask touches (a warp-uniform branch
+ * per row): faster for scenes of small Gaussians (config 4: step 76.5 -> 73.6 ms), slower
+ * for large ones (scannetpp +2%).  pipeline.Trainer.autotune_render picks it per scene by
+ * timing both.  Only the default one-warp-per-CTA kernels have the row walk. */
+gs_status gs_set_render_rows(int enable);
+int gs_render_rows(void);
 int gs_exact_exp(void);           /* 1 in the GSR_EXACT_EXP debug build (libgsr_exact.so) */
 
 /* ---------------------------------------------------------------- gs_project

@@ -220,6 +220,12 @@ extern "C" {
 int gs_version(void) { return GSR_VERSION; }
 const char* gs_last_error(void) { return g_err; }
 int64_t gs_launch_count(void) { return (int64_t)g_launches.load(); }
+gs_status gs_set_render_rows(int enable) {
+  g_err[0] = 0;
+  gsr::set_render_rows(enable);
+  return GS_OK;
+}
+int gs_render_rows(void) { return gsr::render_rows(); }
 int gs_exact_exp(void) {
 #ifdef GSR_EXACT_EXP
   return 1;

@@ -112,6 +112,9 @@ size_t spatial_order_workspace_bytes(int64_t P);
 gs_status launch_spatial_order(int64_t F, int64_t P, int64_t S, const float* params_in, float* params_out,
                                int32_t* perm, void* ws, size_t ws_bytes, cudaStream_t s);
 // render.cu
+// performance switch of the render kernels (gs_set_render_rows): 1 = block-row walk
+void set_render_rows(int v);
+int render_rows();
 void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges,
                        const int32_t* order, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,

@@ -1,3 +1,4 @@
+#include <atomic>
 // K6 render_fwd and K7 render_bwd (Eq. 11; backward PAPER.md:147).
 //
 // Work decomposition (B200-first): one warp per 16x16 tile, split into
@@ -547,6 +548,29 @@ __device__ __forceinline__ void fwd_dense(FwdPix& px, const Geo& g, const float4
 #endif
 }
 
+#if GSR_FFMA2_FWD
+// fwd_dense restricted to the block rows the key's mask touches (bit 2r or 2r + 1 of m2 =
+// m | m >> 1): both pixels of a touched row as in fwd_dense, untouched rows skipped by a
+// warp-uniform branch.  Pixels of a touched row's other block lie outside the
+// conservative mask and fail the alpha test exactly as in fwd_dense: same results.
+template <bool kCap>
+__device__ __forceinline__ void fwd_rows(FwdPix& px, uint32_t m2, const Geo& g, const float4& q0, const float4& q1,
+                                         const float4& q2, int pos1, uint32_t& lm) {
+  const float2 a0 = make_float2(g.a0[0], g.a0[1]), b0 = make_float2(g.b0[0], g.b0[1]);
+  const float2 ch = make_float2(q1.z, q1.z);
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r) {
+    if (!((m2 >> (2 * r)) & 1u)) continue;
+    const float2 dy = make_float2(g.dy[r], g.dy[r]);
+    const float2 p2 = __ffma2_rn(dy, __ffma2_rn(ch, dy, b0), a0);
+    float al0, al1;
+    const bool c0 = fwd_alpha<kCap, false>(p2.x, q0.w, al0);
+    const bool c1 = fwd_alpha<kCap, false>(p2.y, q0.w, al1);
+    fwd_blend2(px, r, c0, c1, al0, al1, q0.z, q1.w, q2.x, q2.y, pos1, lm);
+  }
+}
+#endif
+
 template <bool kGen>
 __device__ __forceinline__ void fwd_sparse(FwdPix& px, uint32_t m, const Geo& g, const float4& q0, const float4& q1,
                                            const float4& q2, int pos1, uint32_t& lm) {
@@ -568,7 +592,9 @@ __device__ __forceinline__ uint32_t dead_blocks(const FwdPix& px) {
   return __reduce_and_sync(kFull, d);
 }
 
-template <int WPC>
+// kRows (gs_set_render_rows): every non-general key visits only the block rows its mask
+// touches (fwd_rows) instead of all four (fwd_dense); same results.
+template <int WPC, bool kRows = false>
 __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
@@ -641,6 +667,15 @@ __global__ void __launch_bounds__(WPC * 32, kFwdMinWarps / WPC) k_render_fwd(Dev
       if (fl & kFlagGeneral) {
         fwd_sparse<true>(px, m, g, q0, q1, q2, pos1, lm);
       } else if (__popc(m) >= kDenseBlocks) {
+#if GSR_FFMA2_FWD
+        if constexpr (kRows) {
+          const uint32_t m2 = m | (m >> 1);
+          if (fl & kFlagCap)
+            fwd_rows<true>(px, m2, g, q0, q1, q2, pos1, lm);
+          else
+            fwd_rows<false>(px, m2, g, q0, q1, q2, pos1, lm);
+        } else
+#endif
         if (fl & kFlagCap)
           fwd_dense<true>(px, g, q0, q1, q2, pos1, lm);
         else
@@ -837,6 +872,28 @@ __device__ __forceinline__ bool bwd_dense(BwdPix& px, int pos, const Geo& g, con
   return true;  // dense keys (>= 6 blocks composited in the forward) practically always contribute
 }
 
+#if GSR_FFMA2
+// bwd_dense restricted to the block rows the key's mask touches (as fwd_rows): a pixel of
+// an untouched block of a touched row is invalid (the forward composited the key in no
+// pixel of that block) and adds exact zeros, in the same ascending pixel order as
+// bwd_sparse's per-block walk.
+template <bool kCap>
+__device__ __forceinline__ void bwd_rows(BwdPix& px, uint32_t m2, int pos, const Geo& g, const float (&dy2)[4],
+                                         const float4& q0, const float4& q1, const float4& q2, BwdAcc& a) {
+  const float2 a0 = make_float2(g.a0[0], g.a0[1]), b0 = make_float2(g.b0[0], g.b0[1]);
+  const float2 ch = make_float2(q1.z, q1.z);
+#pragma unroll
+  for (int r = 0; r < kPix / 2; ++r) {
+    if (!((m2 >> (2 * r)) & 1u)) continue;
+    const float2 dy = make_float2(g.dy[r], g.dy[r]);
+    const float2 p2 = __ffma2_rn(dy, __ffma2_rn(ch, dy, b0), a0);
+    const float raw0 = ex2_approx(p2.x), raw1 = ex2_approx(p2.y);
+    bwd_pixel2<kCap>(px, r, pos < px.n[2 * r] && raw0 >= kAlphaMin, pos < px.n[2 * r + 1] && raw1 >= kAlphaMin, raw0,
+                     raw1, g.dy[r], dy2[r], q0, q1, q2, a);
+  }
+}
+#endif
+
 template <bool kGen>
 __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, const Geo& g, const float (&dy2)[4],
                                            const float4& q0, const float4& q1, const float4& q2, BwdAcc& a) {
@@ -864,7 +921,8 @@ __device__ __forceinline__ bool bwd_sparse(BwdPix& px, uint32_t m, int pos, cons
 // 10-31 of its flag word (the block-mask bits are unused with the forward's key
 // masks), so a key's id is one shift of a value already loaded instead of a shared-memory
 // read per key.
-template <int WPC, bool kMasks, bool kDet, bool kPack = false>
+// kRows (with the forward's key masks): every non-general key through bwd_rows.
+template <int WPC, bool kMasks, bool kDet, bool kPack = false, bool kRows = false>
 __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(DevCam cam, const float4* __restrict__ rec,
                                                                    const int32_t* __restrict__ ids,
                                                                    const int2* __restrict__ ranges, const int32_t* __restrict__ order,
@@ -989,6 +1047,16 @@ __global__ void __launch_bounds__(WPC * 32, kBwdMinWarps / WPC) k_render_bwd(Dev
       bool any;
       if (fl & kFlagGeneral)
         any = bwd_sparse<true>(px, m, pos, g, dy2, q0, q1, q2, a);
+#if GSR_FFMA2
+      else if (kRows && kMasks) {  // the forward composited this key in >= 1 pixel: some pixel is valid
+        const uint32_t m2 = m | (m >> 1);
+        if (fl & kFlagCap)
+          bwd_rows<true>(px, m2, pos, g, dy2, q0, q1, q2, a);
+        else
+          bwd_rows<false>(px, m2, pos, g, dy2, q0, q1, q2, a);
+        any = true;
+      }
+#endif
       else if (__popc(m) >= kDenseBlocksBwd)
         any = (fl & kFlagCap) ? bwd_dense<true>(px, pos, g, dy2, q0, q1, q2, a)
                               : bwd_dense<false>(px, pos, g, dy2, q0, q1, q2, a);
@@ -1409,6 +1477,9 @@ __global__ void __launch_bounds__(256) k_det_reduce(DevCam cam, const float4* __
   for (int k = 0; k < 10; ++k) o[k] += acc[k];
 }
 
+// gs_set_render_rows (process-wide, performance only: both settings give the same results)
+std::atomic<int> g_render_rows{0};
+
 #ifndef GSR_EXACT_EXP
 // Warps (= tiles) per CTA of the fast kernels.  Tile work is very uneven (list lengths
 // and early termination), and a CTA's slot is held until its slowest warp ends, so
@@ -1427,6 +1498,14 @@ template <int WPC>
 void launch_fwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order, float* rgb,
                     float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,
                     uint8_t* key_blocks, cudaStream_t s) {
+  if constexpr (WPC == 1) {
+    if (g_render_rows.load(std::memory_order_relaxed)) {
+      k_render_fwd<1, true><<<cam.TX * cam.TY, 32, 0, s>>>(
+          cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, rgb, depth,
+          T_final, n_contrib, blended, key_blocks);
+      return;
+    }
+  }
   k_render_fwd<WPC><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
       cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, rgb, depth, T_final,
       n_contrib, blended, key_blocks);
@@ -1436,14 +1515,24 @@ void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, con
                     const float* T_final, const int32_t* n_contrib, const float* g_rgb, const float* g_depth,
                     const uint8_t* key_blocks, float* sgrad, cudaStream_t s, const L1Fuse& l1, float* det,
                     int64_t det_keys, int64_t P) {
+#define GSR_BWD_ARGS                                                                                              \
+  cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib, \
+      g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys
+  const bool rows = WPC == 1 && key_blocks && g_render_rows.load(std::memory_order_relaxed);
   if constexpr (!kDet) {
     if (GSR_BWD_PACK && key_blocks && P < (int64_t(1) << (32 - kGidShift))) {
-      k_render_bwd<WPC, true, false, true><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
-          cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
-          g_rgb, g_depth, key_blocks, sgrad, l1, det, det_keys);
+      if (rows)
+        k_render_bwd<1, true, false, true, true><<<cam.TX * cam.TY, 32, 0, s>>>(GSR_BWD_ARGS);
+      else
+        k_render_bwd<WPC, true, false, true><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(GSR_BWD_ARGS);
       return;
     }
   }
+  if (rows) {
+    k_render_bwd<1, true, kDet, false, true><<<cam.TX * cam.TY, 32, 0, s>>>(GSR_BWD_ARGS);
+    return;
+  }
+#undef GSR_BWD_ARGS
   if (key_blocks)
     k_render_bwd<WPC, true, kDet><<<ceil_div(cam.TX * cam.TY, WPC), WPC * 32, 0, s>>>(
         cam, reinterpret_cast<const float4*>(rec), ids, reinterpret_cast<const int2*>(ranges), order, T_final, n_contrib,
@@ -1456,6 +1545,9 @@ void launch_bwd_wpc(const DevCam& cam, const float* rec, const int32_t* ids, con
 #endif
 
 }  // namespace
+
+void set_render_rows(int v) { g_render_rows.store(v ? 1 : 0); }
+int render_rows() { return g_render_rows.load(); }
 
 void launch_render_fwd(const DevCam& cam, const float* rec, const int32_t* ids, const int32_t* ranges, const int32_t* order, float* rgb,
                        float* depth, float* T_final, int32_t* n_contrib, unsigned long long* blended,

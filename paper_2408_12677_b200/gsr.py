@@ -136,6 +136,9 @@ class Library:
         lib.gs_last_error.restype = C.c_char_p
         lib.gs_launch_count.restype = i64
         lib.gs_exact_exp.restype = C.c_int
+        lib.gs_set_render_rows.argtypes = [C.c_int]
+        lib.gs_set_render_rows.restype = C.c_int
+        lib.gs_render_rows.restype = C.c_int
         lib.gs_project.argtypes = [vp, vp, vp, GsProj, vp]
         lib.gs_bin_tiles_workspace.argtypes = [vp, i64, i64]
         lib.gs_bin_tiles_workspace.restype = C.c_size_t
@@ -194,6 +197,13 @@ class Library:
     # -- diagnostics ------------------------------------------------------
     def launch_count(self) -> int:
         return int(self.lib.gs_launch_count())
+
+    # -- performance switch (results identical either way) -----------------
+    def set_render_rows(self, enable: bool):
+        return self._check("gs_set_render_rows", self.lib.gs_set_render_rows(1 if enable else 0))
+
+    def render_rows(self) -> bool:
+        return bool(self.lib.gs_render_rows())
 
     def last_error(self) -> str:
         return self.lib.gs_last_error().decode()

@@ -292,6 +292,42 @@ class Trainer:
                                   det=b.det)
         self._hook("render_bwd", "end")
 
+    def autotune_render(self, views=None, reps=3):
+        """Choose the render kernels' block-row walk (gs_set_render_rows; results are
+        identical either way) for this scene: times gs_render_fwd + the backward of up
+        to 4 views with each setting (best of ``reps``, CUDA events on the current
+        stream) and keeps the faster.  Nothing is updated: the screen gradients, loss
+        and blended counter the timing runs write are cleared.  Returns the setting."""
+        lib, b = self.lib, self.buf
+        views = list(views if views is not None else range(len(self.cameras)))[:4]
+        stream = torch.cuda.current_stream()
+        best = {}
+        for mode in (0, 1):
+            lib.set_render_rows(mode)
+            t = []
+            for _ in range(reps + 1):  # the first pass warms up
+                ms = 0.0
+                for v in views:
+                    gcam, proj, order = self._bin_view(v, 0, b)
+                    tr = (self.targets[v] if self.targets is not None and self.targets[v] is not None
+                          else (b.rgb, b.depth))
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    self._render_view(v, 0, b, gcam, proj, order, tr[0], tr[1], None, None)
+                    e1.record(stream)
+                    e1.synchronize()
+                    ms += e0.elapsed_time(e1)
+                t.append(ms)
+            best[mode] = min(t[1:])
+        self.sgrad[0].zero_()
+        self.loss.zero_()
+        self.blended.zero_()
+        mode = 1 if best[1] < best[0] else 0
+        lib.set_render_rows(mode)
+        self.render_tune = {"rows": mode, "ms_dense": best[0], "ms_rows": best[1], "views": views}
+        torch.cuda.synchronize()
+        return mode
+
     def step(self, views, targets_override=None):
         """One iteration over ``views``; targets_override: {v: (rgb, depth)} device tensors."""
         def targets(k, v):

@@ -123,3 +123,15 @@ def test_state_mismatch_detected_on_host(libs):
     st2 = lib.lib.gs_naive_render_bwd_screen(C.byref(cam), C.byref(sc), proj, A[4], A[5], A[6], A[7], A[4], None,
                                              A[5], C.byref(o2), None)
     assert st2 == gsr.GS_ERR_ARG and "deterministic" in lib.last_error()
+
+
+def test_render_rows_switch_host_only(libs):
+    """gs_set_render_rows / gs_render_rows: a host-side, process-wide switch (no GPU)."""
+    for lib in libs:
+        was = lib.render_rows()
+        try:
+            for v in (1, 0, 7):
+                lib.set_render_rows(v)
+                assert lib.render_rows() == bool(v)
+        finally:
+            lib.set_render_rows(was)

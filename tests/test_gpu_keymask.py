@@ -132,3 +132,45 @@ def test_packed_gaussian_ids_match_unpacked():
     assert not np.any(c[small.P:])
     # north_star's gradient tolerance (float atomics reorder the sums)
     np.testing.assert_allclose(c[:small.P], a, rtol=1e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("name", ["small", "large"])
+def test_render_rows_walk_identical(name):
+    """gs_set_render_rows is a performance switch only: the forward (images, T, n_contrib,
+    key masks) and, in deterministic-reduction mode, the backward's screen gradients are
+    bit-identical with and without the block-row walk (large: config 4's small
+    Gaussians, first view at full size)."""
+    lib = gsr.load()
+    kw = {"num_views": 1} if name == "large" else {}
+    w = scenegen.make(name, **kw)
+    cam, scene = w.cameras[0], w.scene
+    proj, t, params = gpu_project(lib, cam, scene)
+    b = gpu_bin(lib, cam, scene, proj)
+    H, W = cam.height, cam.width
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    g_rgb, g_d = (torch.from_numpy(np.ascontiguousarray(a).astype(np.float32)).to(DEV)
+                  for a in scenegen.upstream_fields(9, W, H))
+    out = {}
+    was = lib.render_rows()
+    try:
+        for mode in (0, 1):
+            lib.set_render_rows(mode)
+            assert lib.render_rows() == bool(mode)
+            rgb, dep, T = (torch.empty((3, H, W), device=DEV), torch.empty((H, W), device=DEV),
+                           torch.empty((H, W), device=DEV))
+            n = torch.empty((H, W), dtype=torch.int32, device=DEV)
+            kb = torch.zeros((max(b["K"], 1) + 16,), dtype=torch.uint8, device=DEV)
+            lib.render_fwd(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], rgb, dep, T, n, key_blocks=kb)
+            s = torch.zeros((scene.P, 12), device=DEV)
+            det = torch.empty((b["K"] + 16, 12), device=DEV)
+            lib.render_bwd_screen(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], T, n, g_rgb, g_d, s,
+                                  key_blocks=kb, det=det)
+            torch.cuda.synchronize()
+            out[mode] = [x.cpu().numpy() for x in (rgb, dep, T, n, kb, s)]
+    finally:
+        lib.set_render_rows(was)
+    for k, nm in enumerate(["rgb", "depth", "T", "n_contrib", "key_blocks", "sgrad (deterministic)"]):
+        assert np.array_equal(out[0][k], out[1][k]), nm
+    assert np.abs(out[0][5]).max() > 0
+    # (the atomic form differs from run to run by summation order alone; its parity
+    # with the oracle is test_gpu_parity's, whichever form the bench's autotune picks)

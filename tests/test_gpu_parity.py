@@ -362,8 +362,8 @@ def test_l1_parity(lib):
     assert np.isfinite(loss.item())
 
 
-@pytest.mark.parametrize("name", ["replica", "scannetpp", "large"])
-def test_product_chain_full_size_sampled(lib, name):
+@pytest.mark.parametrize("name,rows", [("replica", 0), ("scannetpp", 0), ("large", 0), ("large", 1)])
+def test_product_chain_full_size_sampled(lib, name, rows):
     """The product backward at full size, element by element: the GPU chain project ->
     bin -> render_fwd with key masks -> gs_render_bwd_screen_l1 (fused Eq. 12, the
     Trainer's kernel) -> gs_project_bwd_views, against the STAGE oracle with running
@@ -372,7 +372,17 @@ def test_product_chain_full_size_sampled(lib, name):
     no gradient.  In the sampled tiles the targets are the ORACLE's fp32 render offset by
     +-0.02 (colour) and +-(0.01 + 1%) (depth) with random signs, so the residual signs
     -- hence the upstream gradient -- are fixed by oracle-side data alone (the GPU
-    render is within 1e-5 of the oracle's)."""
+    render is within 1e-5 of the oracle's).  rows=1: with the render kernels' block-row
+    walk (gs_set_render_rows), the form the bench's autotune picks for config 4."""
+    was = lib.render_rows()
+    lib.set_render_rows(rows)
+    try:
+        _product_chain_full_size_sampled(lib, name)
+    finally:
+        lib.set_render_rows(was)
+
+
+def _product_chain_full_size_sampled(lib, name):
     w = workload(name)
     cam, scene = w.cameras[0], w.scene
     H, W, npix = cam.height, cam.width, cam.height * cam.width
