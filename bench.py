@@ -641,7 +641,7 @@ def main():
     # --- warm-up (and the render kernels' block-row walk chosen for this scene by timing
     # both forms of a few views' render passes: gs_set_render_rows, same results)
     render_tune = None
-    if batched and not args.profile and os.environ.get("GSR_RENDER_ROWS") is None:
+    if not args.profile and os.environ.get("GSR_RENDER_ROWS") is None:
         tr.autotune_render(step_views(0))
         render_tune = tr.render_tune
     elif os.environ.get("GSR_RENDER_ROWS") is not None:
