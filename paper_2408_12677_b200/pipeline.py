@@ -296,7 +296,8 @@ class Trainer:
         """Choose the render kernels' block-row walk (gs_set_render_rows; results are
         identical either way) for this scene: times gs_render_fwd + the backward of up
         to 4 views with each setting (best of ``reps``, CUDA events on the current
-        stream) and keeps the faster.  Nothing is updated: the screen gradients, loss
+        stream) and keeps the faster (the row walk only if >= 1% faster: config 4
+        measures ~5% faster, scannetpp ~3% slower).  Nothing is updated: the screen gradients, loss
         and blended counter the timing runs write are cleared.  Returns the setting."""
         lib, b = self.lib, self.buf
         views = list(views if views is not None else range(len(self.cameras)))[:4]
@@ -322,7 +323,7 @@ class Trainer:
         self.sgrad[0].zero_()
         self.loss.zero_()
         self.blended.zero_()
-        mode = 1 if best[1] < best[0] else 0
+        mode = 1 if best[1] < 0.99 * best[0] else 0  # the row walk only when clearly faster
         lib.set_render_rows(mode)
         self.render_tune = {"rows": mode, "ms_dense": best[0], "ms_rows": best[1], "views": views}
         torch.cuda.synchronize()
