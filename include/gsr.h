@@ -291,6 +291,22 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views
                                float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
                                void* stream);
 
+/* gs_project_bwd_views (overwrite when accumulate == 0) followed by gs_adam_step_dev's
+ * update of every row (step counter *step_dev advanced once, first; grad not zeroed),
+ * with the optimiser split at the geometry / SH-row boundary: the SH rows (11..F-1,
+ * final once the chain's colour half has run) are updated on `side_stream` while the
+ * geometry half of the chain runs on `stream`, then rows 0..10 on `stream`, which
+ * finally waits for the side stream.  Same results as gs_project_bwd_views +
+ * gs_adam_step_dev (Adam is element-wise); graph-capturable (the side stream forks from
+ * and joins `stream`).  side_stream NULL: no split.  Not thread-safe (two library-owned
+ * events).  n_views >= 1; params, m, v, grad: the model's full [F][P_stride] arrays. */
+gs_status gs_project_bwd_views_adam_dev(int n_views, const gs_camera* cams /*HOST[n_views]*/,
+                                        const gs_scene* scene /*HOST*/, float* params,
+                                        const uint8_t* const* flags /*HOST[n_views] of DEVICE*/,
+                                        float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
+                                        float* m, float* v, const float* lr_per_row /*HOST*/, float beta1,
+                                        float beta2, float eps, int64_t* step_dev, void* stream, void* side_stream);
+
 /* ---------------------------------------------------------------- K13 comparison baseline
  * The "straightforward per-pixel GPU port" the north_star's >= 10x target is measured
  * against (BASELINE.json north_star).  NOT the product path: drop-in

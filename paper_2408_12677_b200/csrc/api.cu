@@ -502,6 +502,62 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams, const gs_scen
   return check_launch("gs_project_bwd_views");
 }
 
+gs_status gs_project_bwd_views_adam_dev(int n_views, const gs_camera* cams, const gs_scene* scene, float* params,
+                                        const uint8_t* const* flags, float* const* sgrads, float* grad, int accumulate,
+                                        float* m, float* v, const float* lr_per_row, float beta1, float beta2,
+                                        float eps, int64_t* step_dev, void* stream, void* side_stream) {
+  static const char* fn = "gs_project_bwd_views_adam_dev";
+  g_err[0] = 0;
+  GS_TRY(check_scene(scene, fn));
+  if (n_views < 1 || !cams || !flags || !sgrads || !step_dev || !lr_per_row || !(beta1 >= 0.f && beta1 < 1.f) ||
+      !(beta2 >= 0.f && beta2 < 1.f) || !(eps >= 0.f)) {
+    set_error("%s: invalid arguments (n_views=%d)", fn, n_views);
+    return GS_ERR_ARG;
+  }
+  if (scene->P == 0) return GS_OK;
+  GS_TRY(check_ptrs(fn, {{params, "params"}, {grad, "grad"}, {m, "m"}, {v, "v"}}));
+  std::vector<DevCam> dc((size_t)n_views);
+  for (int i = 0; i < n_views; ++i) {
+    GS_TRY(check_camera(cams + i, fn));
+    if (!flags[i] || !sgrads[i]) {
+      set_error("%s: view %d has a NULL flags or sgrad pointer", fn, i);
+      return GS_ERR_ARG;
+    }
+    if (!aligned16(sgrads[i])) {
+      set_error("%s: sgrads[%d] is not 16-byte aligned", fn, i);
+      return GS_ERR_ALIGN;
+    }
+    dc[i] = make_devcam(cams[i]);
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream), side = static_cast<cudaStream_t>(side_stream);
+  // library-owned events (created once; only ordering, no timing): the colour half's end
+  // and the side stream's Adam end.  Recorded / waited in stream order, so they also work
+  // inside a CUDA-graph capture (the side stream forks from and joins the captured one).
+  static cudaEvent_t ev_colour = nullptr, ev_side = nullptr;
+  if (!ev_colour) {
+    if (cudaEventCreateWithFlags(&ev_colour, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming) != cudaSuccess)
+      return check_launch(fn);
+  }
+  const int64_t F = rows_of(scene), S = scene->P_stride, split = 11 * S;  // rows 0..10 | SH rows 11..F-1
+  launch_step_inc(step_dev, s);  // t += 1 once, before either half reads it
+  launch_project_bwd_views(n_views, dc.data(), flags, sgrads, scene->P, S, scene->sh_degree, params, grad,
+                           accumulate ? 1 : 0, s, side ? ev_colour : nullptr);
+  if (side) {  // the SH rows' Adam on the side stream, under the geometry half
+    cudaStreamWaitEvent(side, ev_colour, 0);
+    launch_adam(F, S, params, grad + split, m, v, lr_per_row, beta1, beta2, eps, 1.f, 1.f, 0, side, split, F * S, -1,
+                step_dev, false);
+    cudaEventRecord(ev_side, side);
+    launch_adam(F, S, params, grad, m, v, lr_per_row, beta1, beta2, eps, 1.f, 1.f, 0, s, 0, split, -1, step_dev,
+                false);
+    cudaStreamWaitEvent(s, ev_side, 0);
+  } else {
+    launch_adam(F, S, params, grad, m, v, lr_per_row, beta1, beta2, eps, 1.f, 1.f, 0, s, 0, F * S, -1, step_dev,
+                false);
+  }
+  return check_launch(fn);
+}
+
 size_t gs_spatial_order_workspace(const gs_scene* scene) {
   if (!scene || scene->P < 0) return 0;
   return spatial_order_workspace_bytes(scene->P);

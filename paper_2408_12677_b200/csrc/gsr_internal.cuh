@@ -101,7 +101,7 @@ void launch_project_views(int n_views, const DevCam* cams, int64_t P, int64_t S,
                           const gs_proj* outs, cudaStream_t s);
 void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* const* flags, float* const* sgrads,
                               int64_t P, int64_t S, int deg, const float* params, float* grad, int accumulate,
-                              cudaStream_t s);
+                              cudaStream_t s, cudaEvent_t colour_done = nullptr);
 // binning.cu
 size_t bin_workspace_bytes(int64_t P, int64_t key_capacity, int num_tiles);
 gs_status launch_bin_tiles(const DevCam& cam, int64_t P, gs_proj proj, void* ws, size_t ws_bytes,
@@ -141,7 +141,9 @@ void launch_naive_bwd(const DevCam& cam, const float* rec, const int32_t* ids, c
 // optim.cu
 void launch_adam(int64_t F, int64_t P_stride, float* params, float* grad, float* m, float* v, const float* lr,
                  float beta1, float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s,
-                 int64_t begin = 0, int64_t end = -1, int64_t live = -1, int64_t* step_dev = nullptr);
+                 int64_t begin = 0, int64_t end = -1, int64_t live = -1, int64_t* step_dev = nullptr,
+                 bool inc_step = true);
+void launch_step_inc(int64_t* step_dev, cudaStream_t s);
 void launch_adam_dev(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
                      float beta2, float eps, int64_t* step_dev, int zero_grad, cudaStream_t s, int64_t live = -1);
 gs_status launch_adam_peers(int64_t F, int64_t S, int world, int rank, const float* const* grad_peers,

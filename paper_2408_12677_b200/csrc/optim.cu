@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(256) k_l1(int64_t npix, const float* __restric
 
 void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, float* v, const float* lr, float beta1,
                  float beta2, float eps, float bc1, float bc2, int zero_grad, cudaStream_t s, int64_t begin,
-                 int64_t end, int64_t live, int64_t* step_dev) {
+                 int64_t end, int64_t live, int64_t* step_dev, bool inc_step) {
   LrTable t{};
   for (int64_t r = 0; r < F && r < 64; ++r) t.step[r] = step_dev ? lr[r] : lr[r] / bc1;
-  if (step_dev) {
+  if (step_dev && inc_step) {
     k_step_inc<<<1, 1, 0, s>>>(step_dev);
     count_launch();
   }
@@ -232,6 +232,11 @@ void launch_adam(int64_t F, int64_t S, float* params, float* grad, float* m, flo
                                            reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), begin / 4,
                                            end / 4, S / 4, cl4, t, (int)F, beta1, beta2, eps,
                                            step_dev ? 0.f : 1.f / sqrtf(bc2), step_dev, zero_grad);
+  count_launch();
+}
+
+void launch_step_inc(int64_t* step_dev, cudaStream_t s) {
+  k_step_inc<<<1, 1, 0, s>>>(step_dev);
   count_launch();
 }
 

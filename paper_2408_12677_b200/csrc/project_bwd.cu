@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(128, GSR_WIDE_MINB_GEOM) k_project_bwd_geom_wi
 
 void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* const* flags, float* const* sgrads,
                               int64_t P, int64_t S, int deg, const float* params, float* grad, int accumulate,
-                              cudaStream_t s) {
+                              cudaStream_t s, cudaEvent_t colour_done) {
   const int block = 256;
   const int grid = (int)std::min<int64_t>((P + block - 1) / block, (int64_t)sm_count() * 8);
   if (n_views > kMaxViews) {  // one pass per kMaxWide views (the views in the inner loop)
@@ -702,6 +702,8 @@ void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* co
         case 2: k_project_bwd_color_wide<2><<<gridw, 128, 0, s>>>(vb, P, S, params, grad, acc); break;
         default: k_project_bwd_color_wide<3><<<gridw, 128, 0, s>>>(vb, P, S, params, grad, acc); break;
       }
+      // the SH rows (11..F-1) are final after the last pass's colour kernel
+      if (colour_done && v0 + kMaxWide >= n_views) cudaEventRecord(colour_done, s);
       k_project_bwd_geom_wide<<<gridw, 128, 0, s>>>(vb, P, S, params, grad, acc);
       count_launch(2);
     }
@@ -722,6 +724,7 @@ void launch_project_bwd_views(int n_views, const DevCam* cams, const uint8_t* co
       case 2: k_project_bwd_color<2><<<grid, block, 0, s>>>(vb, P, S, params, grad, acc); break;
       default: k_project_bwd_color<3><<<grid, block, 0, s>>>(vb, P, S, params, grad, acc); break;
     }
+    if (colour_done && v0 + kMaxViews >= n_views) cudaEventRecord(colour_done, s);
     k_project_bwd_geom<<<grid, block, 0, s>>>(vb, P, S, params, grad, acc);
     count_launch(2);
   }

@@ -154,6 +154,9 @@ class Library:
         lib.gs_naive_render_fwd.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_naive_render_bwd_screen.argtypes = [vp, vp, GsProj, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         lib.gs_project_bwd_views.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp]
+        lib.gs_project_bwd_views_adam_dev.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp,
+                                                      C.c_float, C.c_float, C.c_float, vp, vp, vp]
+        lib.gs_project_bwd_views_adam_dev.restype = i32
         lib.gs_adam_step.argtypes = [vp, vp, vp, vp, vp, vp, C.c_float, C.c_float, C.c_float, i64, C.c_int, vp]
         lib.gs_spatial_order_workspace.argtypes = [vp]
         lib.gs_spatial_order_workspace.restype = C.c_size_t
@@ -298,6 +301,21 @@ class Library:
         sg = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in sgrads])
         return self._check("gs_project_bwd_views", self.lib.gs_project_bwd_views(
             n, cam_arr, C.byref(sc), _ptr(params), fl, sg, _ptr(grad), 1 if accumulate else 0, _stream(stream)))
+
+    def project_bwd_views_adam_dev(self, cams, sc, params, flags, sgrads, grad, m, v, lr_per_row, step_dev,
+                                   accumulate=False, side_stream=None, beta1=0.9, beta2=0.999, eps=1e-15,
+                                   stream=None):
+        """gs_project_bwd_views + gs_adam_step_dev with the SH rows' update on side_stream
+        (torch stream, None: no split) under the chain's geometry half."""
+        n = len(cams)
+        cam_arr = (GsCamera * max(n, 1))(*cams)
+        fl = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in flags])
+        sg = (C.c_void_p * max(n, 1))(*[t.data_ptr() for t in sgrads])
+        lr = (C.c_float * len(lr_per_row))(*[float(x) for x in lr_per_row])
+        side = C.c_void_p(side_stream.cuda_stream) if side_stream is not None else C.c_void_p(0)
+        return self._check("gs_project_bwd_views_adam_dev", self.lib.gs_project_bwd_views_adam_dev(
+            n, cam_arr, C.byref(sc), _ptr(params), fl, sg, _ptr(grad), 1 if accumulate else 0, _ptr(m), _ptr(v), lr,
+            beta1, beta2, eps, _ptr(step_dev), _stream(stream), side))
 
     # -- visibility-sparse exchange (NEXT-2) -------------------------------
     def visibility_union(self, flags, P, visible, accumulate=False, stream=None):

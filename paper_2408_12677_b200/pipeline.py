@@ -185,6 +185,7 @@ class Trainer:
                       for _ in range(n_sets * self.chunk)]
         self._n_sets = n_sets
         self.num_keys = torch.zeros(len(cameras), dtype=torch.int64, device=device)
+        self._adam_side = None  # side stream of gs_project_bwd_views_adam_dev (created on first use)
         self.blended = torch.zeros(1, dtype=torch.int64, device=device)
         self.loss = torch.zeros(1, dtype=torch.float32, device=device)
         self.hooks = None
@@ -412,6 +413,11 @@ class Trainer:
         chain_ev = [None] * n_sets  # per slot set: the chain that last consumed it
         first = True  # the first chain of an iteration overwrites grad (no zeroing pass needed)
         n_chain = 0
+        # the last chain and Adam in one library call with the SH rows' update on a side
+        # stream under the chain's geometry half (gs_project_bwd_views_adam_dev): the
+        # single-GPU device-step (graph) path; GSR_ADAM_OVERLAP=0 for A/B
+        fuse_tail = (self.optimizer is None and self.allreduce is None and self.device_step and S > 1
+                     and os.environ.get("GSR_ADAM_OVERLAP", "1") != "0")
         for k, v in enumerate(views):
             t_rgb, t_depth, ready, consumed = targets(k, v)
             base = (n_chain % n_sets) * self.chunk  # slot set of the chunk being filled
@@ -452,7 +458,7 @@ class Trainer:
                     done.append(ev)
             if after_view is not None:
                 after_view(k)
-            if len(pending) == self.chunk:
+            if len(pending) == self.chunk and not (fuse_tail and k == len(views) - 1):
                 for ev in done:
                     main.wait_event(ev)
                 done = []
@@ -465,6 +471,17 @@ class Trainer:
                 n_chain += 1
         for ev in done:
             main.wait_event(ev)
+        if fuse_tail and pending:
+            if self._adam_side is None:
+                self._adam_side = torch.cuda.Stream(device=self.device)
+            base, n = (n_chain % n_sets) * self.chunk, len(pending)
+            self._hook("project_bwd", "begin")
+            self.lib.project_bwd_views_adam_dev(pending, m.desc, m.params, self.flags[base:base + n],
+                                                self.sgrad[base:base + n], m.grad, m.m, m.v, m.lr, m.step_dev,
+                                                accumulate=not first, side_stream=self._adam_side)
+            self._hook("project_bwd", "end")
+            m.step_count += 1
+            return
         if pending or first:
             self._chain(pending, accumulate=not first, base=(n_chain % n_sets) * self.chunk)
         m.step_count += 1

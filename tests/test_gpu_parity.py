@@ -310,6 +310,55 @@ def test_chain_end_to_end(lib, name):
 
 
 # ----------------------------------------------------------------------------- Adam / L1
+@pytest.mark.parametrize("n_views,side", [(3, True), (3, False), (11, True)])
+def test_project_bwd_views_adam_dev_matches_separate(lib, n_views, side):
+    """gs_project_bwd_views_adam_dev (the Trainer's graph-path tail: the SH rows' Adam on
+    a side stream under the chain's geometry half) == gs_project_bwd_views +
+    gs_adam_step_dev, bit for bit (gradient, parameters, moments, step counter), and the
+    screen-gradient buffers are left zero; n = 11 takes the wide chain."""
+    w = workload("small")
+    scene = w.scene
+    cams = [scenegen.camera_rt(320, 240, 300.0, 160.0, 120.0, scenegen.rot_y(0.05 * (k - 1)),
+                               [0.1 * (k % 4), -0.05 * (k % 3), 0.02 * k]) for k in range(n_views)]
+    sc = gsr.scene_desc(scene.P, scene.P_stride, scene.sh_degree)
+    params0 = torch.from_numpy(scene.params).to(DEV)
+    flags, sgrads, gcams = [], [], []
+    for k, cam in enumerate(cams):
+        proj, t, _ = gpu_project(lib, cam, scene)
+        b = gpu_bin(lib, cam, scene, proj)
+        out = gpu_render(lib, cam, scene, proj, b["sorted_ids"], b["ranges"])
+        ur, ud = scenegen.upstream_fields(20 + k, 320, 240)
+        sg = torch.zeros((scene.P, 12), dtype=torch.float32, device=DEV)
+        lib.render_bwd_screen(gsr.camera(cam), sc, proj, b["sorted_ids"], b["ranges"], out["T_final"],
+                              out["n_contrib"], torch.from_numpy(ur).to(DEV), torch.from_numpy(ud).to(DEV), sg)
+        flags.append(t["flags"])
+        sgrads.append(sg)
+        gcams.append(gsr.camera(cam))
+    torch.cuda.synchronize()
+    lr = pipeline.lr_per_row(scene.sh_degree)
+    rng = np.random.default_rng(3)
+    m0 = torch.from_numpy((rng.normal(size=params0.shape) * 1e-3).astype(np.float32)).to(DEV)
+    v0 = torch.from_numpy(rng.uniform(0, 1e-4, size=params0.shape).astype(np.float32)).to(DEV)
+    res = {}
+    for mode in ("separate", "fused"):
+        p, m, v = params0.clone(), m0.clone(), v0.clone()
+        g = torch.full_like(p, 7.0)  # overwritten (accumulate = 0)
+        sgs = [x.clone() for x in sgrads]
+        t = torch.full((1,), 4, dtype=torch.int64, device=DEV)
+        if mode == "separate":
+            lib.project_bwd_views(gcams, sc, p, flags, sgs, g, accumulate=False)
+            lib.adam_step_dev(sc, p, g, m, v, lr, t, zero_grad=False)
+        else:
+            lib.project_bwd_views_adam_dev(gcams, sc, p, flags, sgs, g, m, v, lr, t, accumulate=False,
+                                           side_stream=torch.cuda.Stream(device=DEV) if side else None)
+        torch.cuda.synchronize()
+        assert all(int(torch.count_nonzero(x)) == 0 for x in sgs)
+        res[mode] = [x.cpu().numpy() for x in (g, p, m, v, t)]
+    assert np.abs(res["separate"][0]).max() > 0
+    for a, c, nm in zip(res["separate"], res["fused"], ("grad", "params", "m", "v", "step")):
+        assert np.array_equal(a, c), nm
+
+
 def test_adam_parity(lib):
     rng = np.random.default_rng(0)
     P, deg = 1000, 3
