@@ -291,7 +291,9 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views
                                float* const* sgrads /*HOST[n_views] of DEVICE*/, float* grad, int accumulate,
                                void* stream);
 
-/* gs_project_bwd_views (overwrite when accumulate == 0) followed by gs_adam_step_dev's
+/* The end of one optimisation iteration (the explicitly derived
+ * gradient, then the first-order update; Adam per north_star, R20):
+ * gs_project_bwd_views (overwrite when accumulate == 0) followed by gs_adam_step_dev's
  * update of every row (step counter *step_dev advanced once, first; grad not zeroed),
  * with the optimiser split at the geometry / SH-row boundary: the SH rows (11..F-1,
  * final once the chain's colour half has run) are updated on `side_stream` while the
@@ -299,7 +301,9 @@ gs_status gs_project_bwd_views(int n_views, const gs_camera* cams /*HOST[n_views
  * finally waits for the side stream.  Same results as gs_project_bwd_views +
  * gs_adam_step_dev (Adam is element-wise); graph-capturable (the side stream forks from
  * and joins `stream`).  side_stream NULL: no split.  Not thread-safe (two library-owned
- * events).  n_views >= 1; params, m, v, grad: the model's full [F][P_stride] arrays. */
+ * events).  n_views >= 1; params, m, v, grad: the model's full [F][P_stride] arrays.
+ * Errors: GS_ERR_ARG (NULL array, n_views < 1, step_dev NULL, betas outside [0, 1)),
+ * GS_ERR_ALIGN (an sgrad not 16-byte aligned), as gs_project_bwd_views otherwise. */
 gs_status gs_project_bwd_views_adam_dev(int n_views, const gs_camera* cams /*HOST[n_views]*/,
                                         const gs_scene* scene /*HOST*/, float* params,
                                         const uint8_t* const* flags /*HOST[n_views] of DEVICE*/,
