@@ -135,3 +135,25 @@ def test_render_rows_switch_host_only(libs):
                 assert lib.render_rows() == bool(v)
         finally:
             lib.set_render_rows(was)
+
+
+def test_project_bwd_views_adam_dev_host_validation(libs):
+    """gs_project_bwd_views_adam_dev rejects bad arguments before any CUDA call."""
+    from paper_2408_12677_b200 import gsr
+    import scenegen
+    lib = libs[0]
+    sc = gsr.scene_desc(4, 4, 0)
+    lr = (C.c_float * 14)(*([1e-3] * 14))
+    fn = lib.lib.gs_project_bwd_views_adam_dev
+    # n_views < 1
+    st = fn(0, None, C.byref(sc), None, None, None, None, 0, None, None, lr, 0.9, 0.999, 1e-15, None, None, None)
+    assert st == gsr.GS_ERR_ARG and "gs_project_bwd_views_adam_dev" in lib.last_error()
+    cam = (gsr.GsCamera * 1)(gsr.camera(scenegen.identity_camera(64, 48, 60.0, 32.0, 24.0)))
+    fl = (C.c_void_p * 1)(C.c_void_p(0x1000))
+    sg = (C.c_void_p * 1)(C.c_void_p(0x1000))
+    step = C.c_void_p(0x1000)
+    # step_dev NULL; beta outside [0, 1)
+    st = fn(1, cam, C.byref(sc), None, fl, sg, None, 0, None, None, lr, 0.9, 0.999, 1e-15, None, None, None)
+    assert st == gsr.GS_ERR_ARG
+    st = fn(1, cam, C.byref(sc), None, fl, sg, None, 0, None, None, lr, 1.5, 0.999, 1e-15, step, None, None)
+    assert st == gsr.GS_ERR_ARG
