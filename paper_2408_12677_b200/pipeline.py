@@ -418,6 +418,11 @@ class Trainer:
         # single-GPU device-step (graph) path; GSR_ADAM_OVERLAP=0 for A/B
         fuse_tail = (self.optimizer is None and self.allreduce is None and self.device_step and S > 1
                      and os.environ.get("GSR_ADAM_OVERLAP", "1") != "0")
+        # A/B: view k's binning waits for view k - lag's (0: all views bin concurrently)
+        # and views >= 1 for view 0's when head is set (the first render starts sooner)
+        bin_lag = int(os.environ.get("GSR_BIN_LAG", "0"))
+        bin_head = os.environ.get("GSR_BIN_HEAD", "0") != "0"
+        binned_evs = []
         for k, v in enumerate(views):
             t_rgb, t_depth, ready, consumed = targets(k, v)
             base = (n_chain % n_sets) * self.chunk  # slot set of the chunk being filled
@@ -434,10 +439,15 @@ class Trainer:
                     bs.wait_event(buf_ev[bi])
                 if proj_ev is not None:
                     bs.wait_event(proj_ev)
+                if bin_lag and k >= bin_lag:
+                    bs.wait_event(binned_evs[k - bin_lag])
+                if bin_head and k >= 1:
+                    bs.wait_event(binned_evs[0])
                 with torch.cuda.stream(bs):
                     gcam, proj, order = self._bin_view(v, slot, b, projected=proj_ev is not None)
                     binned = torch.cuda.Event()
                     binned.record(bs)
+                binned_evs.append(binned)
                 s.wait_event(binned)
                 with torch.cuda.stream(s):
                     self._render_view(v, slot, b, gcam, proj, order, t_rgb, t_depth, ready, consumed)
