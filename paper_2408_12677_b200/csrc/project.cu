@@ -480,6 +480,12 @@ __device__ __forceinline__ float cam_z(const DevCam& cam, float px, float py, fl
 #ifndef GSR_PROJ_SPEC
 #define GSR_PROJ_SPEC 1
 #endif
+#ifndef GSR_PROJV_SPEC
+#define GSR_PROJV_SPEC 1  // scannetpp 8 views 139 -> 117 us, config 4 416 -> 343 us (bit-identical)
+#endif
+#ifndef GSR_PROJV_MINB
+#define GSR_PROJV_MINB 8  // k_project_views2 CTAs per SM (register cap)
+#endif
 // ---------------------------------------------------------------------------
 // K1 v2 (default): as K1, with the bytes a view does not need left in HBM and twice
 // the Gaussians in flight per SM.
@@ -563,7 +569,7 @@ __global__ void __launch_bounds__(kPjThreads, 10) k_project2(DevCam cam, int64_t
 // the SH coefficients read per visible (Gaussian, view) straight from the rows -- the
 // second and later views hit L1 / L2).  Bit-identical to gs_project.
 template <int DEG>
-__global__ void __launch_bounds__(kPjThreads, 8) k_project_views2(const __grid_constant__ ViewOuts vo, int64_t P,
+__global__ void __launch_bounds__(kPjThreads, GSR_PROJV_MINB) k_project_views2(const __grid_constant__ ViewOuts vo, int64_t P,
                                                                    int64_t S, const float* __restrict__ prm) {
   __shared__ __align__(16) float s_geo[11][kPjThreads];
   __shared__ __align__(8) uint64_t bar[2];
@@ -580,14 +586,24 @@ __global__ void __launch_bounds__(kPjThreads, 8) k_project_views2(const __grid_c
     mbar_arrive_expect_tx(&bar[0], 3u * bytes);
 #pragma unroll 1
     for (int r = 0; r < 3; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[0]);
+#if GSR_PROJV_SPEC
+    // the 8 other rows in the same round trip: with a batch of views around the scene
+    // nearly every CTA has a Gaussian in front of some view
+    mbar_arrive_expect_tx(&bar[1], 8u * bytes);
+#pragma unroll 1
+    for (int r = 3; r < 11; ++r) bulk_g2s(s_geo[r], prm + r * S + i0, bytes, &bar[1]);
+#endif
   }
   mbar_wait(&bar[0], 0);
   const int64_t i = i0 + tid;
   bool front = false;
   if (i < P)
     for (int v = 0; v < vo.n; ++v) front = front || cam_z(vo.cam[v], s_geo[0][tid], s_geo[1][tid], s_geo[2][tid]) > vo.cam[v].z_near;
+#if GSR_PROJV_SPEC
+  mbar_wait(&bar[1], 0);  // also when nothing is in front: no copy may outlive the CTA
+#endif
   const bool any_front = __syncthreads_or(front);
-  if (any_front) {
+  if (!GSR_PROJV_SPEC && any_front) {
     if (tid == 0) {
       mbar_arrive_expect_tx(&bar[1], 8u * bytes);
 #pragma unroll 1
