@@ -483,6 +483,9 @@ __device__ __forceinline__ float cam_z(const DevCam& cam, float px, float py, fl
 #ifndef GSR_PROJV_SPEC
 #define GSR_PROJV_SPEC 1  // scannetpp 8 views 139 -> 117 us, config 4 416 -> 343 us (bit-identical)
 #endif
+#ifndef GSR_PROJ_MINB
+#define GSR_PROJ_MINB 10  // k_project2 CTAs per SM (register cap)
+#endif
 #ifndef GSR_PROJV_MINB
 #define GSR_PROJV_MINB 8  // k_project_views2 CTAs per SM (register cap)
 #endif
@@ -500,7 +503,7 @@ __device__ __forceinline__ float cam_z(const DevCam& cam, float px, float py, fl
 // Same arithmetic as K1 (outputs bit-identical).
 // ---------------------------------------------------------------------------
 template <int DEG>
-__global__ void __launch_bounds__(kPjThreads, 10) k_project2(DevCam cam, int64_t P, int64_t S,
+__global__ void __launch_bounds__(kPjThreads, GSR_PROJ_MINB) k_project2(DevCam cam, int64_t P, int64_t S,
                                                              const float* __restrict__ prm, float4* __restrict__ rec,
                                                              int32_t* __restrict__ radius_out,
                                                              int32_t* __restrict__ tiles_out,

@@ -11,6 +11,7 @@ import scenegen  # noqa: E402
 from paper_2408_12677_b200 import gsr, pipeline  # noqa: E402
 
 cfg, libs = sys.argv[1], sys.argv[2:]
+single = os.environ.get("PROBE_SINGLE", "0") == "1"  # gs_project of view 0 instead
 dev = torch.device("cuda:0")
 w = scenegen.make(cfg, 0)
 outs = {}
@@ -27,13 +28,16 @@ for name in libs * 2:
     for r in range(30):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        lib.project_views(gcams, model.desc, model.params, projs)
+        if single:
+            lib.project(gcams[0], model.desc, model.params, projs[0])
+        else:
+            lib.project_views(gcams, model.desc, model.params, projs)
         e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     ts = sorted(ts[5:])
     sig = [(t["radius"][:model.P].clone(), t["tiles"][:model.P].clone(), t["flags"][:model.P].clone())
-           for _, t in projs_t]
+           for _, t in projs_t[:1 if single else len(projs_t)]]
     if "ref" in outs:
         same = all(torch.equal(a, b) for x, y in zip(outs["ref"], sig) for a, b in zip(x, y))
     else:
